@@ -1,0 +1,177 @@
+/*
+ * sfeec_b200.h -- the C ABI of the B200-native SFEEC leapfrog.
+ *
+ * This is the drop-in boundary for the reference's time-stepping hot path.
+ * The reference has no FFI: its boundary is the C++ API in
+ * /root/reference/proj/include/sfeec/{sparse,dynamics,yee}.hpp, and the
+ * C++ classes in include/sfeec/ (same names and signatures) forward to the
+ * functions below. Each entry point cites the reference interface it
+ * replaces. Conventions:
+ *
+ *   - return 0 on success; SFEEC_EINVAL (1) where the reference throws
+ *     sfeec::InvalidParameter, SFEEC_ECUDA (2) / SFEEC_ENCCL (3) /
+ *     SFEEC_ENOMEM (4) where it would throw std::runtime_error. The message
+ *     is in sfeec_last_error() (thread-local).
+ *   - host buffers are caller-owned and copied; calls are blocking and not
+ *     thread-safe per handle (same as the reference's mutable CFL cache).
+ *   - no CPU fallback: without a usable sm_100 device every compute entry
+ *     point fails with SFEEC_ECUDA.
+ */
+#ifndef SFEEC_B200_H
+#define SFEEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SFEEC_OK = 0,
+  SFEEC_EINVAL = 1,
+  SFEEC_ECUDA = 2,
+  SFEEC_ENCCL = 3,
+  SFEEC_ENOMEM = 4
+};
+
+/* CSR view of a sfeec::SparseOperator (sparse.hpp:14-33): row_ptr[rows+1],
+ * column-sorted col_idx/val, no stored zeros. int64 row pointers so operators
+ * above 2^31 nonzeros fit. */
+typedef struct {
+  int64_t rows, cols;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const double* val;
+} sfeec_csr;
+
+/* CSR owned by the library (returned by the builders); free with sfeec_csr_free. */
+typedef struct {
+  int64_t rows, cols, nnz;
+  int64_t* row_ptr;
+  int32_t* col_idx;
+  double* val;
+} sfeec_csr_owned;
+
+const char* sfeec_last_error(void);
+const char* sfeec_version(void);
+void sfeec_csr_free(sfeec_csr_owned* m);
+/* number of CUDA devices usable by the library (0 without a GPU) */
+int sfeec_device_count(void);
+
+/* ---- the unstructured leapfrog (SplitScheme, dynamics.hpp:31-67) ---------- */
+typedef struct sfeec_dev sfeec_dev;
+
+enum {
+  SFEEC_SPLIT_LIE_TROTTER = 0, /* SplitKind::LieTrotter */
+  SFEEC_SPLIT_STRANG = 1       /* SplitKind::Strang */
+};
+enum {
+  SFEEC_FORM_AE = 0, /* Formulation::AE: first = a */
+  SFEEC_FORM_BE = 1  /* Formulation::BE: first = b = C a */
+};
+/* flags */
+enum {
+  /* q is already symmetric (skip symmetric_part, dynamics.cpp:10-25) */
+  SFEEC_Q_IS_SYMMETRIC = 1,
+  /* bitwise-reference mode: the three sub-flows of dynamics.cpp:80-83,
+   * one thread per CSR row in stored order, separate multiply and add
+   * (no FMA) -- reproduces the reference CPU step bit for bit */
+  SFEEC_STRICT = 2,
+  /* do not run the CFL check on the first step (warn_cfl = false) */
+  SFEEC_NO_CFL_WARN = 4
+};
+
+/* Replaces SplitScheme::SplitScheme (dynamics.hpp:33-36, dynamics.cpp:29-45):
+ * copies Q (symmetrised like symmetric_part unless SFEEC_Q_IS_SYMMETRIC), C,
+ * C^T, M2 and the optional divergence D to device `device`. Errors as the
+ * reference: dt < 0, non-square Q, or inconsistent dimensions -> EINVAL. */
+int sfeec_dev_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* m2,
+                     const sfeec_csr* div /* nullable */, double dt, double eps0, double mu0,
+                     int split_kind, int formulation, int device, int flags,
+                     sfeec_dev** out);
+void sfeec_dev_destroy(sfeec_dev* h);
+
+/* Resident state (FieldState, dynamics.hpp:20-25). n_first = rows of C for
+ * BE, cols of C for AE; n_e = cols of C. */
+int sfeec_dev_set_state(sfeec_dev* h, const double* first, int64_t n_first, const double* e,
+                        int64_t n_e, double time);
+int sfeec_dev_get_state(sfeec_dev* h, double* first, double* e, double* time);
+
+/* nsteps x SplitScheme::step (dynamics.cpp:69-90) on the resident state.
+ * Production mode merges the adjacent half-kicks of consecutive Strang steps
+ * (exact in real arithmetic); SFEEC_STRICT runs the three sub-flows. */
+int sfeec_dev_advance(sfeec_dev* h, int64_t nsteps);
+/* as advance, recording energy (dynamics.cpp:92-102) and the Gauss residual
+ * (dynamics.cpp:104-112; 0 without div) after every diag_every-th step into
+ * the nullable arrays (nsteps / diag_every entries). */
+int sfeec_dev_advance_diag(sfeec_dev* h, int64_t nsteps, int64_t diag_every,
+                           double* energy_hist, double* gauss_hist);
+/* exact sub-flows, dynamics.cpp:47-67; do not advance the clock */
+int sfeec_dev_flow_he(sfeec_dev* h, double dt);
+int sfeec_dev_flow_ha(sfeec_dev* h, double dt);
+int sfeec_dev_energy(sfeec_dev* h, double* out);
+int sfeec_dev_gauss_residual(sfeec_dev* h, double* out);
+/* dynamics.cpp:114-133: 40 power iterations from U(-1,1), seed 0x5fec5fec */
+int sfeec_dev_cfl_number(sfeec_dev* h, double* out);
+/* Q_sym as stored on the device (nnz query with NULL outputs) */
+int sfeec_dev_q_sym(sfeec_dev* h, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx,
+                    double* val);
+
+/* device-resident access for benchmarks / multi-GPU plumbing */
+int sfeec_dev_set_stream(sfeec_dev* h, void* cuda_stream);
+int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e);
+/* number of kernel launches issued by the last advance call */
+int64_t sfeec_dev_last_launches(sfeec_dev* h);
+/* algorithmic HBM bytes of one merged leapfrog step */
+double sfeec_dev_step_bytes(sfeec_dev* h);
+
+/* ---- structured Yee / lumped-mass SFEEC (yee.hpp:12-37) ------------------ */
+typedef struct sfeec_yee sfeec_yee;
+enum { SFEEC_BC_PERIODIC = 0, SFEEC_BC_PEC = 1 };
+
+/* Lumped SFEEC on an nx*ny*nz cubical lattice: Q = I/dV, M2 = dV I
+ * (lumped_mass, yee.cpp:76-81), C with entries +-1/spacing
+ * (operators.cpp:37). bc = PERIODIC reproduces yee_equivalence_check
+ * (yee.cpp:83-135); bc = PEC drops boundary edges. precision 8 = fp64,
+ * 4 = fp32 fields. DOF numbering: sfeec_yee_dof_counts / DESIGN.md. */
+int sfeec_yee_create(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                     double eps0, double mu0, int bc, int precision, int device,
+                     sfeec_yee** out);
+void sfeec_yee_destroy(sfeec_yee* h);
+int sfeec_yee_dof_counts(const sfeec_yee* h, int64_t* n_edges, int64_t* n_faces);
+/* (b, e) state in the SFEEC numbering, always passed as fp64 */
+int sfeec_yee_set_state(sfeec_yee* h, const double* b, const double* e, double time);
+int sfeec_yee_get_state(sfeec_yee* h, double* b, double* e, double* time);
+/* nsteps Strang steps (b half-kicks merged across steps) */
+int sfeec_yee_advance(sfeec_yee* h, int64_t nsteps);
+int sfeec_yee_flow_he(sfeec_yee* h, double dt);
+int sfeec_yee_flow_ha(sfeec_yee* h, double dt);
+int sfeec_yee_energy(sfeec_yee* h, double* out);
+int sfeec_yee_set_stream(sfeec_yee* h, void* cuda_stream);
+/* 0: two-kernel (e-kick, b-kick); 1: fused single-sweep step (default) */
+int sfeec_yee_set_variant(sfeec_yee* h, int variant);
+int64_t sfeec_yee_last_launches(sfeec_yee* h);
+/* Returns (and resets) the accumulated device time of the steady-state step
+ * kernels (the fused sweep, or the e/b-kick pair) measured with CUDA events on
+ * the launch stream, then enables/disables timing for later advance calls. */
+int sfeec_yee_kernel_timing(sfeec_yee* h, int enable, double* ms_total, int64_t* launches);
+double sfeec_yee_step_bytes(sfeec_yee* h);
+
+/* ---- host operator builders (setup, not timed) ---------------------------- */
+/* Lumped Yee operators in the sfeec_yee DOF numbering: C (faces x edges,
+ * +-1/spacing), and the divergence D (cells x faces). Replaces
+ * generate_cubical_lattice + derivative_matrix for Q1 (mesh_cubical.cpp:15-173,
+ * operators.cpp:29-42), extended with PEC. */
+int sfeec_build_yee_curl(int nx, int ny, int nz, double dx, double dy, double dz, int bc,
+                         sfeec_csr_owned* c, sfeec_csr_owned* div);
+/* operator_from_triplets (sparse.cpp:20-61), int64-safe */
+int sfeec_csr_from_triplets(int64_t rows, int64_t cols, int64_t n, const int32_t* r,
+                            const int32_t* c, const double* v, sfeec_csr_owned* out);
+/* symmetric_part (dynamics.cpp:10-25) and transpose (sparse.cpp:75-94) */
+int sfeec_csr_symmetric_part(const sfeec_csr* q, sfeec_csr_owned* out);
+int sfeec_csr_transpose(const sfeec_csr* a, sfeec_csr_owned* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,22 @@
+"""B200-native SFEEC leapfrog (arXiv 2301.01753 hot path).
+
+The compute path is libsfeec_b200.so (hand-written sm_100a CUDA + host C++),
+reached through the C ABI in include/sfeec_b200.h. See DESIGN.md.
+"""
+from ._lib import DeviceError, InvalidParameter, LIB_PATH, lib  # noqa: F401
+from .scheme import (  # noqa: F401
+    FieldState,
+    Formulation,
+    SparseOperator,
+    SplitKind,
+    SplitScheme,
+    UnitSystem,
+    YeeScheme,
+    device_count,
+    make_state,
+    operator_from_triplets,
+    scaled_identity,
+    symmetric_part,
+    transpose,
+    yee_operators,
+)

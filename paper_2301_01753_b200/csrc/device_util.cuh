@@ -1,0 +1,65 @@
+// Device-side helpers shared by the leapfrog and Yee kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "common.hpp"
+
+namespace sfeec_b200 {
+
+#define SFEEC_CUDA(call)                                                               \
+  do {                                                                                 \
+    cudaError_t err_ = (call);                                                         \
+    if (err_ != cudaSuccess)                                                           \
+      throw ::sfeec_b200::Error(err_ == cudaErrorMemoryAllocation ? SFEEC_ENOMEM       \
+                                                                  : SFEEC_ECUDA,       \
+                                std::string(#call) + ": " + cudaGetErrorString(err_)); \
+  } while (0)
+
+#define SFEEC_LAUNCH_CHECK() SFEEC_CUDA(cudaGetLastError())
+
+// One CTA-resident persistent grid worth of blocks for grid-stride kernels:
+// 148 SMs x 8.
+constexpr int kReduceBlocks = 148 * 8;
+constexpr int kReduceThreads = 256;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    n = count;
+    if (count) SFEEC_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) SFEEC_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) SFEEC_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+  }
+};
+
+// Checks there is a usable device and makes `device` current.
+void select_device(int device);
+
+// Deterministic reductions (fixed grid, fixed combine order): dot(x, y) and
+// max |x| over n doubles, result to host.
+double device_dot(const double* x, const double* y, int64_t n, double* partials,
+                  cudaStream_t s);
+double device_max_abs(const double* x, int64_t n, double* partials, cudaStream_t s);
+double device_sumsq(const float* x, int64_t n, double* partials, cudaStream_t s);
+
+}  // namespace sfeec_b200

@@ -1,0 +1,399 @@
+// The unstructured SFEEC leapfrog on one B200: device-resident Q_sym, C, C^T,
+// M2 (and D), state (first, e) and the step sequence of
+//   SplitScheme::flow_he / flow_ha / step   (reference dynamics.cpp:47-90)
+// over CSR operators (reference sparse.hpp:14-33, spmv sparse.cpp:96-104).
+//
+// Two execution modes:
+//   production  merged Strang half-kicks, FMA, sub-warp-per-row CSR-vector or
+//               sliced-ELL kernels chosen per operator (spmv_kernels.cuh);
+//   strict      the reference's three sub-flows, one thread per row in CSR
+//               order, separate multiply/add -> bitwise equal to the CPU step.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+
+#include "device_util.cuh"
+#include "spmv_kernels.cuh"
+
+namespace sfeec_b200 {
+
+struct LeapfrogDev {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int kind = SFEEC_SPLIT_STRANG, form = SFEEC_FORM_BE, flags = 0;
+  double dt = 0, eps0 = 1, mu0 = 1;
+  DevOperator q, c, ct, m2, div;
+  bool has_div = false;
+  int64_t n1 = 0, n2 = 0, n_first = 0;
+  DevBuf<double> first, e, t1, t2, t3, partials;
+  double time = 0;
+  bool warned = false;
+  double cfl_cache = -1;
+  int64_t launches = 0;
+  bool strict() const { return (flags & SFEEC_STRICT) != 0; }
+  double c2() const { return 1.0 / (eps0 * mu0); }
+
+  ~LeapfrogDev() {
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  // y = A x
+  void apply(const DevOperator& a, const double* x, double* y) {
+    if (strict())
+      launch_spmv_strict(a, x, y, stream);
+    else
+      launch_spmv(a, x, y, 0.0, false, stream);
+    ++launches;
+  }
+  // y += alpha * A x   (strict: y = y + alpha*(A x) with separate rounding)
+  void apply_axpy(const DevOperator& a, const double* x, double* y, double alpha) {
+    if (strict())
+      launch_spmv_axpy_strict(a, x, y, alpha, stream);
+    else
+      launch_spmv(a, x, y, alpha, true, stream);
+    ++launches;
+  }
+
+  // dynamics.cpp:47-55
+  void flow_he(double h) {
+    apply(q, e.p, t1.p);
+    if (form == SFEEC_FORM_AE) {
+      axpy_vec(first.p, t1.p, -h, n1);
+    } else {
+      apply_axpy(c, t1.p, first.p, -h);
+    }
+  }
+  void axpy_vec(double* y, const double* x, double alpha, int64_t n) {
+    launch_axpy(y, x, alpha, n, strict(), stream);
+    ++launches;
+  }
+  // dynamics.cpp:57-67
+  void flow_ha(double h) {
+    const double f = h * c2();
+    const double* b = first.p;
+    if (form == SFEEC_FORM_AE) {
+      apply(c, first.p, t3.p);
+      b = t3.p;
+    }
+    apply(m2, b, t2.p);
+    apply_axpy(ct, t2.p, e.p, f);
+  }
+
+  void check_cfl_once() {
+    if ((flags & SFEEC_NO_CFL_WARN) || warned) return;
+    warned = true;
+    double nu = cfl_number();
+    if (nu > 2.0)
+      std::fprintf(stderr,
+                   "sfeec: warning: CFL number %.3g > 2; the splitting is likely unstable at "
+                   "dt = %.3g\n",
+                   nu, dt);
+  }
+
+  void advance(int64_t n) {
+    launches = 0;
+    if (n <= 0) return;
+    check_cfl_once();
+    if (strict() || kind == SFEEC_SPLIT_LIE_TROTTER || form == SFEEC_FORM_AE) {
+      for (int64_t s = 0; s < n; ++s) {
+        if (kind == SFEEC_SPLIT_STRANG) {
+          flow_he(0.5 * dt);
+          flow_ha(dt);
+          flow_he(0.5 * dt);
+        } else {
+          flow_he(dt);
+          flow_ha(dt);
+        }
+      }
+    } else {
+      // merged Strang: He(h/2) [Ha(h) He(h)]^(n-1) Ha(h) He(h/2)
+      flow_he(0.5 * dt);
+      for (int64_t s = 0; s < n; ++s) {
+        flow_ha(dt);
+        flow_he(s == n - 1 ? 0.5 * dt : dt);
+      }
+    }
+    for (int64_t s = 0; s < n; ++s) time = time + dt;  // dynamics.cpp:88, per step
+  }
+
+  // dynamics.cpp:92-102
+  double energy() {
+    apply(q, e.p, t1.p);
+    double he = device_dot(e.p, t1.p, n1, partials.p, stream);
+    const double* b = first.p;
+    if (form == SFEEC_FORM_AE) {
+      apply(c, first.p, t3.p);
+      b = t3.p;
+    }
+    apply(m2, b, t2.p);
+    double ha = device_dot(b, t2.p, n2, partials.p, stream);
+    return 0.5 * (eps0 * he + ha / mu0);
+  }
+
+  // dynamics.cpp:104-112
+  double gauss_residual() {
+    require(form == SFEEC_FORM_BE, "gauss_residual: (b, e) formulation required");
+    if (!has_div) return 0.0;
+    DevBuf<double> db;
+    db.alloc((size_t)div.rows);
+    apply(div, first.p, db.p);
+    return device_max_abs(db.p, div.rows, partials.p, stream);
+  }
+
+  // dynamics.cpp:114-133 (power iteration on Q C^T M2 C, seed 0x5fec5fec)
+  double cfl_number() {
+    if (cfl_cache >= 0) return cfl_cache;
+    std::vector<double> hx((size_t)n1);
+    uint64_t st = 0x5fec5fec;
+    for (auto& v : hx) {
+      uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      z ^= z >> 31;
+      v = -1.0 + 2.0 * ((double)(z >> 11) * 0x1.0p-53);
+    }
+    DevBuf<double> x, y, w2, w3;
+    x.upload(hx.data(), hx.size(), stream);
+    y.alloc((size_t)n1);
+    w2.alloc((size_t)n2);
+    w3.alloc((size_t)n2);
+    double lambda = 0;
+    for (int it = 0; it < 40; ++it) {
+      apply(c, x.p, w2.p);
+      apply(m2, w2.p, w3.p);
+      apply(ct, w3.p, t1.p);
+      apply(q, t1.p, y.p);
+      double nrm = std::sqrt(device_dot(y.p, y.p, n1, partials.p, stream));
+      if (nrm == 0) break;
+      lambda = nrm;
+      launch_scale_copy(x.p, y.p, 1.0 / nrm, nrm, n1, stream);
+    }
+    cfl_cache = dt * std::sqrt(c2() * lambda);
+    return cfl_cache;
+  }
+};
+
+}  // namespace sfeec_b200
+
+using namespace sfeec_b200;
+
+struct sfeec_dev {
+  LeapfrogDev d;
+};
+
+extern "C" {
+
+int sfeec_dev_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* m2,
+                     const sfeec_csr* div, double dt, double eps0, double mu0, int split_kind,
+                     int formulation, int device, int flags, sfeec_dev** out) {
+  return guarded([&] {
+    require(out != nullptr, "sfeec_dev_create: null out");
+    *out = nullptr;
+    require(q && c && m2, "sfeec_dev_create: null operator");
+    csr_validate(*q, "Q");
+    csr_validate(*c, "C");
+    csr_validate(*m2, "M2");
+    if (div) csr_validate(*div, "div");
+    // dynamics.cpp:11-12 then :41-43
+    require(q->rows == q->cols, "SplitScheme: Q must be square");
+    require(dt >= 0, "SplitScheme: dt must be >= 0");
+    require(m2->rows == c->rows && m2->cols == c->rows && q->rows == c->cols,
+            "SplitScheme: operator dimensions inconsistent");
+    require(!div || div->cols == c->rows, "SplitScheme: divergence dimensions inconsistent");
+    require(split_kind == 0 || split_kind == 1, "SplitScheme: unknown split kind");
+    require(formulation == 0 || formulation == 1, "SplitScheme: unknown formulation");
+    select_device(device);
+    auto h = std::make_unique<sfeec_dev>();
+    LeapfrogDev& d = h->d;
+    d.device = device;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    d.own_stream = true;
+    d.kind = split_kind;
+    d.form = formulation;
+    d.flags = flags;
+    d.dt = dt;
+    d.eps0 = eps0;
+    d.mu0 = mu0;
+    HostCSR hq = csr_from_view(*q);
+    if (!(flags & SFEEC_Q_IS_SYMMETRIC)) hq = csr_symmetric_part(hq);
+    HostCSR hc = csr_from_view(*c);
+    HostCSR hct = csr_transpose(hc);
+    HostCSR hm2 = csr_from_view(*m2);
+    bool strict = (flags & SFEEC_STRICT) != 0;
+    d.q.upload(hq, strict, d.stream);
+    d.c.upload(hc, strict, d.stream);
+    d.ct.upload(hct, strict, d.stream);
+    d.m2.upload(hm2, strict, d.stream);
+    if (div) {
+      d.div.upload(csr_from_view(*div), strict, d.stream);
+      d.has_div = true;
+    }
+    d.n1 = c->cols;
+    d.n2 = c->rows;
+    d.n_first = formulation == SFEEC_FORM_BE ? d.n2 : d.n1;
+    d.first.alloc((size_t)d.n_first);
+    d.first.zero(d.stream);
+    d.e.alloc((size_t)d.n1);
+    d.e.zero(d.stream);
+    d.t1.alloc((size_t)d.n1);
+    d.t2.alloc((size_t)std::max<int64_t>(d.n2, 1));
+    d.t3.alloc((size_t)std::max<int64_t>(d.n2, 1));
+    d.partials.alloc(kReduceBlocks + 1);
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    *out = h.release();
+  });
+}
+
+void sfeec_dev_destroy(sfeec_dev* h) { delete h; }
+
+int sfeec_dev_set_state(sfeec_dev* h, const double* first, int64_t n_first, const double* e,
+                        int64_t n_e, double time) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    require(n_first == d.n_first && n_e == d.n1, "spmv: dimension mismatch");
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    if (n_first)
+      SFEEC_CUDA(cudaMemcpyAsync(d.first.p, first, sizeof(double) * (size_t)n_first,
+                                 cudaMemcpyHostToDevice, d.stream));
+    if (n_e)
+      SFEEC_CUDA(cudaMemcpyAsync(d.e.p, e, sizeof(double) * (size_t)n_e,
+                                 cudaMemcpyHostToDevice, d.stream));
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    d.time = time;
+  });
+}
+
+int sfeec_dev_get_state(sfeec_dev* h, double* first, double* e, double* time) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    if (first && d.n_first)
+      SFEEC_CUDA(cudaMemcpyAsync(first, d.first.p, sizeof(double) * (size_t)d.n_first,
+                                 cudaMemcpyDeviceToHost, d.stream));
+    if (e && d.n1)
+      SFEEC_CUDA(cudaMemcpyAsync(e, d.e.p, sizeof(double) * (size_t)d.n1,
+                                 cudaMemcpyDeviceToHost, d.stream));
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    if (time) *time = d.time;
+  });
+}
+
+int sfeec_dev_advance(sfeec_dev* h, int64_t nsteps) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(nsteps >= 0, "advance: nsteps must be >= 0");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.advance(nsteps);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_dev_advance_diag(sfeec_dev* h, int64_t nsteps, int64_t diag_every,
+                           double* energy_hist, double* gauss_hist) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(nsteps >= 0 && diag_every >= 1, "advance_diag: bad step counts");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    int64_t done = 0, slot = 0;
+    while (done < nsteps) {
+      int64_t k = std::min(diag_every, nsteps - done);
+      d.advance(k);
+      done += k;
+      if (k == diag_every) {
+        if (energy_hist) energy_hist[slot] = d.energy();
+        if (gauss_hist) gauss_hist[slot] = d.form == SFEEC_FORM_BE ? d.gauss_residual() : 0.0;
+        ++slot;
+      }
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  });
+}
+
+int sfeec_dev_flow_he(sfeec_dev* h, double dt) {
+  return guarded([&] {
+    require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.flow_he(dt);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_dev_flow_ha(sfeec_dev* h, double dt) {
+  return guarded([&] {
+    require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.flow_ha(dt);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_dev_energy(sfeec_dev* h, double* out) {
+  return guarded([&] {
+    require(h && out, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    *out = h->d.energy();
+  });
+}
+
+int sfeec_dev_gauss_residual(sfeec_dev* h, double* out) {
+  return guarded([&] {
+    require(h && out, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    *out = h->d.gauss_residual();
+  });
+}
+
+int sfeec_dev_cfl_number(sfeec_dev* h, double* out) {
+  return guarded([&] {
+    require(h && out, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    *out = h->d.cfl_number();
+  });
+}
+
+int sfeec_dev_q_sym(sfeec_dev* h, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx,
+                    double* val) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& q = h->d.q;
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    if (nnz) *nnz = q.nnz;
+    q.download_csr(row_ptr, col_idx, val, h->d.stream);
+  });
+}
+
+int sfeec_dev_set_stream(sfeec_dev* h, void* s) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    if (d.own_stream) cudaStreamDestroy(d.stream);
+    d.stream = (cudaStream_t)s;
+    d.own_stream = false;
+  });
+}
+
+int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e) {
+  return guarded([&] {
+    require(h, "null handle");
+    if (first) *first = h->d.first.p;
+    if (e) *e = h->d.e.p;
+  });
+}
+
+int64_t sfeec_dev_last_launches(sfeec_dev* h) { return h ? h->d.launches : -1; }
+
+// 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2)
+double sfeec_dev_step_bytes(sfeec_dev* h) {
+  if (!h) return 0;
+  auto& d = h->d;
+  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz + 10.0 * (double)d.c.nnz +
+         16.0 * (double)(d.n1 + d.n2);
+}
+
+}  // extern "C"

@@ -1,0 +1,300 @@
+// SpMV kernels for the leapfrog chain. All are HBM-bound sparse contractions
+// (~0.17 flop/byte): no tensor cores; the design goals are contiguous
+// (coalesced) streaming of the operator arrays, L1/L2 hits on the gathered
+// neighbour values, and enough loads in flight per SM.
+#include <algorithm>
+#include <cmath>
+
+#include "spmv_kernels.cuh"
+
+namespace sfeec_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int32_t kPad = 0x7fffffff;  // padding slot in the signed sliced layout
+
+// ---- strict: reference-order, no FMA ------------------------------------
+// sparse.cpp:98-103: acc += val*x in stored order; then the flow's axpy
+// (dynamics.cpp:50,53,66) as a separate multiply and add.
+template <bool ACC>
+__global__ void __launch_bounds__(kThreads)
+    k_csr_strict(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                 const double* __restrict__ v, const double* __restrict__ x,
+                 double* __restrict__ y, double alpha) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double acc = 0.0;
+  for (int64_t k = rp[r]; k < rp[r + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], x[ci[k]]));
+  if (ACC)
+    y[r] = __dadd_rn(y[r], __dmul_rn(alpha, acc));
+  else
+    y[r] = acc;
+}
+
+// ---- production CSR-vector: TPR lanes per row, shuffle reduction ---------
+template <int TPR, bool ACC>
+__global__ void __launch_bounds__(kThreads)
+    k_csr_vec(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+              const double* __restrict__ v, const double* __restrict__ x,
+              double* __restrict__ y, double alpha) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gt / TPR;
+  const int lane = threadIdx.x & (TPR - 1);
+  double acc = 0.0;
+  if (row < rows) {
+    const int64_t b = __ldg(rp + row), e = __ldg(rp + row + 1);
+#pragma unroll 4
+    for (int64_t k = b + lane; k < e; k += TPR) acc = fma(__ldg(v + k), __ldg(x + __ldg(ci + k)), acc);
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, TPR);
+  if (lane == 0 && row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
+}
+
+// ---- sliced ELL, one thread per row, 32-row slices, column-major ---------
+template <bool ACC>
+__global__ void __launch_bounds__(kThreads)
+    k_sell_signed(int64_t rows, int64_t n_slices, const int64_t* __restrict__ sp,
+                  const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
+                  double scale, const double* __restrict__ x, double* __restrict__ y,
+                  double alpha) {
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slice >= n_slices) return;
+  const int64_t base = __ldg(sp + slice) + lane;
+  const int w = __ldg(sw + slice);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int32_t p = __ldg(col + base + 32 * (int64_t)k);
+    if (p != kPad) {
+      const double xv = __ldg(x + (p < 0 ? ~p : p));
+      acc += p < 0 ? -xv : xv;
+    }
+  }
+  const int64_t row = slice * 32 + lane;
+  if (row < rows) {
+    const double r = scale * acc;
+    y[row] = ACC ? fma(alpha, r, y[row]) : r;
+  }
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(kThreads)
+    k_sell(int64_t rows, int64_t n_slices, const int64_t* __restrict__ sp,
+           const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
+           const double* __restrict__ val, const double* __restrict__ x,
+           double* __restrict__ y, double alpha) {
+  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slice >= n_slices) return;
+  const int64_t base = __ldg(sp + slice) + lane;
+  const int w = __ldg(sw + slice);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t o = base + 32 * (int64_t)k;
+    acc = fma(__ldg(val + o), __ldg(x + __ldg(col + o)), acc);
+  }
+  const int64_t row = slice * 32 + lane;
+  if (row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha,
+                       int64_t n, int strict) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = strict ? __dadd_rn(y[i], __dmul_rn(alpha, x[i])) : fma(alpha, x[i], y[i]);
+}
+
+__global__ void k_div_copy(double* __restrict__ x, const double* __restrict__ y, double nrm,
+                           int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = y[i] / nrm;  // dynamics.cpp:130
+}
+
+inline unsigned blocks_for(int64_t threads) {
+  return (unsigned)std::max<int64_t>(1, (threads + kThreads - 1) / kThreads);
+}
+
+}  // namespace
+
+void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
+  rows = h.rows;
+  cols = h.cols;
+  nnz = h.nnz();
+  rp.upload(h.row_ptr.data(), h.row_ptr.size(), s);
+  ci.upload(h.col_idx.data(), h.col_idx.size(), s);
+  val.upload(h.val.data(), h.val.size(), s);
+  double avg = rows ? (double)nnz / (double)rows : 0.0;
+  tpr = 1;
+  while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
+  layout = kCsr;
+  if (strict_only || rows == 0 || nnz == 0) return;
+
+  // sliced layouts: 32-row slices, width = longest row of the slice
+  n_slices = (rows + 31) / 32;
+  std::vector<int64_t> hsp((size_t)n_slices + 1, 0);
+  std::vector<int32_t> hsw((size_t)n_slices, 0);
+  for (int64_t sl = 0; sl < n_slices; ++sl) {
+    int64_t w = 0;
+    for (int64_t r = sl * 32; r < std::min(rows, sl * 32 + 32); ++r)
+      w = std::max(w, h.row_ptr[(size_t)r + 1] - h.row_ptr[(size_t)r]);
+    hsw[(size_t)sl] = (int32_t)w;
+    hsp[(size_t)sl + 1] = hsp[(size_t)sl] + 32 * w;
+  }
+  sell_entries = hsp[(size_t)n_slices];
+  const double mag = std::fabs(h.val[0]);
+  bool signed_ok = mag > 0;
+  for (double v : h.val)
+    if (std::fabs(v) != mag) {
+      signed_ok = false;
+      break;
+    }
+  const double pad_ratio = (double)sell_entries / (double)nnz;
+  if (signed_ok && pad_ratio <= 2.5) {
+    layout = kSigned;
+    scale = mag;
+  } else if (pad_ratio <= 1.15) {
+    layout = kSell;
+  } else {
+    return;
+  }
+  std::vector<int32_t> hc((size_t)sell_entries, layout == kSigned ? kPad : 0);
+  std::vector<double> hv;
+  if (layout == kSell) hv.assign((size_t)sell_entries, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t sl = 0; sl < n_slices; ++sl) {
+    for (int lane = 0; lane < 32; ++lane) {
+      int64_t r = sl * 32 + lane;
+      if (r >= rows) break;
+      int64_t b = h.row_ptr[(size_t)r], e = h.row_ptr[(size_t)r + 1];
+      for (int64_t k = b; k < e; ++k) {
+        size_t o = (size_t)(hsp[(size_t)sl] + 32 * (k - b) + lane);
+        int32_t c = h.col_idx[(size_t)k];
+        if (layout == kSigned) {
+          hc[o] = h.val[(size_t)k] < 0 ? ~c : c;
+        } else {
+          hc[o] = c;
+          hv[o] = h.val[(size_t)k];
+        }
+      }
+      // kSell padding keeps val 0 and points at the row's first column (a cached line)
+      if (layout == kSell && e > b)
+        for (int64_t k = e - b; k < hsw[(size_t)sl]; ++k)
+          hc[(size_t)(hsp[(size_t)sl] + 32 * k + lane)] = h.col_idx[(size_t)b];
+    }
+  }
+  slice_ptr.upload(hsp.data(), hsp.size(), s);
+  slice_w.upload(hsw.data(), hsw.size(), s);
+  sell_col.upload(hc.data(), hc.size(), s);
+  if (layout == kSell) sell_val.upload(hv.data(), hv.size(), s);
+  // the host vectors die at return: make the async copies complete first
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+}
+
+void DevOperator::download_csr(int64_t* row_ptr, int32_t* col_idx, double* v,
+                               cudaStream_t s) const {
+  if (row_ptr)
+    SFEEC_CUDA(cudaMemcpyAsync(row_ptr, rp.p, sizeof(int64_t) * (size_t)(rows + 1),
+                               cudaMemcpyDeviceToHost, s));
+  if (col_idx && nnz)
+    SFEEC_CUDA(cudaMemcpyAsync(col_idx, ci.p, sizeof(int32_t) * (size_t)nnz,
+                               cudaMemcpyDeviceToHost, s));
+  if (v && nnz)
+    SFEEC_CUDA(cudaMemcpyAsync(v, val.p, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToHost,
+                               s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+}
+
+void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s) {
+  if (a.rows == 0) return;
+  k_csr_strict<false><<<blocks_for(a.rows), kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p,
+                                                              x, y, 0.0);
+  SFEEC_LAUNCH_CHECK();
+}
+
+void launch_spmv_axpy_strict(const DevOperator& a, const double* x, double* y, double alpha,
+                             cudaStream_t s) {
+  if (a.rows == 0) return;
+  k_csr_strict<true><<<blocks_for(a.rows), kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p,
+                                                             x, y, alpha);
+  SFEEC_LAUNCH_CHECK();
+}
+
+template <bool ACC>
+static void launch_vec(const DevOperator& a, const double* x, double* y, double alpha,
+                       cudaStream_t s) {
+  unsigned g = blocks_for(a.rows * a.tpr);
+  switch (a.tpr) {
+#define SFEEC_TPR(T)                                                                   \
+  case T:                                                                              \
+    k_csr_vec<T, ACC><<<g, kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p, x, y, alpha); \
+    break;
+    SFEEC_TPR(1)
+    SFEEC_TPR(2)
+    SFEEC_TPR(4)
+    SFEEC_TPR(8)
+    SFEEC_TPR(16)
+    SFEEC_TPR(32)
+#undef SFEEC_TPR
+    default:
+      throw Error(SFEEC_ECUDA, "bad threads-per-row");
+  }
+}
+
+void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
+                 bool accumulate, cudaStream_t s) {
+  if (a.rows == 0) return;
+  if (a.nnz == 0) {
+    if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
+    return;
+  }
+  unsigned g = blocks_for(a.n_slices * 32);
+  switch (a.layout) {
+    case DevOperator::kSigned:
+      if (accumulate)
+        k_sell_signed<true><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p,
+                                                   a.slice_w.p, a.sell_col.p, a.scale, x, y,
+                                                   alpha);
+      else
+        k_sell_signed<false><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p,
+                                                    a.slice_w.p, a.sell_col.p, a.scale, x, y,
+                                                    alpha);
+      break;
+    case DevOperator::kSell:
+      if (accumulate)
+        k_sell<true><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p, a.slice_w.p,
+                                            a.sell_col.p, a.sell_val.p, x, y, alpha);
+      else
+        k_sell<false><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p, a.slice_w.p,
+                                             a.sell_col.p, a.sell_val.p, x, y, alpha);
+      break;
+    default:
+      if (accumulate)
+        launch_vec<true>(a, x, y, alpha, s);
+      else
+        launch_vec<false>(a, x, y, alpha, s);
+  }
+  SFEEC_LAUNCH_CHECK();
+}
+
+void launch_axpy(double* y, const double* x, double alpha, int64_t n, bool strict,
+                 cudaStream_t s) {
+  if (n == 0) return;
+  unsigned g = (unsigned)std::min<int64_t>(blocks_for(n), 148 * 16);
+  k_axpy<<<g, kThreads, 0, s>>>(y, x, alpha, n, strict ? 1 : 0);
+  SFEEC_LAUNCH_CHECK();
+}
+
+void launch_scale_copy(double* x, const double* y, double /*inv*/, double nrm, int64_t n,
+                       cudaStream_t s) {
+  if (n == 0) return;
+  unsigned g = (unsigned)std::min<int64_t>(blocks_for(n), 148 * 16);
+  k_div_copy<<<g, kThreads, 0, s>>>(x, y, nrm, n);
+  SFEEC_LAUNCH_CHECK();
+}
+
+}  // namespace sfeec_b200

@@ -1,0 +1,50 @@
+// Device sparse operators and the SpMV kernels of the leapfrog chain
+// (K-Q, K-Cb, K-M2, K-CTe in SURVEY.md 2.4).
+#pragma once
+#include "device_util.cuh"
+
+namespace sfeec_b200 {
+
+// Device copy of one operator. The CSR arrays are always kept (strict mode,
+// export); production mode may add a specialised layout:
+//   kSigned: every |value| equals one scalar (incidence matrices: +-1 for
+//            Whitney P1-, the tets' C); stored as sliced ELL, column-major in
+//            slices of 32 rows, one int32 per entry with the sign in the
+//            top bit (~col for negative) -> 4 B/entry instead of 12.
+//   kSell:   general values, sliced ELL (SELL-32) with per-slice width,
+//            fp64 value + int32 column, column-major inside a slice so a
+//            warp's loads are contiguous. Chosen when padding is small.
+struct DevOperator {
+  enum Layout { kCsr = 0, kSigned = 1, kSell = 2 };
+  int64_t rows = 0, cols = 0, nnz = 0;
+  DevBuf<int64_t> rp;
+  DevBuf<int32_t> ci;
+  DevBuf<double> val;
+  int tpr = 1;  // threads per row for the CSR-vector kernel
+  Layout layout = kCsr;
+  // sliced layouts
+  int64_t n_slices = 0, sell_entries = 0;
+  DevBuf<int64_t> slice_ptr;  // start entry of each slice (n_slices + 1)
+  DevBuf<int32_t> slice_w;    // width of each slice
+  DevBuf<int32_t> sell_col;   // packed (signed) column indices
+  DevBuf<double> sell_val;    // kSell only
+  double scale = 1.0;         // kSigned: |value|
+
+  void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
+  void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
+};
+
+void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s);
+void launch_spmv_axpy_strict(const DevOperator& a, const double* x, double* y, double alpha,
+                             cudaStream_t s);
+// accumulate ? y += alpha * A x : y = A x
+void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
+                 bool accumulate, cudaStream_t s);
+// y += alpha * x   (strict: y + (alpha*x) with separate rounding)
+void launch_axpy(double* y, const double* x, double alpha, int64_t n, bool strict,
+                 cudaStream_t s);
+// x = y / nrm
+void launch_scale_copy(double* x, const double* y, double inv, double nrm, int64_t n,
+                       cudaStream_t s);
+
+}  // namespace sfeec_b200

@@ -1,0 +1,586 @@
+// Structured lumped-mass SFEEC (the Yee special case, config 2) on one B200.
+//
+// With Q = I/dV and M2 = dV I (lumped_mass, reference yee.cpp:76-81) the
+// SplitScheme sub-flows become the FDTD stencils (yee.cpp:31-69):
+//   e-kick  e_a += f*dV * [ (b_a2 - b_a2(-a1))/d_a1 - (b_a1 - b_a1(-a2))/d_a2 ]
+//   b-kick  b_a += h/dV * [ (e_a1(+a2) - e_a1)/d_a2 - (e_a2(+a1) - e_a2)/d_a1 ]
+// (f = dt c^2; b is the SFEEC 2-form, B = dV b). Strang half-kicks of
+// consecutive steps are merged, so advance(n) = b-kick(dt/2), then n-1 fused
+// (e-kick, b-kick) sweeps, then an e-kick and a final b-kick(dt/2).
+//
+// Kernels:
+//   k_bkick / k_ekick   in-place, one thread per storage point (3 comps)
+//   k_fused_pec         one e-kick + b-kick per pass, 2.5-D sweep along z:
+//                       each CTA owns a TX x TY column tile and a z-chunk,
+//                       stages the B planes (with a 1-point halo) and the
+//                       freshly updated E planes in shared memory, so e and b
+//                       are each read once and written once per step:
+//                       2*w*(N1+N2) HBM bytes. Ping-pong
+//                       buffers make tiles and chunks independent (halo
+//                       points are recomputed, never exchanged).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "device_util.cuh"
+#include "yee_layout.hpp"
+
+namespace sfeec_b200 {
+
+template <class T>
+struct Fields {
+  T* c[6];  // ex ey ez bx by bz
+};
+
+template <class T>
+struct YeeCoef {
+  T ce[3];  // e-kick: f*m2/d_x, /d_y, /d_z
+  T cb[3];  // b-kick: h*q/d_x, /d_y, /d_z
+};
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// DOF masks in storage coordinates (PEC), yee_layout.hpp
+__device__ __forceinline__ bool e_dof(const YeeGeom& g, int a, int i, int j, int k) {
+  if (g.bc == 0) return true;
+  const int c[3] = {i, j, k};
+  for (int d = 0; d < 3; ++d) {
+    if (d == a) {
+      if (c[d] < 0 || c[d] >= g.n[d]) return false;
+    } else if (c[d] < 1 || c[d] > g.n[d] - 1) {
+      return false;
+    }
+  }
+  return true;
+}
+__device__ __forceinline__ bool b_dof(const YeeGeom& g, int a, int i, int j, int k) {
+  const int c[3] = {i, j, k};
+  for (int d = 0; d < 3; ++d) {
+    int hi = (g.bc == 0 || d != a) ? g.n[d] - 1 : g.n[d];
+    if (c[d] < 0 || c[d] > hi) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ int wrapm(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }
+
+// ---- unfused, in place ----------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_bkick(YeeGeom g, Fields<T> f, YeeCoef<T> k) {
+  const int64_t np = g.npts();
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < np;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(s % g.S[0]);
+    const int j = (int)((s / g.S[0]) % g.S[1]);
+    const int kk = (int)(s / ((int64_t)g.S[0] * g.S[1]));
+    int ip = i + 1, jp = j + 1, kp = kk + 1;
+    if (g.bc == 0) {
+      ip = wrapm(ip, g.n[0]);
+      jp = wrapm(jp, g.n[1]);
+      kp = wrapm(kp, g.n[2]);
+    }
+    const T* ex = f.c[0];
+    const T* ey = f.c[1];
+    const T* ez = f.c[2];
+    if (b_dof(g, 0, i, j, kk)) {
+      const T ey0 = ey[s], ez0 = ez[s];
+      f.c[3][s] += k.cb[2] * (ey[g.sidx(i, j, kp)] - ey0) - k.cb[1] * (ez[g.sidx(i, jp, kk)] - ez0);
+    }
+    if (b_dof(g, 1, i, j, kk)) {
+      const T ez0 = ez[s], ex0 = ex[s];
+      f.c[4][s] += k.cb[0] * (ez[g.sidx(ip, j, kk)] - ez0) - k.cb[2] * (ex[g.sidx(i, j, kp)] - ex0);
+    }
+    if (b_dof(g, 2, i, j, kk)) {
+      const T ex0 = ex[s], ey0 = ey[s];
+      f.c[5][s] += k.cb[1] * (ex[g.sidx(i, jp, kk)] - ex0) - k.cb[0] * (ey[g.sidx(ip, j, kk)] - ey0);
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_ekick(YeeGeom g, Fields<T> f, YeeCoef<T> k) {
+  const int64_t np = g.npts();
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < np;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(s % g.S[0]);
+    const int j = (int)((s / g.S[0]) % g.S[1]);
+    const int kk = (int)(s / ((int64_t)g.S[0] * g.S[1]));
+    int im = i - 1, jm = j - 1, km = kk - 1;
+    if (g.bc == 0) {
+      im = wrapm(im, g.n[0]);
+      jm = wrapm(jm, g.n[1]);
+      km = wrapm(km, g.n[2]);
+    }
+    const T* bx = f.c[3];
+    const T* by = f.c[4];
+    const T* bz = f.c[5];
+    if (e_dof(g, 0, i, j, kk)) {
+      const T bz0 = bz[s], by0 = by[s];
+      f.c[0][s] += k.ce[1] * (bz0 - bz[g.sidx(i, jm, kk)]) - k.ce[2] * (by0 - by[g.sidx(i, j, km)]);
+    }
+    if (e_dof(g, 1, i, j, kk)) {
+      const T bx0 = bx[s], bz0 = bz[s];
+      f.c[1][s] += k.ce[2] * (bx0 - bx[g.sidx(i, j, km)]) - k.ce[0] * (bz0 - bz[g.sidx(im, j, kk)]);
+    }
+    if (e_dof(g, 2, i, j, kk)) {
+      const T by0 = by[s], bx0 = bx[s];
+      f.c[2][s] += k.ce[0] * (by0 - by[g.sidx(im, j, kk)]) - k.ce[1] * (bx0 - bx[g.sidx(i, jm, kk)]);
+    }
+  }
+}
+
+// ---- fused e-kick + b-kick sweep (PEC) -------------------------------------
+template <class T, int TX, int TY>
+__global__ void __launch_bounds__(TX* TY)
+    k_fused_pec(YeeGeom g, Fields<T> in, Fields<T> out, YeeCoef<T> ck, int kchunk) {
+  constexpr int BX = TX + 2, BY = TY + 2;  // B tile incl. 1-point halo on both sides
+  constexpr int EX = TX + 1, EY = TY + 1;  // E tile incl. 1-point halo on + side
+  __shared__ T sB[2][3][BY][BX];
+  __shared__ T sE[2][3][EY][EX];
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int Z = g.S[2];
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, Z);
+  if (k0 >= Z) return;
+
+  auto load_b = [&](int buf, int kp) {
+    for (int p = tid; p < BX * BY; p += TX * TY) {
+      const int ei = p % BX, ej = p / BX;
+      const int i = i0 - 1 + ei, j = j0 - 1 + ej;
+      const bool in_range = kp >= 0 && kp < Z && i >= 0 && i < g.S[0] && j >= 0 && j < g.S[1];
+      const int64_t s = in_range ? g.sidx(i, j, kp) : 0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sB[buf][c][ej][ei] = in_range ? in.c[3 + c][s] : T(0);
+    }
+  };
+
+  int cur = 0;
+  load_b(1, k0 - 1);  // B_old(k0-1) -> prev
+  for (int kk = k0; kk <= k1; ++kk) {
+    const int prev = cur ^ 1;
+    load_b(cur, kk);
+    __syncthreads();
+    // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
+    for (int p = tid; p < EX * EY; p += TX * TY) {
+      const int li = p % EX, lj = p / EX;
+      const int i = i0 + li, j = j0 + lj;
+      const int bi = li + 1, bj = lj + 1;
+      const bool in_range = kk < Z && i < g.S[0] && j < g.S[1];
+      const int64_t s = in_range ? g.sidx(i, j, kk) : 0;
+      T e[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) e[c] = in_range ? in.c[c][s] : T(0);
+      if (in_range) {
+        if (e_dof(g, 0, i, j, kk))
+          e[0] += ck.ce[1] * (sB[cur][2][bj][bi] - sB[cur][2][bj - 1][bi]) -
+                  ck.ce[2] * (sB[cur][1][bj][bi] - sB[prev][1][bj][bi]);
+        if (e_dof(g, 1, i, j, kk))
+          e[1] += ck.ce[2] * (sB[cur][0][bj][bi] - sB[prev][0][bj][bi]) -
+                  ck.ce[0] * (sB[cur][2][bj][bi] - sB[cur][2][bj][bi - 1]);
+        if (e_dof(g, 2, i, j, kk))
+          e[2] += ck.ce[0] * (sB[cur][1][bj][bi] - sB[cur][1][bj][bi - 1]) -
+                  ck.ce[1] * (sB[cur][0][bj][bi] - sB[cur][0][bj - 1][bi]);
+        if (li < TX && lj < TY && kk < k1) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (e_dof(g, c, i, j, kk)) out.c[c][s] = e[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sE[cur][c][lj][li] = e[c];
+    }
+    __syncthreads();
+    // B_new(kk-1) on the own tile
+    if (kk > k0) {
+      const int li = tid % TX, lj = tid / TX;
+      const int i = i0 + li, j = j0 + lj, kb = kk - 1;
+      if (i < g.S[0] && j < g.S[1]) {
+        const int64_t s = g.sidx(i, j, kb);
+        const int bi = li + 1, bj = lj + 1;
+        if (b_dof(g, 0, i, j, kb))
+          out.c[3][s] = sB[prev][0][bj][bi] +
+                        (ck.cb[2] * (sE[cur][1][lj][li] - sE[prev][1][lj][li]) -
+                         ck.cb[1] * (sE[prev][2][lj + 1][li] - sE[prev][2][lj][li]));
+        if (b_dof(g, 1, i, j, kb))
+          out.c[4][s] = sB[prev][1][bj][bi] +
+                        (ck.cb[0] * (sE[prev][2][lj][li + 1] - sE[prev][2][lj][li]) -
+                         ck.cb[2] * (sE[cur][0][lj][li] - sE[prev][0][lj][li]));
+        if (b_dof(g, 2, i, j, kb))
+          out.c[5][s] = sB[prev][2][bj][bi] +
+                        (ck.cb[1] * (sE[prev][0][lj + 1][li] - sE[prev][0][lj][li]) -
+                         ck.cb[0] * (sE[prev][1][lj][li + 1] - sE[prev][1][lj][li]));
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+}
+
+// state pack/unpack between the SFEEC numbering (fp64) and storage (T)
+template <class T>
+__global__ void k_scatter(YeeGeom g, bool face, const double* __restrict__ src, int64_t n,
+                          Fields<T> f) {
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    int a;
+    int64_t s;
+    g.dof_to_storage(face, id, a, s);
+    f.c[(face ? 3 : 0) + a][s] = (T)src[id];
+  }
+}
+
+template <class T>
+__global__ void k_gather(YeeGeom g, bool face, double* __restrict__ dst, int64_t n,
+                         Fields<T> f) {
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    int a;
+    int64_t s;
+    g.dof_to_storage(face, id, a, s);
+    dst[id] = (double)f.c[(face ? 3 : 0) + a][s];
+  }
+}
+
+}  // namespace
+
+struct YeeDev {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  YeeGeom g;
+  double d[3] = {1, 1, 1};
+  double dt = 0, eps0 = 1, mu0 = 1, dv = 1;
+  int prec = 8;
+  int variant = 1;
+  DevBuf<char> buf[2];
+  int cur = 0;
+  DevBuf<double> stage, partials;
+  double time = 0;
+  int64_t launches = 0;
+  int64_t n_edges = 0, n_faces = 0;
+  // dominant-kernel timing (CUDA events on the launch stream)
+  bool timing = false;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double kernel_ms = 0;
+  int64_t kernel_launches = 0;
+
+  ~YeeDev() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  template <class T>
+  Fields<T> fields(int which) const {
+    Fields<T> f;
+    const int64_t np = g.npts();
+    for (int c = 0; c < 6; ++c) f.c[c] = reinterpret_cast<T*>(buf[which].p) + c * np;
+    return f;
+  }
+  template <class T>
+  YeeCoef<T> coef(double e_factor, double h) const {
+    YeeCoef<T> k;
+    const double m2 = dv, q = 1.0 / dv;
+    for (int a = 0; a < 3; ++a) {
+      k.ce[a] = (T)(e_factor * m2 / d[a]);
+      k.cb[a] = (T)(h * q / d[a]);
+    }
+    return k;
+  }
+  unsigned pt_blocks() const {
+    return (unsigned)std::min<int64_t>((g.npts() + kThreads - 1) / kThreads, 148 * 64);
+  }
+
+  template <class T>
+  void bkick(double h) {
+    k_bkick<T><<<pt_blocks(), kThreads, 0, stream>>>(g, fields<T>(cur), coef<T>(0, h));
+    SFEEC_LAUNCH_CHECK();
+    ++launches;
+  }
+  template <class T>
+  void ekick(double h) {
+    k_ekick<T><<<pt_blocks(), kThreads, 0, stream>>>(g, fields<T>(cur), coef<T>(h / (eps0 * mu0), 0));
+    SFEEC_LAUNCH_CHECK();
+    ++launches;
+  }
+  template <class T>
+  void fused(double h_e, double h_b) {
+    constexpr int TX = 32, TY = 8;
+    const int kchunk = 32;
+    dim3 grid((g.S[0] + TX - 1) / TX, (g.S[1] + TY - 1) / TY, (g.S[2] + kchunk - 1) / kchunk);
+    k_fused_pec<T, TX, TY><<<grid, TX * TY, 0, stream>>>(
+        g, fields<T>(cur), fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kchunk);
+    SFEEC_LAUNCH_CHECK();
+    cur ^= 1;
+    ++launches;
+  }
+
+  template <class T>
+  void advance_t(int64_t n) {
+    bkick<T>(0.5 * dt);
+    const bool use_fused = variant == 1 && g.bc == SFEEC_BC_PEC;
+    const bool t = timing && n > 1;
+    if (t) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
+    for (int64_t s = 0; s + 1 < n; ++s) {
+      if (use_fused) {
+        fused<T>(dt, dt);
+      } else {
+        ekick<T>(dt);
+        bkick<T>(dt);
+      }
+    }
+    if (t) {
+      SFEEC_CUDA(cudaEventRecord(ev[1], stream));
+      SFEEC_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0;
+      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      kernel_ms += ms;
+      kernel_launches += (n - 1) * (use_fused ? 1 : 2);
+    }
+    ekick<T>(dt);
+    bkick<T>(0.5 * dt);
+  }
+
+  void advance(int64_t n) {
+    launches = 0;
+    if (n <= 0) return;
+    if (prec == 8)
+      advance_t<double>(n);
+    else
+      advance_t<float>(n);
+    for (int64_t s = 0; s < n; ++s) time = time + dt;
+  }
+
+  void flow_he(double h) {
+    launches = 0;
+    if (prec == 8)
+      bkick<double>(h);
+    else
+      bkick<float>(h);
+  }
+  void flow_ha(double h) {
+    launches = 0;
+    if (prec == 8)
+      ekick<double>(h);
+    else
+      ekick<float>(h);
+  }
+
+  // 0.5 (eps0 e^T Q e + b^T M2 b / mu0), dynamics.cpp:92-102 with lumped Q, M2
+  double energy() {
+    const int64_t np = g.npts();
+    double se = 0, sb = 0;
+    for (int c = 0; c < 3; ++c) {
+      if (prec == 8) {
+        Fields<double> f = fields<double>(cur);
+        se += device_dot(f.c[c], f.c[c], np, partials.p, stream);
+        sb += device_dot(f.c[3 + c], f.c[3 + c], np, partials.p, stream);
+      } else {
+        Fields<float> f = fields<float>(cur);
+        se += device_sumsq(f.c[c], np, partials.p, stream);
+        sb += device_sumsq(f.c[3 + c], np, partials.p, stream);
+      }
+    }
+    return 0.5 * (eps0 * (se / dv) + (sb * dv) / mu0);
+  }
+
+  void set_state(const double* b, const double* e) {
+    buf[0].zero(stream);
+    buf[1].zero(stream);
+    cur = 0;
+    for (int face = 0; face < 2; ++face) {
+      const int64_t n = face ? n_faces : n_edges;
+      if (!n) continue;
+      SFEEC_CUDA(cudaMemcpyAsync(stage.p, face ? b : e, sizeof(double) * (size_t)n,
+                                 cudaMemcpyHostToDevice, stream));
+      unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+      if (prec == 8)
+        k_scatter<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(cur));
+      else
+        k_scatter<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(cur));
+      SFEEC_LAUNCH_CHECK();
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  void get_state(double* b, double* e) {
+    for (int face = 0; face < 2; ++face) {
+      double* dst = face ? b : e;
+      const int64_t n = face ? n_faces : n_edges;
+      if (!dst || !n) continue;
+      unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+      if (prec == 8)
+        k_gather<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(cur));
+      else
+        k_gather<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(cur));
+      SFEEC_LAUNCH_CHECK();
+      SFEEC_CUDA(cudaMemcpyAsync(dst, stage.p, sizeof(double) * (size_t)n,
+                                 cudaMemcpyDeviceToHost, stream));
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+  }
+};
+
+}  // namespace sfeec_b200
+
+using namespace sfeec_b200;
+
+struct sfeec_yee {
+  YeeDev d;
+};
+
+extern "C" {
+
+int sfeec_yee_create(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                     double eps0, double mu0, int bc, int precision, int device,
+                     sfeec_yee** out) {
+  return guarded([&] {
+    require(out != nullptr, "sfeec_yee_create: null out");
+    *out = nullptr;
+    require(nx >= 1 && ny >= 1 && nz >= 1, "cubical lattice: cell counts must be >= 1");
+    require(dx > 0 && dy > 0 && dz > 0, "cubical lattice: spacings must be > 0");
+    require(dt >= 0, "SplitScheme: dt must be >= 0");
+    require(bc == SFEEC_BC_PERIODIC || bc == SFEEC_BC_PEC, "unknown boundary condition");
+    require(precision == 8 || precision == 4, "precision must be 8 (fp64) or 4 (fp32)");
+    require(bc == SFEEC_BC_PEC || (nx >= 2 && ny >= 2 && nz >= 2),
+            "periodic Yee kernels need >= 2 cells per axis");
+    select_device(device);
+    auto h = std::make_unique<sfeec_yee>();
+    YeeDev& d = h->d;
+    d.device = device;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    d.own_stream = true;
+    d.g = make_yee_geom(nx, ny, nz, bc);
+    d.d[0] = dx;
+    d.d[1] = dy;
+    d.d[2] = dz;
+    d.dv = dx * dy * dz;
+    d.dt = dt;
+    d.eps0 = eps0;
+    d.mu0 = mu0;
+    d.prec = precision;
+    d.n_edges = d.g.edge_off[3];
+    d.n_faces = d.g.face_off[3];
+    const size_t bytes = (size_t)d.g.npts() * 6 * (size_t)precision;
+    d.buf[0].alloc(bytes);
+    d.buf[1].alloc(bytes);
+    d.buf[0].zero(d.stream);
+    d.buf[1].zero(d.stream);
+    d.stage.alloc((size_t)std::max(d.n_edges, d.n_faces));
+    d.partials.alloc(kReduceBlocks + 1);
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    *out = h.release();
+  });
+}
+
+void sfeec_yee_destroy(sfeec_yee* h) { delete h; }
+
+int sfeec_yee_dof_counts(const sfeec_yee* h, int64_t* n_edges, int64_t* n_faces) {
+  return guarded([&] {
+    require(h, "null handle");
+    if (n_edges) *n_edges = h->d.n_edges;
+    if (n_faces) *n_faces = h->d.n_faces;
+  });
+}
+
+int sfeec_yee_set_state(sfeec_yee* h, const double* b, const double* e, double time) {
+  return guarded([&] {
+    require(h && b && e, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.set_state(b, e);
+    h->d.time = time;
+  });
+}
+
+int sfeec_yee_get_state(sfeec_yee* h, double* b, double* e, double* time) {
+  return guarded([&] {
+    require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.get_state(b, e);
+    if (time) *time = h->d.time;
+  });
+}
+
+int sfeec_yee_advance(sfeec_yee* h, int64_t nsteps) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(nsteps >= 0, "advance: nsteps must be >= 0");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.advance(nsteps);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_yee_flow_he(sfeec_yee* h, double dt) {
+  return guarded([&] {
+    require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.flow_he(dt);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_yee_flow_ha(sfeec_yee* h, double dt) {
+  return guarded([&] {
+    require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.flow_ha(dt);
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_yee_energy(sfeec_yee* h, double* out) {
+  return guarded([&] {
+    require(h && out, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    *out = h->d.energy();
+  });
+}
+
+int sfeec_yee_set_stream(sfeec_yee* h, void* s) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    if (d.own_stream) cudaStreamDestroy(d.stream);
+    d.stream = (cudaStream_t)s;
+    d.own_stream = false;
+  });
+}
+
+int sfeec_yee_set_variant(sfeec_yee* h, int variant) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(variant == 0 || variant == 1, "variant must be 0 or 1");
+    h->d.variant = variant;
+  });
+}
+
+int64_t sfeec_yee_last_launches(sfeec_yee* h) { return h ? h->d.launches : -1; }
+
+int sfeec_yee_kernel_timing(sfeec_yee* h, int enable, double* ms_total, int64_t* launches) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    if (ms_total) *ms_total = d.kernel_ms;
+    if (launches) *launches = d.kernel_launches;
+    d.kernel_ms = 0;
+    d.kernel_launches = 0;
+    d.timing = enable != 0;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    for (auto& e : d.ev)
+      if (!e) SFEEC_CUDA(cudaEventCreate(&e));
+  });
+}
+
+// 2 * w * (N1 + N2)
+double sfeec_yee_step_bytes(sfeec_yee* h) {
+  if (!h) return 0;
+  return 2.0 * h->d.prec * (double)(h->d.n_edges + h->d.n_faces);
+}
+
+}  // extern "C"

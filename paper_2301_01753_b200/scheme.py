@@ -1,0 +1,363 @@
+"""Host-side mirror of the reference's operator/step interface.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/sfeec/{sparse,dynamics,yee}.hpp so the parity
+tests read like the reference's own tests:
+
+  SparseOperator          sparse.hpp:14-33 (CSR, sorted columns, no zeros)
+  operator_from_triplets  sparse.cpp:20-61
+  scaled_identity         sparse.cpp:63-73
+  transpose               sparse.cpp:75-94
+  UnitSystem, FieldState, make_state    dynamics.hpp:9-25, dynamics.cpp:135-143
+  SplitScheme             dynamics.hpp:31-67 -- every compute call runs on the
+                          B200 through the C ABI (include/sfeec_b200.h)
+  YeeScheme               the lumped-mass (Yee) special case, yee.hpp:12-37
+
+The step itself never runs on the CPU here: there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import InvalidParameter, DeviceError  # noqa: F401  (re-export)
+
+
+class Formulation(enum.IntEnum):
+    AE = L.FORM_AE
+    BE = L.FORM_BE
+
+
+class SplitKind(enum.IntEnum):
+    LieTrotter = L.SPLIT_LIE_TROTTER
+    Strang = L.SPLIT_STRANG
+
+
+@dataclass
+class UnitSystem:
+    eps0: float = 1.0
+    mu0: float = 1.0
+
+    def c2(self) -> float:
+        return 1.0 / (self.eps0 * self.mu0)
+
+
+@dataclass
+class SparseOperator:
+    """CSR operator, int64 row pointers, int32 columns, fp64 values."""
+
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    val: np.ndarray
+    symmetric: bool = False
+
+    def __post_init__(self):
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int32)
+        self.val = np.ascontiguousarray(self.val, dtype=np.float64)
+
+    def nnz(self) -> int:
+        return int(self.col_idx.size)
+
+    def row_cols(self, r: int) -> np.ndarray:
+        return self.col_idx[self.row_ptr[r]:self.row_ptr[r + 1]]
+
+    def row_vals(self, r: int) -> np.ndarray:
+        return self.val[self.row_ptr[r]:self.row_ptr[r + 1]]
+
+    def at(self, r: int, c: int) -> float:
+        cs = self.row_cols(r)
+        k = np.searchsorted(cs, c)
+        if k < cs.size and cs[k] == c:
+            return float(self.row_vals(r)[k])
+        return 0.0
+
+    def to_dense(self) -> np.ndarray:
+        d = np.zeros((self.rows, self.cols))
+        rows = np.repeat(np.arange(self.rows), np.diff(self.row_ptr))
+        d[rows, self.col_idx] = self.val
+        return d
+
+    def view(self) -> L.sfeec_csr:
+        v = L.sfeec_csr()
+        v.rows, v.cols = self.rows, self.cols
+        v.row_ptr = L.i64ptr(self.row_ptr)
+        v.col_idx = L.i32ptr(self.col_idx)
+        v.val = L.dptr(self.val)
+        return v
+
+    @staticmethod
+    def _from_owned(m: L.sfeec_csr_owned, symmetric=False) -> "SparseOperator":
+        rows, cols, rp, ci, va = L.owned_to_numpy(m)
+        return SparseOperator(rows, cols, rp, ci, va, symmetric)
+
+
+def operator_from_triplets(rows, cols, r, c, v, symmetric=False) -> SparseOperator:
+    """sparse.cpp:20-61 (deterministic, duplicates summed in input order)."""
+    r = np.ascontiguousarray(r, dtype=np.int32)
+    c = np.ascontiguousarray(c, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = L.sfeec_csr_owned()
+    L.check(L.lib().sfeec_csr_from_triplets(rows, cols, r.size, L.i32ptr(r), L.i32ptr(c),
+                                            L.dptr(v), C.byref(out)))
+    return SparseOperator._from_owned(out, symmetric)
+
+
+def scaled_identity(n: int, s: float) -> SparseOperator:
+    """sparse.cpp:63-73."""
+    return SparseOperator(n, n, np.arange(n + 1), np.arange(n), np.full(n, float(s)), True)
+
+
+def transpose(a: SparseOperator) -> SparseOperator:
+    out = L.sfeec_csr_owned()
+    v = a.view()
+    L.check(L.lib().sfeec_csr_transpose(C.byref(v), C.byref(out)))
+    return SparseOperator._from_owned(out, a.symmetric)
+
+
+def symmetric_part(q: SparseOperator) -> SparseOperator:
+    """dynamics.cpp:10-25."""
+    out = L.sfeec_csr_owned()
+    v = q.view()
+    L.check(L.lib().sfeec_csr_symmetric_part(C.byref(v), C.byref(out)))
+    return SparseOperator._from_owned(out, True)
+
+
+@dataclass
+class FieldState:
+    formulation: Formulation = Formulation.AE
+    first: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    e: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    time: float = 0.0
+
+    def copy(self) -> "FieldState":
+        return FieldState(self.formulation, self.first.copy(), self.e.copy(), self.time)
+
+
+def make_state(f: Formulation, first, e, time: float = 0.0) -> FieldState:
+    return FieldState(Formulation(f), np.array(first, dtype=np.float64),
+                      np.array(e, dtype=np.float64), float(time))
+
+
+class SplitScheme:
+    """dynamics.hpp:31-67 on a B200: operators and state live in HBM.
+
+    The formulation is fixed at construction (the device keeps one resident
+    state layout); states of the other formulation raise InvalidParameter.
+    `strict=True` selects the bitwise-reference kernels (SFEEC_STRICT).
+    """
+
+    def __init__(self, kind: SplitKind, dt: float, q: SparseOperator, c: SparseOperator,
+                 m2: SparseOperator, units: UnitSystem | None = None,
+                 div: SparseOperator | None = None, warn_cfl: bool = True, *,
+                 formulation: Formulation = Formulation.BE, strict: bool = False,
+                 q_is_symmetric: bool = False, device: int = 0):
+        units = units or UnitSystem()
+        self._kind, self._dt, self._units = SplitKind(kind), float(dt), units
+        self._formulation = Formulation(formulation)
+        self._c, self._m2 = c, m2
+        flags = (L.STRICT if strict else 0) | (0 if warn_cfl else L.NO_CFL_WARN)
+        flags |= L.Q_IS_SYMMETRIC if q_is_symmetric else 0
+        h = C.c_void_p()
+        qv, cv, mv = q.view(), c.view(), m2.view()
+        dv = div.view() if div is not None else None
+        L.check(L.lib().sfeec_dev_create(
+            C.byref(qv), C.byref(cv), C.byref(mv), C.byref(dv) if dv is not None else None,
+            self._dt, units.eps0, units.mu0, int(self._kind), int(self._formulation), device,
+            flags, C.byref(h)))
+        self._h = h
+        self._n1, self._n2 = c.cols, c.rows
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().sfeec_dev_destroy(h)
+            self._h = None
+
+    # accessors (dynamics.hpp:38-45)
+    def kind(self):
+        return self._kind
+
+    def dt(self):
+        return self._dt
+
+    def units(self):
+        return self._units
+
+    def q_sym(self) -> SparseOperator:
+        nnz = C.c_int64()
+        L.check(L.lib().sfeec_dev_q_sym(self._h, C.byref(nnz), None, None, None))
+        rp = np.zeros(self._n1 + 1, np.int64)
+        ci = np.zeros(nnz.value, np.int32)
+        va = np.zeros(nnz.value)
+        L.check(L.lib().sfeec_dev_q_sym(self._h, None, L.i64ptr(rp), L.i32ptr(ci), L.dptr(va)))
+        return SparseOperator(self._n1, self._n1, rp, ci, va, True)
+
+    def curl(self):
+        return self._c
+
+    def m2(self):
+        return self._m2
+
+    # state transfer
+    def _check_state(self, s: FieldState):
+        if s.formulation != self._formulation:
+            raise InvalidParameter("SplitScheme: state formulation differs from the device's")
+        nf = self._n2 if self._formulation == Formulation.BE else self._n1
+        if s.first.size != nf or s.e.size != self._n1:
+            raise InvalidParameter("spmv: dimension mismatch")
+
+    def load(self, s: FieldState) -> None:
+        self._check_state(s)
+        first = np.ascontiguousarray(s.first, dtype=np.float64)
+        e = np.ascontiguousarray(s.e, dtype=np.float64)
+        L.check(L.lib().sfeec_dev_set_state(self._h, L.dptr(first), first.size, L.dptr(e),
+                                            e.size, s.time))
+
+    def fetch(self) -> FieldState:
+        nf = self._n2 if self._formulation == Formulation.BE else self._n1
+        first, e, t = np.zeros(nf), np.zeros(self._n1), C.c_double()
+        L.check(L.lib().sfeec_dev_get_state(self._h, L.dptr(first), L.dptr(e), C.byref(t)))
+        return FieldState(self._formulation, first, e, t.value)
+
+    # exact sub-flows, dynamics.cpp:47-67 (in place, clock untouched)
+    def flow_he(self, s: FieldState, dt: float) -> None:
+        self.load(s)
+        L.check(L.lib().sfeec_dev_flow_he(self._h, float(dt)))
+        out = self.fetch()
+        s.first[:], s.e[:] = out.first, out.e
+
+    def flow_ha(self, s: FieldState, dt: float) -> None:
+        self.load(s)
+        L.check(L.lib().sfeec_dev_flow_ha(self._h, float(dt)))
+        out = self.fetch()
+        s.first[:], s.e[:] = out.first, out.e
+
+    def step(self, s: FieldState) -> FieldState:
+        """dynamics.cpp:69-90: returns a new state one step later."""
+        return self.advance(s, 1)
+
+    def advance(self, s: FieldState, nsteps: int) -> FieldState:
+        """nsteps x step with the state resident on the device."""
+        self.load(s)
+        L.check(L.lib().sfeec_dev_advance(self._h, int(nsteps)))
+        return self.fetch()
+
+    def advance_diag(self, s: FieldState, nsteps: int, diag_every: int = 1):
+        """advance + energy and Gauss residual after every diag_every steps."""
+        self.load(s)
+        n = nsteps // diag_every
+        en, ga = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        L.check(L.lib().sfeec_dev_advance_diag(self._h, int(nsteps), int(diag_every),
+                                               L.dptr(en), L.dptr(ga)))
+        return self.fetch(), en[:n], ga[:n]
+
+    def energy(self, s: FieldState) -> float:
+        self.load(s)
+        out = C.c_double()
+        L.check(L.lib().sfeec_dev_energy(self._h, C.byref(out)))
+        return out.value
+
+    def gauss_residual(self, s: FieldState) -> float:
+        if s.formulation != Formulation.BE:
+            raise InvalidParameter("gauss_residual: (b, e) formulation required")
+        self.load(s)
+        out = C.c_double()
+        L.check(L.lib().sfeec_dev_gauss_residual(self._h, C.byref(out)))
+        return out.value
+
+    def cfl_number(self) -> float:
+        out = C.c_double()
+        L.check(L.lib().sfeec_dev_cfl_number(self._h, C.byref(out)))
+        return out.value
+
+    # device-resident handles for benchmarks
+    @property
+    def handle(self):
+        return self._h
+
+    def step_bytes(self) -> float:
+        return L.lib().sfeec_dev_step_bytes(self._h)
+
+
+class YeeScheme:
+    """Lumped-mass SFEEC on an nx x ny x nz lattice (Q = I/dV, M2 = dV I).
+
+    State is the (b, e) pair in the sfeec_yee numbering (yee_layout.hpp):
+    periodic = the reference's axis-major ids; PEC = interior edges + all
+    faces. precision 8 or 4 (fp64 / fp32 fields on the device).
+    """
+
+    def __init__(self, nx, ny, nz, dx, dy, dz, dt, units: UnitSystem | None = None,
+                 bc: int = L.BC_PEC, precision: int = 8, device: int = 0):
+        units = units or UnitSystem()
+        h = C.c_void_p()
+        L.check(L.lib().sfeec_yee_create(nx, ny, nz, dx, dy, dz, dt, units.eps0, units.mu0, bc,
+                                         precision, device, C.byref(h)))
+        self._h = h
+        ne, nf = C.c_int64(), C.c_int64()
+        L.check(L.lib().sfeec_yee_dof_counts(h, C.byref(ne), C.byref(nf)))
+        self.n_edges, self.n_faces = ne.value, nf.value
+        self.dt = dt
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().sfeec_yee_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_variant(self, v: int) -> None:
+        L.check(L.lib().sfeec_yee_set_variant(self._h, v))
+
+    def load(self, b, e, time=0.0):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        if b.size != self.n_faces or e.size != self.n_edges:
+            raise InvalidParameter("spmv: dimension mismatch")
+        L.check(L.lib().sfeec_yee_set_state(self._h, L.dptr(b), L.dptr(e), float(time)))
+
+    def fetch(self):
+        b, e, t = np.zeros(self.n_faces), np.zeros(self.n_edges), C.c_double()
+        L.check(L.lib().sfeec_yee_get_state(self._h, L.dptr(b), L.dptr(e), C.byref(t)))
+        return b, e, t.value
+
+    def advance(self, nsteps: int) -> None:
+        L.check(L.lib().sfeec_yee_advance(self._h, int(nsteps)))
+
+    def flow_he(self, dt: float) -> None:
+        L.check(L.lib().sfeec_yee_flow_he(self._h, float(dt)))
+
+    def flow_ha(self, dt: float) -> None:
+        L.check(L.lib().sfeec_yee_flow_ha(self._h, float(dt)))
+
+    def energy(self) -> float:
+        out = C.c_double()
+        L.check(L.lib().sfeec_yee_energy(self._h, C.byref(out)))
+        return out.value
+
+    def step_bytes(self) -> float:
+        return L.lib().sfeec_yee_step_bytes(self._h)
+
+    def last_launches(self) -> int:
+        return int(L.lib().sfeec_yee_last_launches(self._h))
+
+
+def yee_operators(nx, ny, nz, dx, dy, dz, bc=L.BC_PEC):
+    """(C, D) of the lumped Yee system in the sfeec_yee numbering (host builder)."""
+    c, d = L.sfeec_csr_owned(), L.sfeec_csr_owned()
+    L.check(L.lib().sfeec_build_yee_curl(nx, ny, nz, dx, dy, dz, bc, C.byref(c), C.byref(d)))
+    return SparseOperator._from_owned(c), SparseOperator._from_owned(d)
+
+
+def device_count() -> int:
+    return int(L.lib().sfeec_device_count())
