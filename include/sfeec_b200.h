@@ -148,7 +148,9 @@ int sfeec_yee_flow_he(sfeec_yee* h, double dt);
 int sfeec_yee_flow_ha(sfeec_yee* h, double dt);
 int sfeec_yee_energy(sfeec_yee* h, double* out);
 int sfeec_yee_set_stream(sfeec_yee* h, void* cuda_stream);
-/* 0: two-kernel (e-kick, b-kick); 1: fused single-sweep step (default) */
+/* 0: two kernels (e-kick, b-kick); 1: fused single-sweep step with plain
+ * loads; 2 (default): fused sweep, persistent, TMA-pipelined (PEC only;
+ * periodic lattices always use 0) */
 int sfeec_yee_set_variant(sfeec_yee* h, int variant);
 int64_t sfeec_yee_last_launches(sfeec_yee* h);
 /* Returns (and resets) the accumulated device time of the steady-state step

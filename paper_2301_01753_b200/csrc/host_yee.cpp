@@ -126,8 +126,8 @@ void build_yee_operators(int nx, int ny, int nz, double dx, double dy, double dz
       int a;
       int64_t s;
       g.dof_to_storage(true, f, a, s);
-      int c[3] = {(int)(s % g.S[0]), (int)((s / g.S[0]) % g.S[1]),
-                  (int)(s / ((int64_t)g.S[0] * g.S[1]))};
+      int c[3] = {(int)(s % g.P0), (int)((s / g.P0) % g.S[1]),
+                  (int)(s / ((int64_t)g.P0 * g.S[1]))};
       int a1 = (a + 1) % 3, a2 = (a + 2) % 3;
       const double area = L.face_area(a, c);
       struct {

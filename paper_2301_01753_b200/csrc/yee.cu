@@ -23,6 +23,9 @@
 #include <cstring>
 #include <memory>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "device_util.cuh"
 #include "yee_layout.hpp"
 
@@ -73,9 +76,10 @@ __global__ void __launch_bounds__(kThreads) k_bkick(YeeGeom g, Fields<T> f, YeeC
   const int64_t np = g.npts();
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < np;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(s % g.S[0]);
-    const int j = (int)((s / g.S[0]) % g.S[1]);
-    const int kk = (int)(s / ((int64_t)g.S[0] * g.S[1]));
+    const int i = (int)(s % g.P0);
+    const int j = (int)((s / g.P0) % g.S[1]);
+    const int kk = (int)(s / ((int64_t)g.P0 * g.S[1]));
+    if (i >= g.S[0] || kk >= g.S[2]) continue;  // row / tail padding
     int ip = i + 1, jp = j + 1, kp = kk + 1;
     if (g.bc == 0) {
       ip = wrapm(ip, g.n[0]);
@@ -105,9 +109,10 @@ __global__ void __launch_bounds__(kThreads) k_ekick(YeeGeom g, Fields<T> f, YeeC
   const int64_t np = g.npts();
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < np;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(s % g.S[0]);
-    const int j = (int)((s / g.S[0]) % g.S[1]);
-    const int kk = (int)(s / ((int64_t)g.S[0] * g.S[1]));
+    const int i = (int)(s % g.P0);
+    const int j = (int)((s / g.P0) % g.S[1]);
+    const int kk = (int)(s / ((int64_t)g.P0 * g.S[1]));
+    if (i >= g.S[0] || kk >= g.S[2]) continue;  // row / tail padding
     int im = i - 1, jm = j - 1, km = kk - 1;
     if (g.bc == 0) {
       im = wrapm(im, g.n[0]);
@@ -220,6 +225,165 @@ __global__ void __launch_bounds__(TX* TY)
   }
 }
 
+// ---- fused sweep, TMA-pipelined, persistent (PEC; the default) -------------
+// Same arithmetic as k_fused_pec, but every B/E plane tile (with halo) is
+// fetched by one elected thread with cp.async.bulk.tensor (TMA) into an
+// NS-stage shared-memory ring, D = NS-2 planes ahead of the sweep, completion
+// tracked by one mbarrier per stage. Out-of-box coordinates (the -1 halo and
+// the PEC walls) are zero-filled by the TMA unit. CTAs are persistent and take
+// (z-chunk, tile) work units round-robin in chunk-major order, so CTAs running
+// concurrently sweep neighbouring tiles over the same planes and the halo
+// re-reads hit L2. Only the compute domain [0,n)^3 is swept: the faces on the
+// far PEC walls have empty C rows and stay constant (present in both buffers).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+template <class T, int TX, int TY, int BW, int NS>
+struct TmaCfg {
+  static constexpr int kBBox = 3 * (TY + 2) * BW * (int)sizeof(T);  // bytes per B plane tile
+  static constexpr int kEBox = 3 * (TY + 1) * BW * (int)sizeof(T);  // bytes per E plane tile
+  static constexpr int kBStride = (kBBox + 127) / 128 * 128;
+  static constexpr int kEStride = (kEBox + 127) / 128 * 128;
+  static constexpr int kStage = kBStride + kEStride;
+  static constexpr int kEnew = 3 * (TY + 1) * (TX + 1);  // elements per E_new buffer
+  static constexpr int kSmem = NS * kStage + 2 * kEnew * (int)sizeof(T) + NS * 8 + 128;
+};
+
+template <class T, int TX, int TY, int BW, int NS>
+__global__ void __launch_bounds__(TX* TY)
+    k_fused_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
+                YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
+                int n_units) {
+  using Cfg = TmaCfg<T, TX, TY, BW, NS>;
+  constexpr int D = NS - 2;  // prefetch distance (planes)
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + NS * Cfg::kStage + 2 * Cfg::kEnew * sizeof(T));
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapE)) : "memory");
+  }
+  __syncthreads();
+  auto stB = [&](int s) { return reinterpret_cast<const T*>(base + s * Cfg::kStage); };
+  auto stE = [&](int s) { return reinterpret_cast<const T*>(base + s * Cfg::kStage + Cfg::kBStride); };
+  uint32_t gplane = 0;  // planes issued by this CTA so far (stage = gp % NS, parity = gp / NS)
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
+    const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
+    const int k0 = chunk * kchunk, k1 = min(k0 + kchunk, n2);
+    const int P = k1 - k0 + 2;  // local planes p <-> z = k0 - 1 + p
+    auto issue = [&](int p) {
+      const uint32_t gp = gplane + p;
+      const int st = gp % NS;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bars[st], Cfg::kBBox + Cfg::kEBox);
+      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - 1, j0 - 1, k0 - 1 + p, 3);
+      tma_load_4d(base + st * Cfg::kStage + Cfg::kBStride, &mapE, &bars[st], i0, j0, k0 - 1 + p, 0);
+    };
+    if (tid == 0)
+      for (int p = 0; p <= D && p < P; ++p) issue(p);
+    for (int jp = 0; jp + 1 < P; ++jp) {
+      const int kk = k0 + jp;
+      if (tid == 0 && jp + 1 + D < P) issue(jp + 1 + D);
+      const uint32_t gc = gplane + jp + 1, gv = gplane + jp;
+      const int sc = gc % NS, sv = gv % NS;
+      if (jp == 0) mbar_wait(&bars[sv], (gv / NS) & 1);
+      mbar_wait(&bars[sc], (gc / NS) & 1);
+      const T* Bc = stB(sc);
+      const T* Bp = stB(sv);
+      const T* Ec = stE(sc);
+      T* Enc = sEn + (jp & 1) * Cfg::kEnew;
+      T* Enp = sEn + ((jp + 1) & 1) * Cfg::kEnew;
+#define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BW + (x)]
+#define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BW + (x)]
+#define EC(c, y, x) Ec[((c) * (TY + 1) + (y)) * BW + (x)]
+#define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
+      // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
+      for (int p = tid; p < (TX + 1) * (TY + 1); p += TX * TY) {
+        const int li = p % (TX + 1), lj = p / (TX + 1);
+        const int i = i0 + li, j = j0 + lj;
+        const int bi = li + 1, bj = lj + 1;
+        T e0 = EC(0, lj, li), e1 = EC(1, lj, li), e2 = EC(2, lj, li);
+        const bool d0 = e_dof(g, 0, i, j, kk), d1 = e_dof(g, 1, i, j, kk), d2 = e_dof(g, 2, i, j, kk);
+        if (d0)
+          e0 += ck.ce[1] * (BC(2, bj, bi) - BC(2, bj - 1, bi)) - ck.ce[2] * (BC(1, bj, bi) - BP(1, bj, bi));
+        if (d1)
+          e1 += ck.ce[2] * (BC(0, bj, bi) - BP(0, bj, bi)) - ck.ce[0] * (BC(2, bj, bi) - BC(2, bj, bi - 1));
+        if (d2)
+          e2 += ck.ce[0] * (BC(1, bj, bi) - BC(1, bj, bi - 1)) - ck.ce[1] * (BC(0, bj, bi) - BC(0, bj - 1, bi));
+        if (li < TX && lj < TY && kk < k1 && i < n0 && j < n1) {
+          const int64_t s = g.sidx(i, j, kk);
+          if (d0) out.c[0][s] = e0;
+          if (d1) out.c[1][s] = e1;
+          if (d2) out.c[2][s] = e2;
+        }
+        EN(Enc, 0, lj, li) = e0;
+        EN(Enc, 1, lj, li) = e1;
+        EN(Enc, 2, lj, li) = e2;
+      }
+      __syncthreads();
+      // B_new(kk-1) on the own tile
+      if (jp > 0) {
+        const int li = tid % TX, lj = tid / TX;
+        const int i = i0 + li, j = j0 + lj, kb = kk - 1;
+        if (i < n0 && j < n1) {
+          const int64_t s = g.sidx(i, j, kb);
+          const int bi = li + 1, bj = lj + 1;
+          if (b_dof(g, 0, i, j, kb))
+            out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
+                                           ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
+          if (b_dof(g, 1, i, j, kb))
+            out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
+                                           ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
+          if (b_dof(g, 2, i, j, kb))
+            out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
+                                           ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
+        }
+      }
+#undef BC
+#undef BP
+#undef EC
+#undef EN
+      __syncthreads();
+    }
+    gplane += P;
+  }
+}
+
 // state pack/unpack between the SFEEC numbering (fp64) and storage (T)
 template <class T>
 __global__ void k_scatter(YeeGeom g, bool face, const double* __restrict__ src, int64_t n,
@@ -255,7 +419,11 @@ struct YeeDev {
   double d[3] = {1, 1, 1};
   double dt = 0, eps0 = 1, mu0 = 1, dv = 1;
   int prec = 8;
-  int variant = 1;
+  int variant = 2;
+  // TMA descriptors of the two ping-pong buffers (B box, E box), PEC only
+  CUtensorMap mapB[2], mapE[2];
+  bool have_maps = false;
+  int tma_blocks = 0;
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, partials;
@@ -319,14 +487,76 @@ struct YeeDev {
     ++launches;
   }
 
+  static constexpr int kTX = 32, kTY = 8, kNS = 4, kChunk = 32;
+  template <class T>
+  static constexpr int box_w() { return sizeof(T) == 8 ? kTX + 2 : kTX + 4; }
+
+  template <class T>
+  void make_maps() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      SFEEC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn)
+        throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t w = sizeof(T);
+    cuuint64_t dims[4] = {(cuuint64_t)g.S[0], (cuuint64_t)g.S[1], (cuuint64_t)g.S[2], 6};
+    cuuint64_t strides[3] = {(cuuint64_t)g.P0 * w, (cuuint64_t)g.P0 * g.S[1] * w,
+                             (cuuint64_t)g.npts() * w};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    cuuint32_t boxB[4] = {(cuuint32_t)box_w<T>(), kTY + 2, 1, 3};
+    cuuint32_t boxE[4] = {(cuuint32_t)box_w<T>(), kTY + 1, 1, 3};
+    const CUtensorMapDataType dt_ = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                   : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    for (int b = 0; b < 2; ++b) {
+      void* ptr = buf[b].p;
+      for (int which = 0; which < 2; ++which) {
+        CUresult r = encode(which ? &mapE[b] : &mapB[b], dt_, 4, ptr, dims, strides,
+                            which ? boxE : boxB, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
+      }
+    }
+    using Cfg = TmaCfg<T, kTX, kTY, box_w<T>(), kNS>;
+    auto kern = k_fused_tma<T, kTX, kTY, box_w<T>(), kNS>;
+    SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+    int per_sm = 0, sms = 0;
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTX * kTY, Cfg::kSmem));
+    SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    tma_blocks = std::max(1, per_sm) * sms;
+    have_maps = true;
+  }
+
+  template <class T>
+  void fused_tma(double h_e, double h_b) {
+    if (!have_maps) make_maps<T>();
+    using Cfg = TmaCfg<T, kTX, kTY, box_w<T>(), kNS>;
+    const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
+    const int nchunks = (g.n[2] + kChunk - 1) / kChunk;
+    const int n_units = ntx * nty * nchunks;
+    const int grid = std::min(n_units, tma_blocks);
+    k_fused_tma<T, kTX, kTY, box_w<T>(), kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
+        mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
+        ntx, ntx * nty, n_units);
+    SFEEC_LAUNCH_CHECK();
+    cur ^= 1;
+    ++launches;
+  }
+
   template <class T>
   void advance_t(int64_t n) {
     bkick<T>(0.5 * dt);
-    const bool use_fused = variant == 1 && g.bc == SFEEC_BC_PEC;
+    const bool use_fused = variant >= 1 && g.bc == SFEEC_BC_PEC;
     const bool t = timing && n > 1;
     if (t) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
     for (int64_t s = 0; s + 1 < n; ++s) {
-      if (use_fused) {
+      if (use_fused && variant == 2) {
+        fused_tma<T>(dt, dt);
+      } else if (use_fused) {
         fused<T>(dt, dt);
       } else {
         ekick<T>(dt);
@@ -398,11 +628,15 @@ struct YeeDev {
       SFEEC_CUDA(cudaMemcpyAsync(stage.p, face ? b : e, sizeof(double) * (size_t)n,
                                  cudaMemcpyHostToDevice, stream));
       unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
-      if (prec == 8)
-        k_scatter<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(cur));
-      else
-        k_scatter<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(cur));
-      SFEEC_LAUNCH_CHECK();
+      // both ping-pong buffers: the fused sweep never rewrites the constant
+      // PEC boundary faces (empty C rows), so they must be present in both
+      for (int bsel = 0; bsel < 2; ++bsel) {
+        if (prec == 8)
+          k_scatter<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(bsel));
+        else
+          k_scatter<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(bsel));
+        SFEEC_LAUNCH_CHECK();
+      }
     }
     SFEEC_CUDA(cudaStreamSynchronize(stream));
   }
@@ -555,7 +789,7 @@ int sfeec_yee_set_stream(sfeec_yee* h, void* s) {
 int sfeec_yee_set_variant(sfeec_yee* h, int variant) {
   return guarded([&] {
     require(h, "null handle");
-    require(variant == 0 || variant == 1, "variant must be 0 or 1");
+    require(variant >= 0 && variant <= 2, "variant must be 0, 1 or 2");
     h->d.variant = variant;
   });
 }

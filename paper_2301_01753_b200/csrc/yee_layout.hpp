@@ -1,8 +1,8 @@
 // DOF numbering and HBM storage of the structured (Yee / lumped-mass SFEEC)
 // path. Shared by the host builders (host_yee.cpp) and the kernels (yee.cu).
 //
-// Storage: six component arrays (Ex, Ey, Ez, Bx, By, Bz), each X*Y*Z with
-// index s(i,j,k) = i + X*(j + Y*k), i fastest.
+// Storage: six component arrays (Ex, Ey, Ez, Bx, By, Bz), each of np_alloc
+// elements with index s(i,j,k) = i + P0*(j + Y*k), i fastest (P0 = row pitch).
 //   periodic: X,Y,Z = nx,ny,nz; the SFEEC numbering is a*N + s(i,j,k), i.e.
 //             exactly the reference's axis-major ids (mesh_cubical.cpp:11-14,
 //             52-53) and YeeGrid's component-major arrays (yee.hpp:15-17).
@@ -27,11 +27,13 @@ struct YeeGeom {
   int n[3];
   int bc;   // SFEEC_BC_PERIODIC / SFEEC_BC_PEC
   int S[3]; // storage extents X, Y, Z
+  int P0;   // row pitch (elements) >= S[0]; PEC rows padded to 16-byte multiples for TMA
+  int64_t np_alloc;  // elements per component array (padded to a multiple of 32)
   int64_t edge_off[4], face_off[4];
 
-  SFEEC_HD int64_t npts() const { return (int64_t)S[0] * S[1] * S[2]; }
+  SFEEC_HD int64_t npts() const { return np_alloc; }
   SFEEC_HD int64_t sidx(int i, int j, int k) const {
-    return (int64_t)i + (int64_t)S[0] * ((int64_t)j + (int64_t)S[1] * k);
+    return (int64_t)i + (int64_t)P0 * ((int64_t)j + (int64_t)S[1] * k);
   }
   // DOF range of component a: lo[d], ext[d]
   SFEEC_HD void range(bool face, int a, int lo[3], int ext[3]) const {
@@ -92,6 +94,8 @@ inline YeeGeom make_yee_geom(int nx, int ny, int nz, int bc) {
   g.n[2] = nz;
   g.bc = bc;
   for (int d = 0; d < 3; ++d) g.S[d] = bc ? g.n[d] + 1 : g.n[d];
+  g.P0 = bc ? (g.S[0] + 7) / 8 * 8 : g.S[0];
+  g.np_alloc = ((int64_t)g.P0 * g.S[1] * g.S[2] + 31) / 32 * 32;
   g.init_offsets();
   return g;
 }
