@@ -265,10 +265,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-template <class T, int TX, int TY, int BW, int NS>
+// TMA requires the innermost box coordinate to be 16-byte aligned (measured:
+// a -1 start faults with "illegal instruction"), so the B tile starts OFF =
+// 16/sizeof(T) points left of the tile instead of 1; widths are rounded to
+// 16-byte multiples.
+template <class T, int TX, int TY, int NS>
 struct TmaCfg {
-  static constexpr int kBBox = 3 * (TY + 2) * BW * (int)sizeof(T);  // bytes per B plane tile
-  static constexpr int kEBox = 3 * (TY + 1) * BW * (int)sizeof(T);  // bytes per E plane tile
+  static constexpr int kOff = 16 / (int)sizeof(T);
+  static constexpr int kBWB = (((TX + 1 + kOff) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
+  static constexpr int kBWE = (((TX + 1) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
+  static constexpr int kBBox = 3 * (TY + 2) * kBWB * (int)sizeof(T);  // bytes per B plane tile
+  static constexpr int kEBox = 3 * (TY + 1) * kBWE * (int)sizeof(T);  // bytes per E plane tile
   static constexpr int kBStride = (kBBox + 127) / 128 * 128;
   static constexpr int kEStride = (kEBox + 127) / 128 * 128;
   static constexpr int kStage = kBStride + kEStride;
@@ -276,13 +283,14 @@ struct TmaCfg {
   static constexpr int kSmem = NS * kStage + 2 * kEnew * (int)sizeof(T) + NS * 8 + 128;
 };
 
-template <class T, int TX, int TY, int BW, int NS>
+template <class T, int TX, int TY, int NS>
 __global__ void __launch_bounds__(TX* TY)
     k_fused_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                 YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                 int n_units) {
-  using Cfg = TmaCfg<T, TX, TY, BW, NS>;
-  constexpr int D = NS - 2;  // prefetch distance (planes)
+  using Cfg = TmaCfg<T, TX, TY, NS>;
+  constexpr int D = NS - 2;
+  constexpr int BWB = Cfg::kBWB, BWE = Cfg::kBWE, OFF = Cfg::kOff;  // prefetch distance (planes)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(TX* TY)
       const int st = gp % NS;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(&bars[st], Cfg::kBBox + Cfg::kEBox);
-      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - 1, j0 - 1, k0 - 1 + p, 3);
+      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - OFF, j0 - 1, k0 - 1 + p, 3);
       tma_load_4d(base + st * Cfg::kStage + Cfg::kBStride, &mapE, &bars[st], i0, j0, k0 - 1 + p, 0);
     };
     if (tid == 0)
@@ -328,15 +336,15 @@ __global__ void __launch_bounds__(TX* TY)
       const T* Ec = stE(sc);
       T* Enc = sEn + (jp & 1) * Cfg::kEnew;
       T* Enp = sEn + ((jp + 1) & 1) * Cfg::kEnew;
-#define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BW + (x)]
-#define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BW + (x)]
-#define EC(c, y, x) Ec[((c) * (TY + 1) + (y)) * BW + (x)]
+#define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BWB + (x)]
+#define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BWB + (x)]
+#define EC(c, y, x) Ec[((c) * (TY + 1) + (y)) * BWE + (x)]
 #define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
       // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
       for (int p = tid; p < (TX + 1) * (TY + 1); p += TX * TY) {
         const int li = p % (TX + 1), lj = p / (TX + 1);
         const int i = i0 + li, j = j0 + lj;
-        const int bi = li + 1, bj = lj + 1;
+        const int bi = li + OFF, bj = lj + 1;
         T e0 = EC(0, lj, li), e1 = EC(1, lj, li), e2 = EC(2, lj, li);
         const bool d0 = e_dof(g, 0, i, j, kk), d1 = e_dof(g, 1, i, j, kk), d2 = e_dof(g, 2, i, j, kk);
         if (d0)
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(TX* TY)
         const int i = i0 + li, j = j0 + lj, kb = kk - 1;
         if (i < n0 && j < n1) {
           const int64_t s = g.sidx(i, j, kb);
-          const int bi = li + 1, bj = lj + 1;
+          const int bi = li + OFF, bj = lj + 1;
           if (b_dof(g, 0, i, j, kb))
             out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
                                            ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
@@ -488,8 +496,6 @@ struct YeeDev {
   }
 
   static constexpr int kTX = 32, kTY = 8, kNS = 4, kChunk = 32;
-  template <class T>
-  static constexpr int box_w() { return sizeof(T) == 8 ? kTX + 2 : kTX + 4; }
 
   template <class T>
   void make_maps() {
@@ -507,8 +513,9 @@ struct YeeDev {
     cuuint64_t strides[3] = {(cuuint64_t)g.P0 * w, (cuuint64_t)g.P0 * g.S[1] * w,
                              (cuuint64_t)g.npts() * w};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    cuuint32_t boxB[4] = {(cuuint32_t)box_w<T>(), kTY + 2, 1, 3};
-    cuuint32_t boxE[4] = {(cuuint32_t)box_w<T>(), kTY + 1, 1, 3};
+    using Cfg = TmaCfg<T, kTX, kTY, kNS>;
+    cuuint32_t boxB[4] = {(cuuint32_t)Cfg::kBWB, kTY + 2, 1, 3};
+    cuuint32_t boxE[4] = {(cuuint32_t)Cfg::kBWE, kTY + 1, 1, 3};
     const CUtensorMapDataType dt_ = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     for (int b = 0; b < 2; ++b) {
@@ -521,8 +528,7 @@ struct YeeDev {
         if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
       }
     }
-    using Cfg = TmaCfg<T, kTX, kTY, box_w<T>(), kNS>;
-    auto kern = k_fused_tma<T, kTX, kTY, box_w<T>(), kNS>;
+    auto kern = k_fused_tma<T, kTX, kTY, kNS>;
     SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
     int per_sm = 0, sms = 0;
     SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTX * kTY, Cfg::kSmem));
@@ -534,12 +540,12 @@ struct YeeDev {
   template <class T>
   void fused_tma(double h_e, double h_b) {
     if (!have_maps) make_maps<T>();
-    using Cfg = TmaCfg<T, kTX, kTY, box_w<T>(), kNS>;
+    using Cfg = TmaCfg<T, kTX, kTY, kNS>;
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
     const int nchunks = (g.n[2] + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
     const int grid = std::min(n_units, tma_blocks);
-    k_fused_tma<T, kTX, kTY, box_w<T>(), kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
+    k_fused_tma<T, kTX, kTY, kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
         ntx, ntx * nty, n_units);
     SFEEC_LAUNCH_CHECK();
