@@ -280,22 +280,33 @@ struct TmaCfg {
   static constexpr int kEStride = (kEBox + 127) / 128 * 128;
   static constexpr int kStage = kBStride + kEStride;
   static constexpr int kEnew = 3 * (TY + 1) * (TX + 1);  // elements per E_new buffer
-  static constexpr int kSmem = NS * kStage + 2 * kEnew * (int)sizeof(T) + NS * 8 + 128;
+  static constexpr int kBarOff = (NS * kStage + 3 * kEnew * (int)sizeof(T) + 15) / 16 * 16;
+  static constexpr int kSmem = kBarOff + NS * 8 + 128;
+  static constexpr int kD = NS - 3;  // prefetch distance in planes
 };
 
+// One CTA = TX*TY threads. Per plane kk of a unit:
+//   wait(stage of plane kk) -> E_new(kk) on the (TX+1)x(TY+1) region from the
+//   staged B(kk), B(kk-1), E(kk) -> sync -> B_new(kk-1) on the own tile from
+//   E_new(kk-1), E_new(kk) and the staged B(kk-1).
+// One __syncthreads per plane: E_new is triple-buffered and the TMA ring has
+// D + 3 stages, so the producer never overwrites a stage or an E_new buffer
+// that a lagging warp of the previous plane may still read.
 template <class T, int TX, int TY, int NS>
 __global__ void __launch_bounds__(TX* TY)
     k_fused_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                 YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                 int n_units) {
   using Cfg = TmaCfg<T, TX, TY, NS>;
-  constexpr int D = NS - 2;
-  constexpr int BWB = Cfg::kBWB, BWE = Cfg::kBWE, OFF = Cfg::kOff;  // prefetch distance (planes)
+  constexpr int D = Cfg::kD;
+  constexpr int BWB = Cfg::kBWB, BWE = Cfg::kBWE, OFF = Cfg::kOff;
+  constexpr int NT = TX * TY, NE = (TX + 1) * (TY + 1);
+  static_assert(NE <= 2 * NT, "E region needs at most two passes");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + NS * Cfg::kStage + 2 * Cfg::kEnew * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
@@ -304,16 +315,40 @@ __global__ void __launch_bounds__(TX* TY)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapE)) : "memory");
   }
   __syncthreads();
-  auto stB = [&](int s) { return reinterpret_cast<const T*>(base + s * Cfg::kStage); };
-  auto stE = [&](int s) { return reinterpret_cast<const T*>(base + s * Cfg::kStage + Cfg::kBStride); };
   uint32_t gplane = 0;  // planes issued by this CTA so far (stage = gp % NS, parity = gp / NS)
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int64_t kstride = (int64_t)g.P0 * g.S[1];
+  // E-region points of this thread: pass 0 -> p = tid, pass 1 -> p = tid + NT
+  const int pl[2] = {tid, tid + NT};
+  int li_[2], lj_[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    li_[q] = pl[q] % (TX + 1);
+    lj_[q] = pl[q] / (TX + 1);
+  }
+  const bool has2 = tid + NT < NE;
+  const int bli = tid % TX, blj = tid / TX;  // own B point
 
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
     const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
     const int k0 = chunk * kchunk, k1 = min(k0 + kchunk, n2);
     const int P = k1 - k0 + 2;  // local planes p <-> z = k0 - 1 + p
+    // (i, j) parts of the PEC DOF masks (yee_layout.hpp) and write permissions
+    uint32_t m[2];
+    int64_t sij[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = i0 + li_[q], j = j0 + lj_[q];
+      const bool ix = i < n0, iy = i >= 1 && i <= n0 - 1;
+      const bool jx = j < n1, jy = j >= 1 && j <= n1 - 1;
+      const bool own = li_[q] < TX && lj_[q] < TY && i < n0 && j < n1;
+      m[q] = (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u) | (own ? 8u : 0u);
+      sij[q] = (int64_t)i + (int64_t)g.P0 * j;
+    }
+    const bool bown = i0 + bli < n0 && j0 + blj < n1;
+    const int64_t bsij = (int64_t)(i0 + bli) + (int64_t)g.P0 * (j0 + blj);
+
     auto issue = [&](int p) {
       const uint32_t gp = gplane + p;
       const int st = gp % NS;
@@ -331,30 +366,32 @@ __global__ void __launch_bounds__(TX* TY)
       const int sc = gc % NS, sv = gv % NS;
       if (jp == 0) mbar_wait(&bars[sv], (gv / NS) & 1);
       mbar_wait(&bars[sc], (gc / NS) & 1);
-      const T* Bc = stB(sc);
-      const T* Bp = stB(sv);
-      const T* Ec = stE(sc);
-      T* Enc = sEn + (jp & 1) * Cfg::kEnew;
-      T* Enp = sEn + ((jp + 1) & 1) * Cfg::kEnew;
+      const T* __restrict__ Bc = reinterpret_cast<const T*>(base + sc * Cfg::kStage);
+      const T* __restrict__ Bp = reinterpret_cast<const T*>(base + sv * Cfg::kStage);
+      const T* __restrict__ Ec = reinterpret_cast<const T*>(base + sc * Cfg::kStage + Cfg::kBStride);
+      T* Enc = sEn + ((gplane + jp) % 3) * Cfg::kEnew;
+      const T* Enp = sEn + ((gplane + jp + 2) % 3) * Cfg::kEnew;
 #define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BWB + (x)]
 #define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BWB + (x)]
 #define EC(c, y, x) Ec[((c) * (TY + 1) + (y)) * BWE + (x)]
 #define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
+      const bool kin = kk >= 1 && kk <= n2 - 1, kz = kk < n2, kw = kk < k1;
       // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
-      for (int p = tid; p < (TX + 1) * (TY + 1); p += TX * TY) {
-        const int li = p % (TX + 1), lj = p / (TX + 1);
-        const int i = i0 + li, j = j0 + lj;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && !has2) break;
+        const int li = li_[q], lj = lj_[q];
         const int bi = li + OFF, bj = lj + 1;
         T e0 = EC(0, lj, li), e1 = EC(1, lj, li), e2 = EC(2, lj, li);
-        const bool d0 = e_dof(g, 0, i, j, kk), d1 = e_dof(g, 1, i, j, kk), d2 = e_dof(g, 2, i, j, kk);
+        const bool d0 = (m[q] & 1) && kin, d1 = (m[q] & 2) && kin, d2 = (m[q] & 4) && kz;
         if (d0)
           e0 += ck.ce[1] * (BC(2, bj, bi) - BC(2, bj - 1, bi)) - ck.ce[2] * (BC(1, bj, bi) - BP(1, bj, bi));
         if (d1)
           e1 += ck.ce[2] * (BC(0, bj, bi) - BP(0, bj, bi)) - ck.ce[0] * (BC(2, bj, bi) - BC(2, bj, bi - 1));
         if (d2)
           e2 += ck.ce[0] * (BC(1, bj, bi) - BC(1, bj, bi - 1)) - ck.ce[1] * (BC(0, bj, bi) - BC(0, bj - 1, bi));
-        if (li < TX && lj < TY && kk < k1 && i < n0 && j < n1) {
-          const int64_t s = g.sidx(i, j, kk);
+        if ((m[q] & 8) && kw) {
+          const int64_t s = sij[q] + kstride * kk;
           if (d0) out.c[0][s] = e0;
           if (d1) out.c[1][s] = e1;
           if (d2) out.c[2][s] = e2;
@@ -364,34 +401,27 @@ __global__ void __launch_bounds__(TX* TY)
         EN(Enc, 2, lj, li) = e2;
       }
       __syncthreads();
-      // B_new(kk-1) on the own tile
-      if (jp > 0) {
-        const int li = tid % TX, lj = tid / TX;
-        const int i = i0 + li, j = j0 + lj, kb = kk - 1;
-        if (i < n0 && j < n1) {
-          const int64_t s = g.sidx(i, j, kb);
-          const int bi = li + OFF, bj = lj + 1;
-          if (b_dof(g, 0, i, j, kb))
-            out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
-                                           ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
-          if (b_dof(g, 1, i, j, kb))
-            out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
-                                           ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
-          if (b_dof(g, 2, i, j, kb))
-            out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
-                                           ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
-        }
+      // B_new(kk-1) on the own tile (every face of [0,n)^3 is a DOF)
+      if (jp > 0 && bown) {
+        const int li = bli, lj = blj;
+        const int64_t s = bsij + kstride * (kk - 1);
+        const int bi = li + OFF, bj = lj + 1;
+        out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
+                                       ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
+        out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
+                                       ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
+        out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
+                                       ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
       }
 #undef BC
 #undef BP
 #undef EC
 #undef EN
-      __syncthreads();
     }
     gplane += P;
+    __syncthreads();  // unit boundary: the next unit's prologue refills every stage
   }
 }
-
 // state pack/unpack between the SFEEC numbering (fp64) and storage (T)
 template <class T>
 __global__ void k_scatter(YeeGeom g, bool face, const double* __restrict__ src, int64_t n,
@@ -495,7 +525,7 @@ struct YeeDev {
     ++launches;
   }
 
-  static constexpr int kTX = 32, kTY = 8, kNS = 4, kChunk = 32;
+  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32;
 
   template <class T>
   void make_maps() {
