@@ -166,6 +166,29 @@ double sfeec_yee_step_bytes(sfeec_yee* h);
  * operators.cpp:29-42), extended with PEC. */
 int sfeec_build_yee_curl(int nx, int ny, int nz, double dx, double dy, double dz, int bc,
                          sfeec_csr_owned* c, sfeec_csr_owned* div);
+/* Jittered Kuhn/Freudenthal tetrahedral mesh of the unit cube (n^3 cubes x 6
+ * tets), PEC walls, first-order Whitney forms (BASELINE configs 1, 3, 5). New:
+ * the reference meshes are 2-D or periodic cubes; conventions
+ * follow mesh_simplicial.cpp:16-38 (ascending-id orientation) and
+ * operators.cpp:29-42,133-179. Numbering contract: DESIGN.md. */
+typedef struct sfeec_tetmesh sfeec_tetmesh;
+int sfeec_tetmesh_create(int n, double jitter, uint64_t seed, sfeec_tetmesh** out);
+void sfeec_tetmesh_destroy(sfeec_tetmesh* h);
+int sfeec_tetmesh_counts(const sfeec_tetmesh* h, int64_t* n_vertices, int64_t* n_edges,
+                         int64_t* n_faces, int64_t* n_tets);
+/* nullable outputs: xyz[3*nv], edge_vertices[2*N1], face_vertices[3*N2],
+ * tet_vertices[4*T] (ascending vertex ids) */
+int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_vertices,
+                           int64_t* face_vertices, int64_t* tet_vertices);
+/* which: 0 C (faces x interior edges, +-1), 1 M1 (interior edges), 2 M2
+ * (faces), 3 D (tets x faces, +-1) */
+int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
+/* make_pattern (spai.cpp:31-72): kind 0 diagonal, 1 S(M1), 2 S(M1^2); the
+ * pattern is returned as a CSR with unit values */
+int sfeec_make_pattern(const sfeec_csr* m, int kind, sfeec_csr_owned* out);
+/* spai_approximate_inverse (spai.cpp:127-286) on pattern `kind`; report[4] =
+ * {frobenius_residual, avg_nnz_per_row, max_column_residual, fallback_columns} */
+int sfeec_spai(const sfeec_csr* m, int kind, sfeec_csr_owned* q, double* report);
 /* operator_from_triplets (sparse.cpp:20-61), int64-safe */
 int sfeec_csr_from_triplets(int64_t rows, int64_t cols, int64_t n, const int32_t* r,
                             const int32_t* c, const double* v, sfeec_csr_owned* out);

@@ -10,7 +10,10 @@ from .scheme import (  # noqa: F401
     SparseOperator,
     SplitKind,
     SplitScheme,
+    TetMesh,
     UnitSystem,
+    make_pattern,
+    spai_approximate_inverse,
     YeeScheme,
     device_count,
     make_state,

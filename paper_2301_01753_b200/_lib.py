@@ -99,7 +99,15 @@ _SIGS = {
     "sfeec_build_yee_curl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),
-    "sfeec_csr_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _PI32, _PI32, _PD,
+    "sfeec_tetmesh_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    "sfeec_tetmesh_destroy": (None, [_P]),
+    "sfeec_tetmesh_counts": (C.c_int, [_P, _PI64, _PI64, _PI64, _PI64]),
+    "sfeec_tetmesh_geometry": (C.c_int, [_P, _PD, _PI64, _PI64, _PI64]),
+    "sfeec_tetmesh_operator": (C.c_int, [_P, C.c_int, C.POINTER(sfeec_csr_owned)]),
+    "sfeec_make_pattern": (C.c_int, [C.POINTER(sfeec_csr), C.c_int,
+                                     C.POINTER(sfeec_csr_owned)]),
+    "sfeec_spai": (C.c_int, [C.POINTER(sfeec_csr), C.c_int, C.POINTER(sfeec_csr_owned), _PD]),
+    "sfeec_csr_from_triplets":(C.c_int, [C.c_int64, C.c_int64, C.c_int64, _PI32, _PI32, _PD,
                                           C.POINTER(sfeec_csr_owned)]),
     "sfeec_csr_symmetric_part": (C.c_int, [C.POINTER(sfeec_csr), C.POINTER(sfeec_csr_owned)]),
     "sfeec_csr_transpose": (C.c_int, [C.POINTER(sfeec_csr), C.POINTER(sfeec_csr_owned)]),

@@ -359,5 +359,74 @@ def yee_operators(nx, ny, nz, dx, dy, dz, bc=L.BC_PEC):
     return SparseOperator._from_owned(c), SparseOperator._from_owned(d)
 
 
+class TetMesh:
+    """Jittered Kuhn/Freudenthal tet mesh of the unit cube, PEC walls, first-
+    order Whitney forms (host C++ builder; numbering contract in DESIGN.md)."""
+
+    def __init__(self, n: int, jitter: float = 0.1, seed: int = 0):
+        h = C.c_void_p()
+        L.check(L.lib().sfeec_tetmesh_create(int(n), float(jitter), int(seed), C.byref(h)))
+        self._h = h
+        self.n = n
+        c = [C.c_int64() for _ in range(4)]
+        L.check(L.lib().sfeec_tetmesh_counts(h, *[C.byref(x) for x in c]))
+        self.n_vertices, self.n_edges, self.n_faces, self.n_tets = (x.value for x in c)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().sfeec_tetmesh_destroy(h)
+            self._h = None
+
+    def geometry(self):
+        """(xyz[nv,3], edge_vertices[N1,2], face_vertices[N2,3], tet_vertices[T,4])."""
+        xyz = np.zeros((self.n_vertices, 3))
+        ev = np.zeros((self.n_edges, 2), np.int64)
+        fv = np.zeros((self.n_faces, 3), np.int64)
+        tv = np.zeros((self.n_tets, 4), np.int64)
+        L.check(L.lib().sfeec_tetmesh_geometry(self._h, L.dptr(xyz), L.i64ptr(ev), L.i64ptr(fv),
+                                               L.i64ptr(tv)))
+        return xyz, ev, fv, tv
+
+    def _op(self, which, symmetric=False) -> SparseOperator:
+        out = L.sfeec_csr_owned()
+        L.check(L.lib().sfeec_tetmesh_operator(self._h, which, C.byref(out)))
+        return SparseOperator._from_owned(out, symmetric)
+
+    def curl(self) -> SparseOperator:
+        return self._op(0)
+
+    def mass1(self) -> SparseOperator:
+        return self._op(1, True)
+
+    def mass2(self) -> SparseOperator:
+        return self._op(2, True)
+
+    def div(self) -> SparseOperator:
+        return self._op(3)
+
+
+PATTERNS = {"diagonal": 0, "m1": 1, "m1sq": 2}
+
+
+def make_pattern(m: SparseOperator, kind: str = "m1") -> SparseOperator:
+    """spai.cpp:31-72; returns the pattern as a CSR with unit values."""
+    out = L.sfeec_csr_owned()
+    v = m.view()
+    L.check(L.lib().sfeec_make_pattern(C.byref(v), PATTERNS[kind], C.byref(out)))
+    return SparseOperator._from_owned(out)
+
+
+def spai_approximate_inverse(m: SparseOperator, kind: str = "m1"):
+    """spai.cpp:127-286 -> (Q, report dict)."""
+    out = L.sfeec_csr_owned()
+    rep = np.zeros(4)
+    v = m.view()
+    L.check(L.lib().sfeec_spai(C.byref(v), PATTERNS[kind], C.byref(out), L.dptr(rep)))
+    q = SparseOperator._from_owned(out)
+    return q, {"frobenius_residual": rep[0], "avg_nnz_per_row": rep[1],
+               "max_column_residual": rep[2], "fallback_columns": int(rep[3])}
+
+
 def device_count() -> int:
     return int(L.lib().sfeec_device_count())
