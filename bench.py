@@ -7,15 +7,18 @@ cells, lumped masses, PEC walls, Courant 0.5, fp64; E0 = 0, B0 = C A with
 seeded Gaussian A. A "step" is one leapfrog step over all N1 + N2 DOFs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config yee256|yee256_f32]
+                  [--config yee256|yee256_f32|tet16|tet64|tet128]
 
-Under torchrun (N > 1) every rank runs its own 256^3 block (weak scaling).
+Other configs: tet16 = configs[0] (16^3 x 6 tets, S(M1) SPAI, jitter 0.1),
+tet128 = configs[2] (128^3 x 6 tets, jitter 0.15, Gaussian pulse).
+Under torchrun (N > 1) every rank runs its own block (weak scaling).
 `--impl reference` times the reference CPU step (oracle/_ref: the unmodified
 reference SplitScheme::step, dynamics.cpp:69-90) on the host cores.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -32,8 +35,20 @@ METRIC = "edge+face DOF-updates/sec per leapfrog step; achieved HBM GB/s vs peak
 UNIT = "DOF-updates/s"
 
 CONFIGS = {
-    "yee256": dict(n=256, precision=8, dtype="f64"),
-    "yee256_f32": dict(n=256, precision=4, dtype="f32"),
+    "yee256": dict(kind="yee", n=256, precision=8, dtype="f64", ref_n=128,
+                   desc="BASELINE configs[1] Yee/lumped-mass SFEEC, 256^3 cells, PEC, "
+                        "Courant 0.5"),
+    "yee256_f32": dict(kind="yee", n=256, precision=4, dtype="f32", ref_n=128,
+                       desc="BASELINE configs[1] Yee/lumped-mass SFEEC in fp32, 256^3 cells, "
+                            "PEC, Courant 0.5"),
+    "tet16": dict(kind="tet", n=16, jitter=0.1, init="gaussian", dtype="f64", ref_n=16,
+                  desc="BASELINE configs[0]: 16^3 x 6 Kuhn tets, jitter 0.1h, P1-, S(M1) "
+                       "SPAI, PEC, dt = 0.5 CFL"),
+    "tet64": dict(kind="tet", n=64, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
+                  desc="64^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) SPAI, PEC, pulse"),
+    "tet128": dict(kind="tet", n=128, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
+                   desc="BASELINE configs[2]: 128^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) "
+                        "SPAI, PEC, Gaussian pulse width 0.1, dt = 0.5 CFL"),
 }
 
 
@@ -66,7 +81,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -90,6 +105,9 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
 def yee_setup(n, precision, device):
     """Operators + initial state of configs[1] on an n^3 unit cube."""
     import paper_2301_01753_b200 as S
@@ -98,19 +116,138 @@ def yee_setup(n, precision, device):
     dt = 0.5 / (np.sqrt(3.0) * n)  # Courant 0.5: c dt sqrt(sum 1/d^2) = 0.5
     y = S.YeeScheme(n, n, n, h, h, h, dt, bc=1, precision=precision, device=device)
     a = inputs.gaussian(20260101, y.n_edges)
-    # B0 = C A, computed on the device: a b-kick with h = -dV from e = A gives
-    # b = -h * C Q A = C A (Q = I/dV)
+    # B0 = C A on the device: a b-kick with h = -dV from e = A gives b = C A (Q = I/dV)
     y.load(np.zeros(y.n_faces), a)
     y.flow_he(-(h ** 3))
     b0, _, _ = y.fetch()
-    e0 = np.zeros(y.n_edges)
-    return y, b0, e0, dt
+    return y, b0, np.zeros(y.n_edges), dt
+
+
+class YeeRunner:
+    def __init__(self, cfg, device):
+        from paper_2301_01753_b200 import _lib as L
+        self.L = L
+        self.y, self.b0, self.e0, self.dt = yee_setup(cfg["n"], cfg["precision"], device)
+        self.ndof = self.y.n_edges + self.y.n_faces
+        self.n1, self.n2 = self.y.n_edges, self.y.n_faces
+        self.prec = cfg["precision"]
+
+    def set_stream(self, ptr):
+        self.L.check(self.L.lib().sfeec_yee_set_stream(self.y.handle, ctypes.c_void_p(ptr)))
+
+    def load(self):
+        self.y.load(self.b0, self.e0)
+
+    def advance(self, k):
+        self.y.advance(k)
+
+    def launches(self):
+        return self.y.last_launches()
+
+    def timing(self, enable):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self.L.check(self.L.lib().sfeec_yee_kernel_timing(self.y.handle, 1 if enable else 0,
+                                                           ms, n))
+        return ms.value, n.value
+
+    def dominant(self, k_steps):
+        """(name, bytes per launch, avg ms per launch) of the fused sweep."""
+        self.timing(True)
+        self.y.advance(k_steps)
+        ms, n = self.timing(False)
+        return "k_fused_tma (e-kick + b-kick sweep)", self.y.step_bytes(), ms / max(n, 1)
+
+    def step_bytes(self):
+        return self.y.step_bytes()
+
+    def e2e(self, k, torch):
+        L = self.L
+        pin_b = torch.from_numpy(self.b0).pin_memory()
+        pin_e = torch.from_numpy(self.e0).pin_memory()
+        out_b, out_e = torch.empty_like(pin_b).pin_memory(), torch.empty_like(pin_e).pin_memory()
+        t0 = time.perf_counter()
+        L.check(L.lib().sfeec_yee_set_state(self.y.handle, dptr(pin_b), dptr(pin_e), 0.0))
+        self.y.advance(k)
+        L.check(L.lib().sfeec_yee_get_state(self.y.handle, dptr(out_b), dptr(out_e), None))
+        return time.perf_counter() - t0
+
+    kernel_label = "fused e-kick + b-kick z-sweep, TMA-pipelined (k_fused_tma)"
+
+
+def tet_setup(cfg, device):
+    import paper_2301_01753_b200 as S
+    from paper_2301_01753_b200 import configs
+    t0 = time.perf_counter()
+    sys_ = configs.tet_system(cfg["n"], cfg["jitter"], seed=2023)
+    if cfg["init"] == "gaussian":
+        b0, e0, _ = configs.initial_gaussian(sys_, seed=7)
+    else:
+        b0, e0, _ = configs.initial_pulse(sys_, seed=7, npulses=cfg.get("npulses", 1))
+    s = S.SplitScheme(S.SplitKind.Strang, 1.0, sys_.q, sys_.c, sys_.m2, div=sys_.d,
+                      warn_cfl=False, device=device)
+    s.set_dt(configs.cfl_dt(s))
+    setup_s = time.perf_counter() - t0
+    return sys_, s, b0, e0, setup_s
+
+
+class TetRunner:
+    def __init__(self, cfg, device):
+        import paper_2301_01753_b200 as S
+        from paper_2301_01753_b200 import _lib as L
+        self.S, self.L = S, L
+        self.sys, self.s, self.b0, self.e0, self.setup_s = tet_setup(cfg, device)
+        self.n1, self.n2 = self.sys.n1, self.sys.n2
+        self.ndof = self.n1 + self.n2
+        self.dt = self.s.dt()
+
+    def set_stream(self, ptr):
+        self.L.check(self.L.lib().sfeec_dev_set_stream(self.s.handle, ctypes.c_void_p(ptr)))
+
+    def load(self):
+        self.s.load(self.S.make_state(self.S.Formulation.BE, self.b0, self.e0))
+
+    def advance(self, k):
+        self.L.check(self.L.lib().sfeec_dev_advance(self.s.handle, int(k)))
+
+    def launches(self):
+        return self.s.last_launches()
+
+    def dominant(self, k_steps):
+        self.s.kernel_timing(True)
+        self.advance(k_steps)
+        t = self.s.kernel_timing(False)
+        name = max(("K-Q", "K-Cb", "K-CTe", "K-M2"), key=lambda k: t[k]["ms"])
+        self.per_kernel = {k: {"avg_ms": v["ms"] / max(v["launches"], 1),
+                               "bytes_per_launch": v["bytes_per_launch"],
+                               "gbs": v["bytes_per_launch"] / (v["ms"] / max(v["launches"], 1)
+                                                               * 1e-3) / 1e9
+                               if v["ms"] > 0 else None}
+                           for k, v in t.items() if k != "other"}
+        d = t[name]
+        return name, d["bytes_per_launch"], d["ms"] / max(d["launches"], 1)
+
+    def step_bytes(self):
+        return self.s.step_bytes()
+
+    def e2e(self, k, torch):
+        L = self.L
+        pin_b = torch.from_numpy(self.b0).pin_memory()
+        pin_e = torch.from_numpy(self.e0).pin_memory()
+        out_b, out_e = torch.empty_like(pin_b).pin_memory(), torch.empty_like(pin_e).pin_memory()
+        t = ctypes.c_double()
+        t0 = time.perf_counter()
+        L.check(L.lib().sfeec_dev_set_state(self.s.handle, dptr(pin_b), self.n2, dptr(pin_e),
+                                            self.n1, 0.0))
+        self.advance(k)
+        L.check(L.lib().sfeec_dev_get_state(self.s.handle, dptr(out_b), dptr(out_e),
+                                            ctypes.byref(t)))
+        return time.perf_counter() - t0
+
+    kernel_label = "SpMV chain K-M2, K-CTe, K-Q, K-Cb in sliced layouts (spmv_kernels.cu)"
 
 
 def run_ours(args, rank, world, local_rank):
     import torch
-    import paper_2301_01753_b200 as S
-    from paper_2301_01753_b200 import _lib as L
 
     cfg = CONFIGS[args.config]
     torch.cuda.set_device(local_rank)
@@ -118,82 +255,76 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    y, b0, e0, dt = yee_setup(cfg["n"], cfg["precision"], local_rank)
+    R = YeeRunner(cfg, local_rank) if cfg["kind"] == "yee" else TetRunner(cfg, local_rank)
     stream = torch.cuda.current_stream()
-    L.check(L.lib().sfeec_yee_set_stream(y.handle, C_void(stream.cuda_stream)))
-    y.load(b0, e0)
-    ndof = y.n_edges + y.n_faces
-    step_bytes = y.step_bytes()
-
-    y.advance(args.warmup)
+    R.set_stream(stream.cuda_stream)
+    R.load()
+    R.advance(args.warmup)
     torch.cuda.synchronize()
-    L.check(L.lib().sfeec_yee_kernel_timing(y.handle, 1, None, None))
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         start.record(stream)
-        y.advance(args.steps)
+        R.advance(args.steps)
         end.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms = start.elapsed_time(end)
-    launches = y.last_launches()
-    kms, kl = ctypes_double(), ctypes_int64()
-    L.check(L.lib().sfeec_yee_kernel_timing(y.handle, 0, kms, kl))
-    k_avg_ms = kms.value / max(kl.value, 1)
+    launches = R.launches()
+    # dominant kernel: average launch duration with CUDA events on the launch stream
+    kname, kbytes, k_avg_ms = R.dominant(min(args.steps, 200))
     if dist:
         t = torch.tensor([ms, k_avg_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, k_avg_ms = float(t[0]), float(t[1])
-
-    # end to end through the C ABI: pinned host state -> device, K steps, -> host
-    pin_b = torch.from_numpy(b0).pin_memory()
-    pin_e = torch.from_numpy(e0).pin_memory()
-    out_b = torch.empty_like(pin_b).pin_memory()
-    out_e = torch.empty_like(pin_e).pin_memory()
     if dist:
         dist.barrier()
-    t0 = time.perf_counter()
-    L.check(L.lib().sfeec_yee_set_state(y.handle, dptr(pin_b), dptr(pin_e), 0.0))
-    y.advance(args.steps)
-    L.check(L.lib().sfeec_yee_get_state(y.handle, dptr(out_b), dptr(out_e), None))
-    e2e_s = time.perf_counter() - t0
+    e2e_s = R.e2e(args.steps, torch)
     if dist:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
 
     peak, peak_src = hbm_peak()
-    achieved = step_bytes / (k_avg_ms * 1e-3) / 1e9
+    achieved = kbytes / (k_avg_ms * 1e-3) / 1e9
+    ndof = R.ndof
     value = world * ndof * args.steps / (ms * 1e-3)
+    step_gbs = R.step_bytes() / (ms / args.steps * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": cfg["dtype"], "data": "synthetic (seeded Gaussian A, B0 = C A, E0 = 0)",
-        "config": {"workload": f"{args.config}: BASELINE configs[1] Yee/lumped-mass SFEEC, "
-                               f"{cfg['n']}^3 cells per GPU, PEC, Courant 0.5",
-                   "dofs_per_gpu": ndof, "n1_edges": y.n_edges, "n2_faces": y.n_faces,
+        "dtype": cfg["dtype"],
+        "data": "synthetic (seeded: " + ("Gaussian A" if cfg.get("init", "gaussian") ==
+                                         "gaussian" else "Gaussian pulse A")
+                + ", B0 = C A, E0 = 0)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}" + (" per GPU" if world > 1 else ""),
+                   "dofs_per_gpu": ndof, "n1_edges": R.n1, "n2_faces": R.n2, "dt": R.dt,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (fields %.0f MB per buffer)"
-                         % (ndof * cfg["precision"] / 1e6),
-                   "kernel": "fused e-kick + b-kick z-sweep (k_fused_pec)"},
+                   "l2": "inputs larger than L2" if R.step_bytes() > 126e6 * 2
+                         else "working set fits in L2 (latency-bound parity config)",
+                   "kernel": R.kernel_label},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(args.config),
-                     "bytes_per_step": step_bytes, "kernel_avg_ms": k_avg_ms,
+                     "kernel": kname, "bytes_per_launch": kbytes, "kernel_avg_ms": k_avg_ms,
+                     "step_bytes": R.step_bytes(), "step_achieved_gbs": step_gbs,
                      "peak_source": peak_src},
         "e2e": {"value": world * ndof * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(8 * ndof), "d2h_bytes_per_step": int(8 * ndof),
-                "job": f"set_state + advance({args.steps}) + get_state via the C ABI, "
-                       "pinned host buffers"},
+                "job": f"set_state + advance({args.steps}) + get_state through the C ABI "
+                       "from/to pinned host buffers; bytes are per job"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if hasattr(R, "per_kernel"):
+        line["roofline"]["per_kernel"] = R.per_kernel
+    if hasattr(R, "setup_s"):
+        line["config"]["host_setup_s"] = R.setup_s
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_sample(budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_reference_sample(args.config, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -210,26 +341,42 @@ def committed_traffic(config):
         return None
 
 
-def cpu_reference_sample(budget_s=20.0, n=128, max_steps=1000):
+def _ref_operators(config):
+    """(q, c, m2, b0, e0, label) for the reference CPU arm at the sample size."""
+    import paper_2301_01753_b200 as S
+    cfg = CONFIGS[config]
+    n = cfg["ref_n"]
+    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)
+    if cfg["kind"] == "yee":
+        from paper_2301_01753_b200 import inputs
+        from paper_2301_01753_b200.configs import spmv
+        h = 1.0 / n
+        c, _ = S.yee_operators(n, n, n, h, h, h, bc=1)
+        dv = h ** 3
+        n1, n2 = c.cols, c.rows
+        q = (n1, n1, np.arange(n1 + 1), np.arange(n1, dtype=np.int32), np.full(n1, 1.0 / dv))
+        m2 = (n2, n2, np.arange(n2 + 1), np.arange(n2, dtype=np.int32), np.full(n2, dv))
+        a = inputs.gaussian(20260101, n1)
+        return q, tup(c), m2, spmv(c, a), np.zeros(n1), 0.5 / (np.sqrt(3.0) * n), \
+            f"{n}^3 PEC Yee lattice (lumped masses)"
+    from paper_2301_01753_b200 import configs
+    sys_ = configs.tet_system(n, cfg["jitter"], seed=2023)
+    b0, e0, _ = (configs.initial_gaussian(sys_, seed=7) if cfg["init"] == "gaussian"
+                 else configs.initial_pulse(sys_, seed=7))
+    return tup(sys_.q), tup(sys_.c), tup(sys_.m2), b0, e0, 1e-3, \
+        f"{n}^3 x 6 Kuhn tets (P1-, S(M1) SPAI)"
+
+
+def cpu_reference_sample(config, budget_s=20.0, max_steps=1000):
     """The reference SplitScheme::step (oracle/_ref, unmodified reference
     sources) on the same per-DOF workload, timed on the host cores."""
     from oracle import oracle as O
-    import paper_2301_01753_b200 as S
     if not O.ref_available():
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                 "sample": "oracle/_ref missing"}
-    h = 1.0 / n
-    c, _ = S.yee_operators(n, n, n, h, h, h, bc=1)
-    dv = h ** 3
-    n1, n2 = c.cols, c.rows
-    q = (n1, n1, np.arange(n1 + 1), np.arange(n1, dtype=np.int32), np.full(n1, 1.0 / dv))
-    m2 = (n2, n2, np.arange(n2 + 1), np.arange(n2, dtype=np.int32), np.full(n2, dv))
-    dt = 0.5 / (np.sqrt(3.0) * n)
-    ref = O.RefScheme(1, dt, q, (c.rows, c.cols, c.row_ptr, c.col_idx, c.val), m2)
-    from paper_2301_01753_b200 import inputs
-    a = inputs.gaussian(20260101, n1)
-    b = O.ref_spmv((c.rows, c.cols, c.row_ptr, c.col_idx, c.val), a)
-    e = np.zeros(n1)
+    q, c, m2, b, e, dt, label = _ref_operators(config)
+    ref = O.RefScheme(1, dt, q, c, m2)
+    n1, n2 = c[1], c[0]
     b, e, _, _ = ref.steps(True, b, e, 1)  # warm-up
     steps, secs = 0, 0.0
     while secs < budget_s and steps < max_steps:
@@ -238,55 +385,39 @@ def cpu_reference_sample(budget_s=20.0, n=128, max_steps=1000):
         steps += 1
     return {"value": (n1 + n2) * steps / secs, "unit": UNIT, "cores": os.cpu_count(),
             "kind": "reference",
-            "sample": f"{steps} x reference SplitScheme::step (Strang, BE) on the {n}^3 PEC "
-                      f"lattice (N1+N2={n1 + n2}), wall clock, OpenMP threads = all "
-                      f"{os.cpu_count()} host cores; same per-DOF operators as 256^3"}
+            "sample": f"{steps} x reference SplitScheme::step (Strang, BE) on the {label} "
+                      f"(N1+N2={n1 + n2}), wall clock, OpenMP threads = all {os.cpu_count()} "
+                      "host cores; same per-DOF operator structure as the GPU workload"}
 
 
 def run_reference(args, rank, world):
     cfg = CONFIGS[args.config]
     if rank != 0:
         return
-    base = cpu_reference_sample(budget_s=args.ref_budget)
+    base = cpu_reference_sample(args.config, budget_s=args.ref_budget,
+                                max_steps=max(args.steps, 1))
     line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-            "data": "synthetic (seeded Gaussian A, B0 = C A, E0 = 0)",
-            "config": {"workload": f"{args.config}: BASELINE configs[1] Yee/lumped-mass SFEEC "
-                                   "(reference CPU step; bounded per-DOF sample)"},
+            "data": "synthetic (seeded A, B0 = C A, E0 = 0)",
+            "config": {"workload": f"{args.config}: {cfg['desc']} (reference CPU step; "
+                                   "bounded per-DOF sample)"},
             "cpu_baseline": {k: base[k] for k in ("kind", "cores", "sample", "value")},
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    if cfg["precision"] == 4:
+    if cfg.get("precision") == 4:
         line["config"]["note"] = "the reference is fp64 only"
     print(json.dumps(line), flush=True)
 
 
-# small ctypes helpers
-def C_void(p):
-    import ctypes
-    return ctypes.c_void_p(p)
-
-
-def ctypes_double():
-    import ctypes
-    return ctypes.c_double()
-
-
-def ctypes_int64():
-    import ctypes
-    return ctypes.c_int64()
-
-
 def dptr(t):
-    import ctypes
     return ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="yee256")

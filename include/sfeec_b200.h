@@ -124,6 +124,16 @@ int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e);
 int64_t sfeec_dev_last_launches(sfeec_dev* h);
 /* algorithmic HBM bytes of one merged leapfrog step */
 double sfeec_dev_step_bytes(sfeec_dev* h);
+/* change dt (the scheme is otherwise unchanged; the cached CFL number is
+ * rescaled) -- used to set dt = 0.5 * dt_CFL after sfeec_dev_cfl_number */
+int sfeec_dev_set_dt(sfeec_dev* h, double dt);
+/* Returns (and resets) per-kernel-class device time accumulated since the
+ * last call, measured with CUDA events around every launch on the launch
+ * stream, then enables/disables timing. Classes: 0 K-Q (Q e), 1 K-Cb
+ * (C t), 2 K-CTe (C^T u), 3 K-M2 (M2 b), 4 other. ms[5], launches[5] and
+ * bytes[5] (algorithmic bytes per launch) are nullable. */
+int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launches,
+                            double* bytes);
 
 /* ---- structured Yee / lumped-mass SFEEC (yee.hpp:12-37) ------------------ */
 typedef struct sfeec_yee sfeec_yee;

@@ -32,27 +32,69 @@ struct LeapfrogDev {
   bool warned = false;
   double cfl_cache = -1;
   int64_t launches = 0;
+  // per-operator launch timing with CUDA events on the launch stream
+  // (kernel classes: 0 K-Q, 1 K-C, 2 K-CT, 3 K-M2, 4 other)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, size_t>> ev_used;  // (class, first event index)
+  double class_ms[5] = {0, 0, 0, 0, 0};
+  int64_t class_launches[5] = {0, 0, 0, 0, 0};
   bool strict() const { return (flags & SFEEC_STRICT) != 0; }
   double c2() const { return 1.0 / (eps0 * mu0); }
 
   ~LeapfrogDev() {
+    for (auto e : ev_pool) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  int op_class(const DevOperator& a) const {
+    return &a == &q ? 0 : &a == &c ? 1 : &a == &ct ? 2 : &a == &m2 ? 3 : 4;
+  }
+  void tic(const DevOperator& a) {
+    if (!timing) return;
+    const size_t i = ev_used.size() * 2;
+    while (ev_pool.size() < i + 2) {
+      cudaEvent_t e;
+      SFEEC_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    ev_used.push_back({op_class(a), i});
+    SFEEC_CUDA(cudaEventRecord(ev_pool[i], stream));
+  }
+  void toc() {
+    if (!timing) return;
+    SFEEC_CUDA(cudaEventRecord(ev_pool[ev_used.back().second + 1], stream));
+  }
+  void collect_timing() {
+    if (ev_used.empty()) return;
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+    for (auto [cls, i] : ev_used) {
+      float ms = 0;
+      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev_pool[i], ev_pool[i + 1]));
+      class_ms[cls] += ms;
+      class_launches[cls] += 1;
+    }
+    ev_used.clear();
   }
 
   // y = A x
   void apply(const DevOperator& a, const double* x, double* y) {
+    tic(a);
     if (strict())
       launch_spmv_strict(a, x, y, stream);
     else
       launch_spmv(a, x, y, 0.0, false, stream);
+    toc();
     ++launches;
   }
   // y += alpha * A x   (strict: y = y + alpha*(A x) with separate rounding)
   void apply_axpy(const DevOperator& a, const double* x, double* y, double alpha) {
+    tic(a);
     if (strict())
       launch_spmv_axpy_strict(a, x, y, alpha, stream);
     else
       launch_spmv(a, x, y, alpha, true, stream);
+    toc();
     ++launches;
   }
 
@@ -387,6 +429,45 @@ int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e) {
 }
 
 int64_t sfeec_dev_last_launches(sfeec_dev* h) { return h ? h->d.launches : -1; }
+
+int sfeec_dev_set_dt(sfeec_dev* h, double dt) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(dt >= 0, "SplitScheme: dt must be >= 0");
+    auto& d = h->d;
+    if (d.cfl_cache >= 0 && d.dt > 0) d.cfl_cache = d.cfl_cache / d.dt * dt;
+    else d.cfl_cache = -1;
+    d.dt = dt;
+  });
+}
+
+int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launches,
+                            double* bytes) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    d.collect_timing();
+    const DevOperator* ops[4] = {&d.q, &d.c, &d.ct, &d.m2};
+    for (int k = 0; k < 5; ++k) {
+      if (ms) ms[k] = d.class_ms[k];
+      if (launches) launches[k] = d.class_launches[k];
+      d.class_ms[k] = 0;
+      d.class_launches[k] = 0;
+    }
+    // algorithmic bytes per launch of each class (SURVEY.md 8(d) accounting:
+    // 12 B per fp64 nonzero, 5 B per incidence entry (int8 sign + int32
+    // column), 8 B per vector element read or written)
+    if (bytes) {
+      bytes[0] = 12.0 * d.q.nnz + 16.0 * d.n1;   // t = Q e: e gathered once, t written
+      bytes[1] = 5.0 * d.c.nnz + 8.0 * d.n1 + 16.0 * d.n2;  // b -= h C t
+      bytes[2] = 5.0 * d.ct.nnz + 8.0 * d.n2 + 16.0 * d.n1; // e += f C^T u
+      bytes[3] = 12.0 * d.m2.nnz + 16.0 * d.n2;  // u = M2 b
+      bytes[4] = 0;
+    }
+    d.timing = enable != 0;
+  });
+}
 
 // 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2)
 double sfeec_dev_step_bytes(sfeec_dev* h) {

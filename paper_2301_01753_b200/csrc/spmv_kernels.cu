@@ -52,53 +52,37 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0 && row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
 }
 
-// ---- sliced ELL, one thread per row, 32-row slices, column-major ---------
-template <bool ACC>
+// ---- sliced layout: one warp per slice, one lane per row -----------------
+template <bool ACC, bool SIGNED>
 __global__ void __launch_bounds__(kThreads)
-    k_sell_signed(int64_t rows, int64_t n_slices, const int64_t* __restrict__ sp,
-                  const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
-                  double scale, const double* __restrict__ x, double* __restrict__ y,
-                  double alpha) {
-  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (slice >= n_slices) return;
-  const int64_t base = __ldg(sp + slice) + lane;
-  const int w = __ldg(sw + slice);
-  double acc = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < w; ++k) {
-    const int32_t p = __ldg(col + base + 32 * (int64_t)k);
-    if (p != kPad) {
-      const double xv = __ldg(x + (p < 0 ? ~p : p));
-      acc += p < 0 ? -xv : xv;
-    }
-  }
-  const int64_t row = slice * 32 + lane;
-  if (row < rows) {
-    const double r = scale * acc;
-    y[row] = ACC ? fma(alpha, r, y[row]) : r;
-  }
-}
-
-template <bool ACC>
-__global__ void __launch_bounds__(kThreads)
-    k_sell(int64_t rows, int64_t n_slices, const int64_t* __restrict__ sp,
+    k_sell(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
            const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
-           const double* __restrict__ val, const double* __restrict__ x,
+           const double* __restrict__ val, double scale, const double* __restrict__ x,
            double* __restrict__ y, double alpha) {
   const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (slice >= n_slices) return;
-  const int64_t base = __ldg(sp + slice) + lane;
+  const int64_t r0 = __ldg(srow + slice);
+  const int nr = (int)(__ldg(srow + slice + 1) - r0);
+  if (lane >= nr) return;
+  const int64_t base = __ldg(sptr + slice) + lane;
   const int w = __ldg(sw + slice);
   double acc = 0.0;
 #pragma unroll 4
   for (int k = 0; k < w; ++k) {
-    const int64_t o = base + 32 * (int64_t)k;
-    acc = fma(__ldg(val + o), __ldg(x + __ldg(col + o)), acc);
+    const int64_t o = base + (int64_t)k * nr;
+    const int32_t p = __ldg(col + o);
+    if (SIGNED) {
+      if (p != kPad) {
+        const double xv = __ldg(x + (p < 0 ? ~p : p));
+        acc += p < 0 ? -xv : xv;
+      }
+    } else {
+      acc = fma(__ldg(val + o), __ldg(x + p), acc);
+    }
   }
-  const int64_t row = slice * 32 + lane;
-  if (row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
+  const double r = SIGNED ? scale * acc : acc;
+  y[r0 + lane] = ACC ? fma(alpha, r, y[r0 + lane]) : r;
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha,
@@ -132,20 +116,34 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   tpr = 1;
   while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
   layout = kCsr;
-  if (strict_only || rows == 0 || nnz == 0) return;
-
-  // sliced layouts: 32-row slices, width = longest row of the slice
-  n_slices = (rows + 31) / 32;
-  std::vector<int64_t> hsp((size_t)n_slices + 1, 0);
-  std::vector<int32_t> hsw((size_t)n_slices, 0);
-  for (int64_t sl = 0; sl < n_slices; ++sl) {
-    int64_t w = 0;
-    for (int64_t r = sl * 32; r < std::min(rows, sl * 32 + 32); ++r)
-      w = std::max(w, h.row_ptr[(size_t)r + 1] - h.row_ptr[(size_t)r]);
-    hsw[(size_t)sl] = (int32_t)w;
-    hsp[(size_t)sl + 1] = hsp[(size_t)sl] + 32 * w;
+  if (strict_only || rows == 0 || nnz == 0) {
+    SFEEC_CUDA(cudaStreamSynchronize(s));
+    return;
   }
-  sell_entries = hsp[(size_t)n_slices];
+  // greedy slices: <= 32 consecutive rows whose lengths stay within 1/8 of
+  // the slice width
+  std::vector<int64_t> hrow{0}, hptr{0};
+  std::vector<int32_t> hw;
+  {
+    int64_t r = 0;
+    while (r < rows) {
+      int64_t w = h.row_ptr[(size_t)r + 1] - h.row_ptr[(size_t)r];
+      int64_t e = r + 1;
+      while (e < rows && e - r < 32) {
+        int64_t l = h.row_ptr[(size_t)e + 1] - h.row_ptr[(size_t)e];
+        int64_t tol = std::max<int64_t>(1, std::max(w, l) / 8);
+        if (std::llabs(l - w) > tol) break;
+        w = std::max(w, l);
+        ++e;
+      }
+      hw.push_back((int32_t)w);
+      hptr.push_back(hptr.back() + w * (e - r));
+      hrow.push_back(e);
+      r = e;
+    }
+  }
+  n_slices = (int64_t)hw.size();
+  sell_entries = hptr.back();
   const double mag = std::fabs(h.val[0]);
   bool signed_ok = mag > 0;
   for (double v : h.val)
@@ -153,13 +151,15 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
       signed_ok = false;
       break;
     }
+  const double rows_per_slice = (double)rows / (double)n_slices;
   const double pad_ratio = (double)sell_entries / (double)nnz;
-  if (signed_ok && pad_ratio <= 2.5) {
+  if (rows_per_slice >= 8 && signed_ok && pad_ratio <= 2.5) {
     layout = kSigned;
     scale = mag;
-  } else if (pad_ratio <= 1.15) {
+  } else if (rows_per_slice >= 8 && pad_ratio <= 1.15) {
     layout = kSell;
   } else {
+    SFEEC_CUDA(cudaStreamSynchronize(s));
     return;
   }
   std::vector<int32_t> hc((size_t)sell_entries, layout == kSigned ? kPad : 0);
@@ -167,32 +167,45 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   if (layout == kSell) hv.assign((size_t)sell_entries, 0.0);
 #pragma omp parallel for schedule(static)
   for (int64_t sl = 0; sl < n_slices; ++sl) {
-    for (int lane = 0; lane < 32; ++lane) {
-      int64_t r = sl * 32 + lane;
-      if (r >= rows) break;
-      int64_t b = h.row_ptr[(size_t)r], e = h.row_ptr[(size_t)r + 1];
-      for (int64_t k = b; k < e; ++k) {
-        size_t o = (size_t)(hsp[(size_t)sl] + 32 * (k - b) + lane);
-        int32_t c = h.col_idx[(size_t)k];
-        if (layout == kSigned) {
-          hc[o] = h.val[(size_t)k] < 0 ? ~c : c;
-        } else {
-          hc[o] = c;
-          hv[o] = h.val[(size_t)k];
+    const int64_t r0 = hrow[(size_t)sl], nr = hrow[(size_t)sl + 1] - r0;
+    for (int64_t lane = 0; lane < nr; ++lane) {
+      const int64_t r = r0 + lane;
+      const int64_t b = h.row_ptr[(size_t)r], e = h.row_ptr[(size_t)r + 1];
+      for (int64_t k = 0; k < hw[(size_t)sl]; ++k) {
+        const size_t o = (size_t)(hptr[(size_t)sl] + k * nr + lane);
+        if (b + k < e) {
+          const int32_t c = h.col_idx[(size_t)(b + k)];
+          const double v = h.val[(size_t)(b + k)];
+          if (layout == kSigned) {
+            hc[o] = v < 0 ? ~c : c;
+          } else {
+            hc[o] = c;
+            hv[o] = v;
+          }
+        } else if (layout == kSell && e > b) {
+          hc[o] = h.col_idx[(size_t)b];  // val 0, a column the row reads anyway
         }
       }
-      // kSell padding keeps val 0 and points at the row's first column (a cached line)
-      if (layout == kSell && e > b)
-        for (int64_t k = e - b; k < hsw[(size_t)sl]; ++k)
-          hc[(size_t)(hsp[(size_t)sl] + 32 * k + lane)] = h.col_idx[(size_t)b];
     }
   }
-  slice_ptr.upload(hsp.data(), hsp.size(), s);
-  slice_w.upload(hsw.data(), hsw.size(), s);
+  slice_row.upload(hrow.data(), hrow.size(), s);
+  slice_ptr.upload(hptr.data(), hptr.size(), s);
+  slice_w.upload(hw.data(), hw.size(), s);
   sell_col.upload(hc.data(), hc.size(), s);
   if (layout == kSell) sell_val.upload(hv.data(), hv.size(), s);
   // the host vectors die at return: make the async copies complete first
   SFEEC_CUDA(cudaStreamSynchronize(s));
+}
+
+double DevOperator::stream_bytes() const {
+  switch (layout) {
+    case kSigned:
+      return 4.0 * (double)sell_entries;
+    case kSell:
+      return 12.0 * (double)sell_entries;
+    default:
+      return 12.0 * (double)nnz + 8.0 * (double)(rows + 1);
+  }
 }
 
 void DevOperator::download_csr(int64_t* row_ptr, int32_t* col_idx, double* v,
@@ -253,24 +266,22 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
     return;
   }
   unsigned g = blocks_for(a.n_slices * 32);
+#define SFEEC_SELL(ACC, SG)                                                               \
+  k_sell<ACC, SG><<<g, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,       \
+                                         a.slice_w.p, a.sell_col.p, a.sell_val.p, a.scale, x, \
+                                         y, alpha)
   switch (a.layout) {
     case DevOperator::kSigned:
       if (accumulate)
-        k_sell_signed<true><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p,
-                                                   a.slice_w.p, a.sell_col.p, a.scale, x, y,
-                                                   alpha);
+        SFEEC_SELL(true, true);
       else
-        k_sell_signed<false><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p,
-                                                    a.slice_w.p, a.sell_col.p, a.scale, x, y,
-                                                    alpha);
+        SFEEC_SELL(false, true);
       break;
     case DevOperator::kSell:
       if (accumulate)
-        k_sell<true><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p, a.slice_w.p,
-                                            a.sell_col.p, a.sell_val.p, x, y, alpha);
+        SFEEC_SELL(true, false);
       else
-        k_sell<false><<<g, kThreads, 0, s>>>(a.rows, a.n_slices, a.slice_ptr.p, a.slice_w.p,
-                                             a.sell_col.p, a.sell_val.p, x, y, alpha);
+        SFEEC_SELL(false, false);
       break;
     default:
       if (accumulate)
@@ -278,6 +289,7 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
       else
         launch_vec<false>(a, x, y, alpha, s);
   }
+#undef SFEEC_SELL
   SFEEC_LAUNCH_CHECK();
 }
 

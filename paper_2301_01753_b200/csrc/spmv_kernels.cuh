@@ -6,14 +6,17 @@
 namespace sfeec_b200 {
 
 // Device copy of one operator. The CSR arrays are always kept (strict mode,
-// export); production mode may add a specialised layout:
-//   kSigned: every |value| equals one scalar (incidence matrices: +-1 for
-//            Whitney P1-, the tets' C); stored as sliced ELL, column-major in
-//            slices of 32 rows, one int32 per entry with the sign in the
-//            top bit (~col for negative) -> 4 B/entry instead of 12.
-//   kSell:   general values, sliced ELL (SELL-32) with per-slice width,
-//            fp64 value + int32 column, column-major inside a slice so a
-//            warp's loads are contiguous. Chosen when padding is small.
+// export); production mode adds a sliced layout when it pays:
+//   slices: runs of <= 32 consecutive rows of (nearly) equal length, chosen
+//           greedily from the row lengths (the tet numbering groups rows of
+//           one entity type, so slices are full and unpadded). Inside a slice
+//           entry k of row r sits at slice_ptr + k*rows_in_slice + (r - first
+//           row): one warp streams a slice with contiguous loads, one lane
+//           per row, no shuffles, rows summed in CSR order.
+//   kSigned: every |value| equals one scalar (incidence matrices: +-1 for the
+//            Whitney P1- curl); one int32 per entry, sign in the top bit
+//            (~col for negative) -> 4 B/entry instead of 12.
+//   kSell:   general values: fp64 value + int32 column per entry.
 struct DevOperator {
   enum Layout { kCsr = 0, kSigned = 1, kSell = 2 };
   int64_t rows = 0, cols = 0, nnz = 0;
@@ -22,16 +25,18 @@ struct DevOperator {
   DevBuf<double> val;
   int tpr = 1;  // threads per row for the CSR-vector kernel
   Layout layout = kCsr;
-  // sliced layouts
   int64_t n_slices = 0, sell_entries = 0;
-  DevBuf<int64_t> slice_ptr;  // start entry of each slice (n_slices + 1)
-  DevBuf<int32_t> slice_w;    // width of each slice
+  DevBuf<int64_t> slice_row;  // first row of each slice (n_slices + 1)
+  DevBuf<int64_t> slice_ptr;  // first entry of each slice (n_slices + 1)
+  DevBuf<int32_t> slice_w;    // width (entries per row) of each slice
   DevBuf<int32_t> sell_col;   // packed (signed) column indices
   DevBuf<double> sell_val;    // kSell only
   double scale = 1.0;         // kSigned: |value|
 
   void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
   void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
+  // algorithmic bytes of one application in this layout (arrays streamed once)
+  double stream_bytes() const;
 };
 
 void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s);

@@ -29,6 +29,41 @@ def gaussian(seed: int, n: int) -> np.ndarray:
     return np.sqrt(-2.0 * np.log1p(-u[0::2])) * np.cos(2.0 * np.pi * u[1::2])
 
 
+_GL3 = ((0.5 - 0.5 * np.sqrt(0.6), 5.0 / 18.0), (0.5, 8.0 / 18.0),
+        (0.5 + 0.5 * np.sqrt(0.6), 5.0 / 18.0))
+
+
+def pulse_params(seed: int, npulses: int = 1):
+    """Seeded centres x0 in [0.3, 0.7]^3 and unit polarisations p of the
+    Gaussian pulses (configs 3 and 5): u-stream entries 6k..6k+2 give x0,
+    Box-Muller normals 3k..3k+2 of stream seed+1 give p (normalised)."""
+    u = splitmix64_u01(seed, 6 * npulses)
+    g = gaussian(seed + 1, 3 * npulses)
+    out = []
+    for k in range(npulses):
+        x0 = 0.3 + 0.4 * u[6 * k:6 * k + 3]
+        p = g[3 * k:3 * k + 3]
+        out.append((x0, p / np.linalg.norm(p)))
+    return out
+
+
+def pulse_one_form(xyz, edge_vertices, seed: int, sigma: float = 0.1, npulses: int = 1):
+    """Canonical projection of A = sum_k exp(-|x - x0_k|^2 / (2 sigma^2)) p_k
+    onto edges: a_e = int_e A . dx, 3-point Gauss-Legendre along the edge
+    (the integral DOF of the P1 rule, reference form_space.cpp:410-429)."""
+    xa = xyz[edge_vertices[:, 0]]
+    xb = xyz[edge_vertices[:, 1]]
+    d = xb - xa
+    a = np.zeros(len(edge_vertices))
+    for x0, p in pulse_params(seed, npulses):
+        tang = d @ p
+        for s, w in _GL3:
+            x = xa + s * d
+            r2 = np.sum((x - x0) ** 2, axis=1)
+            a += w * np.exp(-r2 / (2.0 * sigma * sigma)) * tang
+    return a
+
+
 def uniform(seed: int, n: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
     """Rng(seed).uniform(lo, hi) x n (core.hpp:59)."""
     return lo + (hi - lo) * splitmix64_u01(seed, n)

@@ -285,6 +285,23 @@ class SplitScheme:
     def step_bytes(self) -> float:
         return L.lib().sfeec_dev_step_bytes(self._h)
 
+    def set_dt(self, dt: float) -> None:
+        L.check(L.lib().sfeec_dev_set_dt(self._h, float(dt)))
+        self._dt = float(dt)
+
+    def last_launches(self) -> int:
+        return int(L.lib().sfeec_dev_last_launches(self._h))
+
+    KERNEL_CLASSES = ("K-Q", "K-Cb", "K-CTe", "K-M2", "other")
+
+    def kernel_timing(self, enable: bool = True) -> dict:
+        """Per-kernel device time since the last call (then (dis)arm timing)."""
+        ms, n, by = np.zeros(5), np.zeros(5, np.int64), np.zeros(5)
+        L.check(L.lib().sfeec_dev_kernel_timing(self._h, 1 if enable else 0, L.dptr(ms),
+                                                L.i64ptr(n), L.dptr(by)))
+        return {k: {"ms": ms[i], "launches": int(n[i]), "bytes_per_launch": by[i]}
+                for i, k in enumerate(self.KERNEL_CLASSES)}
+
 
 class YeeScheme:
     """Lumped-mass SFEEC on an nx x ny x nz lattice (Q = I/dV, M2 = dV I).
