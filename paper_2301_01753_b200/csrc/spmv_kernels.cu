@@ -4,6 +4,7 @@
 // neighbour values, and enough loads in flight per SM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "spmv_kernels.cuh"
 
@@ -52,56 +53,83 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0 && row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
 }
 
-// ---- sliced layout: one warp per slice, one lane per row -----------------
-template <bool ACC, bool SIGNED>
-__global__ void __launch_bounds__(kThreads)
+// ---- sliced layout: persistent warps, one lane per row -------------------
+// Warp w processes slices w, w + W, w + 2W, ... (W = warps in the grid). The
+// metadata of the next slice and the y value of the current row (for the
+// accumulating form) are loaded before the current slice's entries, so the
+// only serialized memory round trips per slice are the ones of the entry
+// chunks: all column/value loads of a chunk of CH entries are issued before
+// any gather and all gathers before any FMA -> 2 * ceil(w / CH) round trips
+// per slice. Operator arrays are read once: streaming loads (ld.global.cs)
+// keep L1/L2 for the gathered vector.
+struct SliceMeta {
+  int64_t r0, ptr;
+  int nr, w;
+};
+
+__device__ __forceinline__ SliceMeta load_meta(const int64_t* __restrict__ srow,
+                                               const int64_t* __restrict__ sptr,
+                                               const int32_t* __restrict__ sw, int64_t s) {
+  SliceMeta m;
+  m.r0 = __ldg(srow + s);
+  m.nr = (int)(__ldg(srow + s + 1) - m.r0);
+  m.ptr = __ldg(sptr + s);
+  m.w = __ldg(sw + s);
+  return m;
+}
+
+template <bool ACC, bool SIGNED, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_sell(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
            const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
            const double* __restrict__ val, double scale, const double* __restrict__ x,
            double* __restrict__ y, double alpha) {
-  const int64_t slice = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (slice >= n_slices) return;
-  const int64_t r0 = __ldg(srow + slice);
-  const int nr = (int)(__ldg(srow + slice + 1) - r0);
-  if (lane >= nr) return;
-  const int64_t base = __ldg(sptr + slice) + lane;
-  const int w = __ldg(sw + slice);
-  double acc = 0.0;
-  // Chunks of CH entries: all column/value loads of a chunk are issued
-  // before any gather and all gathers before any FMA, so a row costs
-  // 2 * ceil(w / CH) memory round trips instead of 2 w (the compiler will
-  // not reorder a plain loop that way). Operator arrays are read once:
-  // streaming loads (ld.global.cs) keep L1/L2 for the gathered vector.
-  constexpr int CH = 8;
-  for (int k0 = 0; k0 < w; k0 += CH) {
-    int32_t p[CH];
-    double v[CH], xv[CH];
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_slices) return;
+  SliceMeta m = load_meta(srow, sptr, sw, s);
+  while (true) {
+    const int64_t sn = s + nwarps;
+    SliceMeta mn;
+    if (sn < n_slices) mn = load_meta(srow, sptr, sw, sn);
+    if (lane < m.nr) {
+      const int64_t row = m.r0 + lane;
+      const double y0 = ACC ? y[row] : 0.0;
+      const int64_t base = m.ptr + lane;
+      double acc = 0.0;
+      for (int k0 = 0; k0 < m.w; k0 += CH) {
+        int32_t p[CH];
+        double v[CH], xv[CH];
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const bool ok = k0 + j < w;
-      const int64_t o = base + (int64_t)(k0 + j) * nr;
-      p[j] = ok ? __ldcs(col + o) : kPad;
-      if (!SIGNED) v[j] = ok ? __ldcs(val + o) : 0.0;
-    }
+        for (int j = 0; j < CH; ++j) {
+          const bool ok = k0 + j < m.w;
+          const int64_t o = base + (int64_t)(k0 + j) * m.nr;
+          p[j] = ok ? __ldcs(col + o) : kPad;
+          if (!SIGNED) v[j] = ok ? __ldcs(val + o) : 0.0;
+        }
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      if (SIGNED) {
-        xv[j] = p[j] != kPad ? __ldg(x + (p[j] < 0 ? ~p[j] : p[j])) : 0.0;
-      } else {
-        xv[j] = p[j] != kPad ? __ldg(x + p[j]) : 0.0;
+        for (int j = 0; j < CH; ++j) {
+          if (SIGNED)
+            xv[j] = p[j] != kPad ? __ldg(x + (p[j] < 0 ? ~p[j] : p[j])) : 0.0;
+          else
+            xv[j] = p[j] != kPad ? __ldg(x + p[j]) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          if (SIGNED)
+            acc += p[j] < 0 ? -xv[j] : xv[j];
+          else
+            acc = fma(v[j], xv[j], acc);
+        }
       }
+      const double r = SIGNED ? scale * acc : acc;
+      y[row] = ACC ? fma(alpha, r, y0) : r;
     }
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      if (SIGNED)
-        acc += p[j] < 0 ? -xv[j] : xv[j];
-      else
-        acc = fma(v[j], xv[j], acc);
-    }
+    if (sn >= n_slices) break;
+    s = sn;
+    m = mn;
   }
-  const double r = SIGNED ? scale * acc : acc;
-  y[r0 + lane] = ACC ? fma(alpha, r, y[r0 + lane]) : r;
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha,
@@ -284,11 +312,29 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
     return;
   }
-  unsigned g = blocks_for(a.n_slices * 32);
-#define SFEEC_SELL(ACC, SG)                                                               \
-  k_sell<ACC, SG><<<g, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,       \
-                                         a.slice_w.p, a.sell_col.p, a.sell_val.p, a.scale, x, \
-                                         y, alpha)
+  // persistent grid sized to the residency of the chosen variant (148 SMs x
+  // MINB CTAs of 8 warps); one warp per slice per iteration.
+  // SFEEC_SELL_VARIANT selects (CH, MINB) for tuning: 0 -> (8,3), 1 -> (4,4), 2 -> (6,4)
+  const char* venv = std::getenv("SFEEC_SELL_VARIANT");
+  const int variant = venv ? std::atoi(venv) : 0;
+  auto grid_for = [&](int minb) {
+    return (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * minb);
+  };
+#define SFEEC_SELL_V(ACC, SG, CH, MB)                                                     \
+  k_sell<ACC, SG, CH, MB><<<grid_for(MB), kThreads, 0, s>>>(                             \
+      a.n_slices, a.slice_row.p, a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p,  \
+      a.scale, x, y, alpha)
+#define SFEEC_SELL(ACC, SG)                 \
+  do {                                      \
+    if (SG)                                 \
+      SFEEC_SELL_V(ACC, SG, 4, 4);          \
+    else if (variant == 1)                  \
+      SFEEC_SELL_V(ACC, SG, 4, 4);          \
+    else if (variant == 2)                  \
+      SFEEC_SELL_V(ACC, SG, 6, 4);          \
+    else                                    \
+      SFEEC_SELL_V(ACC, SG, 8, 3);          \
+  } while (0)
   switch (a.layout) {
     case DevOperator::kSigned:
       if (accumulate)
@@ -309,6 +355,7 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         launch_vec<false>(a, x, y, alpha, s);
   }
 #undef SFEEC_SELL
+#undef SFEEC_SELL_V
   SFEEC_LAUNCH_CHECK();
 }
 
