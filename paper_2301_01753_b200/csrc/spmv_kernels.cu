@@ -316,7 +316,9 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   // MINB CTAs of 8 warps); one warp per slice per iteration.
   // SFEEC_SELL_VARIANT selects (CH, MINB) for tuning: 0 -> (8,3), 1 -> (4,4), 2 -> (6,4)
   const char* venv = std::getenv("SFEEC_SELL_VARIANT");
-  const int variant = venv ? std::atoi(venv) : 0;
+  const int variant = venv ? std::atoi(venv) : 1;
+  const char* senv = std::getenv("SFEEC_SELL_SVARIANT");
+  const int svariant = senv ? std::atoi(senv) : 0;
   auto grid_for = [&](int minb) {
     return (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * minb);
   };
@@ -326,12 +328,21 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
       a.scale, x, y, alpha)
 #define SFEEC_SELL(ACC, SG)                 \
   do {                                      \
-    if (SG)                                 \
-      SFEEC_SELL_V(ACC, SG, 4, 4);          \
-    else if (variant == 1)                  \
+    if (SG) {                               \
+      if (svariant == 1)                    \
+        SFEEC_SELL_V(ACC, SG, 4, 6);        \
+      else if (svariant == 2)               \
+        SFEEC_SELL_V(ACC, SG, 2, 8);        \
+      else if (svariant == 3)               \
+        SFEEC_SELL_V(ACC, SG, 8, 4);        \
+      else                                  \
+        SFEEC_SELL_V(ACC, SG, 4, 4);        \
+    } else if (variant == 1)                \
       SFEEC_SELL_V(ACC, SG, 4, 4);          \
     else if (variant == 2)                  \
-      SFEEC_SELL_V(ACC, SG, 6, 4);          \
+      SFEEC_SELL_V(ACC, SG, 4, 5);          \
+    else if (variant == 3)                  \
+      SFEEC_SELL_V(ACC, SG, 2, 8);          \
     else                                    \
       SFEEC_SELL_V(ACC, SG, 8, 3);          \
   } while (0)
