@@ -117,6 +117,11 @@ int sfeec_dev_cfl_number(sfeec_dev* h, double* out);
 int sfeec_dev_q_sym(sfeec_dev* h, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx,
                     double* val);
 
+/* y = A x on the device (replaces spmv, sparse.cpp:96-104): stored-order
+ * accumulation without FMA, bitwise the reference's result. Stages A per
+ * call; the leapfrog keeps its operators resident instead. */
+int sfeec_spmv(const sfeec_csr* a, const double* x, double* y, int device);
+
 /* device-resident access for benchmarks / multi-GPU plumbing */
 int sfeec_dev_set_stream(sfeec_dev* h, void* cuda_stream);
 int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e);

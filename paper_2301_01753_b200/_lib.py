@@ -76,6 +76,7 @@ _SIGS = {
     "sfeec_dev_gauss_residual": (C.c_int, [_P, _PD]),
     "sfeec_dev_cfl_number": (C.c_int, [_P, _PD]),
     "sfeec_dev_q_sym": (C.c_int, [_P, _PI64, _PI64, _PI32, _PD]),
+    "sfeec_spmv": (C.c_int, [C.POINTER(sfeec_csr), _PD, _PD, C.c_int]),
     "sfeec_dev_set_stream": (C.c_int, [_P, _P]),
     "sfeec_dev_state_device_ptrs": (C.c_int, [_P, C.POINTER(_PD), C.POINTER(_PD)]),
     "sfeec_dev_last_launches": (C.c_int64, [_P]),

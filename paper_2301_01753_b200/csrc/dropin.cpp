@@ -1,0 +1,339 @@
+// The C++ drop-in (include/sfeec/{sparse,dynamics}.hpp) over the C ABI.
+// Mirrors the reference's classes (sparse.hpp:14-66, dynamics.hpp:9-76) and
+// error contract (InvalidParameter for bad parameters, std::runtime_error for
+// device failures). Setup helpers run on the host; every SpMV and every
+// step runs on the B200.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.hpp"
+#include "sfeec/dynamics.hpp"
+
+namespace sfeec {
+
+namespace {
+
+void check(int code) {
+  if (code == SFEEC_OK) return;
+  if (code == SFEEC_EINVAL) throw InvalidParameter(sfeec_last_error());
+  throw std::runtime_error(std::string("sfeec_b200: ") + sfeec_last_error());
+}
+
+// int32 reference CSR <-> int64 C-ABI view
+struct View {
+  std::vector<int64_t> rp;
+  sfeec_csr v;
+  explicit View(const SparseOperator& a) : rp(a.row_ptr.begin(), a.row_ptr.end()) {
+    if (rp.empty()) rp.assign((size_t)a.rows + 1, 0);
+    v.rows = a.rows;
+    v.cols = a.cols;
+    v.row_ptr = rp.data();
+    v.col_idx = a.col_idx.data();
+    v.val = a.val.data();
+  }
+};
+
+SparseOperator from_host(const sfeec_b200::HostCSR& h, bool symmetric) {
+  if (h.nnz() > INT32_MAX || h.rows > INT32_MAX)
+    throw InvalidParameter("operator exceeds the int32 SparseOperator (use the C ABI)");
+  SparseOperator m;
+  m.rows = (int)h.rows;
+  m.cols = (int)h.cols;
+  m.symmetric = symmetric;
+  m.row_ptr.assign(h.row_ptr.begin(), h.row_ptr.end());
+  m.col_idx.assign(h.col_idx.begin(), h.col_idx.end());
+  m.val = h.val;
+  return m;
+}
+
+sfeec_b200::HostCSR to_host(const SparseOperator& a) {
+  sfeec_b200::HostCSR h;
+  h.rows = a.rows;
+  h.cols = a.cols;
+  h.row_ptr.assign(a.row_ptr.begin(), a.row_ptr.end());
+  if (h.row_ptr.empty()) h.row_ptr.assign((size_t)a.rows + 1, 0);
+  h.col_idx.assign(a.col_idx.begin(), a.col_idx.end());
+  h.val = a.val;
+  return h;
+}
+
+}  // namespace
+
+double SparseOperator::at(int r, int c) const {
+  auto cs = row_cols(r);
+  auto it = std::lower_bound(cs.begin(), cs.end(), c);
+  if (it == cs.end() || *it != c) return 0.0;
+  return row_vals(r)[(size_t)(it - cs.begin())];
+}
+
+SparseOperator operator_from_triplets(int rows, int cols, std::vector<Triplet> triplets,
+                                      bool symmetric) {
+  std::vector<int32_t> r(triplets.size()), c(triplets.size());
+  std::vector<double> v(triplets.size());
+  for (size_t i = 0; i < triplets.size(); ++i) {
+    r[i] = triplets[i].r;
+    c[i] = triplets[i].c;
+    v[i] = triplets[i].v;
+  }
+  try {
+    return from_host(sfeec_b200::csr_from_triplets(rows, cols, (int64_t)triplets.size(),
+                                                    r.data(), c.data(), v.data()),
+                     symmetric);
+  } catch (const sfeec_b200::Error& e) {
+    throw InvalidParameter(e.what());
+  }
+}
+
+SparseOperator scaled_identity(int n, double s) {
+  SparseOperator m;
+  m.rows = m.cols = n;
+  m.symmetric = true;
+  m.row_ptr.resize((size_t)n + 1);
+  m.col_idx.resize((size_t)n);
+  m.val.assign((size_t)n, s);
+  for (int i = 0; i <= n; ++i) m.row_ptr[(size_t)i] = i;
+  for (int i = 0; i < n; ++i) m.col_idx[(size_t)i] = i;
+  return m;
+}
+
+SparseOperator transpose(const SparseOperator& a) {
+  return from_host(sfeec_b200::csr_transpose(to_host(a)), a.symmetric);
+}
+
+void spmv(const SparseOperator& a, const double* x, double* y) {
+  View v(a);
+  check(sfeec_spmv(&v.v, x, y, 0));
+}
+
+void spmv_serial(const SparseOperator& a, const double* x, double* y) { spmv(a, x, y); }
+
+std::vector<double> matvec(const SparseOperator& a, const std::vector<double>& x) {
+  if ((int)x.size() != a.cols) throw InvalidParameter("spmv: dimension mismatch");
+  std::vector<double> y((size_t)a.rows);
+  spmv(a, x.data(), y.data());
+  return y;
+}
+
+double max_abs(const SparseOperator& a) {
+  double m = 0;
+  for (double v : a.val) m = std::max(m, std::abs(v));
+  return m;
+}
+
+double max_asymmetry(const SparseOperator& a) {
+  if (a.rows != a.cols) throw InvalidParameter("max_asymmetry: square only");
+  double m = 0;
+  for (int r = 0; r < a.rows; ++r) {
+    auto cs = a.row_cols(r);
+    auto vs = a.row_vals(r);
+    for (size_t k = 0; k < cs.size(); ++k) m = std::max(m, std::abs(vs[k] - a.at(cs[k], r)));
+  }
+  return m;
+}
+
+std::vector<double> to_dense(const SparseOperator& a) {
+  std::vector<double> d((size_t)a.rows * (size_t)a.cols, 0.0);
+  for (int r = 0; r < a.rows; ++r) {
+    auto cs = a.row_cols(r);
+    auto vs = a.row_vals(r);
+    for (size_t k = 0; k < cs.size(); ++k) d[(size_t)r * (size_t)a.cols + (size_t)cs[k]] = vs[k];
+  }
+  return d;
+}
+
+// ---- SplitScheme ------------------------------------------------------------
+namespace {
+SparseOperator symmetric_part(const SparseOperator& q) {
+  if (q.rows != q.cols) throw InvalidParameter("SplitScheme: Q must be square");
+  return from_host(sfeec_b200::csr_symmetric_part(to_host(q)), true);
+}
+}  // namespace
+
+SplitScheme::SplitScheme(SplitKind kind, double dt, const SparseOperator& q,
+                         const SparseOperator& c, const SparseOperator& m2, UnitSystem units,
+                         const SparseOperator* div, bool warn_cfl)
+    : kind_(kind),
+      dt_(dt),
+      units_(units),
+      q_sym_(symmetric_part(q)),
+      c_(c),
+      ct_(transpose(c)),
+      m2_(m2),
+      warn_cfl_(warn_cfl) {
+  if (!(dt >= 0)) throw InvalidParameter("SplitScheme: dt must be >= 0");
+  if (m2_.rows != c_.rows || q_sym_.rows != c_.cols)
+    throw InvalidParameter("SplitScheme: operator dimensions inconsistent");
+  if (div) div_ = *div;
+}
+
+SplitScheme::~SplitScheme() {
+  for (auto& h : dev_)
+    if (h) sfeec_dev_destroy(h);
+}
+
+SplitScheme::SplitScheme(SplitScheme&& o) noexcept
+    : kind_(o.kind_),
+      dt_(o.dt_),
+      units_(o.units_),
+      q_sym_(std::move(o.q_sym_)),
+      c_(std::move(o.c_)),
+      ct_(std::move(o.ct_)),
+      m2_(std::move(o.m2_)),
+      div_(std::move(o.div_)),
+      warn_cfl_(o.warn_cfl_),
+      warned_(o.warned_) {
+  dev_[0] = o.dev_[0];
+  dev_[1] = o.dev_[1];
+  o.dev_[0] = o.dev_[1] = nullptr;
+}
+
+SplitScheme& SplitScheme::operator=(SplitScheme&& o) noexcept {
+  if (this != &o) {
+    this->~SplitScheme();
+    new (this) SplitScheme(std::move(o));
+  }
+  return *this;
+}
+
+sfeec_dev* SplitScheme::device(Formulation f) const {
+  const int i = f == Formulation::BE ? 1 : 0;
+  if (!dev_[i]) {
+    View q(q_sym_), c(c_), m(m2_);
+    std::optional<View> d;
+    if (div_) d.emplace(*div_);
+    check(sfeec_dev_create(&q.v, &c.v, &m.v, d ? &d->v : nullptr, dt_, units_.eps0, units_.mu0,
+                           kind_ == SplitKind::Strang ? SFEEC_SPLIT_STRANG
+                                                      : SFEEC_SPLIT_LIE_TROTTER,
+                           i == 1 ? SFEEC_FORM_BE : SFEEC_FORM_AE, 0,
+                           SFEEC_Q_IS_SYMMETRIC | SFEEC_NO_CFL_WARN, &dev_[i]));
+  }
+  return dev_[i];
+}
+
+void SplitScheme::load(sfeec_dev* h, const FieldState& s) const {
+  check(sfeec_dev_set_state(h, s.first.data(), (int64_t)s.first.size(), s.e.data(),
+                            (int64_t)s.e.size(), s.time));
+}
+
+void SplitScheme::fetch(sfeec_dev* h, FieldState& s) const {
+  double t = 0;
+  check(sfeec_dev_get_state(h, s.first.data(), s.e.data(), &t));
+  s.time = t;
+}
+
+void SplitScheme::flow_he(FieldState& s, double dt) const {
+  sfeec_dev* h = device(s.formulation);
+  double t = s.time;
+  load(h, s);
+  check(sfeec_dev_flow_he(h, dt));
+  fetch(h, s);
+  s.time = t;
+}
+
+void SplitScheme::flow_ha(FieldState& s, double dt) const {
+  sfeec_dev* h = device(s.formulation);
+  double t = s.time;
+  load(h, s);
+  check(sfeec_dev_flow_ha(h, dt));
+  fetch(h, s);
+  s.time = t;
+}
+
+FieldState SplitScheme::step(const FieldState& s) const { return advance(s, 1); }
+
+FieldState SplitScheme::advance(const FieldState& s, std::int64_t nsteps) const {
+  if (warn_cfl_ && !warned_) {  // dynamics.cpp:70-78
+    warned_ = true;
+    double nu = cfl_number();
+    if (nu > 2.0)
+      std::fprintf(stderr,
+                   "sfeec: warning: CFL number %.3g > 2; the splitting is likely unstable at "
+                   "dt = %.3g\n",
+                   nu, dt_);
+  }
+  sfeec_dev* h = device(s.formulation);
+  FieldState out = s;
+  load(h, out);
+  check(sfeec_dev_advance(h, nsteps));
+  fetch(h, out);
+  return out;
+}
+
+double SplitScheme::energy(const FieldState& s) const {
+  sfeec_dev* h = device(s.formulation);
+  load(h, s);
+  double e = 0;
+  check(sfeec_dev_energy(h, &e));
+  return e;
+}
+
+double SplitScheme::gauss_residual(const FieldState& s) const {
+  if (s.formulation != Formulation::BE)
+    throw InvalidParameter("gauss_residual: (b, e) formulation required");
+  sfeec_dev* h = device(s.formulation);
+  load(h, s);
+  double g = 0;
+  check(sfeec_dev_gauss_residual(h, &g));
+  return g;
+}
+
+double SplitScheme::cfl_number() const {
+  sfeec_dev* h = dev_[1] ? dev_[1] : device(Formulation::AE);
+  double nu = 0;
+  check(sfeec_dev_cfl_number(h, &nu));
+  return nu;
+}
+
+FieldState make_state(Formulation f, std::vector<double> first, std::vector<double> e,
+                      double time) {
+  FieldState s;
+  s.formulation = f;
+  s.first = std::move(first);
+  s.e = std::move(e);
+  s.time = time;
+  return s;
+}
+
+// dynamics.cpp:145-185 restated over the device step
+double symplectic_check(const SplitScheme& scheme, int n1, int max_dofs) {
+  if (2 * n1 > max_dofs)
+    throw InvalidParameter("symplectic_check: system too large for the dense check");
+  const int n2 = 2 * n1;
+  std::vector<std::vector<double>> phi((size_t)n2);
+  for (int j = 0; j < n2; ++j) {
+    FieldState s;
+    s.formulation = Formulation::AE;
+    s.first.assign((size_t)n1, 0.0);
+    s.e.assign((size_t)n1, 0.0);
+    if (j < n1)
+      s.first[(size_t)j] = 1.0;
+    else
+      s.e[(size_t)(j - n1)] = 1.0;
+    FieldState t = scheme.step(s);
+    auto& col = phi[(size_t)j];
+    col.resize((size_t)n2);
+    for (int i = 0; i < n1; ++i) col[(size_t)i] = t.first[(size_t)i];
+    for (int i = 0; i < n1; ++i) col[(size_t)(n1 + i)] = t.e[(size_t)i];
+  }
+  const double se = 1.0 / scheme.units().eps0;
+  double dev = 0;
+  for (int i = 0; i < n2; ++i) {
+    const auto& ci = phi[(size_t)i];
+    for (int j = 0; j < n2; ++j) {
+      const auto& cj = phi[(size_t)j];
+      double acc = 0;
+      for (int k = 0; k < n1; ++k)
+        acc += ci[(size_t)k] * (-se * cj[(size_t)(n1 + k)]) +
+               ci[(size_t)(n1 + k)] * (se * cj[(size_t)k]);
+      double target = 0;
+      if (j == i + n1) target = -se;
+      if (i == j + n1) target = se;
+      dev = std::max(dev, std::abs(acc - target));
+    }
+  }
+  return dev;
+}
+
+}  // namespace sfeec

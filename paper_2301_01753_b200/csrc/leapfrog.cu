@@ -430,6 +430,32 @@ int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e) {
 
 int64_t sfeec_dev_last_launches(sfeec_dev* h) { return h ? h->d.launches : -1; }
 
+// spmv (sparse.cpp:96-104) on the device: stored-order accumulation, no FMA,
+// so y is bitwise the reference's. Stages the operator per call.
+int sfeec_spmv(const sfeec_csr* a, const double* x, double* y, int device) {
+  return guarded([&] {
+    require(a && (a->cols == 0 || x) && (a->rows == 0 || y), "null argument");
+    csr_validate(*a, "A");
+    select_device(device);
+    cudaStream_t s;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct Guard {
+      cudaStream_t s;
+      ~Guard() { cudaStreamDestroy(s); }
+    } guard{s};
+    DevOperator op;
+    op.upload(csr_from_view(*a), true, s);
+    DevBuf<double> dx, dy;
+    dx.upload(x, (size_t)a->cols, s);
+    dy.alloc((size_t)a->rows);
+    launch_spmv_strict(op, dx.p, dy.p, s);
+    if (a->rows)
+      SFEEC_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * (size_t)a->rows,
+                                 cudaMemcpyDeviceToHost, s));
+    SFEEC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int sfeec_dev_set_dt(sfeec_dev* h, double dt) {
   return guarded([&] {
     require(h, "null handle");
