@@ -174,6 +174,36 @@ int64_t sfeec_yee_last_launches(sfeec_yee* h);
 int sfeec_yee_kernel_timing(sfeec_yee* h, int enable, double* ms_total, int64_t* launches);
 double sfeec_yee_step_bytes(sfeec_yee* h);
 
+/* ---- multi-GPU: z-slab decomposition of the PEC Yee lattice -------------- */
+/* Slab r of nranks owns global planes [r*nz/nranks, (r+1)*nz/nranks) (the last
+ * slab also the top wall plane) plus one ghost plane below and above. After
+ * every kernel of the step the ghosts are refreshed over NCCL: plane 1 (E, B)
+ * goes to rank-1, the top owned B plane to rank+1. The state of
+ * a slab is passed in its local numbering; sfeec_yee_slab_dof_map gives the
+ * local -> global DOF ids. sfeec_yee_energy on a slab returns its own part. */
+int sfeec_nccl_unique_id(void* out128);
+int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                          double eps0, double mu0, int precision, int rank, int nranks,
+                          const void* nccl_id /* 128 bytes from rank 0 */, int device,
+                          sfeec_yee** out);
+int sfeec_yee_slab_dof_counts(int nx, int ny, int nz, int rank, int nranks, int64_t* n_edges,
+                              int64_t* n_faces);
+int sfeec_yee_slab_dof_map(int nx, int ny, int nz, int rank, int nranks, int64_t* edge_map,
+                           int64_t* face_map);
+/* All slabs of one lattice on ONE device, ghosts exchanged by device copies:
+ * the multi-rank kernels and ghost logic, verifiable with a single GPU.
+ * State in the single-domain PEC numbering. */
+typedef struct sfeec_yee_group sfeec_yee_group;
+int sfeec_yee_group_create(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                           double eps0, double mu0, int precision, int nranks, int device,
+                           sfeec_yee_group** out);
+void sfeec_yee_group_destroy(sfeec_yee_group* h);
+int sfeec_yee_group_set_variant(sfeec_yee_group* h, int variant);
+int sfeec_yee_group_set_state(sfeec_yee_group* h, const double* b, const double* e);
+int sfeec_yee_group_get_state(sfeec_yee_group* h, double* b, double* e);
+int sfeec_yee_group_advance(sfeec_yee_group* h, int64_t nsteps);
+int sfeec_yee_group_energy(sfeec_yee_group* h, double* out);
+
 /* ---- host operator builders (setup, not timed) ---------------------------- */
 /* Lumped Yee operators in the sfeec_yee DOF numbering: C (faces x edges,
  * +-1/spacing), and the divergence D (cells x faces). Replaces

@@ -14,7 +14,11 @@ from .scheme import (  # noqa: F401
     UnitSystem,
     make_pattern,
     spai_approximate_inverse,
+    YeeGroup,
     YeeScheme,
+    YeeSlab,
+    nccl_unique_id,
+    yee_slab_dofs,
     device_count,
     make_state,
     operator_from_triplets,

@@ -99,7 +99,23 @@ _SIGS = {
     "sfeec_yee_last_launches": (C.c_int64, [_P]),
     "sfeec_yee_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64]),
     "sfeec_yee_step_bytes": (C.c_double, [_P]),
-    "sfeec_build_yee_curl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+    "sfeec_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "sfeec_yee_create_slab": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                        C.c_double, C.c_double, C.c_double, C.c_double,
+                                        C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                        C.POINTER(_P)]),
+    "sfeec_yee_slab_dof_counts": (C.c_int, [C.c_int] * 5 + [_PI64, _PI64]),
+    "sfeec_yee_slab_dof_map": (C.c_int, [C.c_int] * 5 + [_PI64, _PI64]),
+    "sfeec_yee_group_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.c_double, C.c_double, C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "sfeec_yee_group_destroy": (None, [_P]),
+    "sfeec_yee_group_set_variant": (C.c_int, [_P, C.c_int]),
+    "sfeec_yee_group_set_state": (C.c_int, [_P, _PD, _PD]),
+    "sfeec_yee_group_get_state": (C.c_int, [_P, _PD, _PD]),
+    "sfeec_yee_group_advance": (C.c_int, [_P, C.c_int64]),
+    "sfeec_yee_group_energy": (C.c_int, [_P, _PD]),
+    "sfeec_build_yee_curl":(C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),
     "sfeec_tetmesh_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(_P)]),

@@ -22,11 +22,13 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <vector>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include "device_util.cuh"
+#include "nccl_loader.hpp"
 #include "yee_layout.hpp"
 
 namespace sfeec_b200 {
@@ -46,10 +48,15 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// DOF masks in storage coordinates (PEC), yee_layout.hpp
-__device__ __forceinline__ bool e_dof(const YeeGeom& g, int a, int i, int j, int k) {
+// DOF masks (PEC), yee_layout.hpp. k is the local storage plane; the masks
+// are evaluated at the global plane k + kofs, and only owned planes count.
+__device__ __forceinline__ bool owned(const YeeGeom& g, int k) {
+  return k >= g.kown_lo && k < g.kown_hi;
+}
+__device__ __forceinline__ bool e_dof(const YeeGeom& g, int a, int i, int j, int kl) {
+  if (!owned(g, kl)) return false;
   if (g.bc == 0) return true;
-  const int c[3] = {i, j, k};
+  const int c[3] = {i, j, kl + g.kofs};
   for (int d = 0; d < 3; ++d) {
     if (d == a) {
       if (c[d] < 0 || c[d] >= g.n[d]) return false;
@@ -59,8 +66,9 @@ __device__ __forceinline__ bool e_dof(const YeeGeom& g, int a, int i, int j, int
   }
   return true;
 }
-__device__ __forceinline__ bool b_dof(const YeeGeom& g, int a, int i, int j, int k) {
-  const int c[3] = {i, j, k};
+__device__ __forceinline__ bool b_dof(const YeeGeom& g, int a, int i, int j, int kl) {
+  if (!owned(g, kl)) return false;
+  const int c[3] = {i, j, kl + g.kofs};
   for (int d = 0; d < 3; ++d) {
     int hi = (g.bc == 0 || d != a) ? g.n[d] - 1 : g.n[d];
     if (c[d] < 0 || c[d] > hi) return false;
@@ -296,7 +304,7 @@ template <class T, int TX, int TY, int NS>
 __global__ void __launch_bounds__(TX* TY)
     k_fused_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                 YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
-                int n_units) {
+                int n_units, int kbeg, int kend) {
   using Cfg = TmaCfg<T, TX, TY, NS>;
   constexpr int D = Cfg::kD;
   constexpr int BWB = Cfg::kBWB, BWE = Cfg::kBWE, OFF = Cfg::kOff;
@@ -332,7 +340,9 @@ __global__ void __launch_bounds__(TX* TY)
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
     const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
-    const int k0 = chunk * kchunk, k1 = min(k0 + kchunk, n2);
+    // local planes [kbeg, kend) are swept (single domain: [0, n); slab: the
+    // owned planes between the ghosts); masks use the global plane kk + kofs
+    const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
     const int P = k1 - k0 + 2;  // local planes p <-> z = k0 - 1 + p
     // (i, j) parts of the PEC DOF masks (yee_layout.hpp) and write permissions
     uint32_t m[2];
@@ -375,7 +385,8 @@ __global__ void __launch_bounds__(TX* TY)
 #define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BWB + (x)]
 #define EC(c, y, x) Ec[((c) * (TY + 1) + (y)) * BWE + (x)]
 #define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
-      const bool kin = kk >= 1 && kk <= n2 - 1, kz = kk < n2, kw = kk < k1;
+      const int kg = kk + g.kofs;
+      const bool kin = kg >= 1 && kg <= n2 - 1, kz = kg < n2, kw = kk < k1;
       // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -449,6 +460,13 @@ __global__ void k_gather(YeeGeom g, bool face, double* __restrict__ dst, int64_t
 
 }  // namespace
 
+// One state-modifying kernel of the step sequence; the multi-slab paths
+// exchange ghost planes after every phase.
+struct Phase {
+  int kind;  // 0 b-kick(h1), 1 e-kick(h1), 2 fused e-kick(h1) + b-kick(h2)
+  double h1, h2;
+};
+
 struct YeeDev {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -473,12 +491,19 @@ struct YeeDev {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   double kernel_ms = 0;
   int64_t kernel_launches = 0;
+  // z-slab decomposition (yee_layout.hpp make_yee_slab)
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
 
   ~YeeDev() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (comm) Nccl::get().comm_destroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
+
+  bool slab() const { return nranks > 1; }
+  int64_t plane() const { return (int64_t)g.P0 * g.S[1]; }
 
   template <class T>
   Fields<T> fields(int which) const {
@@ -571,109 +596,174 @@ struct YeeDev {
   void fused_tma(double h_e, double h_b) {
     if (!have_maps) make_maps<T>();
     using Cfg = TmaCfg<T, kTX, kTY, kNS>;
+    // sweep the owned planes: [0, n) on one domain, [1, nzl + 1) on a slab
+    const int kbeg = slab() ? 1 : 0;
+    const int kend = slab() ? g.S[2] - 1 : g.n[2];
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
-    const int nchunks = (g.n[2] + kChunk - 1) / kChunk;
+    const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
     const int grid = std::min(n_units, tma_blocks);
     k_fused_tma<T, kTX, kTY, kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
-        ntx, ntx * nty, n_units);
+        ntx, ntx * nty, n_units, kbeg, kend);
     SFEEC_LAUNCH_CHECK();
     cur ^= 1;
     ++launches;
   }
 
-  template <class T>
-  void advance_t(int64_t n) {
-    bkick<T>(0.5 * dt);
+  // Strang with merged half-kicks: b(dt/2), n-1 x [e(dt) b(dt)], e(dt), b(dt/2)
+  std::vector<Phase> plan(int64_t n) const {
+    std::vector<Phase> p;
+    if (n <= 0) return p;
     const bool use_fused = variant >= 1 && g.bc == SFEEC_BC_PEC;
-    const bool t = timing && n > 1;
-    if (t) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
+    p.push_back({0, 0.5 * dt, 0});
     for (int64_t s = 0; s + 1 < n; ++s) {
-      if (use_fused && variant == 2) {
-        fused_tma<T>(dt, dt);
-      } else if (use_fused) {
-        fused<T>(dt, dt);
+      if (use_fused) {
+        p.push_back({2, dt, dt});
       } else {
-        ekick<T>(dt);
-        bkick<T>(dt);
+        p.push_back({1, dt, 0});
+        p.push_back({0, dt, 0});
       }
     }
-    if (t) {
-      SFEEC_CUDA(cudaEventRecord(ev[1], stream));
-      SFEEC_CUDA(cudaEventSynchronize(ev[1]));
-      float ms = 0;
-      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-      kernel_ms += ms;
-      kernel_launches += (n - 1) * (use_fused ? 1 : 2);
+    p.push_back({1, dt, 0});
+    p.push_back({0, 0.5 * dt, 0});
+    return p;
+  }
+
+  template <class T>
+  void run_t(const Phase& p) {
+    if (p.kind == 0)
+      bkick<T>(p.h1);
+    else if (p.kind == 1)
+      ekick<T>(p.h1);
+    else if (variant == 2 || slab())
+      fused_tma<T>(p.h1, p.h2);
+    else
+      fused<T>(p.h1, p.h2);
+  }
+  void run(const Phase& p) {
+    if (prec == 8)
+      run_t<double>(p);
+    else
+      run_t<float>(p);
+  }
+
+  // ghost-plane exchange over NCCL (one process per GPU): local plane 1 (E and
+  // B) goes down into the lower neighbour's top ghost; the top owned B plane
+  // goes up into the upper neighbour's bottom ghost. Planes are contiguous in
+  // every component array, so no packing.
+  void exchange_nccl() {
+    if (!slab() || !comm) return;
+    const Nccl& nc = Nccl::get();
+    const ncclDataType_t ty = prec == 8 ? ncclFloat64 : ncclFloat32;
+    const size_t cnt = (size_t)plane();
+    char* base = buf[cur].p;
+    auto at = [&](int comp, int pl) {
+      return base + ((size_t)comp * (size_t)g.npts() + (size_t)pl * cnt) * (size_t)prec;
+    };
+    const int top_owned = g.S[2] - 2, top_ghost = g.S[2] - 1;
+    nc.check(nc.group_start(), "ncclGroupStart");
+    if (rank > 0) {
+      for (int c = 0; c < 6; ++c) nc.check(nc.send(at(c, 1), cnt, ty, rank - 1, comm, stream), "ncclSend");
+      for (int c = 3; c < 6; ++c) nc.check(nc.recv(at(c, 0), cnt, ty, rank - 1, comm, stream), "ncclRecv");
     }
-    ekick<T>(dt);
-    bkick<T>(0.5 * dt);
+    if (rank < nranks - 1) {
+      for (int c = 0; c < 6; ++c)
+        nc.check(nc.recv(at(c, top_ghost), cnt, ty, rank + 1, comm, stream), "ncclRecv");
+      for (int c = 3; c < 6; ++c)
+        nc.check(nc.send(at(c, top_owned), cnt, ty, rank + 1, comm, stream), "ncclSend");
+    }
+    nc.check(nc.group_end(), "ncclGroupEnd");
   }
 
   void advance(int64_t n) {
     launches = 0;
     if (n <= 0) return;
-    if (prec == 8)
-      advance_t<double>(n);
-    else
-      advance_t<float>(n);
+    auto p = plan(n);
+    const bool t = timing && n > 1;
+    for (size_t i = 0; i < p.size(); ++i) {
+      if (t && i == 1) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
+      if (t && i + 2 == p.size()) SFEEC_CUDA(cudaEventRecord(ev[1], stream));
+      run(p[i]);
+      exchange_nccl();
+    }
+    if (t) {
+      SFEEC_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0;
+      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      kernel_ms += ms;
+      kernel_launches += (int64_t)p.size() - 3;
+    }
     for (int64_t s = 0; s < n; ++s) time = time + dt;
   }
 
   void flow_he(double h) {
     launches = 0;
-    if (prec == 8)
-      bkick<double>(h);
-    else
-      bkick<float>(h);
+    run({0, h, 0});
+    exchange_nccl();
   }
   void flow_ha(double h) {
     launches = 0;
-    if (prec == 8)
-      ekick<double>(h);
-    else
-      ekick<float>(h);
+    run({1, h, 0});
+    exchange_nccl();
   }
 
-  // 0.5 (eps0 e^T Q e + b^T M2 b / mu0), dynamics.cpp:92-102 with lumped Q, M2
+  // 0.5 (eps0 e^T Q e + b^T M2 b / mu0), dynamics.cpp:92-102 with lumped Q, M2;
+  // a slab sums its owned planes only (the caller adds the ranks' parts)
   double energy() {
-    const int64_t np = g.npts();
+    const int64_t off = (int64_t)g.kown_lo * plane();
+    const int64_t cnt = std::min<int64_t>((int64_t)(g.kown_hi - g.kown_lo) * plane(), g.npts() - off);
     double se = 0, sb = 0;
     for (int c = 0; c < 3; ++c) {
       if (prec == 8) {
         Fields<double> f = fields<double>(cur);
-        se += device_dot(f.c[c], f.c[c], np, partials.p, stream);
-        sb += device_dot(f.c[3 + c], f.c[3 + c], np, partials.p, stream);
+        se += device_dot(f.c[c] + off, f.c[c] + off, cnt, partials.p, stream);
+        sb += device_dot(f.c[3 + c] + off, f.c[3 + c] + off, cnt, partials.p, stream);
       } else {
         Fields<float> f = fields<float>(cur);
-        se += device_sumsq(f.c[c], np, partials.p, stream);
-        sb += device_sumsq(f.c[3 + c], np, partials.p, stream);
+        se += device_sumsq(f.c[c] + off, cnt, partials.p, stream);
+        sb += device_sumsq(f.c[3 + c] + off, cnt, partials.p, stream);
       }
     }
     return 0.5 * (eps0 * (se / dv) + (sb * dv) / mu0);
   }
 
-  void set_state(const double* b, const double* e) {
+  // device scatter of the (b, e) DOF vectors (already in `stage` buffers)
+  void set_state_dev(const double* b_dev, const double* e_dev) {
     buf[0].zero(stream);
     buf[1].zero(stream);
     cur = 0;
     for (int face = 0; face < 2; ++face) {
       const int64_t n = face ? n_faces : n_edges;
       if (!n) continue;
-      SFEEC_CUDA(cudaMemcpyAsync(stage.p, face ? b : e, sizeof(double) * (size_t)n,
-                                 cudaMemcpyHostToDevice, stream));
       unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
       // both ping-pong buffers: the fused sweep never rewrites the constant
       // PEC boundary faces (empty C rows), so they must be present in both
       for (int bsel = 0; bsel < 2; ++bsel) {
         if (prec == 8)
-          k_scatter<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(bsel));
+          k_scatter<double><<<blocks, 256, 0, stream>>>(g, face, face ? b_dev : e_dev, n,
+                                                        fields<double>(bsel));
         else
-          k_scatter<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(bsel));
+          k_scatter<float><<<blocks, 256, 0, stream>>>(g, face, face ? b_dev : e_dev, n,
+                                                       fields<float>(bsel));
         SFEEC_LAUNCH_CHECK();
       }
     }
+  }
+
+  void set_state(const double* b, const double* e) {
+    DevBuf<double> db;
+    db.alloc((size_t)n_faces);
+    SFEEC_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * (size_t)n_faces, cudaMemcpyHostToDevice,
+                               stream));
+    SFEEC_CUDA(cudaMemcpyAsync(stage.p, e, sizeof(double) * (size_t)n_edges,
+                               cudaMemcpyHostToDevice, stream));
+    set_state_dev(db.p, stage.p);
+    // ghosts of both buffers: exchange once per buffer
+    exchange_nccl();
+    cur ^= 1;
+    exchange_nccl();
+    cur ^= 1;
     SFEEC_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -693,6 +783,76 @@ struct YeeDev {
     }
     SFEEC_CUDA(cudaStreamSynchronize(stream));
   }
+
+  void init(int dev, const YeeGeom& geom, double dx, double dy, double dz, double dt_,
+            double eps0_, double mu0_, int precision) {
+    device = dev;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    own_stream = true;
+    g = geom;
+    d[0] = dx;
+    d[1] = dy;
+    d[2] = dz;
+    dv = dx * dy * dz;
+    dt = dt_;
+    eps0 = eps0_;
+    mu0 = mu0_;
+    prec = precision;
+    n_edges = g.edge_off[3];
+    n_faces = g.face_off[3];
+    const size_t bytes = (size_t)g.npts() * 6 * (size_t)precision;
+    buf[0].alloc(bytes);
+    buf[1].alloc(bytes);
+    buf[0].zero(stream);
+    buf[1].zero(stream);
+    stage.alloc((size_t)std::max<int64_t>(1, std::max(n_edges, n_faces)));
+    partials.alloc(kReduceBlocks + 1);
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+  }
+};
+
+// R slabs of one lattice on ONE device with in-process ghost copies: the same
+// kernels, ghost layout and step plan as the NCCL path, with the transport
+// replaced by cudaMemcpyAsync -- how the multi-rank path is verified with a
+// single GPU (ranks are advanced in lockstep, phase by phase; no kernel ever
+// waits on another).
+struct YeeGroup {
+  std::vector<std::unique_ptr<YeeDev>> s;
+  YeeGeom global;
+
+  void exchange() {
+    const int R = (int)s.size();
+    for (int r = 0; r < R; ++r) {
+      YeeDev& a = *s[(size_t)r];
+      const size_t bytes = (size_t)a.plane() * (size_t)a.prec;
+      auto at = [&](YeeDev& d, int comp, int pl) {
+        return d.buf[d.cur].p +
+               ((size_t)comp * (size_t)d.g.npts() + (size_t)pl * (size_t)d.plane()) * (size_t)d.prec;
+      };
+      if (r > 0) {
+        YeeDev& lo = *s[(size_t)r - 1];
+        for (int c = 0; c < 6; ++c)
+          SFEEC_CUDA(cudaMemcpyAsync(at(lo, c, lo.g.S[2] - 1), at(a, c, 1), bytes,
+                                     cudaMemcpyDeviceToDevice, a.stream));
+      }
+      if (r < R - 1) {
+        YeeDev& hi = *s[(size_t)r + 1];
+        for (int c = 3; c < 6; ++c)
+          SFEEC_CUDA(cudaMemcpyAsync(at(hi, c, 0), at(a, c, a.g.S[2] - 2), bytes,
+                                     cudaMemcpyDeviceToDevice, a.stream));
+      }
+    }
+  }
+  void run_all(const Phase& p) {
+    for (auto& d : s) d->run(p);
+    exchange();
+  }
+  void advance(int64_t n) {
+    auto p = s[0]->plan(n);
+    for (auto& ph : p) run_all(ph);
+    for (auto& d : s)
+      for (int64_t k = 0; k < n; ++k) d->time = d->time + d->dt;
+  }
 };
 
 }  // namespace sfeec_b200
@@ -703,6 +863,41 @@ struct sfeec_yee {
   YeeDev d;
 };
 
+struct sfeec_yee_group {
+  YeeGroup g;
+};
+
+namespace {
+void check_lattice(int nx, int ny, int nz, double dx, double dy, double dz, double dt, int bc,
+                   int precision) {
+  require(nx >= 1 && ny >= 1 && nz >= 1, "cubical lattice: cell counts must be >= 1");
+  require(dx > 0 && dy > 0 && dz > 0, "cubical lattice: spacings must be > 0");
+  require(dt >= 0, "SplitScheme: dt must be >= 0");
+  require(bc == SFEEC_BC_PERIODIC || bc == SFEEC_BC_PEC, "unknown boundary condition");
+  require(precision == 8 || precision == 4, "precision must be 8 (fp64) or 4 (fp32)");
+  require(bc == SFEEC_BC_PEC || (nx >= 2 && ny >= 2 && nz >= 2),
+          "periodic Yee kernels need >= 2 cells per axis");
+}
+// local -> global DOF ids of slab r (host, for set/get of distributed state)
+void slab_maps(int nx, int ny, int nz, int r, int R, int64_t* emap, int64_t* fmap) {
+  YeeGeom gl = make_yee_geom(nx, ny, nz, 1), sl = make_yee_slab(nx, ny, nz, r, R);
+  for (int face = 0; face < 2; ++face) {
+    int64_t* m = face ? fmap : emap;
+    if (!m) continue;
+    const int64_t n = face ? sl.face_off[3] : sl.edge_off[3];
+#pragma omp parallel for schedule(static)
+    for (int64_t id = 0; id < n; ++id) {
+      int a;
+      int64_t st;
+      sl.dof_to_storage(face == 1, id, a, st);
+      int i = (int)(st % sl.P0), j = (int)((st / sl.P0) % sl.S[1]);
+      int k = (int)(st / ((int64_t)sl.P0 * sl.S[1])) + sl.kofs;
+      m[id] = gl.dof_id(face == 1, a, i, j, k);
+    }
+  }
+}
+}  // namespace
+
 extern "C" {
 
 int sfeec_yee_create(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
@@ -711,39 +906,171 @@ int sfeec_yee_create(int nx, int ny, int nz, double dx, double dy, double dz, do
   return guarded([&] {
     require(out != nullptr, "sfeec_yee_create: null out");
     *out = nullptr;
-    require(nx >= 1 && ny >= 1 && nz >= 1, "cubical lattice: cell counts must be >= 1");
-    require(dx > 0 && dy > 0 && dz > 0, "cubical lattice: spacings must be > 0");
-    require(dt >= 0, "SplitScheme: dt must be >= 0");
-    require(bc == SFEEC_BC_PERIODIC || bc == SFEEC_BC_PEC, "unknown boundary condition");
-    require(precision == 8 || precision == 4, "precision must be 8 (fp64) or 4 (fp32)");
-    require(bc == SFEEC_BC_PEC || (nx >= 2 && ny >= 2 && nz >= 2),
-            "periodic Yee kernels need >= 2 cells per axis");
+    check_lattice(nx, ny, nz, dx, dy, dz, dt, bc, precision);
+    select_device(device);
+    auto h = std::make_unique<sfeec_yee>();
+    h->d.init(device, make_yee_geom(nx, ny, nz, bc), dx, dy, dz, dt, eps0, mu0, precision);
+    *out = h.release();
+  });
+}
+
+int sfeec_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    require(out128 != nullptr, "null out");
+    ncclUniqueId id;
+    Nccl::get().check(Nccl::get().get_unique_id(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                          double eps0, double mu0, int precision, int rank, int nranks,
+                          const void* nccl_id, int device, sfeec_yee** out) {
+  return guarded([&] {
+    require(out != nullptr, "sfeec_yee_create_slab: null out");
+    *out = nullptr;
+    check_lattice(nx, ny, nz, dx, dy, dz, dt, SFEEC_BC_PEC, precision);
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    require(nz % nranks == 0 && nz / nranks >= 2, "nz must be a multiple of nranks (>= 2 planes each)");
     select_device(device);
     auto h = std::make_unique<sfeec_yee>();
     YeeDev& d = h->d;
-    d.device = device;
-    SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    d.own_stream = true;
-    d.g = make_yee_geom(nx, ny, nz, bc);
-    d.d[0] = dx;
-    d.d[1] = dy;
-    d.d[2] = dz;
-    d.dv = dx * dy * dz;
-    d.dt = dt;
-    d.eps0 = eps0;
-    d.mu0 = mu0;
-    d.prec = precision;
-    d.n_edges = d.g.edge_off[3];
-    d.n_faces = d.g.face_off[3];
-    const size_t bytes = (size_t)d.g.npts() * 6 * (size_t)precision;
-    d.buf[0].alloc(bytes);
-    d.buf[1].alloc(bytes);
-    d.buf[0].zero(d.stream);
-    d.buf[1].zero(d.stream);
-    d.stage.alloc((size_t)std::max(d.n_edges, d.n_faces));
-    d.partials.alloc(kReduceBlocks + 1);
-    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    if (nranks == 1) {
+      d.init(device, make_yee_geom(nx, ny, nz, SFEEC_BC_PEC), dx, dy, dz, dt, eps0, mu0, precision);
+    } else {
+      require(nccl_id != nullptr, "multi-rank slab needs an NCCL unique id");
+      d.init(device, make_yee_slab(nx, ny, nz, rank, nranks), dx, dy, dz, dt, eps0, mu0, precision);
+      d.rank = rank;
+      d.nranks = nranks;
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, nranks, id, rank), "ncclCommInitRank");
+    }
     *out = h.release();
+  });
+}
+
+int sfeec_yee_slab_dof_map(int nx, int ny, int nz, int rank, int nranks, int64_t* edge_map,
+                           int64_t* face_map) {
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    require(nz % nranks == 0 && nz / nranks >= 2, "nz must be a multiple of nranks (>= 2 planes each)");
+    slab_maps(nx, ny, nz, rank, nranks, edge_map, face_map);
+  });
+}
+
+int sfeec_yee_slab_dof_counts(int nx, int ny, int nz, int rank, int nranks, int64_t* n_edges,
+                              int64_t* n_faces) {
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    require(nz % nranks == 0 && nz / nranks >= 2, "nz must be a multiple of nranks (>= 2 planes each)");
+    YeeGeom g = nranks == 1 ? make_yee_geom(nx, ny, nz, 1) : make_yee_slab(nx, ny, nz, rank, nranks);
+    if (n_edges) *n_edges = g.edge_off[3];
+    if (n_faces) *n_faces = g.face_off[3];
+  });
+}
+
+int sfeec_yee_group_create(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
+                           double eps0, double mu0, int precision, int nranks, int device,
+                           sfeec_yee_group** out) {
+  return guarded([&] {
+    require(out != nullptr, "null out");
+    *out = nullptr;
+    check_lattice(nx, ny, nz, dx, dy, dz, dt, SFEEC_BC_PEC, precision);
+    require(nranks >= 2, "a group needs >= 2 slabs");
+    require(nz % nranks == 0 && nz / nranks >= 2, "nz must be a multiple of nranks (>= 2 planes each)");
+    select_device(device);
+    auto h = std::make_unique<sfeec_yee_group>();
+    h->g.global = make_yee_geom(nx, ny, nz, SFEEC_BC_PEC);
+    for (int r = 0; r < nranks; ++r) {
+      auto d = std::make_unique<YeeDev>();
+      d->init(device, make_yee_slab(nx, ny, nz, r, nranks), dx, dy, dz, dt, eps0, mu0, precision);
+      d->rank = r;
+      d->nranks = nranks;
+      h->g.s.push_back(std::move(d));
+    }
+    // one stream for the whole group keeps the lockstep order
+    for (size_t r = 1; r < h->g.s.size(); ++r) {
+      cudaStreamDestroy(h->g.s[r]->stream);
+      h->g.s[r]->stream = h->g.s[0]->stream;
+      h->g.s[r]->own_stream = false;
+    }
+    *out = h.release();
+  });
+}
+
+void sfeec_yee_group_destroy(sfeec_yee_group* h) { delete h; }
+
+int sfeec_yee_group_set_variant(sfeec_yee_group* h, int variant) {
+  return guarded([&] {
+    require(h && (variant == 0 || variant == 2), "slabs support variants 0 and 2");
+    for (auto& d : h->g.s) d->variant = variant;
+  });
+}
+
+// global (b, e) in the single-domain PEC numbering
+int sfeec_yee_group_set_state(sfeec_yee_group* h, const double* b, const double* e) {
+  return guarded([&] {
+    require(h && b && e, "null argument");
+    auto& G = h->g;
+    const int R = (int)G.s.size();
+    for (int r = 0; r < R; ++r) {
+      YeeDev& d = *G.s[(size_t)r];
+      SFEEC_CUDA(cudaSetDevice(d.device));
+      std::vector<int64_t> em((size_t)d.n_edges), fm((size_t)d.n_faces);
+      slab_maps(G.global.n[0], G.global.n[1], G.global.n[2], r, R, em.data(), fm.data());
+      std::vector<double> lb((size_t)d.n_faces), le((size_t)d.n_edges);
+      for (size_t i = 0; i < lb.size(); ++i) lb[i] = b[fm[i]];
+      for (size_t i = 0; i < le.size(); ++i) le[i] = e[em[i]];
+      DevBuf<double> db;
+      db.upload(lb.data(), lb.size(), d.stream);
+      SFEEC_CUDA(cudaMemcpyAsync(d.stage.p, le.data(), sizeof(double) * le.size(),
+                                 cudaMemcpyHostToDevice, d.stream));
+      d.set_state_dev(db.p, d.stage.p);
+      SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    }
+    for (int k = 0; k < 2; ++k) {  // ghosts of both ping-pong buffers
+      G.exchange();
+      for (auto& d : G.s) d->cur ^= 1;
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(G.s[0]->stream));
+  });
+}
+
+int sfeec_yee_group_get_state(sfeec_yee_group* h, double* b, double* e) {
+  return guarded([&] {
+    require(h && b && e, "null argument");
+    auto& G = h->g;
+    const int R = (int)G.s.size();
+    for (int r = 0; r < R; ++r) {
+      YeeDev& d = *G.s[(size_t)r];
+      std::vector<int64_t> em((size_t)d.n_edges), fm((size_t)d.n_faces);
+      slab_maps(G.global.n[0], G.global.n[1], G.global.n[2], r, R, em.data(), fm.data());
+      std::vector<double> lb((size_t)d.n_faces), le((size_t)d.n_edges);
+      d.get_state(lb.data(), le.data());
+      for (size_t i = 0; i < lb.size(); ++i) b[fm[i]] = lb[i];
+      for (size_t i = 0; i < le.size(); ++i) e[em[i]] = le[i];
+    }
+  });
+}
+
+int sfeec_yee_group_advance(sfeec_yee_group* h, int64_t nsteps) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(nsteps >= 0, "advance: nsteps must be >= 0");
+    SFEEC_CUDA(cudaSetDevice(h->g.s[0]->device));
+    h->g.advance(nsteps);
+    SFEEC_CUDA(cudaStreamSynchronize(h->g.s[0]->stream));
+  });
+}
+
+int sfeec_yee_group_energy(sfeec_yee_group* h, double* out) {
+  return guarded([&] {
+    require(h && out, "null argument");
+    double e = 0;
+    for (auto& d : h->g.s) e += d->energy();
+    *out = e;
   });
 }
 

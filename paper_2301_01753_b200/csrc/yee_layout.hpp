@@ -29,6 +29,11 @@ struct YeeGeom {
   int S[3]; // storage extents X, Y, Z
   int P0;   // row pitch (elements) >= S[0]; PEC rows padded to 16-byte multiples for TMA
   int64_t np_alloc;  // elements per component array (padded to a multiple of 32)
+  // z-slab decomposition (multi-GPU): global k = local storage plane + kofs;
+  // local planes [kown_lo, kown_hi) hold this slab's DOFs, the others are
+  // ghost planes refreshed by the halo exchange. Single domain: kofs = 0,
+  // owned = [0, S[2]).
+  int kofs, kown_lo, kown_hi;
   int64_t edge_off[4], face_off[4];
 
   SFEEC_HD int64_t npts() const { return np_alloc; }
@@ -50,6 +55,11 @@ struct YeeGeom {
       }
       if (ext[d] < 0) ext[d] = 0;
     }
+    // restrict z to the owned planes, in local storage coordinates
+    int zlo = lo[2] > kown_lo + kofs ? lo[2] : kown_lo + kofs;
+    int zhi = lo[2] + ext[2] < kown_hi + kofs ? lo[2] + ext[2] : kown_hi + kofs;
+    lo[2] = zlo - kofs;
+    ext[2] = zhi > zlo ? zhi - zlo : 0;
   }
   SFEEC_HD void init_offsets() {
     for (int f = 0; f < 2; ++f) {
@@ -96,6 +106,24 @@ inline YeeGeom make_yee_geom(int nx, int ny, int nz, int bc) {
   for (int d = 0; d < 3; ++d) g.S[d] = bc ? g.n[d] + 1 : g.n[d];
   g.P0 = bc ? (g.S[0] + 7) / 8 * 8 : g.S[0];
   g.np_alloc = ((int64_t)g.P0 * g.S[1] * g.S[2] + 31) / 32 * 32;
+  g.kofs = 0;
+  g.kown_lo = 0;
+  g.kown_hi = g.S[2];
+  g.init_offsets();
+  return g;
+}
+
+// Slab r of R of a PEC lattice with nz global cells (nz divisible by R):
+// local storage planes 0 (ghost below), 1..nzl (owned), nzl+1 (ghost above;
+// on the last slab this is the global top wall plane, owned and constant).
+inline YeeGeom make_yee_slab(int nx, int ny, int nz, int r, int R) {
+  YeeGeom g = make_yee_geom(nx, ny, nz, 1);
+  const int nzl = nz / R;
+  g.S[2] = nzl + 2;
+  g.np_alloc = ((int64_t)g.P0 * g.S[1] * g.S[2] + 31) / 32 * 32;
+  g.kofs = r * nzl - 1;
+  g.kown_lo = 1;
+  g.kown_hi = (r == R - 1) ? nzl + 2 : nzl + 1;
   g.init_offsets();
   return g;
 }

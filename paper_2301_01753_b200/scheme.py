@@ -369,6 +369,86 @@ class YeeScheme:
         return int(L.lib().sfeec_yee_last_launches(self._h))
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    L.check(L.lib().sfeec_nccl_unique_id(buf))
+    return buf.raw
+
+
+def yee_slab_dofs(nx, ny, nz, rank, nranks):
+    """(edge_map, face_map): local DOF -> global DOF of z-slab `rank`."""
+    ne, nf = C.c_int64(), C.c_int64()
+    L.check(L.lib().sfeec_yee_slab_dof_counts(nx, ny, nz, rank, nranks, C.byref(ne),
+                                              C.byref(nf)))
+    em, fm = np.zeros(ne.value, np.int64), np.zeros(nf.value, np.int64)
+    L.check(L.lib().sfeec_yee_slab_dof_map(nx, ny, nz, rank, nranks, L.i64ptr(em),
+                                           L.i64ptr(fm)))
+    return em, fm
+
+
+class YeeSlab(YeeScheme):
+    """One z-slab of a PEC Yee lattice per GPU (one process per GPU); ghost
+    planes exchanged over NCCL after every kernel. State in the slab's local
+    numbering (yee_slab_dofs); energy() returns this slab's part."""
+
+    def __init__(self, nx, ny, nz, dx, dy, dz, dt, rank, nranks, nccl_id: bytes | None,
+                 units: UnitSystem | None = None, precision: int = 8, device: int = 0):
+        units = units or UnitSystem()
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        L.check(L.lib().sfeec_yee_create_slab(nx, ny, nz, dx, dy, dz, dt, units.eps0, units.mu0,
+                                              precision, rank, nranks, idbuf, device,
+                                              C.byref(h)))
+        self._h = h
+        ne, nf = C.c_int64(), C.c_int64()
+        L.check(L.lib().sfeec_yee_dof_counts(h, C.byref(ne), C.byref(nf)))
+        self.n_edges, self.n_faces = ne.value, nf.value
+        self.dt = dt
+
+
+class YeeGroup:
+    """All z-slabs of one PEC lattice on one GPU, ghosts copied on the device:
+    the multi-rank step verified with a single GPU. Global PEC numbering."""
+
+    def __init__(self, nx, ny, nz, dx, dy, dz, dt, nranks, units: UnitSystem | None = None,
+                 precision: int = 8, device: int = 0):
+        units = units or UnitSystem()
+        h = C.c_void_p()
+        L.check(L.lib().sfeec_yee_group_create(nx, ny, nz, dx, dy, dz, dt, units.eps0,
+                                               units.mu0, precision, nranks, device,
+                                               C.byref(h)))
+        self._h = h
+        c, _ = yee_operators(nx, ny, nz, dx, dy, dz)
+        self.n_edges, self.n_faces = c.cols, c.rows
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().sfeec_yee_group_destroy(h)
+            self._h = None
+
+    def set_variant(self, v):
+        L.check(L.lib().sfeec_yee_group_set_variant(self._h, v))
+
+    def load(self, b, e):
+        b = np.ascontiguousarray(b, np.float64)
+        e = np.ascontiguousarray(e, np.float64)
+        L.check(L.lib().sfeec_yee_group_set_state(self._h, L.dptr(b), L.dptr(e)))
+
+    def fetch(self):
+        b, e = np.zeros(self.n_faces), np.zeros(self.n_edges)
+        L.check(L.lib().sfeec_yee_group_get_state(self._h, L.dptr(b), L.dptr(e)))
+        return b, e
+
+    def advance(self, n):
+        L.check(L.lib().sfeec_yee_group_advance(self._h, int(n)))
+
+    def energy(self):
+        out = C.c_double()
+        L.check(L.lib().sfeec_yee_group_energy(self._h, C.byref(out)))
+        return out.value
+
+
 def yee_operators(nx, ny, nz, dx, dy, dz, bc=L.BC_PEC):
     """(C, D) of the lumped Yee system in the sfeec_yee numbering (host builder)."""
     c, d = L.sfeec_csr_owned(), L.sfeec_csr_owned()
