@@ -29,6 +29,22 @@ def gaussian(seed: int, n: int) -> np.ndarray:
     return np.sqrt(-2.0 * np.log1p(-u[0::2])) * np.cos(2.0 * np.pi * u[1::2])
 
 
+def gaussian_ids(seed: int, ids: np.ndarray) -> np.ndarray:
+    """Entries `ids` of gaussian(seed, n): a rank can draw its part of a global
+    vector without generating the rest."""
+    ids = np.asarray(ids, dtype=np.uint64)
+    k = np.empty(2 * ids.size, dtype=np.uint64)
+    k[0::2] = 2 * ids
+    k[1::2] = 2 * ids + np.uint64(1)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (k + np.uint64(1)) * _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return np.sqrt(-2.0 * np.log1p(-u[0::2])) * np.cos(2.0 * np.pi * u[1::2])
+
+
 _GL3 = ((0.5 - 0.5 * np.sqrt(0.6), 5.0 / 18.0), (0.5, 8.0 / 18.0),
         (0.5 + 0.5 * np.sqrt(0.6), 5.0 / 18.0))
 
