@@ -204,6 +204,30 @@ int sfeec_yee_group_get_state(sfeec_yee_group* h, double* b, double* e);
 int sfeec_yee_group_advance(sfeec_yee_group* h, int64_t nsteps);
 int sfeec_yee_group_energy(sfeec_yee_group* h, double* out);
 
+/* ---- multi-GPU: z-slab partition of the unstructured (tet) leapfrog ------- */
+/* With the k-major tet numbering a slab of vertex planes owns a contiguous id
+ * range; local vectors cover one halo plane each side. Operators: Q_sym and
+ * C^T with owned-edge rows, C and M2 with owned-face rows, columns in the
+ * local ranges. edge_range / face_range = {local length, owned lo, owned hi,
+ * first owned plane length, last owned plane length}. Built by
+ * paper_2301_01753_b200.partition.slab_system. */
+typedef struct sfeec_part sfeec_part;
+int sfeec_part_create(const sfeec_csr* q_sym, const sfeec_csr* c, const sfeec_csr* ct,
+                      const sfeec_csr* m2, const int64_t* edge_range, const int64_t* face_range,
+                      double dt, double eps0, double mu0, int rank, int nranks,
+                      const void* nccl_id /* NULL: local transport */, int device,
+                      sfeec_part** out);
+void sfeec_part_destroy(sfeec_part* h);
+int sfeec_part_set_state(sfeec_part* h, const double* b_owned, const double* e_owned, double time);
+int sfeec_part_get_state(sfeec_part* h, double* b_owned, double* e_owned, double* time);
+/* merged-Strang steps with NCCL halo exchange (one process per GPU) */
+int sfeec_part_advance(sfeec_part* h, int64_t nsteps);
+/* the same program for all ranks' handles on one device, halos copied */
+int sfeec_part_advance_local(sfeec_part** hs, int nranks, int64_t nsteps);
+int sfeec_part_energy(sfeec_part* h, double* out);  /* this rank's part */
+int sfeec_part_energy_local(sfeec_part** hs, int nranks, double* out);
+int64_t sfeec_part_last_launches(sfeec_part* h);
+
 /* ---- host operator builders (setup, not timed) ---------------------------- */
 /* Lumped Yee operators in the sfeec_yee DOF numbering: C (faces x edges,
  * +-1/spacing), and the divergence D (cells x faces). Replaces

@@ -115,7 +115,18 @@ _SIGS = {
     "sfeec_yee_group_get_state": (C.c_int, [_P, _PD, _PD]),
     "sfeec_yee_group_advance": (C.c_int, [_P, C.c_int64]),
     "sfeec_yee_group_energy": (C.c_int, [_P, _PD]),
-    "sfeec_build_yee_curl":(C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+    "sfeec_part_create": (C.c_int, [C.POINTER(sfeec_csr)] * 4 + [_PI64, _PI64, C.c_double,
+                                    C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p,
+                                    C.c_int, C.POINTER(_P)]),
+    "sfeec_part_destroy": (None, [_P]),
+    "sfeec_part_set_state": (C.c_int, [_P, _PD, _PD, C.c_double]),
+    "sfeec_part_get_state": (C.c_int, [_P, _PD, _PD, _PD]),
+    "sfeec_part_advance": (C.c_int, [_P, C.c_int64]),
+    "sfeec_part_advance_local": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int64]),
+    "sfeec_part_energy": (C.c_int, [_P, _PD]),
+    "sfeec_part_energy_local": (C.c_int, [C.POINTER(_P), C.c_int, _PD]),
+    "sfeec_part_last_launches": (C.c_int64, [_P]),
+    "sfeec_build_yee_curl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),
     "sfeec_tetmesh_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(_P)]),

@@ -1,0 +1,146 @@
+"""z-slab partition of the unstructured (tet) leapfrog.
+
+The tet DOF numbering is k-major: entities whose base vertex
+lies in vertex planes [P_r, P_{r+1}) form one contiguous id range. Rank r owns
+that range; its local vectors cover planes [P_r - 1, P_{r+1}] (a one-plane
+halo each side -- every operator row of an owned entity only references
+entities within one plane: the first-order one-layer halo). Local operators
+are row slices with columns shifted by the local start: no renumbering.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .scheme import SparseOperator, symmetric_part, transpose
+
+
+def plane_splits(n: int, nranks: int) -> np.ndarray:
+    """Vertex-plane boundaries P_0 = 0 < ... < P_R = n + 1 (balanced)."""
+    if not 1 <= nranks <= n + 1:
+        raise ValueError("need 1 <= nranks <= n + 1")
+    return np.array([(r * (n + 1)) // nranks for r in range(nranks + 1)])
+
+
+def entity_plane_offsets(base_vertices: np.ndarray, n: int) -> np.ndarray:
+    """off[k] = first id whose base vertex is in plane k (k = 0..n+1)."""
+    planes = base_vertices // ((n + 1) * (n + 1))
+    if np.any(np.diff(planes) < 0):
+        raise ValueError("numbering is not k-major")
+    return np.searchsorted(planes, np.arange(n + 2), side="left")
+
+
+@dataclass
+class LocalSystem:
+    rank: int
+    nranks: int
+    q: SparseOperator   # Q_sym, owned edges x local edges
+    ct: SparseOperator  # C^T, owned edges x local faces
+    c: SparseOperator   # C, owned faces x local edges
+    m2: SparseOperator  # M2, owned faces x local faces
+    edge_range: np.ndarray  # len, own_lo, own_hi, first_len, last_len (local indices)
+    face_range: np.ndarray
+    edge_global: tuple  # (global start of the local range, owned global lo, hi)
+    face_global: tuple
+
+
+def _rows(a: SparseOperator, lo: int, hi: int, col0: int, ncols: int) -> SparseOperator:
+    rp = a.row_ptr[lo:hi + 1] - a.row_ptr[lo]
+    sl = slice(int(a.row_ptr[lo]), int(a.row_ptr[hi]))
+    ci = a.col_idx[sl].astype(np.int64) - col0
+    if ci.size and (ci.min() < 0 or ci.max() >= ncols):
+        raise ValueError("operator row references entities beyond the one-plane halo")
+    return SparseOperator(hi - lo, ncols, rp, ci.astype(np.int32), a.val[sl].copy())
+
+
+def slab_system(sys_, rank: int, nranks: int, q_sym: SparseOperator | None = None,
+                ct: SparseOperator | None = None) -> LocalSystem:
+    """Local operators of rank `rank` (sys_ is a configs.TetSystem)."""
+    n = sys_.mesh.n
+    _, ev, fv, _ = sys_.mesh.geometry()
+    P = plane_splits(n, nranks)
+    q_sym = q_sym if q_sym is not None else symmetric_part(sys_.q)
+    ct = ct if ct is not None else transpose(sys_.c)
+    out = {}
+    for kind, base in (("e", ev[:, 0]), ("f", fv[:, 0])):
+        off = entity_plane_offsets(base, n)
+        p0, p1 = P[rank], P[rank + 1]
+        g_lo = off[max(p0 - 1, 0)]
+        g_hi = off[min(p1 + 1, n + 1)]
+        o_lo, o_hi = off[p0], off[p1]
+        first = off[p0 + 1] - off[p0]
+        last = off[p1] - off[p1 - 1]
+        rng = np.array([g_hi - g_lo, o_lo - g_lo, o_hi - g_lo, first, last], np.int64)
+        out[kind] = (rng, (int(g_lo), int(o_lo), int(o_hi)))
+    (er, eg), (fr, fg) = out["e"], out["f"]
+    return LocalSystem(
+        rank, nranks,
+        q=_rows(q_sym, eg[1], eg[2], eg[0], int(er[0])),
+        ct=_rows(ct, eg[1], eg[2], fg[0], int(fr[0])),
+        c=_rows(sys_.c, fg[1], fg[2], eg[0], int(er[0])),
+        m2=_rows(sys_.m2, fg[1], fg[2], fg[0], int(fr[0])),
+        edge_range=er, face_range=fr, edge_global=eg, face_global=fg)
+
+
+class TetPart:
+    """One rank's partitioned device leapfrog (sfeec_part)."""
+
+    def __init__(self, ls: LocalSystem, dt: float, eps0=1.0, mu0=1.0, nccl_id: bytes | None = None,
+                 device: int = 0):
+        h = C.c_void_p()
+        views = [ls.q.view(), ls.c.view(), ls.ct.view(), ls.m2.view()]
+        self._keep = (ls, views)
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        L.check(L.lib().sfeec_part_create(*[C.byref(v) for v in views],
+                                          L.i64ptr(ls.edge_range), L.i64ptr(ls.face_range),
+                                          float(dt), eps0, mu0, ls.rank, ls.nranks, idbuf,
+                                          device, C.byref(h)))
+        self._h = h
+        self.ls = ls
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().sfeec_part_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def load_global(self, b, e, time=0.0):
+        eg, fg = self.ls.edge_global, self.ls.face_global
+        bo = np.ascontiguousarray(b[fg[1]:fg[2]], np.float64)
+        eo = np.ascontiguousarray(e[eg[1]:eg[2]], np.float64)
+        L.check(L.lib().sfeec_part_set_state(self._h, L.dptr(bo), L.dptr(eo), time))
+
+    def fetch_into(self, b, e):
+        eg, fg = self.ls.edge_global, self.ls.face_global
+        bo, eo, t = np.zeros(fg[2] - fg[1]), np.zeros(eg[2] - eg[1]), C.c_double()
+        L.check(L.lib().sfeec_part_get_state(self._h, L.dptr(bo), L.dptr(eo), C.byref(t)))
+        b[fg[1]:fg[2]] = bo
+        e[eg[1]:eg[2]] = eo
+        return t.value
+
+    def advance(self, n):
+        L.check(L.lib().sfeec_part_advance(self._h, int(n)))
+
+    def energy(self):
+        out = C.c_double()
+        L.check(L.lib().sfeec_part_energy(self._h, C.byref(out)))
+        return out.value
+
+
+def advance_local(parts: list[TetPart], n: int) -> None:
+    arr = (C.c_void_p * len(parts))(*[p.handle for p in parts])
+    L.check(L.lib().sfeec_part_advance_local(arr, len(parts), int(n)))
+
+
+def energy_local(parts: list[TetPart]) -> float:
+    arr = (C.c_void_p * len(parts))(*[p.handle for p in parts])
+    out = C.c_double()
+    L.check(L.lib().sfeec_part_energy_local(arr, len(parts), C.byref(out)))
+    return out.value

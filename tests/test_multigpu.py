@@ -84,3 +84,133 @@ def test_group_lockstep_bitwise_equals_single_domain(world, variant):
     b2, e2 = grp.fetch()
     assert np.array_equal(b1, b2) and np.array_equal(e1, e2)
     assert grp.energy() == pytest.approx(one.energy(), rel=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# tet mesh: z-slab partition with one-plane halos
+# ---------------------------------------------------------------------------
+from paper_2301_01753_b200 import configs, partition  # noqa: E402
+
+
+def _csr(a):
+    import scipy.sparse as sp
+    return sp.csr_matrix((a.val, a.col_idx, a.row_ptr), shape=(a.rows, a.cols))
+
+
+@pytest.fixture(scope="module")
+def tet_sys():
+    return configs.tet_system(7, 0.1, seed=11)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_tet_slab_operators_reproduce_global_rows(tet_sys, world):
+    qs = S.symmetric_part(tet_sys.q)
+    ct = S.transpose(tet_sys.c)
+    rng = np.random.default_rng(0)
+    xe, xf = rng.standard_normal(tet_sys.n1), rng.standard_normal(tet_sys.n2)
+    owned_e, owned_f = [], []
+    for r in range(world):
+        ls = partition.slab_system(tet_sys, r, world, qs, ct)
+        eg, fg = ls.edge_global, ls.face_global
+        le, lf = xe[eg[0]:eg[0] + ls.edge_range[0]], xf[fg[0]:fg[0] + ls.face_range[0]]
+        np.testing.assert_array_equal(_csr(ls.q) @ le, (_csr(qs) @ xe)[eg[1]:eg[2]])
+        np.testing.assert_array_equal(_csr(ls.ct) @ lf, (_csr(ct) @ xf)[eg[1]:eg[2]])
+        np.testing.assert_array_equal(_csr(ls.c) @ le, (_csr(tet_sys.c) @ xe)[fg[1]:fg[2]])
+        np.testing.assert_array_equal(_csr(ls.m2) @ lf, (_csr(tet_sys.m2) @ xf)[fg[1]:fg[2]])
+        owned_e.append(eg[1:])
+        owned_f.append(fg[1:])
+        if r > 0:  # halo below == upper end of the previous rank's owned range
+            assert ls.edge_range[1] == prev.edge_range[4] and ls.face_range[1] == prev.face_range[4]
+            assert prev.edge_range[0] - prev.edge_range[2] == ls.edge_range[3]
+        prev = ls
+    for owned, total in ((owned_e, tet_sys.n1), (owned_f, tet_sys.n2)):
+        assert owned[0][0] == 0 and owned[-1][1] == total
+        assert all(owned[i][1] == owned[i + 1][0] for i in range(world - 1))
+
+
+def _tet_worker(rank, world, port, out):
+    """One merged Strang step per rank on CPU: local rows + gloo halo exchange
+    (the host logic the NCCL path runs), compared with the global step."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    sys_ = configs.tet_system(6, 0.1, seed=3)
+    ls = partition.slab_system(sys_, rank, world)
+    q, ct, c, m2 = (_csr(a) for a in (ls.q, ls.ct, ls.c, ls.m2))
+    rng = np.random.default_rng(1)
+    e_g, b_g = rng.standard_normal(sys_.n1), rng.standard_normal(sys_.n2)
+    er, fr = ls.edge_range, ls.face_range
+    eg, fg = ls.edge_global, ls.face_global
+    e = e_g[eg[0]:eg[0] + er[0]].copy()
+    b = b_g[fg[0]:fg[0] + fr[0]].copy()
+    t, u = np.zeros(er[0]), np.zeros(fr[0])
+
+    def exch(v, rngv):
+        ln, lo, hi, first, last = (int(x) for x in rngv)
+        reqs = []
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(v[lo:lo + first].copy()), rank - 1))
+            buf = torch.zeros(lo, dtype=torch.float64)
+            dist.recv(buf, rank - 1)
+            v[:lo] = buf.numpy()
+        if rank < world - 1:
+            reqs.append(dist.isend(torch.from_numpy(v[hi - last:hi].copy()), rank + 1))
+            buf = torch.zeros(ln - hi, dtype=torch.float64)
+            dist.recv(buf, rank + 1)
+            v[hi:] = buf.numpy()
+        for rq in reqs:
+            rq.wait()
+
+    dt = 0.01
+    o = lambda rr: slice(int(rr[1]), int(rr[2]))
+    exch(e, er); t[o(er)] = q @ e; exch(t, er); b[o(fr)] -= 0.5 * dt * (c @ t)
+    exch(b, fr); u[o(fr)] = m2 @ b; exch(u, fr); e[o(er)] += dt * (ct @ u)
+    exch(e, er); t[o(er)] = q @ e; exch(t, er); b[o(fr)] -= 0.5 * dt * (c @ t)
+    got = [None] * world
+    dist.all_gather_object(got, (eg, fg, e[o(er)].tolist(), b[o(fr)].tolist()))
+    if rank == 0:
+        qg, cg, m2g = _csr(S.symmetric_part(sys_.q)), _csr(sys_.c), _csr(sys_.m2)
+        bb = b_g - 0.5 * dt * (cg @ (qg @ e_g))
+        ee = e_g + dt * (cg.T @ (m2g @ bb))
+        bb = bb - 0.5 * dt * (cg @ (qg @ ee))
+        err = 0.0
+        for egr, fgr, el, bl in got:
+            err = max(err, np.max(np.abs(np.array(el) - ee[egr[1]:egr[2]])),
+                      np.max(np.abs(np.array(bl) - bb[fgr[1]:fgr[2]])))
+        out.put(err)
+    dist.destroy_process_group()
+
+
+def test_tet_partitioned_step_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tet_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_tet_partition_lockstep_bitwise_equals_single(tet_sys, world):
+    b0, e0, _ = configs.initial_pulse(tet_sys, seed=2)
+    dt = 0.003
+    one = S.SplitScheme(S.SplitKind.Strang, dt, tet_sys.q, tet_sys.c, tet_sys.m2, warn_cfl=False)
+    ref = one.advance(S.make_state(S.Formulation.BE, b0, e0), 25)
+    qs, ct = S.symmetric_part(tet_sys.q), S.transpose(tet_sys.c)
+    parts = [partition.TetPart(partition.slab_system(tet_sys, r, world, qs, ct), dt)
+             for r in range(world)]
+    for p in parts:
+        p.load_global(b0, e0)
+    partition.advance_local(parts, 25)
+    b, e = np.zeros(tet_sys.n2), np.zeros(tet_sys.n1)
+    for p in parts:
+        p.fetch_into(b, e)
+    assert np.array_equal(b, ref.first) and np.array_equal(e, ref.e)
+    assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
