@@ -132,6 +132,40 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---- plain ELL for narrow operators: one thread per row ------------------
+template <bool ACC, bool SIGNED, int W>
+__global__ void __launch_bounds__(kThreads)
+    k_ell(int64_t rows, const int32_t* __restrict__ col, const double* __restrict__ val,
+          double scale, const double* __restrict__ x, double* __restrict__ y, double alpha) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const double y0 = ACC ? y[r] : 0.0;
+  int32_t p[W];
+  double v[W], xv[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    p[k] = __ldcs(col + (int64_t)k * rows + r);
+    if (!SIGNED) v[k] = __ldcs(val + (int64_t)k * rows + r);
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    if (SIGNED)
+      xv[k] = p[k] != kPad ? __ldg(x + (p[k] < 0 ? ~p[k] : p[k])) : 0.0;
+    else
+      xv[k] = __ldg(x + p[k]);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    if (SIGNED)
+      acc += p[k] < 0 ? -xv[k] : xv[k];
+    else
+      acc = fma(v[k], xv[k], acc);
+  }
+  const double res = SIGNED ? scale * acc : acc;
+  y[r] = ACC ? fma(alpha, res, y0) : res;
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha,
                        int64_t n, int strict) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -206,6 +240,44 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   } else if (rows_per_slice >= 8 && pad_ratio <= 1.15) {
     layout = kSell;
   } else {
+    SFEEC_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  // narrow operators (C: 3, C^T: <= 6, M2: 7 per row) go to plain ELL: one
+  // thread per row, entry k of row r at k*rows + r, no slice metadata and
+  // no persistent loop -- the short rows are latency-bound, so every row's
+  // loads must be independent and the grid as large as the row count
+  int64_t wmax = 0;
+  for (int64_t r = 0; r < rows; ++r) wmax = std::max(wmax, h.row_ptr[(size_t)r + 1] - h.row_ptr[(size_t)r]);
+  const double ell_pad = (double)(rows * wmax) / (double)nnz;
+  if (wmax >= 1 && wmax <= 8 && ell_pad <= (layout == kSigned ? 1.3 : 1.1)) {
+    ell = true;
+    ell_w = (int)wmax;
+    sell_entries = rows * wmax;
+    std::vector<int32_t> ec((size_t)sell_entries, layout == kSigned ? kPad : 0);
+    std::vector<double> evv;
+    if (layout == kSell) evv.assign((size_t)sell_entries, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r) {
+      const int64_t b = h.row_ptr[(size_t)r], e = h.row_ptr[(size_t)r + 1];
+      for (int64_t k = 0; k < wmax; ++k) {
+        const size_t o = (size_t)(k * rows + r);
+        if (b + k < e) {
+          const int32_t c = h.col_idx[(size_t)(b + k)];
+          const double v = h.val[(size_t)(b + k)];
+          if (layout == kSigned) {
+            ec[o] = v < 0 ? ~c : c;
+          } else {
+            ec[o] = c;
+            evv[o] = v;
+          }
+        } else if (layout == kSell) {
+          ec[o] = e > b ? h.col_idx[(size_t)b] : 0;  // val 0
+        }
+      }
+    }
+    sell_col.upload(ec.data(), ec.size(), s);
+    if (layout == kSell) sell_val.upload(evv.data(), evv.size(), s);
     SFEEC_CUDA(cudaStreamSynchronize(s));
     return;
   }
@@ -310,6 +382,39 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   if (a.rows == 0) return;
   if (a.nnz == 0) {
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
+    return;
+  }
+  if (a.ell && a.layout != DevOperator::kCsr) {
+    const unsigned g = blocks_for(a.rows);
+    const bool sg = a.layout == DevOperator::kSigned;
+#define SFEEC_ELL_W(W)                                                                       \
+  case W:                                                                                    \
+    if (sg) {                                                                                \
+      if (accumulate)                                                                        \
+        k_ell<true, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha); \
+      else                                                                                   \
+        k_ell<false, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha); \
+    } else {                                                                                 \
+      if (accumulate)                                                                        \
+        k_ell<true, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha); \
+      else                                                                                   \
+        k_ell<false, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha); \
+    }                                                                                        \
+    break;
+    switch (a.ell_w) {
+      SFEEC_ELL_W(1)
+      SFEEC_ELL_W(2)
+      SFEEC_ELL_W(3)
+      SFEEC_ELL_W(4)
+      SFEEC_ELL_W(5)
+      SFEEC_ELL_W(6)
+      SFEEC_ELL_W(7)
+      SFEEC_ELL_W(8)
+      default:
+        throw Error(SFEEC_ECUDA, "bad ELL width");
+    }
+#undef SFEEC_ELL_W
+    SFEEC_LAUNCH_CHECK();
     return;
   }
   // persistent grid sized to the residency of the chosen variant (148 SMs x

@@ -32,6 +32,8 @@ struct DevOperator {
   DevBuf<int32_t> sell_col;   // packed (signed) column indices
   DevBuf<double> sell_val;    // kSell only
   double scale = 1.0;         // kSigned: |value|
+  bool ell = false;           // narrow operator stored as plain ELL (width ell_w)
+  int ell_w = 0;
 
   void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
   void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
