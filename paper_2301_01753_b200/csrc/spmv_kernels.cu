@@ -132,6 +132,61 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---- sliced layout, two lanes per row (wide rows, e.g. Q_sym ~16/row) -----
+// A warp takes half a slice pair: lanes 2i, 2i+1 share row i of 16 rows and
+// take alternate entries, so each lane holds <= CH entries of a <= 2*CH row
+// in one chunk: 2 memory round trips per row, then one shuffle. Persistent
+// warps with the next slice's metadata prefetched, as k_sell.
+template <bool ACC, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_sell_tpr2(int64_t n_slices, const int64_t* __restrict__ srow,
+                const int64_t* __restrict__ sptr, const int32_t* __restrict__ sw,
+                const int32_t* __restrict__ col, const double* __restrict__ val,
+                const double* __restrict__ x, double* __restrict__ y, double alpha) {
+  const int lane = threadIdx.x & 31;
+  const int half = lane & 1, rl = lane >> 1;  // row within the 16-row group
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // work item = (slice, 16-row group g in {0,1})
+  const int64_t n_items = 2 * n_slices;
+  int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (it >= n_items) return;
+  SliceMeta m = load_meta(srow, sptr, sw, it >> 1);
+  while (true) {
+    const int64_t itn = it + nwarps;
+    SliceMeta mn;
+    if (itn < n_items) mn = load_meta(srow, sptr, sw, itn >> 1);
+    const int li = (int)(it & 1) * 16 + rl;  // row index inside the slice
+    const bool active = li < m.nr;
+    double acc = 0.0, y0 = 0.0;
+    const int64_t row = m.r0 + li;
+    if (active) {
+      if (ACC && half == 0) y0 = y[row];
+      const int64_t base = m.ptr + li;
+      for (int k0 = 0; k0 < m.w; k0 += 2 * CH) {
+        int32_t p[CH];
+        double v[CH], xv[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int k = k0 + 2 * j + half;
+          const bool ok = k < m.w;
+          const int64_t o = base + (int64_t)k * m.nr;
+          p[j] = ok ? __ldcs(col + o) : -1;
+          v[j] = ok ? __ldcs(val + o) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) xv[j] = p[j] >= 0 ? __ldg(x + p[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) acc = fma(v[j], xv[j], acc);
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (active && half == 0) y[row] = ACC ? fma(alpha, acc, y0) : acc;
+    if (itn >= n_items) break;
+    it = itn;
+    m = mn;
+  }
+}
+
 // ---- plain ELL for narrow operators: one thread per row ------------------
 template <bool ACC, bool SIGNED, int W>
 __global__ void __launch_bounds__(kThreads)
@@ -459,10 +514,29 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         SFEEC_SELL(false, true);
       break;
     case DevOperator::kSell:
-      if (accumulate)
+      if (variant >= 5) {
+#define SFEEC_TPR2(CH, MB)                                                                   \
+  do {                                                                                       \
+    const unsigned g2 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 64), 148 * MB);  \
+    if (accumulate)                                                                          \
+      k_sell_tpr2<true, CH, MB><<<g2, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,           \
+          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);              \
+    else                                                                                     \
+      k_sell_tpr2<false, CH, MB><<<g2, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,          \
+          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);              \
+  } while (0)
+        if (variant == 5)
+          SFEEC_TPR2(8, 4);
+        else if (variant == 6)
+          SFEEC_TPR2(4, 4);
+        else
+          SFEEC_TPR2(8, 3);
+#undef SFEEC_TPR2
+      } else if (accumulate) {
         SFEEC_SELL(true, false);
-      else
+      } else {
         SFEEC_SELL(false, false);
+      }
       break;
     default:
       if (accumulate)

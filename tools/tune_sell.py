@@ -9,7 +9,7 @@ import bench  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 96
 R = bench.TetRunner(dict(bench.CONFIGS["tet128"], n=n), 0)
 R.load()
-for v, sv in (("1", "0"), ("1", "0")):
+for v, sv in (("1", "0"), ("5", "0"), ("6", "0"), ("7", "0"), ("1", "0")):
     os.environ["SFEEC_SELL_VARIANT"] = v
     os.environ["SFEEC_SELL_SVARIANT"] = sv
     R.advance(5)
