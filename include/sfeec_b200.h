@@ -252,6 +252,19 @@ int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_ve
 /* which: 0 C (faces x interior edges, +-1), 1 M1 (interior edges), 2 M2
  * (faces), 3 D (tets x faces, +-1) */
 int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
+/* The same first-order S(M1) system assembled ON THE DEVICE (C, D, M1, M2,
+ * SPAI, Q_sym; bitwise the host builders' operators) and wrapped in a
+ * leapfrog handle (BE formulation). counts = {N1, N2, T} (nullable). The
+ * setup path for 128^3 / 256^3 (configs 3, 5). */
+int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                         int split_kind, int device, int flags, int with_div, sfeec_dev** out,
+                         int64_t* counts);
+/* device-assembled operators, downloaded (parity tests); nullable outputs */
+int sfeec_tet_dev_operators(int n, double jitter, uint64_t seed, int device, sfeec_csr_owned* c,
+                            sfeec_csr_owned* m2, sfeec_csr_owned* d, sfeec_csr_owned* q_sym,
+                            sfeec_csr_owned* ct);
+/* y = A x with a resident operator of the handle: 0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D */
+int sfeec_dev_apply(sfeec_dev* h, int which, const double* x, double* y);
 /* make_pattern (spai.cpp:31-72): kind 0 diagonal, 1 S(M1), 2 S(M1^2); the
  * pattern is returned as a CSR with unit values */
 int sfeec_make_pattern(const sfeec_csr* m, int kind, sfeec_csr_owned* out);

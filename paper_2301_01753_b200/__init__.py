@@ -24,6 +24,8 @@ from .scheme import (  # noqa: F401
     operator_from_triplets,
     scaled_identity,
     symmetric_part,
+    tet_device_operators,
+    tet_device_scheme,
     transpose,
     yee_operators,
 )

@@ -115,7 +115,13 @@ _SIGS = {
     "sfeec_yee_group_get_state": (C.c_int, [_P, _PD, _PD]),
     "sfeec_yee_group_advance": (C.c_int, [_P, C.c_int64]),
     "sfeec_yee_group_energy": (C.c_int, [_P, _PD]),
-    "sfeec_part_create": (C.c_int, [C.POINTER(sfeec_csr)] * 4 + [_PI64, _PI64, C.c_double,
+    "sfeec_tet_dev_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                       C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(_P), _PI64]),
+    "sfeec_tet_dev_operators": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int] +
+                                [C.POINTER(sfeec_csr_owned)] * 5),
+    "sfeec_dev_apply": (C.c_int, [_P, C.c_int, _PD, _PD]),
+    "sfeec_part_create":(C.c_int, [C.POINTER(sfeec_csr)] * 4 + [_PI64, _PI64, C.c_double,
                                     C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p,
                                     C.c_int, C.POINTER(_P)]),
     "sfeec_part_destroy": (None, [_P]),

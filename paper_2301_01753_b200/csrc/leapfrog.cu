@@ -25,6 +25,7 @@ struct LeapfrogDev {
   int kind = SFEEC_SPLIT_STRANG, form = SFEEC_FORM_BE, flags = 0;
   double dt = 0, eps0 = 1, mu0 = 1;
   DevOperator q, c, ct, m2, div;
+  HostCSR q_host;  // Q_sym for export when the device keeps no CSR copy
   bool has_div = false;
   int64_t n1 = 0, n2 = 0, n_first = 0;
   DevBuf<double> first, e, t1, t2, t3, partials;
@@ -225,6 +226,54 @@ struct sfeec_dev {
   LeapfrogDev d;
 };
 
+
+// Builds a device handle from host operators (Q already symmetric). Shared by
+// sfeec_dev_create and the device-assembled tet system (tet_device.cu).
+sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR* hdiv, double dt,
+                              double eps0, double mu0, int split_kind, int formulation,
+                              int device, int flags) {
+  select_device(device);
+  auto h = std::make_unique<sfeec_dev>();
+  LeapfrogDev& d = h->d;
+  d.device = device;
+  SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  d.own_stream = true;
+  d.kind = split_kind;
+  d.form = formulation;
+  d.flags = flags;
+  d.dt = dt;
+  d.eps0 = eps0;
+  d.mu0 = mu0;
+  const bool strict = (flags & SFEEC_STRICT) != 0;
+  d.n1 = hc.cols;
+  d.n2 = hc.rows;
+  {
+    HostCSR hct = csr_transpose(hc);
+    d.ct.upload(hct, strict, d.stream);
+  }
+  d.c.upload(hc, strict, d.stream);
+  hc = HostCSR();
+  d.m2.upload(hm2, strict, d.stream);
+  hm2 = HostCSR();
+  d.q.upload(hq, strict, d.stream);
+  if (!d.q.has_csr()) d.q_host = std::move(hq);
+  if (hdiv) {
+    d.div.upload(*hdiv, strict, d.stream);
+    d.has_div = true;
+  }
+  d.n_first = formulation == SFEEC_FORM_BE ? d.n2 : d.n1;
+  d.first.alloc((size_t)d.n_first);
+  d.first.zero(d.stream);
+  d.e.alloc((size_t)d.n1);
+  d.e.zero(d.stream);
+  d.t1.alloc((size_t)d.n1);
+  d.t2.alloc((size_t)std::max<int64_t>(d.n2, 1));
+  d.t3.alloc((size_t)std::max<int64_t>(d.n2, 1));
+  d.partials.alloc(kReduceBlocks + 1);
+  SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  return h.release();
+}
+
 extern "C" {
 
 int sfeec_dev_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* m2,
@@ -246,45 +295,12 @@ int sfeec_dev_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* m2
     require(!div || div->cols == c->rows, "SplitScheme: divergence dimensions inconsistent");
     require(split_kind == 0 || split_kind == 1, "SplitScheme: unknown split kind");
     require(formulation == 0 || formulation == 1, "SplitScheme: unknown formulation");
-    select_device(device);
-    auto h = std::make_unique<sfeec_dev>();
-    LeapfrogDev& d = h->d;
-    d.device = device;
-    SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    d.own_stream = true;
-    d.kind = split_kind;
-    d.form = formulation;
-    d.flags = flags;
-    d.dt = dt;
-    d.eps0 = eps0;
-    d.mu0 = mu0;
     HostCSR hq = csr_from_view(*q);
     if (!(flags & SFEEC_Q_IS_SYMMETRIC)) hq = csr_symmetric_part(hq);
-    HostCSR hc = csr_from_view(*c);
-    HostCSR hct = csr_transpose(hc);
-    HostCSR hm2 = csr_from_view(*m2);
-    bool strict = (flags & SFEEC_STRICT) != 0;
-    d.q.upload(hq, strict, d.stream);
-    d.c.upload(hc, strict, d.stream);
-    d.ct.upload(hct, strict, d.stream);
-    d.m2.upload(hm2, strict, d.stream);
-    if (div) {
-      d.div.upload(csr_from_view(*div), strict, d.stream);
-      d.has_div = true;
-    }
-    d.n1 = c->cols;
-    d.n2 = c->rows;
-    d.n_first = formulation == SFEEC_FORM_BE ? d.n2 : d.n1;
-    d.first.alloc((size_t)d.n_first);
-    d.first.zero(d.stream);
-    d.e.alloc((size_t)d.n1);
-    d.e.zero(d.stream);
-    d.t1.alloc((size_t)d.n1);
-    d.t2.alloc((size_t)std::max<int64_t>(d.n2, 1));
-    d.t3.alloc((size_t)std::max<int64_t>(d.n2, 1));
-    d.partials.alloc(kReduceBlocks + 1);
-    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
-    *out = h.release();
+    std::unique_ptr<HostCSR> hd;
+    if (div) hd = std::make_unique<HostCSR>(csr_from_view(*div));
+    *out = make_dev_from_host(std::move(hq), csr_from_view(*c), csr_from_view(*m2), hd.get(), dt,
+                              eps0, mu0, split_kind, formulation, device, flags);
   });
 }
 
@@ -405,7 +421,14 @@ int sfeec_dev_q_sym(sfeec_dev* h, int64_t* nnz, int64_t* row_ptr, int32_t* col_i
     auto& q = h->d.q;
     SFEEC_CUDA(cudaSetDevice(h->d.device));
     if (nnz) *nnz = q.nnz;
-    q.download_csr(row_ptr, col_idx, val, h->d.stream);
+    if (q.has_csr()) {
+      q.download_csr(row_ptr, col_idx, val, h->d.stream);
+    } else {
+      const HostCSR& hq = h->d.q_host;
+      if (row_ptr) std::memcpy(row_ptr, hq.row_ptr.data(), sizeof(int64_t) * hq.row_ptr.size());
+      if (col_idx) std::memcpy(col_idx, hq.col_idx.data(), sizeof(int32_t) * hq.col_idx.size());
+      if (val) std::memcpy(val, hq.val.data(), sizeof(double) * hq.val.size());
+    }
   });
 }
 
@@ -453,6 +476,26 @@ int sfeec_spmv(const sfeec_csr* a, const double* x, double* y, int device) {
       SFEEC_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * (size_t)a->rows,
                                  cudaMemcpyDeviceToHost, s));
     SFEEC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// y = A x with one of the handle's resident operators (0 Q_sym, 1 C, 2 C^T,
+// 3 M2, 4 D): e.g. B0 = C A for a device-assembled system
+int sfeec_dev_apply(sfeec_dev* h, int which, const double* x, double* y) {
+  return guarded([&] {
+    require(h && x && y, "null argument");
+    auto& d = h->d;
+    DevOperator* ops[5] = {&d.q, &d.c, &d.ct, &d.m2, &d.div};
+    require(which >= 0 && which < 5 && (which != 4 || d.has_div), "unknown operator");
+    DevOperator& a = *ops[which];
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    DevBuf<double> dx, dy;
+    dx.upload(x, (size_t)a.cols, d.stream);
+    dy.alloc((size_t)a.rows);
+    d.apply(a, dx.p, dy.p);
+    SFEEC_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * (size_t)a.rows, cudaMemcpyDeviceToHost,
+                               d.stream));
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
   });
 }
 

@@ -334,6 +334,7 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
     sell_col.upload(ec.data(), ec.size(), s);
     if (layout == kSell) sell_val.upload(evv.data(), evv.size(), s);
     SFEEC_CUDA(cudaStreamSynchronize(s));
+    drop_csr();
     return;
   }
   std::vector<int32_t> hc((size_t)sell_entries, layout == kSigned ? kPad : 0);
@@ -367,6 +368,8 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   slice_w.upload(hw.data(), hw.size(), s);
   sell_col.upload(hc.data(), hc.size(), s);
   if (layout == kSell) sell_val.upload(hv.data(), hv.size(), s);
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  drop_csr();
   // the host vectors die at return: make the async copies complete first
   SFEEC_CUDA(cudaStreamSynchronize(s));
 }

@@ -36,6 +36,14 @@ struct DevOperator {
   int ell_w = 0;
 
   void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
+  // production layouts make the CSR copy redundant: free it (halves the
+  // footprint of Q_sym at 256^3); has_csr() tells export paths
+  void drop_csr() {
+    rp.reset();
+    ci.reset();
+    val.reset();
+  }
+  bool has_csr() const { return rp.p != nullptr; }
   void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
   // algorithmic bytes of one application in this layout (arrays streamed once)
   double stream_bytes() const;

@@ -285,6 +285,20 @@ class SplitScheme:
     def step_bytes(self) -> float:
         return L.lib().sfeec_dev_step_bytes(self._h)
 
+    def apply(self, which: str, x: np.ndarray) -> np.ndarray:
+        """y = A x with a resident operator: 'q_sym', 'c', 'ct', 'm2' or 'div'."""
+        idx = {"q_sym": 0, "c": 1, "ct": 2, "m2": 3, "div": 4}[which]
+        rows = {"q_sym": self._n1, "c": self._n2, "ct": self._n1, "m2": self._n2}
+        x = np.ascontiguousarray(x, np.float64)
+        n_out = rows.get(which)
+        if n_out is None:  # div: cells; ask via a probe-free bound
+            n_out = getattr(self, "n_tets", None)
+            if n_out is None:
+                raise InvalidParameter("apply('div') needs the cell count")
+        y = np.zeros(n_out)
+        L.check(L.lib().sfeec_dev_apply(self._h, idx, L.dptr(x), L.dptr(y)))
+        return y
+
     def set_dt(self, dt: float) -> None:
         L.check(L.lib().sfeec_dev_set_dt(self._h, float(dt)))
         self._dt = float(dt)
@@ -501,6 +515,38 @@ class TetMesh:
 
     def div(self) -> SparseOperator:
         return self._op(3)
+
+
+def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.0,
+                      kind: SplitKind = SplitKind.Strang, units: UnitSystem | None = None,
+                      with_div: bool = True, warn_cfl: bool = False,
+                      device: int = 0) -> "SplitScheme":
+    """First-order S(M1) tet system assembled on the B200 (C, D, M1, M2, SPAI,
+    Q_sym), wrapped as a (b, e) SplitScheme. Operators stay in HBM."""
+    units = units or UnitSystem()
+    h = C.c_void_p()
+    counts = np.zeros(3, np.int64)
+    flags = 0 if warn_cfl else L.NO_CFL_WARN
+    L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
+                                         units.mu0, int(SplitKind(kind)), device, flags,
+                                         1 if with_div else 0, C.byref(h), L.i64ptr(counts)))
+    s = SplitScheme.__new__(SplitScheme)
+    s._h = h
+    s._kind, s._dt, s._units = SplitKind(kind), float(dt), units
+    s._formulation = Formulation.BE
+    s._c = s._m2 = None
+    s._n1, s._n2 = int(counts[0]), int(counts[1])
+    s.n_tets = int(counts[2])
+    return s
+
+
+def tet_device_operators(n: int, jitter: float = 0.1, seed: int = 0, device: int = 0) -> dict:
+    """Device-assembled C, M2, D, Q_sym and C^T, downloaded (parity tests)."""
+    outs = [L.sfeec_csr_owned() for _ in range(5)]
+    L.check(L.lib().sfeec_tet_dev_operators(int(n), float(jitter), int(seed), device,
+                                            *[C.byref(o) for o in outs]))
+    names = ("c", "m2", "d", "q_sym", "ct")
+    return {k: SparseOperator._from_owned(o, k in ("m2", "q_sym")) for k, o in zip(names, outs)}
 
 
 PATTERNS = {"diagonal": 0, "m1": 1, "m1sq": 2}
