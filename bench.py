@@ -49,6 +49,9 @@ CONFIGS = {
     "tet128": dict(kind="tet", n=128, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
                    desc="BASELINE configs[2]: 128^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) "
                         "SPAI, PEC, Gaussian pulse width 0.1, dt = 0.5 CFL"),
+    "tet256": dict(kind="tet", n=256, jitter=0.1, init="pulse", npulses=8, dtype="f64", ref_n=64,
+                   desc="BASELINE configs[4]: 256^3 x 6 Kuhn tets (100.7M tets), jitter 0.1h, "
+                        "P1-, S(M1) SPAI, PEC, 8 Gaussian pulses, dt = 0.5 CFL"),
 }
 
 
@@ -201,19 +204,24 @@ class YeeRunner:
 
 
 def tet_setup(cfg, device):
+    """Mesh numbering on the host; C, D, M1, M2, SPAI and Q_sym assembled on the
+    device (tet_device.cu, bitwise the host builders); dt = 0.5 CFL."""
     import paper_2301_01753_b200 as S
-    from paper_2301_01753_b200 import configs
+    from paper_2301_01753_b200 import configs, inputs
     t0 = time.perf_counter()
-    sys_ = configs.tet_system(cfg["n"], cfg["jitter"], seed=2023)
+    s = S.tet_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
+                            device=device)
+    mesh = S.TetMesh(cfg["n"], cfg["jitter"], 2023)  # host geometry for the initial A
+    xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
     if cfg["init"] == "gaussian":
-        b0, e0, _ = configs.initial_gaussian(sys_, seed=7)
+        a = inputs.gaussian(7, s._n1)
     else:
-        b0, e0, _ = configs.initial_pulse(sys_, seed=7, npulses=cfg.get("npulses", 1))
-    s = S.SplitScheme(S.SplitKind.Strang, 1.0, sys_.q, sys_.c, sys_.m2, div=sys_.d,
-                      warn_cfl=False, device=device)
+        a = inputs.pulse_one_form(xyz, ev, 7, 0.1, cfg.get("npulses", 1))
+    del xyz, ev, mesh
+    b0 = s.apply("c", a)
     s.set_dt(configs.cfl_dt(s))
     setup_s = time.perf_counter() - t0
-    return sys_, s, b0, e0, setup_s
+    return (s._n1, s._n2), s, b0, np.zeros(s._n1), setup_s
 
 
 class TetRunner:
@@ -221,8 +229,7 @@ class TetRunner:
         import paper_2301_01753_b200 as S
         from paper_2301_01753_b200 import _lib as L
         self.S, self.L = S, L
-        self.sys, self.s, self.b0, self.e0, self.setup_s = tet_setup(cfg, device)
-        self.n1, self.n2 = self.sys.n1, self.sys.n2
+        (self.n1, self.n2), self.s, self.b0, self.e0, self.setup_s = tet_setup(cfg, device)
         self.ndof = self.n1 + self.n2
         self.dt = self.s.dt()
 

@@ -489,14 +489,16 @@ class TetMesh:
             L.lib().sfeec_tetmesh_destroy(h)
             self._h = None
 
-    def geometry(self):
-        """(xyz[nv,3], edge_vertices[N1,2], face_vertices[N2,3], tet_vertices[T,4])."""
+    def geometry(self, faces: bool = True, tets: bool = True):
+        """(xyz[nv,3], edge_vertices[N1,2], face_vertices[N2,3], tet_vertices[T,4]);
+        faces/tets=False skip those arrays (None)."""
         xyz = np.zeros((self.n_vertices, 3))
         ev = np.zeros((self.n_edges, 2), np.int64)
-        fv = np.zeros((self.n_faces, 3), np.int64)
-        tv = np.zeros((self.n_tets, 4), np.int64)
-        L.check(L.lib().sfeec_tetmesh_geometry(self._h, L.dptr(xyz), L.i64ptr(ev), L.i64ptr(fv),
-                                               L.i64ptr(tv)))
+        fv = np.zeros((self.n_faces, 3), np.int64) if faces else None
+        tv = np.zeros((self.n_tets, 4), np.int64) if tets else None
+        L.check(L.lib().sfeec_tetmesh_geometry(self._h, L.dptr(xyz), L.i64ptr(ev),
+                                               L.i64ptr(fv) if faces else None,
+                                               L.i64ptr(tv) if tets else None))
         return xyz, ev, fv, tv
 
     def _op(self, which, symmetric=False) -> SparseOperator:
