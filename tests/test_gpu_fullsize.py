@@ -1,0 +1,102 @@
+"""GPU parity at BASELINE.json's full sizes, where the CPU oracle cannot run
+every step: size-independent properties of the scheme plus a few oracle steps.
+
+config 2 (Yee 256^3, PEC, 1000 steps): Gauss law D b = 0 kept to round-off,
+symplectic energy bounded, fused TMA sweep == unfused kernels, fp32 tracks
+fp64. config 3 (128^3 x 6 tets, device-assembled S(M1) system): 5 production
+steps against the C oracle on the downloaded operators (<= 1e-12), the Gauss
+residual and the energy history over 200 steps.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2301_01753_b200 as S
+from paper_2301_01753_b200 import configs, inputs
+from oracle import oracle as O
+from tests.conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(a):
+    return sp.csr_matrix((a.val, a.col_idx, a.row_ptr), shape=(a.rows, a.cols))
+
+
+@pytest.fixture(scope="module")
+def yee256():
+    import bench
+    y, b0, e0, dt = bench.yee_setup(256, 8, 0)
+    h = 1.0 / 256
+    _, d = S.yee_operators(256, 256, 256, h, h, h)
+    return y, b0, e0, dt, _csr(d)
+
+
+def test_config2_gauss_law_and_energy_over_1000_steps(yee256):
+    y, b0, e0, dt, d = yee256
+    scale = np.abs(b0).max()
+    assert np.abs(d @ b0).max() <= 1e-9 * scale * 256  # B0 = C A is divergence free
+    y.load(b0, e0)
+    energies = [y.energy()]
+    for _ in range(10):
+        y.advance(100)
+        energies.append(y.energy())
+    b, e, t = y.fetch()
+    assert t == pytest.approx(1000 * dt, rel=1e-12)
+    assert np.abs(d @ b).max() <= 1e-9 * scale * 256
+    en = np.array(energies)
+    assert (en.max() - en.min()) / en[0] <= 0.05  # bounded oscillation (test_dynamics.cpp:342)
+
+
+def test_config2_fused_sweep_equals_unfused_at_full_size(yee256):
+    y, b0, e0, dt, _ = yee256
+    out = []
+    for v in (2, 0):
+        y.set_variant(v)
+        y.load(b0, e0)
+        y.advance(20)
+        out.append(y.fetch())
+    y.set_variant(2)
+    assert rel_l2(out[0][0], out[1][0]) <= 1e-14 and rel_l2(out[0][1], out[1][1]) <= 1e-14
+
+
+def test_config2_fp32_tracks_fp64(yee256):
+    y, b0, e0, dt, _ = yee256
+    h = 1.0 / 256
+    y32 = S.YeeScheme(256, 256, 256, h, h, h, dt, bc=1, precision=4)
+    for s in (y, y32):
+        s.load(b0, e0)
+        s.advance(200)
+    b64, e64, _ = y.fetch()
+    b32, e32, _ = y32.fetch()
+    assert rel_l2(b32, b64) <= 1e-4 and rel_l2(e32, e64) <= 1e-4
+
+
+@pytest.fixture(scope="module")
+def tet128():
+    s = S.tet_device_scheme(128, 0.15, seed=2023, dt=1.0, with_div=True)
+    mesh = S.TetMesh(128, 0.15, 2023)
+    xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
+    a = inputs.pulse_one_form(xyz, ev, 7)
+    b0 = s.apply("c", a)
+    s.set_dt(configs.cfl_dt(s))
+    return s, b0, np.zeros(s._n1)
+
+
+def test_config3_first_steps_match_oracle(tet128):
+    s, b0, e0 = tet128
+    ops = S.tet_device_operators(128, 0.15, seed=2023)
+    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)
+    port = O.PortScheme(1, s.dt(), tup(ops["q_sym"]), tup(ops["c"]), tup(ops["m2"]),
+                        q_is_symmetric=True)
+    pb, pe, _ = port.steps(b0, e0, 5)
+    out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 5)
+    assert rel_l2(out.first, pb) <= 1e-12 and rel_l2(out.e, pe) <= 1e-12
+
+
+def test_config3_gauss_and_energy_history(tet128):
+    s, b0, e0 = tet128
+    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 200, 20)
+    assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
+    assert (en.max() - en.min()) / en[0] <= 0.05
+    assert s.cfl_number() == pytest.approx(1.0, rel=1e-9)
