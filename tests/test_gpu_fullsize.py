@@ -45,7 +45,13 @@ def test_config2_gauss_law_and_energy_over_1000_steps(yee256):
     assert t == pytest.approx(1000 * dt, rel=1e-12)
     assert np.abs(d @ b).max() <= 1e-9 * scale * 256
     en = np.array(energies)
-    assert (en.max() - en.min()) / en[0] <= 0.05  # bounded oscillation (test_dynamics.cpp:342)
+    # symplectic: the energy stays in a band (test_dynamics.cpp:342-368). The
+    # white-noise B0 = C A puts its energy at grid-scale frequencies, where the
+    # integer-step energy differs from the conserved modified energy by
+    # O((omega dt)^2) ~ 10% at Courant 0.5: a one-off shift once e builds up,
+    # then a flat history.
+    assert (en.max() - en.min()) / en[0] <= 0.10
+    assert (en[1:].max() - en[1:].min()) / en[1] <= 1e-3
 
 
 def test_config2_fused_sweep_equals_unfused_at_full_size(yee256):
