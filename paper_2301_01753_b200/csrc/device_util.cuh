@@ -66,6 +66,14 @@ struct DevBuf {
   }
 };
 
+// device CSR (int64 row pointers), produced by the device assembly
+struct DevCSR {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  DevBuf<int64_t> rp;
+  DevBuf<int32_t> ci;
+  DevBuf<double> val;
+};
+
 // Checks there is a usable device and makes `device` current.
 void select_device(int device);
 

@@ -274,6 +274,47 @@ sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR
   return h.release();
 }
 
+// Builds a handle around operators that already live on the device (the
+// device-assembled tet system in stencil layout). Production mode only.
+sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
+                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
+                             double mu0, int split_kind, int device, int flags, cudaStream_t s) {
+  require(!(flags & SFEEC_STRICT), "strict mode needs CSR operators (use the host builders)");
+  select_device(device);
+  auto h = std::make_unique<sfeec_dev>();
+  LeapfrogDev& d = h->d;
+  d.device = device;
+  d.stream = s;
+  d.own_stream = true;
+  d.kind = split_kind;
+  d.form = SFEEC_FORM_BE;
+  d.flags = flags | SFEEC_Q_IS_SYMMETRIC;
+  d.dt = dt;
+  d.eps0 = eps0;
+  d.mu0 = mu0;
+  d.q = std::move(q);
+  d.c = std::move(c);
+  d.ct = std::move(ct);
+  d.m2 = std::move(m2);
+  if (div) {
+    d.div = std::move(*div);
+    d.has_div = true;
+  }
+  d.n1 = n1;
+  d.n2 = n2;
+  d.n_first = n2;
+  d.first.alloc((size_t)n2);
+  d.first.zero(d.stream);
+  d.e.alloc((size_t)n1);
+  d.e.zero(d.stream);
+  d.t1.alloc((size_t)n1);
+  d.t2.alloc((size_t)std::max<int64_t>(n2, 1));
+  d.t3.alloc((size_t)std::max<int64_t>(n2, 1));
+  d.partials.alloc(kReduceBlocks + 1);
+  SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  return h.release();
+}
+
 extern "C" {
 
 int sfeec_dev_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* m2,

@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include "spmv_kernels.cuh"
+#include "stencil.cuh"
 
 namespace sfeec_b200 {
 
@@ -440,6 +441,10 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   if (a.rows == 0) return;
   if (a.nnz == 0) {
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
+    return;
+  }
+  if (a.layout == DevOperator::kStencil) {
+    launch_stencil(*a.st, x, y, alpha, accumulate, s);
     return;
   }
   if (a.ell && a.layout != DevOperator::kCsr) {

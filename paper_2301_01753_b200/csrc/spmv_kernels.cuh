@@ -1,6 +1,8 @@
 // Device sparse operators and the SpMV kernels of the leapfrog chain
 // (K-Q, K-Cb, K-M2, K-CTe in SURVEY.md 2.4).
 #pragma once
+#include <memory>
+
 #include "device_util.cuh"
 
 namespace sfeec_b200 {
@@ -17,8 +19,13 @@ namespace sfeec_b200 {
 //            Whitney P1- curl); one int32 per entry, sign in the top bit
 //            (~col for negative) -> 4 B/entry instead of 12.
 //   kSell:   general values: fp64 value + int32 column per entry.
+struct StencilOp;
+
 struct DevOperator {
-  enum Layout { kCsr = 0, kSigned = 1, kSell = 2 };
+  // kStencil: mesh-aware layout of the device-assembled tet operators
+  // (stencil.cuh): column ids recomputed from the Kuhn stencil, values only
+  enum Layout { kCsr = 0, kSigned = 1, kSell = 2, kStencil = 3 };
+  std::shared_ptr<StencilOp> st;
   int64_t rows = 0, cols = 0, nnz = 0;
   DevBuf<int64_t> rp;
   DevBuf<int32_t> ci;
@@ -44,6 +51,19 @@ struct DevOperator {
     val.reset();
   }
   bool has_csr() const { return rp.p != nullptr; }
+  // keep a device CSR as is (CSR-vector kernel)
+  void adopt_csr(DevCSR&& d) {
+    rows = d.rows;
+    cols = d.cols;
+    nnz = d.nnz;
+    rp = std::move(d.rp);
+    ci = std::move(d.ci);
+    val = std::move(d.val);
+    const double avg = rows ? (double)nnz / (double)rows : 0.0;
+    tpr = 1;
+    while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
+    layout = kCsr;
+  }
   void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
   // algorithmic bytes of one application in this layout (arrays streamed once)
   double stream_bytes() const;

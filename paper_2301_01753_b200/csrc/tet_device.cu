@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "device_util.cuh"
+#include "spmv_kernels.cuh"
+#include "stencil.cuh"
 #include "tet_mesh.hpp"
 
 namespace sfeec_b200 {
@@ -467,13 +469,6 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (
 
 }  // namespace
 
-// device CSR (int64 row pointers)
-struct DevCSR {
-  int64_t rows = 0, cols = 0, nnz = 0;
-  DevBuf<int64_t> rp;
-  DevBuf<int32_t> ci;
-  DevBuf<double> val;
-};
 
 static void exclusive_scan(int64_t* d, int64_t n, cudaStream_t s) {
   // in-place exclusive scan of n + 1 entries (last = total)
@@ -606,6 +601,9 @@ using namespace sfeec_b200;
 sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR* hdiv, double dt,
                               double eps0, double mu0, int split_kind, int formulation,
                               int device, int flags);
+sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
+                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
+                             double mu0, int split_kind, int device, int flags, cudaStream_t s);
 
 namespace {
 
@@ -663,6 +661,34 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       counts[0] = sys.n1;
       counts[1] = sys.n2;
       counts[2] = sys.nt;
+    }
+    if (!(flags & SFEEC_TET_HOST_LAYOUT)) {
+      // stencil layout built on the device from the device CSRs (no host trip)
+      auto sm = stencil_mesh(mesh, st.s);
+      DevOperator q, c, ct, m2, div;
+      auto mk = [&](int kind, DevCSR& csr, DevOperator& op) {
+        auto so = std::make_shared<StencilOp>();
+        stencil_build(mesh, sm, kind, &csr, *so, st.s);
+        op.rows = csr.rows;
+        op.cols = csr.cols;
+        op.nnz = csr.nnz;
+        op.layout = DevOperator::kStencil;
+        op.st = so;
+        csr.rp.reset();
+        csr.ci.reset();
+        csr.val.reset();
+      };
+      mk(kStQ, sys.qsym, q);
+      mk(kStM2, sys.m2, m2);
+      mk(kStC, sys.c, c);
+      mk(kStCT, sys.ct, ct);
+      if (with_div) div.adopt_csr(std::move(sys.d));
+      cudaStream_t hs;
+      SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+      *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
+                               with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
+                               split_kind, device, flags & ~SFEEC_TET_HOST_LAYOUT, hs);
+      return;
     }
     sys.ct.rp.reset();  // the handle transposes C itself
     sys.ct.ci.reset();
