@@ -256,10 +256,12 @@ int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* o
  * SPAI, Q_sym; bitwise the host builders' operators) and wrapped in a
  * leapfrog handle (BE formulation). counts = {N1, N2, T} (nullable). The
  * setup path for 128^3 / 256^3 (configs 3, 5). */
-/* flag for sfeec_tet_dev_create: build the generic sliced/ELL layouts through
- * the host instead of the default device-built stencil layout (stencil.cuh:
- * column ids recomputed from the Kuhn stencil, values-only streams) */
-enum { SFEEC_TET_HOST_LAYOUT = 8 };
+/* layout flags for sfeec_tet_dev_create. Default: the sliced / ELL layouts
+ * built on the device. HOST_LAYOUT: the same layouts built through the host
+ * (the sfeec_dev_create path). STENCIL_LAYOUT: column ids recomputed from the
+ * Kuhn stencil, values-only streams (stencil.cuh; fewer bytes but a longer
+ * latency chain -- measured slower, kept for reference) */
+enum { SFEEC_TET_HOST_LAYOUT = 8, SFEEC_TET_STENCIL_LAYOUT = 16 };
 int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                          int split_kind, int device, int flags, int with_div, sfeec_dev** out,
                          int64_t* counts);

@@ -375,6 +375,164 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   SFEEC_CUDA(cudaStreamSynchronize(s));
 }
 
+namespace {
+
+__global__ void k_abs_uniform(int64_t nnz, const double* __restrict__ v, int* __restrict__ not_uniform) {
+  const double m = fabs(v[0]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (fabs(v[i]) != m) *not_uniform = 1;
+}
+
+// CSR -> ELL (column-major, width w), one thread per row
+__global__ void k_to_ell(int64_t rows, int w, bool sg, const int64_t* __restrict__ rp,
+                         const int32_t* __restrict__ ci, const double* __restrict__ cv,
+                         int32_t* __restrict__ ec, double* __restrict__ ev) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t b = rp[r], e = rp[r + 1];
+  for (int k = 0; k < w; ++k) {
+    const int64_t o = (int64_t)k * rows + r;
+    if (b + k < e) {
+      const int32_t c = ci[b + k];
+      if (sg) {
+        ec[o] = cv[b + k] < 0 ? ~c : c;
+      } else {
+        ec[o] = c;
+        ev[o] = cv[b + k];
+      }
+    } else if (sg) {
+      ec[o] = kPad;
+    } else {
+      ec[o] = e > b ? ci[b] : 0;
+      ev[o] = 0.0;
+    }
+  }
+}
+
+// CSR -> sliced layout, one warp per slice
+__global__ void k_to_sell(int64_t n_slices, bool sg, const int64_t* __restrict__ srow,
+                          const int64_t* __restrict__ sptr, const int32_t* __restrict__ sw,
+                          const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ cv, int32_t* __restrict__ sc,
+                          double* __restrict__ sv) {
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl >= n_slices) return;
+  const int64_t r0 = srow[sl], nr = srow[sl + 1] - r0;
+  if (lane >= nr) return;
+  const int64_t r = r0 + lane, b = rp[r], e = rp[r + 1];
+  for (int k = 0; k < sw[sl]; ++k) {
+    const int64_t o = sptr[sl] + (int64_t)k * nr + lane;
+    if (b + k < e) {
+      const int32_t c = ci[b + k];
+      if (sg) {
+        sc[o] = cv[b + k] < 0 ? ~c : c;
+      } else {
+        sc[o] = c;
+        sv[o] = cv[b + k];
+      }
+    } else if (sg) {
+      sc[o] = kPad;
+    } else {
+      sc[o] = e > b ? ci[b] : 0;
+      sv[o] = 0.0;
+    }
+  }
+}
+
+}  // namespace
+
+void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
+  rows = d.rows;
+  cols = d.cols;
+  nnz = d.nnz;
+  layout = kCsr;
+  const double avg = rows ? (double)nnz / (double)rows : 0.0;
+  tpr = 1;
+  while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
+  if (rows == 0 || nnz == 0) {
+    adopt_csr(std::move(d));
+    return;
+  }
+  std::vector<int64_t> hrp((size_t)rows + 1);
+  SFEEC_CUDA(cudaMemcpyAsync(hrp.data(), d.rp.p, sizeof(int64_t) * hrp.size(),
+                             cudaMemcpyDeviceToHost, s));
+  DevBuf<int> flag;
+  flag.alloc(1);
+  flag.zero(s);
+  k_abs_uniform<<<148 * 8, 256, 0, s>>>(nnz, d.val.p, flag.p);
+  SFEEC_LAUNCH_CHECK();
+  int not_uniform = 0;
+  SFEEC_CUDA(cudaMemcpyAsync(&not_uniform, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  // the same layout decisions as upload()
+  std::vector<int64_t> hrow{0}, hptr{0};
+  std::vector<int32_t> hw;
+  int64_t wmax = 0;
+  for (int64_t r = 0; r < rows; ++r) wmax = std::max(wmax, hrp[(size_t)r + 1] - hrp[(size_t)r]);
+  {
+    int64_t r = 0;
+    while (r < rows) {
+      int64_t w = hrp[(size_t)r + 1] - hrp[(size_t)r];
+      int64_t e = r + 1;
+      while (e < rows && e - r < 32) {
+        int64_t l = hrp[(size_t)e + 1] - hrp[(size_t)e];
+        int64_t tol = std::max<int64_t>(1, std::max(w, l) / 8);
+        if (std::llabs(l - w) > tol) break;
+        w = std::max(w, l);
+        ++e;
+      }
+      hw.push_back((int32_t)w);
+      hptr.push_back(hptr.back() + w * (e - r));
+      hrow.push_back(e);
+      r = e;
+    }
+  }
+  n_slices = (int64_t)hw.size();
+  const bool signed_ok = not_uniform == 0;
+  const double rows_per_slice = (double)rows / (double)n_slices;
+  const double pad_ratio = (double)hptr.back() / (double)nnz;
+  if (rows_per_slice >= 8 && signed_ok && pad_ratio <= 2.5) {
+    layout = kSigned;
+    SFEEC_CUDA(cudaMemcpyAsync(&scale, d.val.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SFEEC_CUDA(cudaStreamSynchronize(s));
+    scale = std::fabs(scale);
+  } else if (rows_per_slice >= 8 && pad_ratio <= 1.15) {
+    layout = kSell;
+  } else {
+    adopt_csr(std::move(d));
+    return;
+  }
+  const bool sg = layout == kSigned;
+  const double ell_pad = (double)(rows * wmax) / (double)nnz;
+  if (wmax >= 1 && wmax <= 8 && ell_pad <= (sg ? 1.3 : 1.1)) {
+    ell = true;
+    ell_w = (int)wmax;
+    sell_entries = rows * wmax;
+    sell_col.alloc((size_t)sell_entries);
+    if (!sg) sell_val.alloc((size_t)sell_entries);
+    k_to_ell<<<blocks_for(rows), kThreads, 0, s>>>(rows, ell_w, sg, d.rp.p, d.ci.p, d.val.p,
+                                                   sell_col.p, sell_val.p);
+  } else {
+    sell_entries = hptr.back();
+    slice_row.upload(hrow.data(), hrow.size(), s);
+    slice_ptr.upload(hptr.data(), hptr.size(), s);
+    slice_w.upload(hw.data(), hw.size(), s);
+    sell_col.alloc((size_t)sell_entries);
+    if (!sg) sell_val.alloc((size_t)sell_entries);
+    k_to_sell<<<blocks_for(n_slices * 32), kThreads, 0, s>>>(n_slices, sg, slice_row.p,
+                                                             slice_ptr.p, slice_w.p, d.rp.p,
+                                                             d.ci.p, d.val.p, sell_col.p,
+                                                             sell_val.p);
+  }
+  SFEEC_LAUNCH_CHECK();
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  d.rp.reset();
+  d.ci.reset();
+  d.val.reset();
+}
+
 double DevOperator::stream_bytes() const {
   switch (layout) {
     case kSigned:

@@ -51,6 +51,10 @@ struct DevOperator {
     val.reset();
   }
   bool has_csr() const { return rp.p != nullptr; }
+  // production layout built on the device from a device CSR (same layout
+  // decisions as upload(); only the row pointers visit the host); the CSR
+  // buffers are consumed
+  void upload_device(DevCSR&& d, cudaStream_t s);
   // keep a device CSR as is (CSR-vector kernel)
   void adopt_csr(DevCSR&& d) {
     rows = d.rows;

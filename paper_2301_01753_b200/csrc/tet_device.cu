@@ -662,7 +662,23 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       counts[1] = sys.n2;
       counts[2] = sys.nt;
     }
-    if (!(flags & SFEEC_TET_HOST_LAYOUT)) {
+    if (!(flags & SFEEC_TET_HOST_LAYOUT) && !(flags & SFEEC_TET_STENCIL_LAYOUT)) {
+      // default: the sliced / ELL layouts built on the device from the device
+      // CSRs (only row pointers visit the host)
+      DevOperator q, c, ct, m2, div;
+      q.upload_device(std::move(sys.qsym), st.s);
+      m2.upload_device(std::move(sys.m2), st.s);
+      c.upload_device(std::move(sys.c), st.s);
+      ct.upload_device(std::move(sys.ct), st.s);
+      if (with_div) div.upload_device(std::move(sys.d), st.s);
+      cudaStream_t hs;
+      SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+      *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
+                               with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
+                               split_kind, device, flags, hs);
+      return;
+    }
+    if (flags & SFEEC_TET_STENCIL_LAYOUT) {
       // stencil layout built on the device from the device CSRs (no host trip)
       auto sm = stencil_mesh(mesh, st.s);
       DevOperator q, c, ct, m2, div;
@@ -687,7 +703,7 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
       *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
                                with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
-                               split_kind, device, flags & ~SFEEC_TET_HOST_LAYOUT, hs);
+                               split_kind, device, flags & ~SFEEC_TET_STENCIL_LAYOUT, hs);
       return;
     }
     sys.ct.rp.reset();  // the handle transposes C itself

@@ -521,11 +521,12 @@ class TetMesh:
 
 def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.0,
                       kind: SplitKind = SplitKind.Strang, units: UnitSystem | None = None,
-                      with_div: bool = True, warn_cfl: bool = False, layout: str = "stencil",
+                      with_div: bool = True, warn_cfl: bool = False, layout: str = "device",
                       device: int = 0) -> "SplitScheme":
     """First-order S(M1) tet system assembled on the B200 (C, D, M1, M2, SPAI,
     Q_sym), wrapped as a (b, e) SplitScheme. Operators stay in HBM.
-    layout: "stencil" (default; columns recomputed from the Kuhn stencil) or
+    layout: "device" (default: sliced/ELL layouts built on the GPU), "stencil"
+    (columns recomputed from the Kuhn stencil; slower, kept for reference) or
     "host" (generic sliced/ELL layouts built through the host)."""
     units = units or UnitSystem()
     h = C.c_void_p()
@@ -533,8 +534,10 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
     flags = 0 if warn_cfl else L.NO_CFL_WARN
     if layout == "host":
         flags |= 8  # SFEEC_TET_HOST_LAYOUT
-    elif layout != "stencil":
-        raise InvalidParameter("layout must be 'stencil' or 'host'")
+    elif layout == "stencil":
+        flags |= 16  # SFEEC_TET_STENCIL_LAYOUT
+    elif layout != "device":
+        raise InvalidParameter("layout must be 'device', 'host' or 'stencil'")
     L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                          units.mu0, int(SplitKind(kind)), device, flags,
                                          1 if with_div else 0, C.byref(h), L.i64ptr(counts)))
