@@ -433,6 +433,165 @@ __global__ void __launch_bounds__(TX* TY)
     __syncthreads();  // unit boundary: the next unit's prologue refills every stage
   }
 }
+// ---- variant 3: B planes by TMA, E planes by register prefetch ------------
+// Same sweep and arithmetic as k_fused_tma, but each thread loads the old E
+// values of its <= 2 region points one plane ahead into registers (plain
+// coalesced loads; each is read by exactly one thread) instead of staging E
+// through shared memory. The stage shrinks to the B tile, so three CTAs fit
+// per SM instead of two.
+template <class T, int TX, int TY, int NS>
+struct TmaCfgB {
+  static constexpr int kOff = 16 / (int)sizeof(T);
+  static constexpr int kBWB = (((TX + 1 + kOff) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
+  static constexpr int kBBox = 3 * (TY + 2) * kBWB * (int)sizeof(T);
+  static constexpr int kStage = (kBBox + 127) / 128 * 128;
+  static constexpr int kEnew = 3 * (TY + 1) * (TX + 1);
+  static constexpr int kBarOff = (NS * kStage + 3 * kEnew * (int)sizeof(T) + 15) / 16 * 16;
+  static constexpr int kSmem = kBarOff + NS * 8 + 128;
+  static constexpr int kD = NS - 3;
+};
+
+template <class T, int TX, int TY, int NS>
+__global__ void __launch_bounds__(TX* TY)
+    k_fused_tma_b(const __grid_constant__ CUtensorMap mapB, YeeGeom g, Fields<T> in,
+                  Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
+                  int n_units, int kbeg, int kend) {
+  using Cfg = TmaCfgB<T, TX, TY, NS>;
+  constexpr int D = Cfg::kD;
+  constexpr int BWB = Cfg::kBWB, OFF = Cfg::kOff;
+  constexpr int NT = TX * TY, NE = (TX + 1) * (TY + 1);
+  static_assert(NE <= 2 * NT, "E region needs at most two passes");
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  __syncthreads();
+  uint32_t gplane = 0;
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int64_t kstride = (int64_t)g.P0 * g.S[1];
+  const int pl[2] = {tid, tid + NT};
+  int li_[2], lj_[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    li_[q] = pl[q] % (TX + 1);
+    lj_[q] = pl[q] / (TX + 1);
+  }
+  const bool has2 = tid + NT < NE;
+  const int bli = tid % TX, blj = tid / TX;
+
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
+    const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
+    const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
+    const int P = k1 - k0 + 2;
+    uint32_t m[2];
+    int64_t sij[2];
+    bool inr[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = i0 + li_[q], j = j0 + lj_[q];
+      const bool ix = i < n0, iy = i >= 1 && i <= n0 - 1;
+      const bool jx = j < n1, jy = j >= 1 && j <= n1 - 1;
+      const bool own = li_[q] < TX && lj_[q] < TY && i < n0 && j < n1;
+      m[q] = (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u) | (own ? 8u : 0u);
+      sij[q] = (int64_t)i + (int64_t)g.P0 * j;
+      inr[q] = (q == 0 || has2) && i < g.S[0] && j < g.S[1];
+    }
+    const bool bown = i0 + bli < n0 && j0 + blj < n1;
+    const int64_t bsij = (int64_t)(i0 + bli) + (int64_t)g.P0 * (j0 + blj);
+    // old E of plane k0 for the thread's region points
+    T ec[2][3], en[2][3];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ec[q][c] = inr[q] ? in.c[c][sij[q] + kstride * k0] : T(0);
+
+    auto issue = [&](int p) {
+      const uint32_t gp = gplane + p;
+      const int st = gp % NS;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bars[st], Cfg::kBBox);
+      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - OFF, j0 - 1, k0 - 1 + p, 3);
+    };
+    if (tid == 0)
+      for (int p = 0; p <= D && p < P; ++p) issue(p);
+    for (int jp = 0; jp + 1 < P; ++jp) {
+      const int kk = k0 + jp;
+      if (tid == 0 && jp + 1 + D < P) issue(jp + 1 + D);
+      // prefetch the old E of the next plane into registers
+      const bool more = kk + 1 <= k1;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) en[q][c] = (more && inr[q]) ? in.c[c][sij[q] + kstride * (kk + 1)] : T(0);
+      const uint32_t gc = gplane + jp + 1, gv = gplane + jp;
+      const int sc = gc % NS, sv = gv % NS;
+      if (jp == 0) mbar_wait(&bars[sv], (gv / NS) & 1);
+      mbar_wait(&bars[sc], (gc / NS) & 1);
+      const T* __restrict__ Bc = reinterpret_cast<const T*>(base + sc * Cfg::kStage);
+      const T* __restrict__ Bp = reinterpret_cast<const T*>(base + sv * Cfg::kStage);
+      T* Enc = sEn + ((gplane + jp) % 3) * Cfg::kEnew;
+      const T* Enp = sEn + ((gplane + jp + 2) % 3) * Cfg::kEnew;
+#define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BWB + (x)]
+#define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BWB + (x)]
+#define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
+      const int kg = kk + g.kofs;
+      const bool kin = kg >= 1 && kg <= n2 - 1, kz = kg < n2, kw = kk < k1;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && !has2) break;
+        const int li = li_[q], lj = lj_[q];
+        const int bi = li + OFF, bj = lj + 1;
+        T e0 = ec[q][0], e1 = ec[q][1], e2 = ec[q][2];
+        const bool d0 = (m[q] & 1) && kin, d1 = (m[q] & 2) && kin, d2 = (m[q] & 4) && kz;
+        if (d0)
+          e0 += ck.ce[1] * (BC(2, bj, bi) - BC(2, bj - 1, bi)) - ck.ce[2] * (BC(1, bj, bi) - BP(1, bj, bi));
+        if (d1)
+          e1 += ck.ce[2] * (BC(0, bj, bi) - BP(0, bj, bi)) - ck.ce[0] * (BC(2, bj, bi) - BC(2, bj, bi - 1));
+        if (d2)
+          e2 += ck.ce[0] * (BC(1, bj, bi) - BC(1, bj, bi - 1)) - ck.ce[1] * (BC(0, bj, bi) - BC(0, bj - 1, bi));
+        if ((m[q] & 8) && kw) {
+          const int64_t s = sij[q] + kstride * kk;
+          if (d0) out.c[0][s] = e0;
+          if (d1) out.c[1][s] = e1;
+          if (d2) out.c[2][s] = e2;
+        }
+        EN(Enc, 0, lj, li) = e0;
+        EN(Enc, 1, lj, li) = e1;
+        EN(Enc, 2, lj, li) = e2;
+      }
+      __syncthreads();
+      if (jp > 0 && bown) {
+        const int li = bli, lj = blj;
+        const int64_t s = bsij + kstride * (kk - 1);
+        const int bi = li + OFF, bj = lj + 1;
+        out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
+                                       ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
+        out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
+                                       ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
+        out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
+                                       ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
+      }
+#undef BC
+#undef BP
+#undef EN
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ec[q][c] = en[q][c];
+    }
+    gplane += P;
+    __syncthreads();
+  }
+}
+
 // state pack/unpack between the SFEEC numbering (fp64) and storage (T)
 template <class T>
 __global__ void k_scatter(YeeGeom g, bool face, const double* __restrict__ src, int64_t n,
@@ -479,7 +638,7 @@ struct YeeDev {
   // TMA descriptors of the two ping-pong buffers (B box, E box), PEC only
   CUtensorMap mapB[2], mapE[2];
   bool have_maps = false;
-  int tma_blocks = 0;
+  int tma_blocks = 0, tma_blocks_b = 0;
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, partials;
@@ -602,6 +761,24 @@ struct YeeDev {
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
+    if (variant == 3) {
+      using CfgB = TmaCfgB<T, kTX, kTY, kNS>;
+      auto kb = k_fused_tma_b<T, kTX, kTY, kNS>;
+      if (!tma_blocks_b) {
+        SFEEC_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgB::kSmem));
+        int per_sm = 0, sms = 0;
+        SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, kTX * kTY, CfgB::kSmem));
+        SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        tma_blocks_b = std::max(1, per_sm) * sms;
+      }
+      kb<<<std::min(n_units, tma_blocks_b), kTX * kTY, CfgB::kSmem, stream>>>(
+          mapB[cur], g, fields<T>(cur), fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
+          kChunk, ntx, ntx * nty, n_units, kbeg, kend);
+      SFEEC_LAUNCH_CHECK();
+      cur ^= 1;
+      ++launches;
+      return;
+    }
     const int grid = std::min(n_units, tma_blocks);
     k_fused_tma<T, kTX, kTY, kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
@@ -636,7 +813,7 @@ struct YeeDev {
       bkick<T>(p.h1);
     else if (p.kind == 1)
       ekick<T>(p.h1);
-    else if (variant == 2 || slab())
+    else if (variant >= 2 || slab())
       fused_tma<T>(p.h1, p.h2);
     else
       fused<T>(p.h1, p.h2);
@@ -1004,7 +1181,7 @@ void sfeec_yee_group_destroy(sfeec_yee_group* h) { delete h; }
 
 int sfeec_yee_group_set_variant(sfeec_yee_group* h, int variant) {
   return guarded([&] {
-    require(h && (variant == 0 || variant == 2), "slabs support variants 0 and 2");
+    require(h && (variant == 0 || variant >= 2) && variant <= 3, "slabs support variants 0, 2 and 3");
     for (auto& d : h->g.s) d->variant = variant;
   });
 }
@@ -1152,7 +1329,7 @@ int sfeec_yee_set_stream(sfeec_yee* h, void* s) {
 int sfeec_yee_set_variant(sfeec_yee* h, int variant) {
   return guarded([&] {
     require(h, "null handle");
-    require(variant >= 0 && variant <= 2, "variant must be 0, 1 or 2");
+    require(variant >= 0 && variant <= 3, "variant must be 0, 1, 2 or 3");
     h->d.variant = variant;
   });
 }

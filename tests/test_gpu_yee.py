@@ -47,7 +47,7 @@ def _pec_case(nx, ny, nz, d, dt, steps, seed=3):
     return b0, e0, pb, pe, ph, port
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("dims", [(6, 5, 7), (33, 9, 40), (40, 17, 3), (64, 16, 65)])
 def test_pec_matches_oracle(variant, dims):
     d = (1.0, 0.8, 1.25)
@@ -67,7 +67,7 @@ def test_fused_equals_unfused_closely():
     dims, d = (37, 21, 70), (1.0, 1.0, 1.0)
     rng = np.random.default_rng(0)
     ys = []
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3):
         y = S.YeeScheme(*dims, *d, 0.3, bc=L.BC_PEC)
         y.set_variant(v)
         if not ys:
@@ -75,7 +75,7 @@ def test_fused_equals_unfused_closely():
         y.load(b0, e0)
         y.advance(25)
         ys.append(y.fetch())
-    for k in (1, 2):
+    for k in (1, 2, 3):
         assert rel_l2(ys[k][0], ys[0][0]) <= 1e-14 and rel_l2(ys[k][1], ys[0][1]) <= 1e-14
 
 

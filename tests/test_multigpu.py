@@ -67,7 +67,7 @@ def test_slab_maps_are_z_ordered_single_process(world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("variant", [2, 0])
+@pytest.mark.parametrize("variant", [2, 3, 0])
 def test_group_lockstep_bitwise_equals_single_domain(world, variant):
     dims, d = (37, 21, 16 * world), (1.0, 0.9, 1.1)
     rng = np.random.default_rng(world)
