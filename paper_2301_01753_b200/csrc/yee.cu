@@ -653,10 +653,15 @@ struct YeeDev {
   // z-slab decomposition (yee_layout.hpp make_yee_slab)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;  // overlapped halo exchange
+  cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
 
   ~YeeDev() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_xch) cudaEventDestroy(ev_xch);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (comm) Nccl::get().comm_destroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -751,13 +756,36 @@ struct YeeDev {
     have_maps = true;
   }
 
+  // planes swept by the fused kernel: [0, n) on one domain, [1, nzl + 1) on a slab
+  int sweep_beg() const { return slab() ? 1 : 0; }
+  int sweep_end() const { return slab() ? g.S[2] - 1 : g.n[2]; }
+  int sweep_chunks() const { return (sweep_end() - sweep_beg() + kChunk - 1) / kChunk; }
+
   template <class T>
   void fused_tma(double h_e, double h_b) {
+    launch_range<T>(h_e, h_b, sweep_beg(), sweep_end());
+    cur ^= 1;
+  }
+
+  // Split sweep for overlapping the halo exchange: part 0 = the bottom and top
+  // z-chunks (they produce every plane a neighbour needs), part 1 = the rest.
+  // Neither flips the buffers.
+  template <class T>
+  void fused_part(double h_e, double h_b, int part) {
+    const int kb = sweep_beg(), ke = sweep_end(), nch = sweep_chunks();
+    if (part == 0) {
+      launch_range<T>(h_e, h_b, kb, std::min(kb + kChunk, ke));
+      if (nch >= 2) launch_range<T>(h_e, h_b, kb + (nch - 1) * kChunk, ke);
+    } else if (nch >= 3) {
+      launch_range<T>(h_e, h_b, kb + kChunk, kb + (nch - 1) * kChunk);
+    }
+  }
+
+  // fused sweep over local planes [kbeg, kend): reads buf[cur], writes buf[cur^1]
+  template <class T>
+  void launch_range(double h_e, double h_b, int kbeg, int kend) {
     if (!have_maps) make_maps<T>();
     using Cfg = TmaCfg<T, kTX, kTY, kNS>;
-    // sweep the owned planes: [0, n) on one domain, [1, nzl + 1) on a slab
-    const int kbeg = slab() ? 1 : 0;
-    const int kend = slab() ? g.S[2] - 1 : g.n[2];
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
@@ -775,7 +803,6 @@ struct YeeDev {
           mapB[cur], g, fields<T>(cur), fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
           kChunk, ntx, ntx * nty, n_units, kbeg, kend);
       SFEEC_LAUNCH_CHECK();
-      cur ^= 1;
       ++launches;
       return;
     }
@@ -784,8 +811,29 @@ struct YeeDev {
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
         ntx, ntx * nty, n_units, kbeg, kend);
     SFEEC_LAUNCH_CHECK();
-    cur ^= 1;
     ++launches;
+  }
+
+  // one fused step on a slab with the NCCL exchange overlapped: boundary
+  // chunks -> (comm stream) exchange of the new buffer's edge planes, while the
+  // interior chunks run; the compute stream waits for the exchange before the
+  // next kernel reads the ghosts. The exchange touches only ghost planes and
+  // the boundary chunks' planes, the interior sweep only interior planes.
+  template <class T>
+  void fused_overlapped(double h_e, double h_b) {
+    if (!comm_stream) {
+      SFEEC_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+      SFEEC_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
+      SFEEC_CUDA(cudaEventCreateWithFlags(&ev_xch, cudaEventDisableTiming));
+    }
+    fused_part<T>(h_e, h_b, 0);
+    SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
+    SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
+    exchange_nccl(cur ^ 1, comm_stream);
+    SFEEC_CUDA(cudaEventRecord(ev_xch, comm_stream));
+    fused_part<T>(h_e, h_b, 1);
+    SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
+    cur ^= 1;
   }
 
   // Strang with merged half-kicks: b(dt/2), n-1 x [e(dt) b(dt)], e(dt), b(dt/2)
@@ -829,12 +877,14 @@ struct YeeDev {
   // B) goes down into the lower neighbour's top ghost; the top owned B plane
   // goes up into the upper neighbour's bottom ghost. Planes are contiguous in
   // every component array, so no packing.
-  void exchange_nccl() {
+  void exchange_nccl() { exchange_nccl(cur, stream); }
+  void exchange_nccl(int bufsel, cudaStream_t es) {
     if (!slab() || !comm) return;
     const Nccl& nc = Nccl::get();
     const ncclDataType_t ty = prec == 8 ? ncclFloat64 : ncclFloat32;
     const size_t cnt = (size_t)plane();
-    char* base = buf[cur].p;
+    char* base = buf[bufsel].p;
+    cudaStream_t stream = es;
     auto at = [&](int comp, int pl) {
       return base + ((size_t)comp * (size_t)g.npts() + (size_t)pl * cnt) * (size_t)prec;
     };
@@ -858,9 +908,17 @@ struct YeeDev {
     if (n <= 0) return;
     auto p = plan(n);
     const bool t = timing && n > 1;
+    const bool overlap = slab() && comm && variant >= 2;
     for (size_t i = 0; i < p.size(); ++i) {
       if (t && i == 1) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
       if (t && i + 2 == p.size()) SFEEC_CUDA(cudaEventRecord(ev[1], stream));
+      if (overlap && p[i].kind == 2) {
+        if (prec == 8)
+          fused_overlapped<double>(p[i].h1, p[i].h2);
+        else
+          fused_overlapped<float>(p[i].h1, p[i].h2);
+        continue;
+      }
       run(p[i]);
       exchange_nccl();
     }
@@ -997,13 +1055,14 @@ struct YeeGroup {
   std::vector<std::unique_ptr<YeeDev>> s;
   YeeGeom global;
 
-  void exchange() {
+  // flip = 1: exchange into the buffers being written (the split sweep)
+  void exchange(int flip = 0) {
     const int R = (int)s.size();
     for (int r = 0; r < R; ++r) {
       YeeDev& a = *s[(size_t)r];
       const size_t bytes = (size_t)a.plane() * (size_t)a.prec;
       auto at = [&](YeeDev& d, int comp, int pl) {
-        return d.buf[d.cur].p +
+        return d.buf[d.cur ^ flip].p +
                ((size_t)comp * (size_t)d.g.npts() + (size_t)pl * (size_t)d.plane()) * (size_t)d.prec;
       };
       if (r > 0) {
@@ -1021,6 +1080,25 @@ struct YeeGroup {
     }
   }
   void run_all(const Phase& p) {
+    if (p.kind == 2 && s[0]->variant >= 2) {
+      // the NCCL path's overlapped schedule, serialised: boundary chunks,
+      // exchange into the new buffers, interior chunks, flip
+      for (auto& d : s) {
+        if (d->prec == 8)
+          d->fused_part<double>(p.h1, p.h2, 0);
+        else
+          d->fused_part<float>(p.h1, p.h2, 0);
+      }
+      exchange(1);
+      for (auto& d : s) {
+        if (d->prec == 8)
+          d->fused_part<double>(p.h1, p.h2, 1);
+        else
+          d->fused_part<float>(p.h1, p.h2, 1);
+        d->cur ^= 1;
+      }
+      return;
+    }
     for (auto& d : s) d->run(p);
     exchange();
   }
