@@ -69,7 +69,7 @@ def test_slab_maps_are_z_ordered_single_process(world):
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("variant", [2, 3, 0])
 def test_group_lockstep_bitwise_equals_single_domain(world, variant):
-    dims, d = (37, 21, 40 * world), (1.0, 0.9, 1.1)
+    dims, d = (37, 21, 70 * world), (1.0, 0.9, 1.1)  # 3 z-chunks per slab: boundary + interior
     rng = np.random.default_rng(world)
     one = S.YeeScheme(*dims, *d, 0.2, bc=1)
     one.set_variant(variant)
