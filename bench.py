@@ -7,11 +7,13 @@ cells, lumped masses, PEC walls, Courant 0.5, fp64; E0 = 0, B0 = C A with
 seeded Gaussian A. A "step" is one leapfrog step over all N1 + N2 DOFs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config yee256|yee256_f32|tet16|tet64|tet128]
+                  [--config yee256|yee256_f32|tet16|tet64|tet128|tet256]
 
 Other configs: tet16 = configs[0] (16^3 x 6 tets, S(M1) SPAI, jitter 0.1),
-tet128 = configs[2] (128^3 x 6 tets, jitter 0.15, Gaussian pulse).
-Under torchrun (N > 1) every rank runs its own block (weak scaling).
+tet128 = configs[2] (128^3 x 6 tets, jitter 0.15, Gaussian pulse), tet256.
+Under torchrun (N > 1) the Yee configs run one 256^3 block per rank stacked in
+z (weak scaling); the tet configs split the one mesh into N z-slabs (strong
+scaling).
 `--impl reference` times the reference CPU step (oracle/_ref: the unmodified
 reference SplitScheme::step, dynamics.cpp:69-90) on the host cores.
 """
@@ -279,6 +281,96 @@ class TetRunner:
     kernel_label = "SpMV chain K-M2, K-CTe, K-Q, K-Cb in sliced layouts (spmv_kernels.cu)"
 
 
+class TetSlabRunner:
+    """Rank `rank` of the tet system split into z-slabs (strong scaling: the
+    mesh is fixed, every rank assembles it on its own GPU and keeps its owned
+    rows; partition.cu, 4 NCCL halo exchanges per step)."""
+
+    scaling = "strong"
+    kernel_label = ("SpMV chain K-M2, K-CTe, K-Q, K-Cb over the owned rows + NCCL halo-plane "
+                    "exchange before each (partition.cu)")
+
+    def __init__(self, cfg, device, rank, world, dist):
+        import paper_2301_01753_b200 as S
+        from paper_2301_01753_b200 import inputs, partition
+        t0 = time.perf_counter()
+        ids = [None]
+        if world > 1:
+            ids = [S.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+        self.p = partition.TetPart.from_device(cfg["n"], cfg["jitter"], 2023, rank, world,
+                                               nccl_id=ids[0], device=device)
+        ls = self.p.ls
+        eg, er, fg = ls.edge_global, ls.edge_range, ls.face_global
+        if cfg["init"] == "gaussian":
+            a = inputs.gaussian_ids(7, np.arange(eg[0], eg[0] + er[0]))
+        else:
+            mesh = S.TetMesh(cfg["n"], cfg["jitter"], 2023)
+            xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
+            a = inputs.pulse_one_form(xyz, ev[eg[0]:eg[0] + er[0]], 7, 0.1, cfg.get("npulses", 1))
+            del xyz, ev, mesh
+        self.b0 = self.p.apply("c", a)                 # owned faces of C A
+        self.e0 = np.zeros(eg[2] - eg[1])
+        self.n1, self.n2 = ls.n1, ls.n2
+        self.ndof = ls.n1 + ls.n2                       # whole job (strong scaling)
+        self.dt = self.p.dt
+        self.setup_s = time.perf_counter() - t0
+        self._stream = None
+
+    def stream(self, torch):
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.p.device_ptrs()[2])
+        return self._stream
+
+    def set_stream(self, ptr):
+        pass  # the partition handle keeps its own stream (stream() above)
+
+    @property
+    def L(self):
+        from paper_2301_01753_b200 import _lib
+        return _lib
+
+    def load(self):
+        L = self.L
+        L.check(L.lib().sfeec_part_set_state(self.p.handle, L.dptr(self.b0), L.dptr(self.e0), 0.0))
+
+    def advance(self, k):
+        self.p.advance(k)
+
+    def launches(self):
+        return self.p.last_launches()
+
+    def dominant(self, k_steps):
+        self.p.kernel_timing(True)
+        self.advance(k_steps)
+        t = self.p.kernel_timing(False)
+        self.per_kernel = {k: {"avg_ms": v["ms"] / max(v["launches"], 1),
+                               "launches": v["launches"],
+                               "bytes_per_launch": v["bytes_per_launch"],
+                               "gbs": v["bytes_per_launch"] / (v["ms"] / max(v["launches"], 1)
+                                                               * 1e-3) / 1e9
+                               if v["ms"] > 0 and v["bytes_per_launch"] > 0 else None}
+                           for k, v in t.items()}
+        name = max(("K-Q", "K-Cb", "K-CTe", "K-M2"), key=lambda k: t[k]["ms"])
+        d = t[name]
+        return name, d["bytes_per_launch"], d["ms"] / max(d["launches"], 1)
+
+    def step_bytes(self):
+        return self.p.step_bytes()
+
+    def e2e(self, k, torch):
+        L = self.L
+        pin_b = torch.from_numpy(self.b0).pin_memory()
+        pin_e = torch.from_numpy(self.e0).pin_memory()
+        out_b, out_e = torch.empty_like(pin_b).pin_memory(), torch.empty_like(pin_e).pin_memory()
+        t0 = time.perf_counter()
+        L.check(L.lib().sfeec_part_set_state(self.p.handle, dptr(pin_b), dptr(pin_e), 0.0))
+        self.advance(k)
+        L.check(L.lib().sfeec_part_get_state(self.p.handle, dptr(out_b), dptr(out_e), None))
+        self.e2e_bytes = 8 * (self.b0.size + self.e0.size)
+        return time.perf_counter() - t0
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -288,10 +380,19 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    R = (YeeRunner(cfg, local_rank, rank, world, dist) if cfg["kind"] == "yee"
-         else TetRunner(cfg, local_rank))
-    stream = torch.cuda.current_stream()
-    R.set_stream(stream.cuda_stream)
+    if cfg["kind"] == "yee":
+        R = YeeRunner(cfg, local_rank, rank, world, dist)
+    elif world > 1 or args.partitioned:
+        R = TetSlabRunner(cfg, local_rank, rank, world, dist)
+    else:
+        R = TetRunner(cfg, local_rank)
+    if hasattr(R, "stream"):
+        stream = R.stream(torch)
+    else:
+        stream = torch.cuda.current_stream()
+        R.set_stream(stream.cuda_stream)
+    strong = getattr(R, "scaling", "weak") == "strong"
+    units = R.ndof if strong else world * R.ndof  # DOFs the whole job advances per step
     R.load()
     R.advance(args.warmup)
     torch.cuda.synchronize()
@@ -325,22 +426,25 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = hbm_peak()
     achieved = kbytes / (k_avg_ms * 1e-3) / 1e9
     ndof = R.ndof
-    value = world * ndof * args.steps / (ms * 1e-3)
+    value = units * args.steps / (ms * 1e-3)
     step_gbs = R.step_bytes() / (ms / args.steps * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": cfg["dtype"],
         "data": "synthetic (seeded: " + ("Gaussian A" if cfg.get("init", "gaussian") ==
                                          "gaussian" else "Gaussian pulse A")
                 + ", B0 = C A, E0 = 0)",
         "config": {"workload": f"{args.config}: {cfg['desc']}" + (
                        f" per GPU (global {cfg['n']}x{cfg['n']}x{cfg['n'] * world})"
-                       if world > 1 and cfg["kind"] == "yee" else (" per GPU" if world > 1 else "")),
-                   "dofs_per_gpu": ndof, "n1_edges": R.n1, "n2_faces": R.n2, "dt": R.dt,
+                       if world > 1 and cfg["kind"] == "yee" else (" (whole mesh over all GPUs)"
+                                                                    if world > 1 else "")),
+                   "dofs_per_gpu": ndof if not strong else ndof / world,
+                   "n1_edges": R.n1, "n2_faces": R.n2, "dt": R.dt,
                    "parallelism": (f"z-slabs x{world}, NCCL ghost exchange" if cfg["kind"] == "yee"
-                                   else f"replicas x{world}") if world > 1 else "single GPU",
+                                   else f"z-slabs x{world}, NCCL halo-plane exchange")
+                                  if world > 1 else "single GPU",
                    "l2": "inputs larger than L2" if R.step_bytes() > 126e6 * 2
                          else "working set fits in L2 (latency-bound parity config)",
                    "kernel": R.kernel_label},
@@ -349,8 +453,9 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": kname, "bytes_per_launch": kbytes, "kernel_avg_ms": k_avg_ms,
                      "step_bytes": R.step_bytes(), "step_achieved_gbs": step_gbs,
                      "peak_source": peak_src},
-        "e2e": {"value": world * ndof * args.steps / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": int(8 * ndof), "d2h_bytes_per_step": int(8 * ndof),
+        "e2e": {"value": units * args.steps / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)),
+                "d2h_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)),
                 "job": f"set_state + advance({args.steps}) + get_state through the C ABI "
                        "from/to pinned host buffers; bytes are per job"},
         "gpu_launches": int(launches),
@@ -459,6 +564,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="yee256")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="tet configs at N=1: run the z-slab partition path (one slab)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)
     args = ap.parse_args()

@@ -227,6 +227,27 @@ int sfeec_part_advance_local(sfeec_part** hs, int nranks, int64_t nsteps);
 int sfeec_part_energy(sfeec_part* h, double* out);  /* this rank's part */
 int sfeec_part_energy_local(sfeec_part** hs, int nranks, double* out);
 int64_t sfeec_part_last_launches(sfeec_part* h);
+/* One rank's slab of the tet system of BASELINE configs 1/3/5, assembled on
+ * ITS OWN device (tet_device.cu) and row-sliced there: no host CSR. dt <= 0:
+ * dt = 0.5 x the CFL estimate of the FULL operators (the single-GPU
+ * tet_device_scheme + configs.cfl_dt value, bitwise). info (nullable, 19):
+ * {N1, N2, edge_range[5], face_range[5], edge_global[3] = {local start, owned
+ * lo, owned hi}, face_global[3], dt}, dt as the bits of a double. */
+int sfeec_part_create_tet(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                          int rank, int nranks, const void* nccl_id, int device,
+                          sfeec_part** out, int64_t* info);
+/* y_owned = A x_local on the device, host buffers; which: 0 Q_sym, 1 C,
+ * 2 C^T, 3 M2 (e.g. the BE initial b = C a from a local-range potential) */
+int sfeec_part_apply(sfeec_part* h, int which, const double* x_local, double* y_owned);
+/* device pointers of the local (halo-extended) b and e and the compute
+ * stream, for zero-copy loads / timing (nullable) */
+int sfeec_part_device_ptrs(sfeec_part* h, double** b_local, double** e_local, void** stream);
+/* per-class launch timing (as sfeec_dev_kernel_timing; classes 0 K-Q, 1 K-Cb,
+ * 2 K-CTe, 3 K-M2, 4 halo exchange), arrays of 5, nullable */
+int sfeec_part_kernel_timing(sfeec_part* h, int enable, double* ms, int64_t* launches,
+                             double* bytes);
+/* this rank's algorithmic bytes per step (SURVEY.md 8(d) over its rows) */
+double sfeec_part_step_bytes(sfeec_part* h);
 
 /* ---- host operator builders (setup, not timed) ---------------------------- */
 /* Lumped Yee operators in the sfeec_yee DOF numbering: C (faces x edges,

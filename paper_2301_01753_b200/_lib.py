@@ -132,6 +132,13 @@ _SIGS = {
     "sfeec_part_energy": (C.c_int, [_P, _PD]),
     "sfeec_part_energy_local": (C.c_int, [C.POINTER(_P), C.c_int, _PD]),
     "sfeec_part_last_launches": (C.c_int64, [_P]),
+    "sfeec_part_create_tet": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                        C.c_double, C.c_int, C.c_int, _P, C.c_int,
+                                        C.POINTER(_P), _PI64]),
+    "sfeec_part_apply": (C.c_int, [_P, C.c_int, _PD, _PD]),
+    "sfeec_part_device_ptrs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "sfeec_part_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64, _PD]),
+    "sfeec_part_step_bytes": (C.c_double, [_P]),
     "sfeec_build_yee_curl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),

@@ -18,6 +18,8 @@
 #include "device_util.cuh"
 #include "nccl_loader.hpp"
 #include "spmv_kernels.cuh"
+#include "tet_device.hpp"
+#include "tet_mesh.hpp"
 
 namespace sfeec_b200 {
 
@@ -36,10 +38,44 @@ struct PartDev {
   DevBuf<double> e, t, b, u, partials;
   double time = 0;
   int64_t launches = 0;
+  // per-class launch timing with CUDA events on the compute stream
+  // (0 K-Q, 1 K-Cb, 2 K-CTe, 3 K-M2, 4 halo exchange)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, size_t>> ev_used;
+  double class_ms[5] = {0, 0, 0, 0, 0};
+  int64_t class_launches[5] = {0, 0, 0, 0, 0};
 
   ~PartDev() {
+    for (auto ev : ev_pool) cudaEventDestroy(ev);
     if (comm) Nccl::get().comm_destroy(comm);
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  void tic(int cls) {
+    if (!timing) return;
+    const size_t i = ev_used.size() * 2;
+    while (ev_pool.size() < i + 2) {
+      cudaEvent_t ev;
+      SFEEC_CUDA(cudaEventCreate(&ev));
+      ev_pool.push_back(ev);
+    }
+    ev_used.push_back({cls, i});
+    SFEEC_CUDA(cudaEventRecord(ev_pool[i], stream));
+  }
+  void toc() {
+    if (timing) SFEEC_CUDA(cudaEventRecord(ev_pool[ev_used.back().second + 1], stream));
+  }
+  void collect_timing() {
+    if (ev_used.empty()) return;
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+    for (auto [cls, i] : ev_used) {
+      float ms = 0;
+      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev_pool[i], ev_pool[i + 1]));
+      class_ms[cls] += ms;
+      class_launches[cls] += 1;
+    }
+    ev_used.clear();
   }
 
   // op codes of the step program
@@ -71,13 +107,16 @@ struct PartDev {
   }
 
   void kernel(const Step& s) {
+    if (s.op < kQ) return;
+    tic(s.op == kQ ? 0 : s.op == kCb ? 1 : s.op == kCTe ? 2 : 3);
     switch (s.op) {
       case kQ: launch_spmv(q, e.p, t.p + r1.own_lo, 0.0, false, stream); break;
       case kCb: launch_spmv(c, t.p, b.p + r2.own_lo, s.alpha, true, stream); break;
       case kM2: launch_spmv(m2, b.p, u.p + r2.own_lo, 0.0, false, stream); break;
       case kCTe: launch_spmv(ct, u.p, e.p + r1.own_lo, s.alpha, true, stream); break;
-      default: return;
+      default: break;
     }
+    toc();
     ++launches;
   }
 
@@ -104,10 +143,26 @@ struct PartDev {
   }
 
   void run(const Step& s) {
-    if (s.op <= kXu)
+    if (s.op <= kXu) {
+      if (nranks == 1 || !comm) return;
+      tic(4);
       exchange_nccl(s.op);
-    else
+      toc();
+    } else {
       kernel(s);
+    }
+  }
+
+  // SURVEY.md 8(d) accounting of this rank's rows (as sfeec_dev_step_bytes)
+  double op_bytes(int cls) const {
+    const double o1 = (double)(r1.own_hi - r1.own_lo), o2 = (double)(r2.own_hi - r2.own_lo);
+    switch (cls) {
+      case 0: return 12.0 * (double)q.nnz + 16.0 * o1;
+      case 1: return 5.0 * (double)c.nnz + 8.0 * o1 + 16.0 * o2;
+      case 2: return 5.0 * (double)ct.nnz + 8.0 * o2 + 16.0 * o1;
+      case 3: return 12.0 * (double)m2.nnz + 16.0 * o2;
+      default: return 0.0;
+    }
   }
 
   void advance(int64_t n) {
@@ -159,6 +214,82 @@ struct sfeec_part {
   PartDev d;
 };
 
+sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
+                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
+                             double mu0, int split_kind, int device, int flags, cudaStream_t s);
+
+namespace {
+
+void part_ranges(PartDev& d, const int64_t* edge_range, const int64_t* face_range) {
+  PartRange* rs[2] = {&d.r1, &d.r2};
+  const int64_t* in[2] = {edge_range, face_range};
+  for (int k = 0; k < 2; ++k) {
+    rs[k]->len = in[k][0];
+    rs[k]->own_lo = in[k][1];
+    rs[k]->own_hi = in[k][2];
+    rs[k]->first_len = in[k][3];
+    rs[k]->last_len = in[k][4];
+    require(0 <= rs[k]->own_lo && rs[k]->own_lo <= rs[k]->own_hi && rs[k]->own_hi <= rs[k]->len,
+            "partition: bad owned range");
+  }
+}
+
+void part_setup(PartDev& d, double dt, double eps0, double mu0, int rank, int nranks, int device) {
+  select_device(device);
+  d.device = device;
+  d.rank = rank;
+  d.nranks = nranks;
+  d.dt = dt;
+  d.eps0 = eps0;
+  d.mu0 = mu0;
+  SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+}
+
+// state vectors, reduction scratch and (multi-rank with an id) the NCCL
+// communicator -- collective over the ranks
+void part_finish(PartDev& d, const void* nccl_id) {
+  for (auto* v : {&d.e, &d.t}) {
+    v->alloc((size_t)std::max<int64_t>(1, d.r1.len));
+    v->zero(d.stream);
+  }
+  for (auto* v : {&d.b, &d.u}) {
+    v->alloc((size_t)std::max<int64_t>(1, d.r2.len));
+    v->zero(d.stream);
+  }
+  d.partials.alloc(kReduceBlocks + 1);
+  SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  if (d.nranks > 1 && nccl_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, d.nranks, id, d.rank), "ncclCommInitRank");
+  }
+}
+
+// partition.py plane_splits / entity_plane_offsets / slab_system: the rank's
+// {len, own_lo, own_hi, first_len, last_len} and {local start, owned lo, hi}
+void slab_range(const std::vector<int64_t>& base, int n, int rank, int nranks, int64_t rng[5],
+                int64_t glob[3]) {
+  const int64_t plane = (int64_t)(n + 1) * (n + 1);
+  std::vector<int64_t> off((size_t)n + 2);
+  for (int k = 0; k <= n + 1; ++k)
+    off[(size_t)k] = std::lower_bound(base.begin(), base.end(), (int64_t)k * plane) - base.begin();
+  const int p0 = (int)((int64_t)rank * (n + 1) / nranks);
+  const int p1 = (int)((int64_t)(rank + 1) * (n + 1) / nranks);
+  const int64_t g_lo = off[(size_t)std::max(p0 - 1, 0)];
+  const int64_t g_hi = off[(size_t)std::min(p1 + 1, n + 1)];
+  const int64_t o_lo = off[(size_t)p0], o_hi = off[(size_t)p1];
+  rng[0] = g_hi - g_lo;
+  rng[1] = o_lo - g_lo;
+  rng[2] = o_hi - g_lo;
+  rng[3] = off[(size_t)p0 + 1] - off[(size_t)p0];
+  rng[4] = off[(size_t)p1] - off[(size_t)p1 - 1];
+  glob[0] = g_lo;
+  glob[1] = o_lo;
+  glob[2] = o_hi;
+}
+
+}  // namespace
+
 extern "C" {
 
 int sfeec_part_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* ct,
@@ -176,49 +307,18 @@ int sfeec_part_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* c
     require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
     auto h = std::make_unique<sfeec_part>();
     PartDev& d = h->d;
-    PartRange* rs[2] = {&d.r1, &d.r2};
-    const int64_t* in[2] = {edge_range, face_range};
-    for (int k = 0; k < 2; ++k) {
-      rs[k]->len = in[k][0];
-      rs[k]->own_lo = in[k][1];
-      rs[k]->own_hi = in[k][2];
-      rs[k]->first_len = in[k][3];
-      rs[k]->last_len = in[k][4];
-      require(0 <= rs[k]->own_lo && rs[k]->own_lo <= rs[k]->own_hi && rs[k]->own_hi <= rs[k]->len,
-              "partition: bad owned range");
-    }
+    part_ranges(d, edge_range, face_range);
     const int64_t o1 = d.r1.own_hi - d.r1.own_lo, o2 = d.r2.own_hi - d.r2.own_lo;
     require(q->rows == o1 && q->cols == d.r1.len, "partition: Q must be owned edges x local edges");
     require(ct->rows == o1 && ct->cols == d.r2.len, "partition: C^T must be owned edges x local faces");
     require(c->rows == o2 && c->cols == d.r1.len, "partition: C must be owned faces x local edges");
     require(m2->rows == o2 && m2->cols == d.r2.len, "partition: M2 must be owned faces x local faces");
-    select_device(device);
-    d.device = device;
-    d.rank = rank;
-    d.nranks = nranks;
-    d.dt = dt;
-    d.eps0 = eps0;
-    d.mu0 = mu0;
-    SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    part_setup(d, dt, eps0, mu0, rank, nranks, device);
     d.q.upload(csr_from_view(*q), false, d.stream);
     d.c.upload(csr_from_view(*c), false, d.stream);
     d.ct.upload(csr_from_view(*ct), false, d.stream);
     d.m2.upload(csr_from_view(*m2), false, d.stream);
-    for (auto* v : {&d.e, &d.t}) {
-      v->alloc((size_t)std::max<int64_t>(1, d.r1.len));
-      v->zero(d.stream);
-    }
-    for (auto* v : {&d.b, &d.u}) {
-      v->alloc((size_t)std::max<int64_t>(1, d.r2.len));
-      v->zero(d.stream);
-    }
-    d.partials.alloc(kReduceBlocks + 1);
-    if (nranks > 1 && nccl_id) {
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
-      Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, nranks, id, rank), "ncclCommInitRank");
-    }
-    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    part_finish(d, nccl_id);
     *out = h.release();
   });
 }
@@ -325,5 +425,131 @@ int sfeec_part_energy_local(sfeec_part** hs, int nranks, double* out) {
 }
 
 int64_t sfeec_part_last_launches(sfeec_part* h) { return h ? h->d.launches : -1; }
+
+int sfeec_part_create_tet(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                          int rank, int nranks, const void* nccl_id, int device,
+                          sfeec_part** out, int64_t* info) {
+  return guarded([&] {
+    require(out != nullptr, "null out");
+    *out = nullptr;
+    require(n >= 1, "tet mesh: n must be >= 1");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    require(nranks <= n + 1, "partition: need nranks <= n + 1 vertex planes");
+    auto h = std::make_unique<sfeec_part>();
+    PartDev& d = h->d;
+    part_setup(d, dt > 0 ? dt : 0.0, eps0, mu0, rank, nranks, device);
+    int64_t er[5], fr[5], eg[3], fg[3];
+    DevTetSystem sys;
+    {
+      TetMesh mesh;
+      mesh.build(n, jitter, seed);
+      slab_range(mesh.edge_v, n, rank, nranks, er, eg);
+      slab_range(mesh.face_v, n, rank, nranks, fr, fg);
+      build_tet_system_device(mesh, false, sys, d.stream);
+    }
+    part_ranges(d, er, fr);
+    // owned rows, columns in the local (halo-extended) ranges
+    DevCSR lq, lct, lc, lm2;
+    slice_rows_device(sys.qsym, eg[1], eg[2], eg[0], er[0], lq, d.stream);
+    slice_rows_device(sys.ct, eg[1], eg[2], fg[0], fr[0], lct, d.stream);
+    slice_rows_device(sys.c, fg[1], fg[2], eg[0], er[0], lc, d.stream);
+    slice_rows_device(sys.m2, fg[1], fg[2], fg[0], fr[0], lm2, d.stream);
+    if (dt <= 0) {
+      // the single-GPU value: a dt = 1 handle on the full operators in the
+      // same layouts, 0.5 x 2 / nu (configs.cfl_dt)
+      DevOperator q, c, ct, m2;
+      q.upload_device(std::move(sys.qsym), d.stream);
+      m2.upload_device(std::move(sys.m2), d.stream);
+      c.upload_device(std::move(sys.c), d.stream);
+      ct.upload_device(std::move(sys.ct), d.stream);
+      cudaStream_t hs;
+      SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+      std::unique_ptr<sfeec_dev, void (*)(sfeec_dev*)> full(
+          make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2), nullptr,
+                            sys.n1, sys.n2, 1.0, eps0, mu0, SFEEC_SPLIT_STRANG, device,
+                            SFEEC_NO_CFL_WARN, hs),
+          sfeec_dev_destroy);
+      double nu = 0;
+      require(sfeec_dev_cfl_number(full.get(), &nu) == 0, "partition: CFL estimate failed");
+      require(nu > 0, "partition: zero CFL estimate");
+      d.dt = 0.5 * 2.0 * 1.0 / nu;
+    }
+    const int64_t n1 = sys.n1, n2 = sys.n2;
+    sys = DevTetSystem();
+    d.q.upload_device(std::move(lq), d.stream);
+    d.ct.upload_device(std::move(lct), d.stream);
+    d.c.upload_device(std::move(lc), d.stream);
+    d.m2.upload_device(std::move(lm2), d.stream);
+    part_finish(d, nccl_id);
+    if (info) {
+      info[0] = n1;
+      info[1] = n2;
+      for (int k = 0; k < 5; ++k) {
+        info[2 + k] = er[k];
+        info[7 + k] = fr[k];
+      }
+      for (int k = 0; k < 3; ++k) {
+        info[12 + k] = eg[k];
+        info[15 + k] = fg[k];
+      }
+      std::memcpy(&info[18], &d.dt, sizeof(double));
+    }
+    *out = h.release();
+  });
+}
+
+int sfeec_part_apply(sfeec_part* h, int which, const double* x_local, double* y_owned) {
+  return guarded([&] {
+    require(h && x_local && y_owned, "null argument");
+    auto& d = h->d;
+    DevOperator* ops[4] = {&d.q, &d.c, &d.ct, &d.m2};
+    require(which >= 0 && which < 4, "unknown operator");
+    DevOperator& a = *ops[which];
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    DevBuf<double> dx, dy;
+    dx.upload(x_local, (size_t)std::max<int64_t>(1, a.cols), d.stream);
+    dy.alloc((size_t)std::max<int64_t>(1, a.rows));
+    launch_spmv(a, dx.p, dy.p, 0.0, false, d.stream);
+    SFEEC_CUDA(cudaMemcpyAsync(y_owned, dy.p, sizeof(double) * (size_t)a.rows,
+                               cudaMemcpyDeviceToHost, d.stream));
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  });
+}
+
+int sfeec_part_device_ptrs(sfeec_part* h, double** b_local, double** e_local, void** stream) {
+  return guarded([&] {
+    require(h, "null handle");
+    if (b_local) *b_local = h->d.b.p;
+    if (e_local) *e_local = h->d.e.p;
+    if (stream) *stream = (void*)h->d.stream;
+  });
+}
+
+int sfeec_part_kernel_timing(sfeec_part* h, int enable, double* ms, int64_t* launches,
+                             double* bytes) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    d.collect_timing();
+    for (int k = 0; k < 5; ++k) {
+      if (ms) ms[k] = d.class_ms[k];
+      if (launches) launches[k] = d.class_launches[k];
+      if (bytes) bytes[k] = d.op_bytes(k);
+      d.class_ms[k] = 0;
+      d.class_launches[k] = 0;
+    }
+    d.timing = enable != 0;
+  });
+}
+
+// this rank's share of sfeec_dev_step_bytes: 12 nnz(Q) + 12 nnz(M2) +
+// 5 (nnz(C) + nnz(C^T)) + 16 (owned edges + owned faces)
+double sfeec_part_step_bytes(sfeec_part* h) {
+  if (!h) return 0;
+  const auto& d = h->d;
+  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz + 5.0 * (double)(d.c.nnz + d.ct.nnz) +
+         16.0 * (double)(d.r1.own_hi - d.r1.own_lo + d.r2.own_hi - d.r2.own_lo);
+}
 
 }  // extern "C"

@@ -16,6 +16,7 @@
 #include "device_util.cuh"
 #include "spmv_kernels.cuh"
 #include "stencil.cuh"
+#include "tet_device.hpp"
 #include "tet_mesh.hpp"
 
 namespace sfeec_b200 {
@@ -537,11 +538,49 @@ static void transpose_dev(const DevCSR& a, DevCSR& t, cudaStream_t s) {
   SFEEC_CUDA(cudaStreamSynchronize(s));
 }
 
-struct DevTetSystem {
-  DevCSR c, ct, m2, d, qsym;
-  int64_t n1 = 0, n2 = 0, nt = 0;
-  int64_t fallback = 0;
-};
+namespace {
+__global__ void k_slice_rp(int64_t n, const int64_t* __restrict__ rp, int64_t r0,
+                           int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) out[i] = rp[r0 + i] - rp[r0];
+}
+__global__ void k_slice_ci(int64_t nnz, const int32_t* __restrict__ ci, const double* __restrict__ v,
+                           int64_t off, int64_t c0, int64_t ncols, int32_t* __restrict__ oci,
+                           double* __restrict__ ov, int* __restrict__ bad) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int64_t c = (int64_t)ci[off + k] - c0;
+  if (c < 0 || c >= ncols) *bad = 1;
+  oci[k] = (int32_t)c;
+  ov[k] = v[off + k];
+}
+}  // namespace
+
+void slice_rows_device(const DevCSR& a, int64_t r0, int64_t r1, int64_t c0, int64_t ncols,
+                       DevCSR& out, cudaStream_t s) {
+  int64_t off = 0, end = 0;
+  SFEEC_CUDA(cudaMemcpyAsync(&off, a.rp.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaMemcpyAsync(&end, a.rp.p + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  out.rows = r1 - r0;
+  out.cols = ncols;
+  out.nnz = end - off;
+  out.rp.alloc((size_t)out.rows + 1);
+  out.ci.alloc((size_t)std::max<int64_t>(1, out.nnz));
+  out.val.alloc((size_t)std::max<int64_t>(1, out.nnz));
+  DevBuf<int> bad;
+  bad.alloc(1);
+  bad.zero(s);
+  k_slice_rp<<<nblk(out.rows + 1, 256), 256, 0, s>>>(out.rows, a.rp.p, r0, out.rp.p);
+  if (out.nnz)
+    k_slice_ci<<<nblk(out.nnz, 256), 256, 0, s>>>(out.nnz, a.ci.p, a.val.p, off, c0, ncols,
+                                                   out.ci.p, out.val.p, bad.p);
+  SFEEC_LAUNCH_CHECK();
+  int hb = 0;
+  SFEEC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  require(hb == 0, "partition: an owned row references entities beyond the one-plane halo");
+}
 
 // Builds the first-order S(M1) system of mesh `h` on the current device.
 void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s) {

@@ -1,0 +1,23 @@
+// Device-assembled tet system (tet_device.cu), shared with the partitioned
+// path (partition.cu).
+#pragma once
+#include "device_util.cuh"
+#include "tet_mesh.hpp"
+
+namespace sfeec_b200 {
+
+struct DevTetSystem {
+  DevCSR c, ct, m2, d, qsym;
+  int64_t n1 = 0, n2 = 0, nt = 0;
+  int64_t fallback = 0;
+};
+
+// C, D (optional), M1 -> S(M1) SPAI -> Q_sym, M2 and C^T of mesh `h`, built on
+// the current device, bitwise the host builders' operators
+void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s);
+
+// rows [r0, r1) of `a` with columns shifted by -c0 into [0, ncols)
+void slice_rows_device(const DevCSR& a, int64_t r0, int64_t r1, int64_t c0, int64_t ncols,
+                       DevCSR& out, cudaStream_t s);
+
+}  // namespace sfeec_b200

@@ -85,8 +85,24 @@ def slab_system(sys_, rank: int, nranks: int, q_sym: SparseOperator | None = Non
         edge_range=er, face_range=fr, edge_global=eg, face_global=fg)
 
 
+@dataclass
+class SlabInfo:
+    """Ranges of a device-built slab (sfeec_part_create_tet info)."""
+    rank: int
+    nranks: int
+    n1: int
+    n2: int
+    edge_range: np.ndarray
+    face_range: np.ndarray
+    edge_global: tuple
+    face_global: tuple
+    dt: float
+
+
 class TetPart:
     """One rank's partitioned device leapfrog (sfeec_part)."""
+
+    KERNEL_CLASSES = ("K-Q", "K-Cb", "K-CTe", "K-M2", "exchange")
 
     def __init__(self, ls: LocalSystem, dt: float, eps0=1.0, mu0=1.0, nccl_id: bytes | None = None,
                  device: int = 0):
@@ -100,6 +116,33 @@ class TetPart:
                                           device, C.byref(h)))
         self._h = h
         self.ls = ls
+
+    @classmethod
+    def from_device(cls, n: int, jitter: float, seed: int, rank: int, nranks: int,
+                    dt: float = 0.0, eps0=1.0, mu0=1.0, nccl_id: bytes | None = None,
+                    device: int = 0) -> "TetPart":
+        """Rank `rank`'s slab of the config-1/3/5 tet system, assembled and
+        row-sliced on its own device (no host CSR). dt <= 0: 0.5 x the CFL
+        estimate of the full operators (bitwise configs.cfl_dt of the
+        single-GPU tet_device_scheme)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        info = np.zeros(19, np.int64)
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        L.check(L.lib().sfeec_part_create_tet(int(n), float(jitter), int(seed), float(dt), eps0,
+                                              mu0, int(rank), int(nranks), idbuf, int(device),
+                                              C.byref(h), L.i64ptr(info)))
+        self._h = h
+        self._keep = None
+        self.ls = SlabInfo(rank, nranks, int(info[0]), int(info[1]), info[2:7].copy(),
+                           info[7:12].copy(), tuple(int(x) for x in info[12:15]),
+                           tuple(int(x) for x in info[15:18]),
+                           float(info[18:19].view(np.float64)[0]))
+        return self
+
+    @property
+    def dt(self) -> float:
+        return self.ls.dt
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -132,6 +175,39 @@ class TetPart:
         out = C.c_double()
         L.check(L.lib().sfeec_part_energy(self._h, C.byref(out)))
         return out.value
+
+    def apply(self, which: str, x_local: np.ndarray) -> np.ndarray:
+        """Owned rows of A x for a local-range x (A in q, c, ct, m2)."""
+        k = {"q": 0, "c": 1, "ct": 2, "m2": 3}[which]
+        er, fr = self.ls.edge_range, self.ls.face_range
+        ncols = int(er[0] if which in ("q", "c") else fr[0])
+        nrows = int(er[2] - er[1] if which in ("q", "ct") else fr[2] - fr[1])
+        x = np.ascontiguousarray(x_local, np.float64)
+        if x.shape != (ncols,):
+            raise ValueError(f"apply({which}): x must have {ncols} entries")
+        y = np.zeros(nrows)
+        L.check(L.lib().sfeec_part_apply(self._h, k, L.dptr(x), L.dptr(y)))
+        return y
+
+    def device_ptrs(self):
+        """(b_local, e_local, stream) device addresses."""
+        b, e, s = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.check(L.lib().sfeec_part_device_ptrs(self._h, C.byref(b), C.byref(e), C.byref(s)))
+        return b.value, e.value, s.value
+
+    def last_launches(self) -> int:
+        return int(L.lib().sfeec_part_last_launches(self._h))
+
+    def step_bytes(self) -> float:
+        return float(L.lib().sfeec_part_step_bytes(self._h))
+
+    def kernel_timing(self, enable: bool = True) -> dict:
+        """Per-class device time since the last call (then (dis)arm timing)."""
+        ms, n, by = np.zeros(5), np.zeros(5, np.int64), np.zeros(5)
+        L.check(L.lib().sfeec_part_kernel_timing(self._h, 1 if enable else 0, L.dptr(ms),
+                                                 L.i64ptr(n), L.dptr(by)))
+        return {k: {"ms": ms[i], "launches": int(n[i]), "bytes_per_launch": by[i]}
+                for i, k in enumerate(self.KERNEL_CLASSES)}
 
 
 def advance_local(parts: list[TetPart], n: int) -> None:

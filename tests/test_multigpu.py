@@ -214,3 +214,41 @@ def test_tet_partition_lockstep_bitwise_equals_single(tet_sys, world):
         p.fetch_into(b, e)
     assert np.array_equal(b, ref.first) and np.array_equal(e, ref.e)
     assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_tet_device_slabs_bitwise_equal_single_device(world):
+    """Slabs assembled and row-sliced on the device (the multi-GPU bench
+    setup): same ranges as the host slicing, the single-GPU dt bitwise, the
+    initial b = C a from local potentials, and 20 lockstep steps bitwise the
+    single-GPU device scheme."""
+    from paper_2301_01753_b200 import inputs
+    n, jit, seed = 7, 0.1, 2023
+    one = S.tet_device_scheme(n, jit, seed=seed, dt=1.0, with_div=False)
+    dt = configs.cfl_dt(one)
+    one.set_dt(dt)
+    parts = [partition.TetPart.from_device(n, jit, seed, r, world) for r in range(world)]
+    sys_ = configs.tet_system(n, jit, seed=seed)
+    a = inputs.gaussian(7, one._n1)
+    b0 = one.apply("c", a)
+    e0 = np.zeros(one._n1)
+    for r, p in enumerate(parts):
+        assert p.dt == dt
+        assert (p.ls.n1, p.ls.n2) == (one._n1, one._n2)
+        ls = partition.slab_system(sys_, r, world)
+        assert np.array_equal(p.ls.edge_range, ls.edge_range)
+        assert np.array_equal(p.ls.face_range, ls.face_range)
+        assert p.ls.edge_global == ls.edge_global and p.ls.face_global == ls.face_global
+        eg, er, fg = p.ls.edge_global, p.ls.edge_range, p.ls.face_global
+        assert np.array_equal(p.apply("c", a[eg[0]:eg[0] + er[0]]), b0[fg[1]:fg[2]])
+        p.load_global(b0, e0)
+    ref = one.advance(S.make_state(S.Formulation.BE, b0, e0), 20)
+    partition.advance_local(parts, 20)
+    b, e = np.zeros(one._n2), np.zeros(one._n1)
+    for p in parts:
+        p.fetch_into(b, e)
+    assert np.array_equal(b, ref.first) and np.array_equal(e, ref.e)
+    assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
+    t = parts[0].kernel_timing(True)
+    assert set(t) == set(partition.TetPart.KERNEL_CLASSES)
