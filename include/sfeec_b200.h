@@ -273,6 +273,17 @@ int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_ve
 /* which: 0 C (faces x interior edges, +-1), 1 M1 (interior edges), 2 M2
  * (faces), 3 D (tets x faces, +-1) */
 int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
+/* Second-order trimmed forms P2^- on the same mesh (BASELINE config 4; the
+ * reference's P2^- is 2-D only, form_space.cpp:41-166 -- the 3-D element
+ * follows its DOF conventions). 1-forms: 2 moments per
+ * interior edge + 2 per interior face; 2-forms: 3 per face + 3 per tet;
+ * 3-forms: 4 per tet. k-major numbering (z-slabs are contiguous ranges). */
+int sfeec_tetmesh_p2_counts(const sfeec_tetmesh* h, int64_t* n1, int64_t* n2, int64_t* n3);
+/* which: 0 C (N2 x N1), 1 M1, 2 M2, 3 D (N3 x N2) */
+int sfeec_tetmesh_p2_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
+/* per DOF of form 1 or 2: entity id (edge / face for 1-forms, face / tet for
+ * 2-forms) and kind | slot << 1 (kind 0 = the lower-dimensional entity) */
+int sfeec_tetmesh_p2_dofs(const sfeec_tetmesh* h, int form, int64_t* entity, int8_t* kind_slot);
 /* The same first-order S(M1) system assembled ON THE DEVICE (C, D, M1, M2,
  * SPAI, Q_sym; bitwise the host builders' operators) and wrapped in a
  * leapfrog handle (BE formulation). counts = {N1, N2, T} (nullable). The

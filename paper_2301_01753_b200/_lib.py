@@ -147,6 +147,9 @@ _SIGS = {
     "sfeec_tetmesh_counts": (C.c_int, [_P, _PI64, _PI64, _PI64, _PI64]),
     "sfeec_tetmesh_geometry": (C.c_int, [_P, _PD, _PI64, _PI64, _PI64]),
     "sfeec_tetmesh_operator": (C.c_int, [_P, C.c_int, C.POINTER(sfeec_csr_owned)]),
+    "sfeec_tetmesh_p2_counts": (C.c_int, [_P, _PI64, _PI64, _PI64]),
+    "sfeec_tetmesh_p2_operator": (C.c_int, [_P, C.c_int, C.POINTER(sfeec_csr_owned)]),
+    "sfeec_tetmesh_p2_dofs": (C.c_int, [_P, C.c_int, _PI64, C.POINTER(C.c_int8)]),
     "sfeec_make_pattern": (C.c_int, [C.POINTER(sfeec_csr), C.c_int,
                                      C.POINTER(sfeec_csr_owned)]),
     "sfeec_spai": (C.c_int, [C.POINTER(sfeec_csr), C.c_int, C.POINTER(sfeec_csr_owned), _PD]),

@@ -518,6 +518,28 @@ class TetMesh:
     def div(self) -> SparseOperator:
         return self._op(3)
 
+    # ---- second order (P2^-, BASELINE config 4) ----
+    def p2_counts(self) -> tuple[int, int, int]:
+        """(N1, N2, N3) of the P2^- 1-, 2- and 3-form spaces (PEC)."""
+        c = [C.c_int64() for _ in range(3)]
+        L.check(L.lib().sfeec_tetmesh_p2_counts(self._h, *[C.byref(x) for x in c]))
+        return tuple(x.value for x in c)
+
+    def p2_operator(self, which: str) -> SparseOperator:
+        """'c' (N2 x N1), 'm1', 'm2' or 'd' (N3 x N2) of the P2^- system."""
+        k = {"c": 0, "m1": 1, "m2": 2, "d": 3}[which]
+        out = L.sfeec_csr_owned()
+        L.check(L.lib().sfeec_tetmesh_p2_operator(self._h, k, C.byref(out)))
+        return SparseOperator._from_owned(out, which in ("m1", "m2"))
+
+    def p2_dofs(self, form: int):
+        """(entity id, kind | slot << 1) per P2^- DOF of form 1 or 2."""
+        n = self.p2_counts()[form - 1]
+        ent, ks = np.zeros(n, np.int64), np.zeros(n, np.int8)
+        L.check(L.lib().sfeec_tetmesh_p2_dofs(self._h, form, L.i64ptr(ent),
+                                              ks.ctypes.data_as(C.POINTER(C.c_int8))))
+        return ent, ks
+
 
 def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.0,
                       kind: SplitKind = SplitKind.Strang, units: UnitSystem | None = None,
