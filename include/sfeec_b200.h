@@ -284,6 +284,22 @@ int sfeec_tetmesh_p2_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned
 /* per DOF of form 1 or 2: entity id (edge / face for 1-forms, face / tet for
  * 2-forms) and kind | slot << 1 (kind 0 = the lower-dimensional entity) */
 int sfeec_tetmesh_p2_dofs(const sfeec_tetmesh* h, int form, int64_t* entity, int8_t* kind_slot);
+/* The config-4 system on the device: C, M1, M2 (D) from the host builders,
+ * then S(M1^2) with the M1^2 values, the SPAI on S(M1^2) (one CTA per
+ * column: blocked Cholesky of the ~300x300 Gram, the 1e-12 trace pivot test
+ * of spai.cpp:213-216), Q_sym and C^T on the GPU, wrapped in a leapfrog
+ * handle (BE). counts (nullable, 5) = {N1, N2, N3, nnz(Q_sym), fallback
+ * columns}. Columns failing the pivot test -> EINVAL (host builder). */
+int sfeec_p2_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                        int split_kind, int device, int flags, int with_div, sfeec_dev** out,
+                        int64_t* counts);
+/* the device-built config-4 operators, downloaded (nullable outputs) */
+int sfeec_p2_dev_operators(int n, double jitter, uint64_t seed, int device, sfeec_csr_owned* c,
+                           sfeec_csr_owned* m2, sfeec_csr_owned* d, sfeec_csr_owned* q_sym,
+                           sfeec_csr_owned* ct);
+/* the device S(M1^2) SPAI of a caller's symmetric M1 (Q by rows, not
+ * symmetrised; spai_approximate_inverse with PatternKind::M1Squared) */
+int sfeec_p2_spai_device(const sfeec_csr* m1, int device, sfeec_csr_owned* q, int64_t* fallback);
 /* The same first-order S(M1) system assembled ON THE DEVICE (C, D, M1, M2,
  * SPAI, Q_sym; bitwise the host builders' operators) and wrapped in a
  * leapfrog handle (BE formulation). counts = {N1, N2, T} (nullable). The

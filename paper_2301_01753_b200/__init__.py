@@ -22,6 +22,9 @@ from .scheme import (  # noqa: F401
     device_count,
     make_state,
     operator_from_triplets,
+    p2_device_operators,
+    p2_device_scheme,
+    spai_device,
     scaled_identity,
     symmetric_part,
     tet_device_operators,

@@ -150,6 +150,13 @@ _SIGS = {
     "sfeec_tetmesh_p2_counts": (C.c_int, [_P, _PI64, _PI64, _PI64]),
     "sfeec_tetmesh_p2_operator": (C.c_int, [_P, C.c_int, C.POINTER(sfeec_csr_owned)]),
     "sfeec_tetmesh_p2_dofs": (C.c_int, [_P, C.c_int, _PI64, C.POINTER(C.c_int8)]),
+    "sfeec_p2_dev_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                      C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(_P), _PI64]),
+    "sfeec_p2_dev_operators": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int] +
+                               [C.POINTER(sfeec_csr_owned)] * 5),
+    "sfeec_p2_spai_device": (C.c_int, [C.POINTER(sfeec_csr), C.c_int, C.POINTER(sfeec_csr_owned),
+                                       _PI64]),
     "sfeec_make_pattern": (C.c_int, [C.POINTER(sfeec_csr), C.c_int,
                                      C.POINTER(sfeec_csr_owned)]),
     "sfeec_spai": (C.c_int, [C.POINTER(sfeec_csr), C.c_int, C.POINTER(sfeec_csr_owned), _PD]),

@@ -471,7 +471,7 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (
 }  // namespace
 
 
-static void exclusive_scan(int64_t* d, int64_t n, cudaStream_t s) {
+void exclusive_scan(int64_t* d, int64_t n, cudaStream_t s) {
   // in-place exclusive scan of n + 1 entries (last = total)
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, d, d, n + 1, s);
@@ -498,7 +498,7 @@ static void build_op(const DMesh& m, int64_t rows, int64_t cols, DevCSR& out, cu
   SFEEC_LAUNCH_CHECK();
 }
 
-static void transpose_dev(const DevCSR& a, DevCSR& t, cudaStream_t s) {
+void transpose_dev(const DevCSR& a, DevCSR& t, cudaStream_t s) {
   t.rows = a.cols;
   t.cols = a.rows;
   t.nnz = a.nnz;
@@ -536,6 +536,12 @@ static void transpose_dev(const DevCSR& a, DevCSR& t, cudaStream_t s) {
   cub::DeviceScan::InclusiveSum(tb2.p, tmp2, (int64_t*)cnt.p, t.rp.p, t.rows + 1, s);
   SFEEC_LAUNCH_CHECK();
   SFEEC_CUDA(cudaStreamSynchronize(s));
+}
+
+void qsym_device(int64_t n, const int64_t* rp, const int32_t* ci, const double* qcol, double* out,
+                 cudaStream_t s) {
+  k_qsym<<<nblk(n, 256), 256, 0, s>>>(n, rp, ci, qcol, out);
+  SFEEC_LAUNCH_CHECK();
 }
 
 namespace {

@@ -16,6 +16,15 @@ struct DevTetSystem {
 // the current device, bitwise the host builders' operators
 void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s);
 
+// in-place exclusive scan of d[0..n] (d[n] = total)
+void exclusive_scan(int64_t* d, int64_t n, cudaStream_t s);
+// t = a^T (cub radix sort on (col, row) keys)
+void transpose_dev(const DevCSR& a, DevCSR& t, cudaStream_t s);
+// out[k] = 0.5 Q(r, c) + 0.5 Q(c, r) on a symmetric pattern (rp, ci), where
+// qcol holds the SPAI columns in pattern layout (qcol[rp[c] + a] = q_c[a])
+void qsym_device(int64_t n, const int64_t* rp, const int32_t* ci, const double* qcol, double* out,
+                 cudaStream_t s);
+
 // rows [r0, r1) of `a` with columns shifted by -c0 into [0, ncols)
 void slice_rows_device(const DevCSR& a, int64_t r0, int64_t r1, int64_t c0, int64_t ncols,
                        DevCSR& out, cudaStream_t s);

@@ -582,6 +582,48 @@ def tet_device_operators(n: int, jitter: float = 0.1, seed: int = 0, device: int
     return {k: SparseOperator._from_owned(o, k in ("m2", "q_sym")) for k, o in zip(names, outs)}
 
 
+def p2_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.0,
+                     kind: SplitKind = SplitKind.Strang, units: UnitSystem | None = None,
+                     with_div: bool = True, warn_cfl: bool = False,
+                     device: int = 0) -> "SplitScheme":
+    """Second-order P2^- system with the S(M1^2) SPAI (BASELINE config 4):
+    C, M1, M2, D from the host builders; S(M1^2), SPAI, Q_sym and C^T on the
+    B200; wrapped as a (b, e) SplitScheme."""
+    units = units or UnitSystem()
+    h = C.c_void_p()
+    counts = np.zeros(5, np.int64)
+    flags = 0 if warn_cfl else L.NO_CFL_WARN
+    L.check(L.lib().sfeec_p2_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
+                                        units.mu0, int(SplitKind(kind)), device, flags,
+                                        1 if with_div else 0, C.byref(h), L.i64ptr(counts)))
+    s = SplitScheme.__new__(SplitScheme)
+    s._h = h
+    s._kind, s._dt, s._units = SplitKind(kind), float(dt), units
+    s._formulation = Formulation.BE
+    s._c = s._m2 = None
+    s._n1, s._n2 = int(counts[0]), int(counts[1])
+    s.n3, s.nnz_q = int(counts[2]), int(counts[3])
+    return s
+
+
+def p2_device_operators(n: int, jitter: float = 0.1, seed: int = 0, device: int = 0) -> dict:
+    """Device-built config-4 C, M2, D, Q_sym and C^T, downloaded (parity tests)."""
+    outs = [L.sfeec_csr_owned() for _ in range(5)]
+    L.check(L.lib().sfeec_p2_dev_operators(int(n), float(jitter), int(seed), device,
+                                           *[C.byref(o) for o in outs]))
+    names = ("c", "m2", "d", "q_sym", "ct")
+    return {k: SparseOperator._from_owned(o, k in ("m2", "q_sym")) for k, o in zip(names, outs)}
+
+
+def spai_device(m: SparseOperator, device: int = 0):
+    """S(M1^2) SPAI of m on the GPU -> (Q by rows, fallback columns)."""
+    out = L.sfeec_csr_owned()
+    fb = C.c_int64()
+    v = m.view()
+    L.check(L.lib().sfeec_p2_spai_device(C.byref(v), device, C.byref(out), C.byref(fb)))
+    return SparseOperator._from_owned(out), fb.value
+
+
 PATTERNS = {"diagonal": 0, "m1": 1, "m1sq": 2}
 
 
