@@ -51,6 +51,12 @@ CONFIGS = {
     "tet128": dict(kind="tet", n=128, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
                    desc="BASELINE configs[2]: 128^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) "
                         "SPAI, PEC, Gaussian pulse width 0.1, dt = 0.5 CFL"),
+    "p2_64": dict(kind="p2", n=64, jitter=0.1, init="gaussian", dtype="f64", ref_n=10,
+                  desc="BASELINE configs[3]: 64^3 x 6 Kuhn tets, jitter 0.1h, P2-, S(M1^2) "
+                       "(2-ring) SPAI, PEC, dt = 0.5 CFL"),
+    "p2_32": dict(kind="p2", n=32, jitter=0.1, init="gaussian", dtype="f64", ref_n=10,
+                  desc="32^3 x 6 Kuhn tets, jitter 0.1h, P2-, S(M1^2) SPAI, PEC (smaller "
+                       "config-4 system)"),
     "tet256": dict(kind="tet", n=256, jitter=0.1, init="pulse", npulses=8, dtype="f64", ref_n=64,
                    desc="BASELINE configs[4]: 256^3 x 6 Kuhn tets (100.7M tets), jitter 0.1h, "
                         "P1-, S(M1) SPAI, PEC, 8 Gaussian pulses, dt = 0.5 CFL"),
@@ -211,6 +217,12 @@ def tet_setup(cfg, device):
     import paper_2301_01753_b200 as S
     from paper_2301_01753_b200 import configs, inputs
     t0 = time.perf_counter()
+    if cfg["kind"] == "p2":
+        s = S.p2_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
+                               device=device)
+        b0 = s.apply("c", inputs.gaussian(7, s._n1))
+        s.set_dt(configs.cfl_dt(s))
+        return (s._n1, s._n2), s, b0, np.zeros(s._n1), time.perf_counter() - t0
     s = S.tet_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
                             device=device)
     mesh = S.TetMesh(cfg["n"], cfg["jitter"], 2023)  # host geometry for the initial A
@@ -383,6 +395,8 @@ def run_ours(args, rank, world, local_rank):
     if cfg["kind"] == "yee":
         R = YeeRunner(cfg, local_rank, rank, world, dist)
     elif world > 1 or args.partitioned:
+        if cfg["kind"] == "p2":
+            raise SystemExit("the P2 (config 4) bench path is single-GPU in this build")
         R = TetSlabRunner(cfg, local_rank, rank, world, dist)
     else:
         R = TetRunner(cfg, local_rank)
@@ -502,6 +516,15 @@ def _ref_operators(config):
         return q, tup(c), m2, spmv(c, a), np.zeros(n1), 0.5 / (np.sqrt(3.0) * n), \
             f"{n}^3 PEC Yee lattice (lumped masses)"
     from paper_2301_01753_b200 import configs
+    if cfg["kind"] == "p2":
+        from paper_2301_01753_b200 import inputs
+        from paper_2301_01753_b200.configs import spmv
+        mesh = S.TetMesh(n, cfg["jitter"], 2023)
+        c, m1, m2 = mesh.p2_operator("c"), mesh.p2_operator("m1"), mesh.p2_operator("m2")
+        q, _ = S.spai_approximate_inverse(m1, "m1sq")
+        a = inputs.gaussian(7, c.cols)
+        return tup(q), tup(c), tup(m2), spmv(c, a), np.zeros(c.cols), 1e-3, \
+            f"{n}^3 x 6 Kuhn tets (P2-, S(M1^2) SPAI)"
     sys_ = configs.tet_system(n, cfg["jitter"], seed=2023)
     b0, e0, _ = (configs.initial_gaussian(sys_, seed=7) if cfg["init"] == "gaussian"
                  else configs.initial_pulse(sys_, seed=7))

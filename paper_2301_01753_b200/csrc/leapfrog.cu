@@ -569,9 +569,12 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
     // 12 B per fp64 nonzero, 5 B per incidence entry (int8 sign + int32
     // column), 8 B per vector element read or written)
     if (bytes) {
+      // an incidence C (+-1) streams 5 B per entry, a general one (P2-) 12 B
+      const double cb = d.c.layout == DevOperator::kSigned ? 5.0 : 12.0;
+      const double ctb = d.ct.layout == DevOperator::kSigned ? 5.0 : 12.0;
       bytes[0] = 12.0 * d.q.nnz + 16.0 * d.n1;   // t = Q e: e gathered once, t written
-      bytes[1] = 5.0 * d.c.nnz + 8.0 * d.n1 + 16.0 * d.n2;  // b -= h C t
-      bytes[2] = 5.0 * d.ct.nnz + 8.0 * d.n2 + 16.0 * d.n1; // e += f C^T u
+      bytes[1] = cb * d.c.nnz + 8.0 * d.n1 + 16.0 * d.n2;  // b -= h C t
+      bytes[2] = ctb * d.ct.nnz + 8.0 * d.n2 + 16.0 * d.n1; // e += f C^T u
       bytes[3] = 12.0 * d.m2.nnz + 16.0 * d.n2;  // u = M2 b
       bytes[4] = 0;
     }
@@ -579,11 +582,13 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
   });
 }
 
-// 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2)
+// 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2); a
+// non-incidence C (P2-, config 4) streams 12 B per entry
 double sfeec_dev_step_bytes(sfeec_dev* h) {
   if (!h) return 0;
   auto& d = h->d;
-  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz + 10.0 * (double)d.c.nnz +
+  const double cb = d.c.layout == DevOperator::kSigned ? 5.0 : 12.0;  // +-1 incidence or P2-
+  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz + 2.0 * cb * (double)d.c.nnz +
          16.0 * (double)(d.n1 + d.n2);
 }
 

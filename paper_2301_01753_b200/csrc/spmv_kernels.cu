@@ -54,6 +54,39 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0 && row < rows) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
 }
 
+// ---- wide rows (avg >= 64 nnz, e.g. the S(M1^2) SPAI of config 4): a warp
+// per row, U entries per lane per round with every column/value load issued
+// before any gather and every gather before any FMA; the operator is
+// streamed (ld.global.cs) so L2 keeps the gathered vector.
+template <bool ACC, int U>
+__global__ void __launch_bounds__(kThreads)
+    k_csr_wide(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+               const double* __restrict__ v, const double* __restrict__ x,
+               double* __restrict__ y, double alpha) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t b = __ldg(rp + row), e = __ldg(rp + row + 1);
+  double acc = 0.0;
+  for (int64_t k0 = b + lane; k0 < e; k0 += 32 * U) {
+    int c[U];
+    double w[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + 32 * u;
+      c[u] = k < e ? __ldcs(ci + k) : 0;
+      w[u] = k < e ? __ldcs(v + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fma(w[u], xv[u], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[row] = ACC ? fma(alpha, acc, y[row]) : acc;
+}
+
 // ---- sliced layout: persistent warps, one lane per row -------------------
 // Warp w processes slices w, w + W, w + 2W, ... (W = warps in the grid). The
 // metadata of the next slice and the y value of the current row (for the
@@ -242,6 +275,14 @@ inline unsigned blocks_for(int64_t threads) {
 
 }  // namespace
 
+// rows this wide stream better as plain CSR with a warp per row
+// (k_csr_wide) than sliced; SFEEC_WIDE_CSR=0 keeps the sliced layout (A/B)
+static bool wide_rows(double avg) {
+  const char* env = std::getenv("SFEEC_WIDE_CSR");
+  if (env && std::atoi(env) == 0) return false;
+  return avg >= 64.0;
+}
+
 void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   rows = h.rows;
   cols = h.cols;
@@ -253,7 +294,7 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   tpr = 1;
   while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
   layout = kCsr;
-  if (strict_only || rows == 0 || nnz == 0) {
+  if (strict_only || rows == 0 || nnz == 0 || wide_rows(avg)) {
     SFEEC_CUDA(cudaStreamSynchronize(s));
     return;
   }
@@ -451,7 +492,7 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
   const double avg = rows ? (double)nnz / (double)rows : 0.0;
   tpr = 1;
   while (tpr < 32 && tpr * 2 <= avg) tpr *= 2;
-  if (rows == 0 || nnz == 0) {
+  if (rows == 0 || nnz == 0 || wide_rows(avg)) {
     adopt_csr(std::move(d));
     return;
   }
@@ -577,6 +618,17 @@ template <bool ACC>
 static void launch_vec(const DevOperator& a, const double* x, double* y, double alpha,
                        cudaStream_t s) {
   unsigned g = blocks_for(a.rows * a.tpr);
+  if (a.tpr == 32) {
+    const char* env = std::getenv("SFEEC_WIDE_U");
+    const int u = env ? std::atoi(env) : 4;
+    if (u == 2)
+      k_csr_wide<ACC, 2><<<g, kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p, x, y, alpha);
+    else if (u == 8)
+      k_csr_wide<ACC, 8><<<g, kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p, x, y, alpha);
+    else
+      k_csr_wide<ACC, 4><<<g, kThreads, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p, x, y, alpha);
+    return;
+  }
   switch (a.tpr) {
 #define SFEEC_TPR(T)                                                                   \
   case T:                                                                              \
