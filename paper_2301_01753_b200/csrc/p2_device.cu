@@ -12,7 +12,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -101,9 +104,9 @@ __global__ void k_sq_rows(int64_t n, const int64_t* __restrict__ rp, const int32
 }
 
 // ---- large-pattern SPAI ----------------------------------------------------
-constexpr int kT = 256;    // threads per CTA
+constexpr int kT = 512;    // threads per CTA
 constexpr int kNb = 32;    // panel width
-constexpr int kKmax = 512; // largest pattern column
+constexpr int kKmax = 512; // largest pattern column (= kT: a panel row per thread)
 
 struct SpaiSmem {
   double panel[kKmax * kNb];
@@ -112,6 +115,8 @@ struct SpaiSmem {
   double lbb[kNb * kNb];
   int32_t idx[kKmax];
   double red[kT / 32];
+  double colj[kNb];
+  double piv;
 };
 
 __device__ __forceinline__ int find_sorted(const int32_t* a, int k, int32_t v) {
@@ -155,7 +160,8 @@ __global__ void __launch_bounds__(kT, 1)
       S.idx[a] = pci[b0 + a];
       S.y[a] = 0.0;
     }
-    for (int64_t e = tid; e < (int64_t)k * k; e += kT) G[e] = 0.0;
+    for (int bcol = warp; bcol < k; bcol += kT / 32)  // lower triangle only
+      for (int a = bcol + lane; a < k; a += 32) G[a + (int64_t)bcol * ld] = 0.0;
     __syncthreads();
     // Gram: G(a, b) = (M^2)(I_a, I_b), lower triangle (I_b <= I_a)
     for (int a = warp; a < k; a += kT / 32) {
@@ -182,41 +188,58 @@ __global__ void __launch_bounds__(kT, 1)
     bool ok = true;
     for (int p0 = 0; p0 < k && ok; p0 += kNb) {
       const int w = min(kNb, k - p0), m = k - p0;
-      double* P = S.panel;  // P[i + j m], column j of the panel, rows p0 + i
-      for (int e = tid; e < m * w; e += kT) {
-        const int i = e % m, j = e / m;
-        P[e] = G[(p0 + i) + (int64_t)(p0 + j) * ld];
-      }
-      __syncthreads();
-      for (int j = 0; j < w; ++j) {
-        const double d = P[j + j * m];
-        if (!(d > 0.0)) {
-          ok = false;
-          break;
+      // panel factorization with the panel rows in registers: thread i owns
+      // panel row i (m <= kKmax = kT); per column: pivot, scale, rank-1 update
+      // of the later panel columns from the broadcast column j
+      double* P = S.panel;  // P[i + j m]: the factored panel, for the trailing update
+      const int i = tid;
+      double r[kNb];
+#pragma unroll
+      for (int j = 0; j < kNb; ++j)
+        r[j] = (i < m && j < w && i >= j) ? G[(p0 + i) + (int64_t)(p0 + j) * ld] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kNb; ++j) {
+        if (j < w && ok) {  // uniform
+          if (i == j) S.piv = r[j];
+          __syncthreads();
+          const double d = S.piv;
+          if (d > 0.0) {
+            dmin = fmin(dmin, d);
+            const double inv = rsqrt(d);  // one rsqrt instead of sqrt + divide per step
+            if (i == j)
+              r[j] = d * inv;
+            else if (i > j)
+              r[j] = r[j] * inv;
+            if (i > j && i < w) S.colj[i] = r[j];
+          } else {
+            ok = false;
+          }
+          __syncthreads();
+          if (ok) {
+#pragma unroll
+            for (int jj = j + 1; jj < kNb; ++jj)
+              if (jj < w && i >= jj) r[jj] = fma(-r[j], S.colj[jj], r[jj]);
+          }
         }
-        dmin = fmin(dmin, d);
-        const double ljj = sqrt(d);
-        __syncthreads();
-        for (int i = j + tid; i < m; i += kT) P[i + j * m] = i == j ? ljj : P[i + j * m] / ljj;
-        __syncthreads();
-        const int nc = w - j - 1;
-        for (int e = tid; e < (m - j - 1) * nc; e += kT) {
-          const int jj = j + 1 + e / (m - j - 1);
-          const int i = j + 1 + e % (m - j - 1);
-          if (i >= jj) P[i + jj * m] -= P[i + j * m] * P[jj + j * m];
-        }
-        __syncthreads();
       }
       if (!ok) break;
-      for (int e = tid; e < m * w; e += kT) {
-        const int i = e % m, j = e / m;
-        if (i >= j) G[(p0 + i) + (int64_t)(p0 + j) * ld] = P[e];
+      if (i < m) {
+#pragma unroll
+        for (int j = 0; j < kNb; ++j)
+          if (j < w) {
+            P[i + j * m] = r[j];
+            if (i >= j) G[(p0 + i) + (int64_t)(p0 + j) * ld] = r[j];
+          }
       }
-      // trailing update of rows / cols [p0 + w, k): 64 x 64 tiles, 4 x 4 per thread
+      __syncthreads();
+      // trailing update of rows / cols [p0 + w, k): 64 x 64 tiles, 4 x 4 per
+      // thread, two 256-thread groups on alternate tiles; the G tile is loaded
+      // before the panel products so its latency overlaps them
       const int mt = m - w;
       const int ntile = (mt + 63) / 64;
-      const int tx = tid & 15, ty = tid >> 4;
-      for (int tile = 0; tile < ntile * (ntile + 1) / 2; ++tile) {
+      const int t256 = tid & 255, grp = tid >> 8;
+      const int tx = t256 & 15, ty = t256 >> 4;
+      for (int tile = grp; tile < ntile * (ntile + 1) / 2; tile += kT / 256) {
         int ti = 0;
         while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
         const int tj = tile - ti * (ti + 1) / 2;
@@ -224,7 +247,11 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+          for (int v = 0; v < 4; ++v) {
+            const int r = ti * 64 + tx + 16 * u, c = tj * 64 + ty + 16 * v;
+            acc[u][v] = (r < mt && c < mt && r >= c)
+                            ? G[(p0 + w + r) + (int64_t)(p0 + w + c) * ld] : 0.0;
+          }
         for (int t = 0; t < w; ++t) {
           double a[4], bv[4];
 #pragma unroll
@@ -240,17 +267,14 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], bv[v], acc[u][v]);
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(-a[u], bv[v], acc[u][v]);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             const int r = ti * 64 + tx + 16 * u, c = tj * 64 + ty + 16 * v;
-            if (r < mt && c < mt && r >= c) {
-              double* g = G + (p0 + w + r) + (int64_t)(p0 + w + c) * ld;
-              *g = *g - acc[u][v];
-            }
+            if (r < mt && c < mt && r >= c) G[(p0 + w + r) + (int64_t)(p0 + w + c) * ld] = acc[u][v];
           }
       }
       __syncthreads();
@@ -374,9 +398,23 @@ int64_t spai_big_device(const DevCSR& m1, const DevCSR& sq, DevBuf<double>& qcol
   qcol.alloc((size_t)std::max<int64_t>(1, sq.nnz));
   const size_t smem = sizeof(SpaiSmem);
   SFEEC_CUDA(cudaFuncSetAttribute(k_spai_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0, e1;
+  SFEEC_CUDA(cudaEventCreate(&e0));
+  SFEEC_CUDA(cudaEventCreate(&e1));
+  SFEEC_CUDA(cudaEventRecord(e0, s));
   k_spai_big<<<grid, kT, smem, s>>>(n, sq.rp.p, sq.ci.p, sq.val.p, m1.rp.p, m1.ci.p, m1.val.p, ws.p,
                                     qcol.p, flags.p);
   SFEEC_LAUNCH_CHECK();
+  SFEEC_CUDA(cudaEventRecord(e1, s));
+  if (std::getenv("SFEEC_VERBOSE")) {
+    float ms = 0;
+    SFEEC_CUDA(cudaEventSynchronize(e1));
+    SFEEC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    std::fprintf(stderr, "sfeec spai: %lld columns, k_max %lld, kernel %.1f ms (%.2f us/column/CTA)\n",
+                 (long long)n, (long long)kmax, ms, 1e3 * ms * grid / (double)n);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   std::vector<int32_t> hf((size_t)n);
   SFEEC_CUDA(cudaMemcpyAsync(hf.data(), flags.p, sizeof(int32_t) * hf.size(), cudaMemcpyDeviceToHost, s));
   SFEEC_CUDA(cudaStreamSynchronize(s));
@@ -387,6 +425,16 @@ int64_t spai_big_device(const DevCSR& m1, const DevCSR& sq, DevBuf<double>& qcol
 
 void build_p2_system_device(const TetMesh& mesh, const P2Dofs& dofs, bool want_div,
                             DevP2System& out, cudaStream_t s) {
+  const bool verbose = std::getenv("SFEEC_VERBOSE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!verbose) return;
+    SFEEC_CUDA(cudaStreamSynchronize(s));
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "sfeec p2 setup: %-28s %8.3f s\n", what,
+                 std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
+  };
   auto up = [&](HostCSR&& h, DevCSR& d) {
     d.rows = h.rows;
     d.cols = h.cols;
@@ -401,13 +449,17 @@ void build_p2_system_device(const TetMesh& mesh, const P2Dofs& dofs, bool want_d
   out.n3 = dofs.n3;
   DevCSR m1;
   up(p2_mass(mesh, dofs, 1), m1);
+  lap("host M1 + upload");
   up(p2_curl(mesh, dofs), out.c);
   up(p2_mass(mesh, dofs, 2), out.m2);
   if (want_div) up(p2_div(mesh, dofs), out.d);
+  lap("host C, M2, D + upload");
   DevCSR sq;
   square_pattern_device(m1, sq, s);
+  lap("S(M1^2) pattern + values");
   DevBuf<double> qcol;
   out.fallback = spai_big_device(m1, sq, qcol, s);
+  lap("SPAI (device)");
   require(out.fallback == 0,
           "device SPAI: some columns need the eigenvalue-thresholded fallback; use the host builder");
   m1 = DevCSR();
@@ -420,6 +472,7 @@ void build_p2_system_device(const TetMesh& mesh, const P2Dofs& dofs, bool want_d
   out.qsym.rp = std::move(sq.rp);
   out.qsym.ci = std::move(sq.ci);
   transpose_dev(out.c, out.ct, s);
+  lap("Q_sym + C^T");
 }
 
 }  // namespace sfeec_b200

@@ -275,12 +275,14 @@ inline unsigned blocks_for(int64_t threads) {
 
 }  // namespace
 
-// rows this wide stream better as plain CSR with a warp per row
-// (k_csr_wide) than sliced; SFEEC_WIDE_CSR=0 keeps the sliced layout (A/B)
+// SFEEC_WIDE_CSR=1: rows of >= 64 entries stay plain CSR with a warp per row
+// (k_csr_wide). Measured on config 4 (S(M1^2) Q, ~308 per row): faster at
+// 32^3 (4.79 vs 3.81 TB/s) but slower at 64^3 (4.28 vs 4.66 TB/s), where the
+// sliced layout's lane-per-row gathers coalesce better (consecutive rows'
+// j-th neighbours are consecutive ids); so the sliced layout is the default.
 static bool wide_rows(double avg) {
   const char* env = std::getenv("SFEEC_WIDE_CSR");
-  if (env && std::atoi(env) == 0) return false;
-  return avg >= 64.0;
+  return env && std::atoi(env) == 1 && avg >= 64.0;
 }
 
 void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
