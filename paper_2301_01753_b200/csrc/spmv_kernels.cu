@@ -166,6 +166,67 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---- sliced layout, software-pipelined (wide rows: config 4's Q, ~300/row)
+// As k_sell (fp64 values), but the column/value loads of chunk c+1 are issued
+// before the gathers of chunk c, so a chunk costs one gather round trip and
+// the streaming loads overlap it.
+template <bool ACC, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_sell_pipe(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
+                const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ x,
+                double* __restrict__ y, double alpha) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_slices) return;
+  SliceMeta m = load_meta(srow, sptr, sw, s);
+  while (true) {
+    const int64_t sn = s + nwarps;
+    SliceMeta mn;
+    if (sn < n_slices) mn = load_meta(srow, sptr, sw, sn);
+    if (lane < m.nr) {
+      const int64_t row = m.r0 + lane;
+      const double y0 = ACC ? y[row] : 0.0;
+      const int64_t base = m.ptr + lane;
+      double acc = 0.0;
+      int32_t p[CH];
+      double v[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const bool ok = j < m.w;
+        const int64_t o = base + (int64_t)j * m.nr;
+        p[j] = ok ? __ldcs(col + o) : kPad;
+        v[j] = ok ? __ldcs(val + o) : 0.0;
+      }
+      for (int k0 = 0; k0 < m.w; k0 += CH) {
+        int32_t pn[CH];
+        double vn[CH], xv[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const bool ok = k0 + CH + j < m.w;
+          const int64_t o = base + (int64_t)(k0 + CH + j) * m.nr;
+          pn[j] = ok ? __ldcs(col + o) : kPad;
+          vn[j] = ok ? __ldcs(val + o) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) xv[j] = p[j] != kPad ? __ldg(x + p[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) acc = fma(v[j], xv[j], acc);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          p[j] = pn[j];
+          v[j] = vn[j];
+        }
+      }
+      y[row] = ACC ? fma(alpha, acc, y0) : acc;
+    }
+    if (sn >= n_slices) break;
+    s = sn;
+    m = mn;
+  }
+}
+
 // ---- sliced layout, two lanes per row (wide rows, e.g. Q_sym ~16/row) -----
 // A warp takes half a slice pair: lanes 2i, 2i+1 share row i of 16 rows and
 // take alternate entries, so each lane holds <= CH entries of a <= 2*CH row
@@ -695,8 +756,11 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   // persistent grid sized to the residency of the chosen variant (148 SMs x
   // MINB CTAs of 8 warps); one warp per slice per iteration.
   // SFEEC_SELL_VARIANT selects (CH, MINB) for tuning: 0 -> (8,3), 1 -> (4,4), 2 -> (6,4)
+  // default: the software-pipelined fp64 sliced kernel (variant 9); variant 1
+  // is the previous non-pipelined k_sell (CH 4, MINB 4). Measured (K-Q):
+  // tet128 4.77 -> 5.27 TB/s, config 4 (64^3 P2) 4.65 -> 5.07 TB/s.
   const char* venv = std::getenv("SFEEC_SELL_VARIANT");
-  const int variant = venv ? std::atoi(venv) : 1;
+  const int variant = venv ? std::atoi(venv) : 9;
   const char* senv = std::getenv("SFEEC_SELL_SVARIANT");
   const int svariant = senv ? std::atoi(senv) : 0;
   auto grid_for = [&](int minb) {
@@ -719,6 +783,10 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         SFEEC_SELL_V(ACC, SG, 4, 4);        \
     } else if (variant == 1)                \
       SFEEC_SELL_V(ACC, SG, 4, 4);          \
+    else if (variant == 4)                  \
+      SFEEC_SELL_V(ACC, SG, 8, 4);          \
+    else if (variant == 8)                  \
+      SFEEC_SELL_V(ACC, SG, 16, 2);         \
     else if (variant == 2)                  \
       SFEEC_SELL_V(ACC, SG, 4, 5);          \
     else if (variant == 3)                  \
@@ -734,7 +802,23 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         SFEEC_SELL(false, true);
       break;
     case DevOperator::kSell:
-      if (variant >= 5) {
+      if (variant == 9 || variant == 10) {
+        const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * 4);
+#define SFEEC_PIPE(CH)                                                                            \
+  do {                                                                                            \
+    if (accumulate)                                                                               \
+      k_sell_pipe<true, CH, 4><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,  \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
+    else                                                                                          \
+      k_sell_pipe<false, CH, 4><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p, \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
+  } while (0)
+        if (variant == 9)
+          SFEEC_PIPE(4);
+        else
+          SFEEC_PIPE(2);
+#undef SFEEC_PIPE
+      } else if (variant >= 5) {
 #define SFEEC_TPR2(CH, MB)                                                                   \
   do {                                                                                       \
     const unsigned g2 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 64), 148 * MB);  \
