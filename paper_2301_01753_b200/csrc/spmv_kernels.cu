@@ -802,21 +802,27 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         SFEEC_SELL(false, true);
       break;
     case DevOperator::kSell:
-      if (variant == 9 || variant == 10) {
-        const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * 4);
-#define SFEEC_PIPE(CH)                                                                            \
+      if (variant >= 9 && variant <= 13) {
+#define SFEEC_PIPE(CH, MB)                                                                        \
   do {                                                                                            \
+    const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \
     if (accumulate)                                                                               \
-      k_sell_pipe<true, CH, 4><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,  \
+      k_sell_pipe<true, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p, \
           a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
     else                                                                                          \
-      k_sell_pipe<false, CH, 4><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p, \
+      k_sell_pipe<false, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,\
           a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
   } while (0)
-        if (variant == 9)
-          SFEEC_PIPE(4);
+        if (variant == 10)
+          SFEEC_PIPE(2, 4);
+        else if (variant == 11)
+          SFEEC_PIPE(4, 5);
+        else if (variant == 12)
+          SFEEC_PIPE(2, 8);
+        else if (variant == 13)
+          SFEEC_PIPE(3, 6);
         else
-          SFEEC_PIPE(2);
+          SFEEC_PIPE(4, 4);
 #undef SFEEC_PIPE
       } else if (variant >= 5) {
 #define SFEEC_TPR2(CH, MB)                                                                   \
