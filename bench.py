@@ -296,7 +296,8 @@ class TetRunner:
 class TetSlabRunner:
     """Rank `rank` of the tet system split into z-slabs (strong scaling: the
     mesh is fixed, every rank assembles it on its own GPU and keeps its owned
-    rows; partition.cu, 4 NCCL halo exchanges per step)."""
+    rows; partition.cu, 4 NCCL halo exchanges per step; one-plane halo for
+    P1-, two-plane for config 4's S(M1^2) Q)."""
 
     scaling = "strong"
     kernel_label = ("SpMV chain K-M2, K-CTe, K-Q, K-Cb over the owned rows + NCCL halo-plane "
@@ -311,7 +312,8 @@ class TetSlabRunner:
             ids = [S.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(ids, src=0)
         self.p = partition.TetPart.from_device(cfg["n"], cfg["jitter"], 2023, rank, world,
-                                               nccl_id=ids[0], device=device)
+                                               nccl_id=ids[0], device=device,
+                                               order=2 if cfg["kind"] == "p2" else 1)
         ls = self.p.ls
         eg, er, fg = ls.edge_global, ls.edge_range, ls.face_global
         if cfg["init"] == "gaussian":
@@ -395,8 +397,6 @@ def run_ours(args, rank, world, local_rank):
     if cfg["kind"] == "yee":
         R = YeeRunner(cfg, local_rank, rank, world, dist)
     elif world > 1 or args.partitioned:
-        if cfg["kind"] == "p2":
-            raise SystemExit("the P2 (config 4) bench path is single-GPU in this build")
         R = TetSlabRunner(cfg, local_rank, rank, world, dist)
     else:
         R = TetRunner(cfg, local_rank)

@@ -236,6 +236,12 @@ int64_t sfeec_part_last_launches(sfeec_part* h);
 int sfeec_part_create_tet(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                           int rank, int nranks, const void* nccl_id, int device,
                           sfeec_part** out, int64_t* info);
+/* The same for the config-4 system (P2-, S(M1^2) SPAI, p2_device.cu): its Q
+ * reaches two vertex planes, so local vectors carry a two-plane halo and the
+ * exchanges move two planes; every rank must own >= 2 vertex planes. */
+int sfeec_part_create_p2(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                         int rank, int nranks, const void* nccl_id, int device,
+                         sfeec_part** out, int64_t* info);
 /* y_owned = A x_local on the device, host buffers; which: 0 Q_sym, 1 C,
  * 2 C^T, 3 M2 (e.g. the BE initial b = C a from a local-range potential) */
 int sfeec_part_apply(sfeec_part* h, int which, const double* x_local, double* y_owned);

@@ -135,6 +135,9 @@ _SIGS = {
     "sfeec_part_create_tet": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
                                         C.c_double, C.c_int, C.c_int, _P, C.c_int,
                                         C.POINTER(_P), _PI64]),
+    "sfeec_part_create_p2": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                       C.c_double, C.c_int, C.c_int, _P, C.c_int,
+                                       C.POINTER(_P), _PI64]),
     "sfeec_part_apply": (C.c_int, [_P, C.c_int, _PD, _PD]),
     "sfeec_part_device_ptrs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "sfeec_part_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64, _PD]),

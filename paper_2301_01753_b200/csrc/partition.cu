@@ -18,6 +18,7 @@
 #include "device_util.cuh"
 #include "nccl_loader.hpp"
 #include "spmv_kernels.cuh"
+#include "p2_device.hpp"
 #include "tet_device.hpp"
 #include "tet_mesh.hpp"
 
@@ -267,22 +268,25 @@ void part_finish(PartDev& d, const void* nccl_id) {
 
 // partition.py plane_splits / entity_plane_offsets / slab_system: the rank's
 // {len, own_lo, own_hi, first_len, last_len} and {local start, owned lo, hi}
-void slab_range(const std::vector<int64_t>& base, int n, int rank, int nranks, int64_t rng[5],
-                int64_t glob[3]) {
+// with an h-plane halo (h = 1 first order, 2 for the S(M1^2) Q of config 4).
+// `base` = base vertex of each DOF's entity: its plane is nondecreasing.
+void slab_range(const std::vector<int64_t>& base, int n, int rank, int nranks, int h,
+                int64_t rng[5], int64_t glob[3]) {
   const int64_t plane = (int64_t)(n + 1) * (n + 1);
   std::vector<int64_t> off((size_t)n + 2);
   for (int k = 0; k <= n + 1; ++k)
     off[(size_t)k] = std::lower_bound(base.begin(), base.end(), (int64_t)k * plane) - base.begin();
   const int p0 = (int)((int64_t)rank * (n + 1) / nranks);
   const int p1 = (int)((int64_t)(rank + 1) * (n + 1) / nranks);
-  const int64_t g_lo = off[(size_t)std::max(p0 - 1, 0)];
-  const int64_t g_hi = off[(size_t)std::min(p1 + 1, n + 1)];
+  require(p1 - p0 >= h, "partition: every rank must own at least `halo` vertex planes");
+  const int64_t g_lo = off[(size_t)std::max(p0 - h, 0)];
+  const int64_t g_hi = off[(size_t)std::min(p1 + h, n + 1)];
   const int64_t o_lo = off[(size_t)p0], o_hi = off[(size_t)p1];
   rng[0] = g_hi - g_lo;
   rng[1] = o_lo - g_lo;
   rng[2] = o_hi - g_lo;
-  rng[3] = off[(size_t)p0 + 1] - off[(size_t)p0];
-  rng[4] = off[(size_t)p1] - off[(size_t)p1 - 1];
+  rng[3] = off[(size_t)p0 + h] - off[(size_t)p0];  // first h owned planes (sent down)
+  rng[4] = off[(size_t)p1] - off[(size_t)p1 - h];  // last h owned planes (sent up)
   glob[0] = g_lo;
   glob[1] = o_lo;
   glob[2] = o_hi;
@@ -426,15 +430,82 @@ int sfeec_part_energy_local(sfeec_part** hs, int nranks, double* out) {
 
 int64_t sfeec_part_last_launches(sfeec_part* h) { return h ? h->d.launches : -1; }
 
+}  // extern "C"
+
+namespace {
+
+// Slices a device-built system into rank d.rank's slab and finishes the handle:
+// owned rows, local columns; dt <= 0 -> 0.5 x the CFL estimate of the full
+// operators (the single-GPU value, bitwise); info as sfeec_part_create_tet.
+void part_from_system(PartDev& d, DevCSR& qsym, DevCSR& c, DevCSR& ct, DevCSR& m2, int64_t n1,
+                      int64_t n2, const int64_t er[5], const int64_t fr[5], const int64_t eg[3],
+                      const int64_t fg[3], double dt, double eps0, double mu0, int device,
+                      const void* nccl_id, int64_t* info) {
+  part_ranges(d, er, fr);
+  DevCSR lq, lct, lc, lm2;
+  slice_rows_device(qsym, eg[1], eg[2], eg[0], er[0], lq, d.stream);
+  slice_rows_device(ct, eg[1], eg[2], fg[0], fr[0], lct, d.stream);
+  slice_rows_device(c, fg[1], fg[2], eg[0], er[0], lc, d.stream);
+  slice_rows_device(m2, fg[1], fg[2], fg[0], fr[0], lm2, d.stream);
+  if (dt <= 0) {
+    DevOperator oq, oc, oct, om2;
+    oq.upload_device(std::move(qsym), d.stream);
+    om2.upload_device(std::move(m2), d.stream);
+    oc.upload_device(std::move(c), d.stream);
+    oct.upload_device(std::move(ct), d.stream);
+    cudaStream_t hs;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+    std::unique_ptr<sfeec_dev, void (*)(sfeec_dev*)> full(
+        make_dev_from_ops(std::move(oq), std::move(oc), std::move(oct), std::move(om2), nullptr,
+                          n1, n2, 1.0, eps0, mu0, SFEEC_SPLIT_STRANG, device, SFEEC_NO_CFL_WARN,
+                          hs),
+        sfeec_dev_destroy);
+    double nu = 0;
+    require(sfeec_dev_cfl_number(full.get(), &nu) == 0, "partition: CFL estimate failed");
+    require(nu > 0, "partition: zero CFL estimate");
+    d.dt = 0.5 * 2.0 * 1.0 / nu;
+  }
+  qsym = DevCSR();
+  c = DevCSR();
+  ct = DevCSR();
+  m2 = DevCSR();
+  d.q.upload_device(std::move(lq), d.stream);
+  d.ct.upload_device(std::move(lct), d.stream);
+  d.c.upload_device(std::move(lc), d.stream);
+  d.m2.upload_device(std::move(lm2), d.stream);
+  part_finish(d, nccl_id);
+  if (info) {
+    info[0] = n1;
+    info[1] = n2;
+    for (int k = 0; k < 5; ++k) {
+      info[2 + k] = er[k];
+      info[7 + k] = fr[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+      info[12 + k] = eg[k];
+      info[15 + k] = fg[k];
+    }
+    std::memcpy(&info[18], &d.dt, sizeof(double));
+  }
+}
+
+void check_part_args(int n, int rank, int nranks, sfeec_part** out) {
+  require(out != nullptr, "null out");
+  *out = nullptr;
+  require(n >= 1, "tet mesh: n must be >= 1");
+  require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+  require(nranks <= n + 1, "partition: need nranks <= n + 1 vertex planes");
+}
+
+}  // namespace
+
+extern "C" {
+
 int sfeec_part_create_tet(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                           int rank, int nranks, const void* nccl_id, int device,
                           sfeec_part** out, int64_t* info) {
   return guarded([&] {
-    require(out != nullptr, "null out");
-    *out = nullptr;
-    require(n >= 1, "tet mesh: n must be >= 1");
-    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
-    require(nranks <= n + 1, "partition: need nranks <= n + 1 vertex planes");
+    check_part_args(n, rank, nranks, out);
     auto h = std::make_unique<sfeec_part>();
     PartDev& d = h->d;
     part_setup(d, dt > 0 ? dt : 0.0, eps0, mu0, rank, nranks, device);
@@ -443,57 +514,53 @@ int sfeec_part_create_tet(int n, double jitter, uint64_t seed, double dt, double
     {
       TetMesh mesh;
       mesh.build(n, jitter, seed);
-      slab_range(mesh.edge_v, n, rank, nranks, er, eg);
-      slab_range(mesh.face_v, n, rank, nranks, fr, fg);
+      slab_range(mesh.edge_v, n, rank, nranks, 1, er, eg);
+      slab_range(mesh.face_v, n, rank, nranks, 1, fr, fg);
       build_tet_system_device(mesh, false, sys, d.stream);
     }
-    part_ranges(d, er, fr);
-    // owned rows, columns in the local (halo-extended) ranges
-    DevCSR lq, lct, lc, lm2;
-    slice_rows_device(sys.qsym, eg[1], eg[2], eg[0], er[0], lq, d.stream);
-    slice_rows_device(sys.ct, eg[1], eg[2], fg[0], fr[0], lct, d.stream);
-    slice_rows_device(sys.c, fg[1], fg[2], eg[0], er[0], lc, d.stream);
-    slice_rows_device(sys.m2, fg[1], fg[2], fg[0], fr[0], lm2, d.stream);
-    if (dt <= 0) {
-      // the single-GPU value: a dt = 1 handle on the full operators in the
-      // same layouts, 0.5 x 2 / nu (configs.cfl_dt)
-      DevOperator q, c, ct, m2;
-      q.upload_device(std::move(sys.qsym), d.stream);
-      m2.upload_device(std::move(sys.m2), d.stream);
-      c.upload_device(std::move(sys.c), d.stream);
-      ct.upload_device(std::move(sys.ct), d.stream);
-      cudaStream_t hs;
-      SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
-      std::unique_ptr<sfeec_dev, void (*)(sfeec_dev*)> full(
-          make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2), nullptr,
-                            sys.n1, sys.n2, 1.0, eps0, mu0, SFEEC_SPLIT_STRANG, device,
-                            SFEEC_NO_CFL_WARN, hs),
-          sfeec_dev_destroy);
-      double nu = 0;
-      require(sfeec_dev_cfl_number(full.get(), &nu) == 0, "partition: CFL estimate failed");
-      require(nu > 0, "partition: zero CFL estimate");
-      d.dt = 0.5 * 2.0 * 1.0 / nu;
-    }
-    const int64_t n1 = sys.n1, n2 = sys.n2;
-    sys = DevTetSystem();
-    d.q.upload_device(std::move(lq), d.stream);
-    d.ct.upload_device(std::move(lct), d.stream);
-    d.c.upload_device(std::move(lc), d.stream);
-    d.m2.upload_device(std::move(lm2), d.stream);
-    part_finish(d, nccl_id);
-    if (info) {
-      info[0] = n1;
-      info[1] = n2;
-      for (int k = 0; k < 5; ++k) {
-        info[2 + k] = er[k];
-        info[7 + k] = fr[k];
+    part_from_system(d, sys.qsym, sys.c, sys.ct, sys.m2, sys.n1, sys.n2, er, fr, eg, fg, dt, eps0,
+                     mu0, device, nccl_id, info);
+    *out = h.release();
+  });
+}
+
+int sfeec_part_create_p2(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
+                         int rank, int nranks, const void* nccl_id, int device,
+                         sfeec_part** out, int64_t* info) {
+  return guarded([&] {
+    check_part_args(n, rank, nranks, out);
+    auto h = std::make_unique<sfeec_part>();
+    PartDev& d = h->d;
+    part_setup(d, dt > 0 ? dt : 0.0, eps0, mu0, rank, nranks, device);
+    int64_t er[5], fr[5], eg[3], fg[3];
+    DevP2System sys;
+    {
+      TetMesh mesh;
+      mesh.build(n, jitter, seed);
+      P2Dofs dofs;
+      dofs.build(mesh);
+      // base vertex of each DOF's entity (k-major: planes nondecreasing)
+      std::vector<int64_t> b1((size_t)dofs.n1), b2((size_t)dofs.n2);
+      for (int64_t i = 0; i < dofs.n1; ++i) {
+        const int64_t e = dofs.ent1[(size_t)i];
+        b1[(size_t)i] = (dofs.ks1[(size_t)i] & 1) ? mesh.face_v[(size_t)e] : mesh.edge_v[(size_t)e];
       }
-      for (int k = 0; k < 3; ++k) {
-        info[12 + k] = eg[k];
-        info[15 + k] = fg[k];
+      for (int64_t i = 0; i < dofs.n2; ++i) {
+        const int64_t e = dofs.ent2[(size_t)i];
+        if (dofs.ks2[(size_t)i] & 1) {
+          const int64_t cube = e / 6;
+          b2[(size_t)i] = mesh.vid((int)(cube % n), (int)((cube / n) % n), (int)(cube / ((int64_t)n * n)));
+        } else {
+          b2[(size_t)i] = mesh.face_v[(size_t)e];
+        }
       }
-      std::memcpy(&info[18], &d.dt, sizeof(double));
+      // Q = S(M1^2) SPAI reaches two vertex planes: a two-plane halo
+      slab_range(b1, n, rank, nranks, 2, er, eg);
+      slab_range(b2, n, rank, nranks, 2, fr, fg);
+      build_p2_system_device(mesh, dofs, false, sys, d.stream);
     }
+    part_from_system(d, sys.qsym, sys.c, sys.ct, sys.m2, sys.n1, sys.n2, er, fr, eg, fg, dt, eps0,
+                     mu0, device, nccl_id, info);
     *out = h.release();
   });
 }

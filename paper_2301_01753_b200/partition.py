@@ -57,22 +57,30 @@ def _rows(a: SparseOperator, lo: int, hi: int, col0: int, ncols: int) -> SparseO
 
 
 def slab_system(sys_, rank: int, nranks: int, q_sym: SparseOperator | None = None,
-                ct: SparseOperator | None = None) -> LocalSystem:
-    """Local operators of rank `rank` (sys_ is a configs.TetSystem)."""
+                ct: SparseOperator | None = None, halo: int = 1,
+                bases: tuple | None = None) -> LocalSystem:
+    """Local operators of rank `rank` (sys_ has .mesh, .q, .c, .m2). halo =
+    vertex planes each side (1 first order, 2 for config 4's S(M1^2) Q);
+    bases = (base vertex per 1-form DOF, per 2-form DOF), default the
+    first-order edges / faces."""
     n = sys_.mesh.n
-    _, ev, fv, _ = sys_.mesh.geometry()
+    if bases is None:
+        _, ev, fv, _ = sys_.mesh.geometry()
+        bases = (ev[:, 0], fv[:, 0])
     P = plane_splits(n, nranks)
+    if np.any(np.diff(P) < halo):
+        raise ValueError("every rank must own at least `halo` vertex planes")
     q_sym = q_sym if q_sym is not None else symmetric_part(sys_.q)
     ct = ct if ct is not None else transpose(sys_.c)
     out = {}
-    for kind, base in (("e", ev[:, 0]), ("f", fv[:, 0])):
+    for kind, base in (("e", bases[0]), ("f", bases[1])):
         off = entity_plane_offsets(base, n)
         p0, p1 = P[rank], P[rank + 1]
-        g_lo = off[max(p0 - 1, 0)]
-        g_hi = off[min(p1 + 1, n + 1)]
+        g_lo = off[max(p0 - halo, 0)]
+        g_hi = off[min(p1 + halo, n + 1)]
         o_lo, o_hi = off[p0], off[p1]
-        first = off[p0 + 1] - off[p0]
-        last = off[p1] - off[p1 - 1]
+        first = off[p0 + halo] - off[p0]
+        last = off[p1] - off[p1 - halo]
         rng = np.array([g_hi - g_lo, o_lo - g_lo, o_hi - g_lo, first, last], np.int64)
         out[kind] = (rng, (int(g_lo), int(o_lo), int(o_hi)))
     (er, eg), (fr, fg) = out["e"], out["f"]
@@ -120,18 +128,19 @@ class TetPart:
     @classmethod
     def from_device(cls, n: int, jitter: float, seed: int, rank: int, nranks: int,
                     dt: float = 0.0, eps0=1.0, mu0=1.0, nccl_id: bytes | None = None,
-                    device: int = 0) -> "TetPart":
-        """Rank `rank`'s slab of the config-1/3/5 tet system, assembled and
-        row-sliced on its own device (no host CSR). dt <= 0: 0.5 x the CFL
-        estimate of the full operators (bitwise configs.cfl_dt of the
-        single-GPU tet_device_scheme)."""
+                    device: int = 0, order: int = 1) -> "TetPart":
+        """Rank `rank`'s slab of the tet system, assembled and row-sliced on
+        its own device (no host CSR): order 1 = configs 1/3/5 (P1-, S(M1),
+        one-plane halo), order 2 = config 4 (P2-, S(M1^2), two-plane halo).
+        dt <= 0: 0.5 x the CFL estimate of the full operators (bitwise
+        configs.cfl_dt of the single-GPU device scheme)."""
         self = cls.__new__(cls)
         h = C.c_void_p()
         info = np.zeros(19, np.int64)
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        L.check(L.lib().sfeec_part_create_tet(int(n), float(jitter), int(seed), float(dt), eps0,
-                                              mu0, int(rank), int(nranks), idbuf, int(device),
-                                              C.byref(h), L.i64ptr(info)))
+        fn = L.lib().sfeec_part_create_tet if order == 1 else L.lib().sfeec_part_create_p2
+        L.check(fn(int(n), float(jitter), int(seed), float(dt), eps0, mu0, int(rank), int(nranks),
+                   idbuf, int(device), C.byref(h), L.i64ptr(info)))
         self._h = h
         self._keep = None
         self.ls = SlabInfo(rank, nranks, int(info[0]), int(info[1]), info[2:7].copy(),

@@ -252,3 +252,72 @@ def test_tet_device_slabs_bitwise_equal_single_device(world):
     assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
     t = parts[0].kernel_timing(True)
     assert set(t) == set(partition.TetPart.KERNEL_CLASSES)
+
+
+def _p2_bases(mesh):
+    _, ev, fv, tv = mesh.geometry()
+    e1, k1 = mesh.p2_dofs(1)
+    e2, k2 = mesh.p2_dofs(2)
+    b1 = np.where(k1 & 1, fv[np.minimum(e1, len(fv) - 1), 0], ev[np.minimum(e1, len(ev) - 1), 0])
+    b2 = np.where(k2 & 1, tv[np.minimum(e2, len(tv) - 1), 0], fv[np.minimum(e2, len(fv) - 1), 0])
+    return b1, b2
+
+
+def test_p2_two_plane_halo_slabs_reproduce_global_rows():
+    """Config 4's Q has the S(M1^2) pattern, which reaches two vertex planes:
+    with halo = 2 the slab operators reproduce the global rows exactly, with
+    halo = 1 slicing must refuse (a row would leave the halo). M1^2 stands in
+    for Q here (same pattern; the host SPAI is too slow for the CPU suite)."""
+    from types import SimpleNamespace
+    import scipy.sparse as sp
+    n, world = 5, 2
+    mesh = S.TetMesh(n, 0.1, 5)
+    c, m1, m2 = mesh.p2_operator("c"), mesh.p2_operator("m1"), mesh.p2_operator("m2")
+    M1 = _csr(m1)
+    Q = (M1 @ M1).tocsr()
+    Q.sort_indices()
+    q = S.SparseOperator(Q.shape[0], Q.shape[1], Q.indptr.astype(np.int64),
+                         Q.indices.astype(np.int32), Q.data.copy(), True)
+    sys_ = SimpleNamespace(mesh=mesh, q=q, c=c, m2=m2)
+    bases = _p2_bases(mesh)
+    ct = S.transpose(c)
+    rng = np.random.default_rng(2)
+    xe, xf = rng.standard_normal(c.cols), rng.standard_normal(c.rows)
+    for r in range(world):
+        ls = partition.slab_system(sys_, r, world, q, ct, halo=2, bases=bases)
+        eg, fg = ls.edge_global, ls.face_global
+        le, lf = xe[eg[0]:eg[0] + ls.edge_range[0]], xf[fg[0]:fg[0] + ls.face_range[0]]
+        np.testing.assert_array_equal(_csr(ls.q) @ le, (Q @ xe)[eg[1]:eg[2]])
+        np.testing.assert_array_equal(_csr(ls.c) @ le, (_csr(c) @ xe)[fg[1]:fg[2]])
+        np.testing.assert_array_equal(_csr(ls.ct) @ lf, (_csr(ct) @ xf)[eg[1]:eg[2]])
+        np.testing.assert_array_equal(_csr(ls.m2) @ lf, (_csr(m2) @ xf)[fg[1]:fg[2]])
+    with pytest.raises(ValueError):
+        partition.slab_system(sys_, 0, world, q, ct, halo=1, bases=bases)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2_device_slabs_bitwise_equal_single_device(world):
+    """Config-4 slabs (two-plane halo) built on the device, 15 lockstep steps:
+    bitwise the single-GPU P2 device scheme."""
+    from paper_2301_01753_b200 import inputs
+    n, jit, seed = 5, 0.1, 2023
+    one = S.p2_device_scheme(n, jit, seed, dt=1.0, with_div=False)
+    dt = configs.cfl_dt(one)
+    one.set_dt(dt)
+    parts = [partition.TetPart.from_device(n, jit, seed, r, world, order=2) for r in range(world)]
+    a = inputs.gaussian(7, one._n1)
+    b0 = one.apply("c", a)
+    e0 = np.zeros(one._n1)
+    for p in parts:
+        assert p.dt == dt
+        eg, er, fg = p.ls.edge_global, p.ls.edge_range, p.ls.face_global
+        assert np.array_equal(p.apply("c", a[eg[0]:eg[0] + er[0]]), b0[fg[1]:fg[2]])
+        p.load_global(b0, e0)
+    ref = one.advance(S.make_state(S.Formulation.BE, b0, e0), 15)
+    partition.advance_local(parts, 15)
+    b, e = np.zeros(one._n2), np.zeros(one._n1)
+    for p in parts:
+        p.fetch_into(b, e)
+    assert np.array_equal(b, ref.first) and np.array_equal(e, ref.e)
+    assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
