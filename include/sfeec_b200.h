@@ -325,6 +325,10 @@ int sfeec_tet_dev_operators(int n, double jitter, uint64_t seed, int device, sfe
                             sfeec_csr_owned* ct);
 /* y = A x with a resident operator of the handle: 0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D */
 int sfeec_dev_apply(sfeec_dev* h, int which, const double* x, double* y);
+/* apply_curl_of_curl (operators.cpp:268-290): y = Q_sym C^T M2 C a with the
+ * resident operators (the curl-curl of the Fig. 3 accuracy study); host a[N1],
+ * y[N1] */
+int sfeec_dev_curl_curl(sfeec_dev* h, const double* a, double* y);
 /* make_pattern (spai.cpp:31-72): kind 0 diagonal, 1 S(M1), 2 S(M1^2); the
  * pattern is returned as a CSR with unit values */
 int sfeec_make_pattern(const sfeec_csr* m, int kind, sfeec_csr_owned* out);

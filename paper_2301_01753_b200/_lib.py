@@ -121,6 +121,7 @@ _SIGS = {
     "sfeec_tet_dev_operators": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int] +
                                 [C.POINTER(sfeec_csr_owned)] * 5),
     "sfeec_dev_apply": (C.c_int, [_P, C.c_int, _PD, _PD]),
+    "sfeec_dev_curl_curl": (C.c_int, [_P, _PD, _PD]),
     "sfeec_part_create":(C.c_int, [C.POINTER(sfeec_csr)] * 4 + [_PI64, _PI64, C.c_double,
                                     C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p,
                                     C.c_int, C.POINTER(_P)]),

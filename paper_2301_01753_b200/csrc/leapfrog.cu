@@ -540,6 +540,30 @@ int sfeec_dev_apply(sfeec_dev* h, int which, const double* x, double* y) {
   });
 }
 
+// apply_curl_of_curl (reference operators.cpp:268-290): y = Q C^T M2 C a,
+// host buffers; the intermediates stay on the device
+int sfeec_dev_curl_curl(sfeec_dev* h, const double* a, double* y) {
+  return guarded([&] {
+    require(h && a && y, "null argument");
+    auto& d = h->d;
+    require(d.c.cols == d.n1 && d.m2.rows == d.c.rows, "apply_curl_of_curl: dimension mismatch");
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    DevBuf<double> da, dw2, dw3, dw1, dy;
+    da.upload(a, (size_t)d.n1, d.stream);
+    dw2.alloc((size_t)std::max<int64_t>(1, d.n2));
+    dw3.alloc((size_t)std::max<int64_t>(1, d.n2));
+    dw1.alloc((size_t)d.n1);
+    dy.alloc((size_t)d.n1);
+    d.apply(d.c, da.p, dw2.p);
+    d.apply(d.m2, dw2.p, dw3.p);
+    d.apply(d.ct, dw3.p, dw1.p);
+    d.apply(d.q, dw1.p, dy.p);
+    SFEEC_CUDA(cudaMemcpyAsync(y, dy.p, sizeof(double) * (size_t)d.n1, cudaMemcpyDeviceToHost,
+                               d.stream));
+    SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+  });
+}
+
 int sfeec_dev_set_dt(sfeec_dev* h, double dt) {
   return guarded([&] {
     require(h, "null handle");

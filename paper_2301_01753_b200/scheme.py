@@ -285,6 +285,15 @@ class SplitScheme:
     def step_bytes(self) -> float:
         return L.lib().sfeec_dev_step_bytes(self._h)
 
+    def curl_of_curl(self, a: np.ndarray) -> np.ndarray:
+        """apply_curl_of_curl (operators.cpp:268-290): Q_sym C^T M2 C a on the device."""
+        a = np.ascontiguousarray(a, np.float64)
+        if a.size != self._n1:
+            raise InvalidParameter("apply_curl_of_curl: dimension mismatch")
+        y = np.zeros(self._n1)
+        L.check(L.lib().sfeec_dev_curl_curl(self._h, L.dptr(a), L.dptr(y)))
+        return y
+
     def apply(self, which: str, x: np.ndarray) -> np.ndarray:
         """y = A x with a resident operator: 'q_sym', 'c', 'ct', 'm2' or 'div'."""
         idx = {"q_sym": 0, "c": 1, "ct": 2, "m2": 3, "div": 4}[which]
