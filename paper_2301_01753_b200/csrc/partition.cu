@@ -7,10 +7,15 @@
 // local operators are the owned rows with columns shifted into that range:
 //   Q_sym, C^T : rows = owned edges      C, M2 : rows = owned faces
 // The merged Strang step needs four halo refreshes (b before K-M2, u before
-// K-CTe, e before K-Q, t before K-Cb); each sends the first owned plane down
-// and the last owned plane up (contiguous ranges, no packing) with
-// ncclSend/ncclRecv on the compute stream, or -- to verify the multi-rank
-// path on one GPU -- with device copies between handles advanced in lockstep.
+// K-CTe, e before K-Q, t before K-Cb); each sends the first owned plane(s)
+// down and the last owned plane(s) up (contiguous ranges, no packing) with
+// ncclSend/ncclRecv. Each operator is split by output rows (SplitOp): the
+// producing kernel computes the rows to be sent first, the exchange then runs
+// on a comm stream beside the interior rows, and the next kernel waits on it.
+// To verify the multi-rank path on one GPU, handles advanced in lockstep run
+// the same split schedule with device copies between phases.
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -28,14 +33,55 @@ struct PartRange {
   int64_t len = 0, own_lo = 0, own_hi = 0, first_len = 0, last_len = 0;
 };
 
+// An operator split by output rows: the rows whose values the lower / upper
+// neighbour needs come first, the interior rows after, so the halo exchange of
+// the produced vector can overlap the interior part. Each part is an ordinary
+// sliced / ELL operator, so every row's arithmetic (and result) is unchanged.
+struct SplitOp {
+  DevOperator part[3];  // 0: rows sent down, 1: rows sent up, 2: interior
+  int64_t row0[3] = {0, 0, 0};
+  int64_t rows = 0, cols = 0, nnz = 0;
+  bool incidence = false;  // +-1 entries (5 B per entry in the algorithmic count)
+
+  void build(DevCSR&& a, int64_t lo_rows, int64_t hi_rows, cudaStream_t s) {
+    rows = a.rows;
+    cols = a.cols;
+    nnz = a.nnz;
+    const int64_t lo = std::min(lo_rows, rows);
+    const int64_t hi = std::min(hi_rows, rows - lo);
+    const int64_t r0[3] = {0, rows - hi, lo}, r1[3] = {lo, rows, rows - hi};
+    for (int k = 0; k < 3; ++k) {
+      row0[k] = r0[k];
+      if (r1[k] <= r0[k]) continue;
+      DevCSR sub;
+      slice_rows_device(a, r0[k], r1[k], 0, cols, sub, s);
+      part[k].upload_device(std::move(sub), s);
+      incidence = incidence || part[k].layout == DevOperator::kSigned;
+    }
+  }
+  // which: 0 / 1 / 2 a single part, -1 the boundary parts, -2 all
+  void launch(int which, const double* x, double* y, double alpha, bool acc,
+              cudaStream_t s) const {
+    for (int k = 0; k < 3; ++k) {
+      const bool sel = which == -2 || (which == -1 && k < 2) || which == k;
+      if (sel && part[k].rows > 0) launch_spmv(part[k], x, y + row0[k], alpha, acc, s);
+    }
+  }
+};
+
 struct PartDev {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // overlap: the exchange of a produced vector runs on comm_stream while the
+  // interior rows are computed; the next kernel waits for it (ev_xch)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
+  bool overlap = true, xch_pending = false;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   double dt = 0, eps0 = 1, mu0 = 1;
   PartRange r1, r2;  // edges, faces
-  DevOperator q, c, ct, m2;
+  SplitOp q, c, ct, m2;
   DevBuf<double> e, t, b, u, partials;
   double time = 0;
   int64_t launches = 0;
@@ -49,7 +95,10 @@ struct PartDev {
 
   ~PartDev() {
     for (auto ev : ev_pool) cudaEventDestroy(ev);
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_xch) cudaEventDestroy(ev_xch);
     if (comm) Nccl::get().comm_destroy(comm);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -107,15 +156,55 @@ struct PartDev {
     return p;
   }
 
-  void kernel(const Step& s) {
+  void operands(Op op, const SplitOp*& A, const double*& x, double*& y, bool& acc) {
+    acc = false;
+    switch (op) {
+      case kQ: A = &q; x = e.p; y = t.p + r1.own_lo; break;
+      case kCb: A = &c; x = t.p; y = b.p + r2.own_lo; acc = true; break;
+      case kM2: A = &m2; x = b.p; y = u.p + r2.own_lo; break;
+      case kCTe: A = &ct; x = u.p; y = e.p + r1.own_lo; acc = true; break;
+      default: A = nullptr; x = nullptr; y = nullptr; break;
+    }
+  }
+  // one part selection of a kernel (the lockstep driver's split schedule)
+  void kernel_part(const Step& s, int which) {
+    const SplitOp* A;
+    const double* x;
+    double* y;
+    bool acc;
+    operands(s.op, A, x, y, acc);
+    if (A) A->launch(which, x, y, s.alpha, acc, stream);
+    if (which != -1) ++launches;
+  }
+
+  // the exchange that follows each kernel in the program
+  static Op produced(Op k) { return k == kQ ? kXt : k == kCb ? kXb : k == kM2 ? kXu : kXe; }
+
+  // xchg: the program's next step exchanges this kernel's output -- with
+  // NCCL and overlap on, the boundary rows go first and the exchange runs on
+  // comm_stream beside the interior rows
+  void kernel(const Step& s, bool xchg = false) {
     if (s.op < kQ) return;
+    if (xch_pending) {  // this kernel reads the halo exchanged last
+      SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
+      xch_pending = false;
+    }
     tic(s.op == kQ ? 0 : s.op == kCb ? 1 : s.op == kCTe ? 2 : 3);
-    switch (s.op) {
-      case kQ: launch_spmv(q, e.p, t.p + r1.own_lo, 0.0, false, stream); break;
-      case kCb: launch_spmv(c, t.p, b.p + r2.own_lo, s.alpha, true, stream); break;
-      case kM2: launch_spmv(m2, b.p, u.p + r2.own_lo, 0.0, false, stream); break;
-      case kCTe: launch_spmv(ct, u.p, e.p + r1.own_lo, s.alpha, true, stream); break;
-      default: break;
+    const SplitOp* A = nullptr;
+    const double* x = nullptr;
+    double* y = nullptr;
+    bool acc = false;
+    operands(s.op, A, x, y, acc);
+    if (xchg && overlap && nranks > 1 && comm) {
+      A->launch(-1, x, y, s.alpha, acc, stream);
+      SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
+      SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
+      exchange_nccl(produced(s.op), comm_stream);
+      SFEEC_CUDA(cudaEventRecord(ev_xch, comm_stream));
+      xch_pending = true;
+      A->launch(2, x, y, s.alpha, acc, stream);
+    } else {
+      A->launch(-2, x, y, s.alpha, acc, stream);
     }
     toc();
     ++launches;
@@ -124,7 +213,8 @@ struct PartDev {
   double* vec(Op x) { return x == kXe ? e.p : x == kXt ? t.p : x == kXb ? b.p : u.p; }
   const PartRange& range(Op x) const { return (x == kXe || x == kXt) ? r1 : r2; }
 
-  void exchange_nccl(Op x) {
+  void exchange_nccl(Op x) { exchange_nccl(x, stream); }
+  void exchange_nccl(Op x, cudaStream_t stream) {
     if (nranks == 1 || !comm) return;
     const Nccl& nc = Nccl::get();
     const PartRange& R = range(x);
@@ -143,15 +233,28 @@ struct PartDev {
     nc.check(nc.group_end(), "ncclGroupEnd");
   }
 
-  void run(const Step& s) {
-    if (s.op <= kXu) {
-      if (nranks == 1 || !comm) return;
-      tic(4);
-      exchange_nccl(s.op);
-      toc();
-    } else {
-      kernel(s);
+  void advance(int64_t n) {
+    launches = 0;
+    const auto prog = program(n);
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const Step& s = prog[i];
+      if (s.op <= kXu) {
+        if (nranks == 1 || !comm) continue;
+        if (overlap && i > 0 && prog[i - 1].op >= kQ && produced(prog[i - 1].op) == s.op)
+          continue;  // already in flight beside the interior rows
+        tic(4);
+        exchange_nccl(s.op, stream);
+        toc();
+      } else {
+        const bool xchg = i + 1 < prog.size() && prog[i + 1].op == produced(s.op);
+        kernel(s, xchg);
+      }
     }
+    if (xch_pending) {
+      SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
+      xch_pending = false;
+    }
+    for (int64_t k = 0; k < n; ++k) time = time + dt;
   }
 
   // SURVEY.md 8(d) accounting of this rank's rows (as sfeec_dev_step_bytes)
@@ -159,24 +262,19 @@ struct PartDev {
     const double o1 = (double)(r1.own_hi - r1.own_lo), o2 = (double)(r2.own_hi - r2.own_lo);
     switch (cls) {
       case 0: return 12.0 * (double)q.nnz + 16.0 * o1;
-      case 1: return 5.0 * (double)c.nnz + 8.0 * o1 + 16.0 * o2;
-      case 2: return 5.0 * (double)ct.nnz + 8.0 * o2 + 16.0 * o1;
+      case 1: return (c.incidence ? 5.0 : 12.0) * (double)c.nnz + 8.0 * o1 + 16.0 * o2;
+      case 2: return (ct.incidence ? 5.0 : 12.0) * (double)ct.nnz + 8.0 * o2 + 16.0 * o1;
       case 3: return 12.0 * (double)m2.nnz + 16.0 * o2;
       default: return 0.0;
     }
   }
 
-  void advance(int64_t n) {
-    launches = 0;
-    for (const auto& s : program(n)) run(s);
-    for (int64_t k = 0; k < n; ++k) time = time + dt;
-  }
 
   // this rank's part of 0.5 (eps0 e^T Q e + b^T M2 b / mu0); halos of e and b
   // must be current (the callers refresh them)
   double energy() {
-    launch_spmv(q, e.p, t.p + r1.own_lo, 0.0, false, stream);
-    launch_spmv(m2, b.p, u.p + r2.own_lo, 0.0, false, stream);
+    q.launch(-2, e.p, t.p + r1.own_lo, 0.0, false, stream);
+    m2.launch(-2, b.p, u.p + r2.own_lo, 0.0, false, stream);
     double he = device_dot(e.p + r1.own_lo, t.p + r1.own_lo, r1.own_hi - r1.own_lo, partials.p, stream);
     double ha = device_dot(b.p + r2.own_lo, u.p + r2.own_lo, r2.own_hi - r2.own_lo, partials.p, stream);
     return 0.5 * (eps0 * he + ha / mu0);
@@ -235,6 +333,29 @@ void part_ranges(PartDev& d, const int64_t* edge_range, const int64_t* face_rang
   }
 }
 
+DevCSR to_dev(const HostCSR& h, cudaStream_t s) {
+  DevCSR d;
+  d.rows = h.rows;
+  d.cols = h.cols;
+  d.nnz = (int64_t)h.val.size();
+  d.rp.upload(h.row_ptr.data(), h.row_ptr.size(), s);
+  d.ci.upload(h.col_idx.data(), std::max<size_t>(1, h.col_idx.size()), s);
+  d.val.upload(h.val.data(), std::max<size_t>(1, h.val.size()), s);
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  return d;
+}
+
+// the local operators split by output rows (rows sent down / up first)
+void part_ops(PartDev& d, DevCSR&& q, DevCSR&& c, DevCSR&& ct, DevCSR&& m2) {
+  const bool lo = d.rank > 0, hi = d.rank < d.nranks - 1;
+  const int64_t lo1 = lo ? d.r1.first_len : 0, hi1 = hi ? d.r1.last_len : 0;
+  const int64_t lo2 = lo ? d.r2.first_len : 0, hi2 = hi ? d.r2.last_len : 0;
+  d.q.build(std::move(q), lo1, hi1, d.stream);
+  d.ct.build(std::move(ct), lo1, hi1, d.stream);
+  d.c.build(std::move(c), lo2, hi2, d.stream);
+  d.m2.build(std::move(m2), lo2, hi2, d.stream);
+}
+
 void part_setup(PartDev& d, double dt, double eps0, double mu0, int rank, int nranks, int device) {
   select_device(device);
   d.device = device;
@@ -244,6 +365,11 @@ void part_setup(PartDev& d, double dt, double eps0, double mu0, int rank, int nr
   d.eps0 = eps0;
   d.mu0 = mu0;
   SFEEC_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  SFEEC_CUDA(cudaStreamCreateWithFlags(&d.comm_stream, cudaStreamNonBlocking));
+  SFEEC_CUDA(cudaEventCreateWithFlags(&d.ev_bnd, cudaEventDisableTiming));
+  SFEEC_CUDA(cudaEventCreateWithFlags(&d.ev_xch, cudaEventDisableTiming));
+  const char* ov = std::getenv("SFEEC_PART_OVERLAP");
+  d.overlap = !(ov && std::atoi(ov) == 0);
 }
 
 // state vectors, reduction scratch and (multi-rank with an id) the NCCL
@@ -318,10 +444,8 @@ int sfeec_part_create(const sfeec_csr* q, const sfeec_csr* c, const sfeec_csr* c
     require(c->rows == o2 && c->cols == d.r1.len, "partition: C must be owned faces x local edges");
     require(m2->rows == o2 && m2->cols == d.r2.len, "partition: M2 must be owned faces x local faces");
     part_setup(d, dt, eps0, mu0, rank, nranks, device);
-    d.q.upload(csr_from_view(*q), false, d.stream);
-    d.c.upload(csr_from_view(*c), false, d.stream);
-    d.ct.upload(csr_from_view(*ct), false, d.stream);
-    d.m2.upload(csr_from_view(*m2), false, d.stream);
+    part_ops(d, to_dev(csr_from_view(*q), d.stream), to_dev(csr_from_view(*c), d.stream),
+             to_dev(csr_from_view(*ct), d.stream), to_dev(csr_from_view(*m2), d.stream));
     part_finish(d, nccl_id);
     *out = h.release();
   });
@@ -385,11 +509,25 @@ int sfeec_part_advance_local(sfeec_part** hs, int nranks, int64_t nsteps) {
     cudaStream_t s = v[0]->stream;
     auto prog = v[0]->program(nsteps);
     for (auto* d : v) d->launches = 0;
-    for (const auto& st : prog) {
+    auto sync_all = [&] {
+      for (auto* d : v) SFEEC_CUDA(cudaStreamSynchronize(d->stream));
+    };
+    // the schedule of the overlapped NCCL path: boundary rows, exchange,
+    // interior rows (here the exchange is device copies between phases)
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const auto& st = prog[i];
       if (st.op <= PartDev::kXu) {
-        for (auto* d : v) SFEEC_CUDA(cudaStreamSynchronize(d->stream));
+        if (i > 0 && prog[i - 1].op >= PartDev::kQ && PartDev::produced(prog[i - 1].op) == st.op)
+          continue;  // exchanged inside the producing kernel's schedule
+        sync_all();
         local_exchange(v, st.op);
-        for (auto* d : v) SFEEC_CUDA(cudaStreamSynchronize(d->stream));
+        sync_all();
+      } else if (i + 1 < prog.size() && prog[i + 1].op == PartDev::produced(st.op)) {
+        for (auto* d : v) d->kernel_part(st, -1);
+        sync_all();
+        local_exchange(v, PartDev::produced(st.op));
+        sync_all();
+        for (auto* d : v) d->kernel_part(st, 2);
       } else {
         for (auto* d : v) d->kernel(st);
       }
@@ -469,10 +607,7 @@ void part_from_system(PartDev& d, DevCSR& qsym, DevCSR& c, DevCSR& ct, DevCSR& m
   c = DevCSR();
   ct = DevCSR();
   m2 = DevCSR();
-  d.q.upload_device(std::move(lq), d.stream);
-  d.ct.upload_device(std::move(lct), d.stream);
-  d.c.upload_device(std::move(lc), d.stream);
-  d.m2.upload_device(std::move(lm2), d.stream);
+  part_ops(d, std::move(lq), std::move(lc), std::move(lct), std::move(lm2));
   part_finish(d, nccl_id);
   if (info) {
     info[0] = n1;
@@ -569,14 +704,14 @@ int sfeec_part_apply(sfeec_part* h, int which, const double* x_local, double* y_
   return guarded([&] {
     require(h && x_local && y_owned, "null argument");
     auto& d = h->d;
-    DevOperator* ops[4] = {&d.q, &d.c, &d.ct, &d.m2};
+    SplitOp* ops[4] = {&d.q, &d.c, &d.ct, &d.m2};
     require(which >= 0 && which < 4, "unknown operator");
-    DevOperator& a = *ops[which];
+    SplitOp& a = *ops[which];
     SFEEC_CUDA(cudaSetDevice(d.device));
     DevBuf<double> dx, dy;
     dx.upload(x_local, (size_t)std::max<int64_t>(1, a.cols), d.stream);
     dy.alloc((size_t)std::max<int64_t>(1, a.rows));
-    launch_spmv(a, dx.p, dy.p, 0.0, false, d.stream);
+    a.launch(-2, dx.p, dy.p, 0.0, false, d.stream);
     SFEEC_CUDA(cudaMemcpyAsync(y_owned, dy.p, sizeof(double) * (size_t)a.rows,
                                cudaMemcpyDeviceToHost, d.stream));
     SFEEC_CUDA(cudaStreamSynchronize(d.stream));
@@ -615,7 +750,8 @@ int sfeec_part_kernel_timing(sfeec_part* h, int enable, double* ms, int64_t* lau
 double sfeec_part_step_bytes(sfeec_part* h) {
   if (!h) return 0;
   const auto& d = h->d;
-  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz + 5.0 * (double)(d.c.nnz + d.ct.nnz) +
+  return 12.0 * (double)d.q.nnz + 12.0 * (double)d.m2.nnz +
+         (d.c.incidence ? 5.0 : 12.0) * (double)(d.c.nnz + d.ct.nnz) +
          16.0 * (double)(d.r1.own_hi - d.r1.own_lo + d.r2.own_hi - d.r2.own_lo);
 }
 
