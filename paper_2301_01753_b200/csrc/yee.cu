@@ -20,6 +20,7 @@
 //                       points are recomputed, never exchanged).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -433,6 +434,250 @@ __global__ void __launch_bounds__(TX* TY)
     __syncthreads();  // unit boundary: the next unit's prologue refills every stage
   }
 }
+// ---- variant 4: two leapfrog steps per z-sweep (temporal blocking) --------
+// The sweep of k_fused_tma advances one (e-kick, b-kick) pair per pass; this
+// one advances two: per plane z of a unit it computes
+//   E1(z) -> B1(z-1) -> E2(z-1) -> B2(z-2)
+// (1 = after the first pair, 2 = after the second), keeping E1, B1 and E2 in
+// shared memory (triple-buffered planes) and writing only E2 and B2, so e and
+// b are read and written once per TWO steps. The regions shrink by one point
+// per half step on the sides the staggered differences reach (E uses B at
+// -1, B uses E at +1): E1 on [i0-1, i0+TX+1] x [j0-1, j0+TY+1], B1 on
+// [i0-1, i0+TX] x [j0-1, j0+TY], E2 on [i0, i0+TX] x [j0, j0+TY], B2 on the
+// tile; the B0 / E0 boxes start at i0 - OFF (TMA's 16-byte alignment; OFF =
+// 16/sizeof(T) >= 2). Every point update is the same expression as in
+// k_fused_tma (yee_e_upd / yee_b_upd), so the result equals two single
+// sweeps. Three barriers per plane; NS = D + 2 TMA stages.
+template <class T, int TX, int TY, int NS>
+struct TmaCfg2 {
+  static constexpr int kOff = 16 / (int)sizeof(T);
+  static constexpr int kBW = (((TX + 2 + kOff) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
+  static constexpr int kBBox = 3 * (TY + 4) * kBW * (int)sizeof(T);  // B0: y in [j0-2, j0+TY+1]
+  static constexpr int kEBox = 3 * (TY + 3) * kBW * (int)sizeof(T);  // E0: y in [j0-1, j0+TY+1]
+  static constexpr int kBStride = (kBBox + 127) / 128 * 128;
+  static constexpr int kEStride = (kEBox + 127) / 128 * 128;
+  static constexpr int kStage = kBStride + kEStride;
+  static constexpr int kX1 = TX + 3, kY1 = TY + 3;  // E1 region, origin (i0-1, j0-1)
+  static constexpr int kXB = TX + 2, kYB = TY + 2;  // B1 region, origin (i0-1, j0-1)
+  static constexpr int kX2 = TX + 1, kY2 = TY + 1;  // E2 region, origin (i0, j0)
+  static constexpr int kE1 = 3 * kX1 * kY1, kB1 = 3 * kXB * kYB, kE2 = 3 * kX2 * kY2;
+  static constexpr int kBufBytes = 3 * (kE1 + kB1 + kE2) * (int)sizeof(T);
+  static constexpr int kBarOff = (NS * kStage + kBufBytes + 15) / 16 * 16;
+  static constexpr int kSmem = kBarOff + NS * 8 + 128;
+  static constexpr int kD = NS - 2;  // prefetch distance in planes
+};
+
+// E DOF mask bits of (i, j) (yee_layout.hpp): 1 Ex, 2 Ey, 4 Ez (z parts apart)
+__device__ __forceinline__ uint32_t e_mask_xy(int i, int j, int n0, int n1) {
+  const bool ix = i >= 0 && i < n0, iy = i >= 1 && i <= n0 - 1;
+  const bool jx = j >= 0 && j < n1, jy = j >= 1 && j <= n1 - 1;
+  return (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u);
+}
+
+template <class T, int TX, int TY, int NS, int NTH>
+__global__ void __launch_bounds__(NTH)
+    k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
+                 YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
+                 int n_units, int kbeg, int kend) {
+  using Cfg = TmaCfg2<T, TX, TY, NS>;
+  constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
+  constexpr int NT = NTH;  // threads; regions are covered in QN passes
+  constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, XB = Cfg::kXB, YB = Cfg::kYB, X2 = Cfg::kX2,
+                Y2 = Cfg::kY2;
+  constexpr int N1 = X1 * Y1, NB = XB * YB, N2 = X2 * Y2;
+  constexpr int QN = (N1 + NT - 1) / NT;
+  static_assert(NB <= N1 && N2 <= N1 && TX * TY <= NT, "pass counts");
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);
+  T* sB1 = sE1 + 3 * Cfg::kE1;
+  T* sE2 = sB1 + 3 * Cfg::kB1;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapE)) : "memory");
+  }
+  __syncthreads();
+  uint32_t gplane = 0;
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int64_t kstride = (int64_t)g.P0 * g.S[1];
+  // region coordinates of this thread's points (pass 0: tid, pass 1: tid + NT)
+  int x1[QN], y1[QN], xb[QN], yb[QN], x2[QN], y2[QN];
+#pragma unroll
+  for (int q = 0; q < QN; ++q) {
+    const int p = tid + q * NT;
+    x1[q] = p % X1;
+    y1[q] = p / X1;
+    xb[q] = p % XB;
+    yb[q] = p / XB;
+    x2[q] = p % X2;
+    y2[q] = p / X2;
+  }
+  const int bx = tid % TX, by = tid / TX;  // own B2 point (tid < TX * TY)
+  const bool bthr = tid < TX * TY;
+
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
+    const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
+    const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
+    const int P = k1 - k0 + 4;  // local planes p <-> z = k0 - 2 + p
+    uint32_t m1[QN], mb[QN], m2[QN];
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      const int i1 = i0 - 1 + x1[q], j1 = j0 - 1 + y1[q];
+      m1[q] = tid + q * NT < N1 ? e_mask_xy(i1, j1, n0, n1) : 0u;
+      const int ib = i0 - 1 + xb[q], jb = j0 - 1 + yb[q];
+      mb[q] = (tid + q * NT < NB && ib >= 0 && ib < n0 && jb >= 0 && jb < n1) ? 1u : 0u;
+      const int i2 = i0 + x2[q], j2 = j0 + y2[q];
+      const bool own = x2[q] < TX && y2[q] < TY && i2 < n0 && j2 < n1;
+      m2[q] = tid + q * NT < N2 ? (e_mask_xy(i2, j2, n0, n1) | (own ? 8u : 0u)) : 0u;
+    }
+    const bool bown = bthr && i0 + bx < n0 && j0 + by < n1;
+    const int64_t bsij = (int64_t)(i0 + bx) + (int64_t)g.P0 * (j0 + by);
+
+    auto issue = [&](int p) {
+      const uint32_t gp = gplane + p;
+      const int st = gp % NS;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bars[st], Cfg::kBBox + Cfg::kEBox);
+      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - OFF, j0 - 2, k0 - 2 + p, 3);
+      tma_load_4d(base + st * Cfg::kStage + Cfg::kBStride, &mapE, &bars[st], i0 - OFF, j0 - 1,
+                  k0 - 2 + p, 0);
+    };
+    if (tid == 0)
+      for (int p = 0; p < D && p < P; ++p) issue(p);
+    for (int p = 0; p < P; ++p) {
+      if (tid == 0 && p + D < P) issue(p + D);
+      const uint32_t gc = gplane + p;
+      mbar_wait(&bars[gc % NS], (gc / NS) & 1);
+      const int z = k0 - 2 + p;
+      const T* __restrict__ B0c = reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage);
+      const T* __restrict__ B0p = reinterpret_cast<const T*>(base + ((gc + NS - 1) % NS) * Cfg::kStage);
+      const T* __restrict__ E0c =
+          reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage + Cfg::kBStride);
+      T* E1c = sE1 + (gc % 3) * Cfg::kE1;              // E1(z)
+      const T* E1p = sE1 + ((gc + 2) % 3) * Cfg::kE1;  // E1(z-1)
+      T* B1c = sB1 + ((gc + 2) % 3) * Cfg::kB1;        // B1(z-1)
+      const T* B1p = sB1 + ((gc + 1) % 3) * Cfg::kB1;  // B1(z-2)
+      T* E2c = sE2 + ((gc + 2) % 3) * Cfg::kE2;        // E2(z-1)
+      const T* E2p = sE2 + ((gc + 1) % 3) * Cfg::kE2;  // E2(z-2)
+#define B0C(c, y, x) B0c[((c) * (TY + 4) + (y)) * BW + (x)]
+#define B0P(c, y, x) B0p[((c) * (TY + 4) + (y)) * BW + (x)]
+#define E0C(c, y, x) E0c[((c) * (TY + 3) + (y)) * BW + (x)]
+#define E1(buf, c, y, x) buf[((c) * Y1 + (y)) * X1 + (x)]
+#define B1(buf, c, y, x) buf[((c) * YB + (y)) * XB + (x)]
+#define E2(buf, c, y, x) buf[((c) * Y2 + (y)) * X2 + (x)]
+      // ---- phase 1: E1(z) on the E1 region (global i = i0-1+x, j = j0-1+y)
+      if (p >= 1) {
+        const int zg = z + g.kofs;
+        const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          if (tid + q * NT >= N1) break;
+          const int x = x1[q], y = y1[q];
+          const int bi = x + OFF - 1, bj = y + 1;  // B0 box: x from i0-OFF, y from j0-2
+          const int ei = x + OFF - 1, ej = y;      // E0 box: x from i0-OFF, y from j0-1
+          T e0 = E0C(0, ej, ei), e1 = E0C(1, ej, ei), e2 = E0C(2, ej, ei);
+          if ((m1[q] & 1) && kin)
+            e0 += ck.ce[1] * (B0C(2, bj, bi) - B0C(2, bj - 1, bi)) - ck.ce[2] * (B0C(1, bj, bi) - B0P(1, bj, bi));
+          if ((m1[q] & 2) && kin)
+            e1 += ck.ce[2] * (B0C(0, bj, bi) - B0P(0, bj, bi)) - ck.ce[0] * (B0C(2, bj, bi) - B0C(2, bj, bi - 1));
+          if ((m1[q] & 4) && kz)
+            e2 += ck.ce[0] * (B0C(1, bj, bi) - B0C(1, bj, bi - 1)) - ck.ce[1] * (B0C(0, bj, bi) - B0C(0, bj - 1, bi));
+          E1(E1c, 0, y, x) = e0;
+          E1(E1c, 1, y, x) = e1;
+          E1(E1c, 2, y, x) = e2;
+        }
+      }
+      __syncthreads();
+      // ---- phase 2: B1(z-1) on the B1 region (global i = i0-1+x, j = j0-1+y)
+      if (p >= 2) {
+        const int zb = z - 1;
+        const int zg = zb + g.kofs;
+        const bool kb = zg >= 0 && zg < n2;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          if (tid + q * NT >= NB) break;
+          const int x = xb[q], y = yb[q];
+          const int bi = x + OFF - 1, bj = y + 1;  // B0 box coordinates of (i, j)
+          T v0 = B0P(0, bj, bi), v1 = B0P(1, bj, bi), v2 = B0P(2, bj, bi);
+          if (mb[q] && kb) {  // E1 region coordinates of (i, j): (x, y)
+            v0 = v0 + (ck.cb[2] * (E1(E1c, 1, y, x) - E1(E1p, 1, y, x)) -
+                       ck.cb[1] * (E1(E1p, 2, y + 1, x) - E1(E1p, 2, y, x)));
+            v1 = v1 + (ck.cb[0] * (E1(E1p, 2, y, x + 1) - E1(E1p, 2, y, x)) -
+                       ck.cb[2] * (E1(E1c, 0, y, x) - E1(E1p, 0, y, x)));
+            v2 = v2 + (ck.cb[1] * (E1(E1p, 0, y + 1, x) - E1(E1p, 0, y, x)) -
+                       ck.cb[0] * (E1(E1p, 1, y, x + 1) - E1(E1p, 1, y, x)));
+          }
+          B1(B1c, 0, y, x) = v0;
+          B1(B1c, 1, y, x) = v1;
+          B1(B1c, 2, y, x) = v2;
+        }
+      }
+      __syncthreads();
+      // ---- phase 3: E2(z-1) on the E2 region (global i = i0+x, j = j0+y)
+      if (p >= 3) {
+        const int ze = z - 1;
+        const int zg = ze + g.kofs;
+        const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
+        const bool kw = ze >= k0 && ze < k1;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          if (tid + q * NT >= N2) break;
+          const int x = x2[q], y = y2[q];
+          const int ex = x + 1, ey = y + 1;  // E1 region coordinates of (i, j)
+          const int cx = x + 1, cy = y + 1;  // B1 region coordinates of (i, j)
+          T e0 = E1(E1p, 0, ey, ex), e1 = E1(E1p, 1, ey, ex), e2 = E1(E1p, 2, ey, ex);
+          const bool d0 = (m2[q] & 1) && kin, d1 = (m2[q] & 2) && kin, d2 = (m2[q] & 4) && kz;
+          if (d0)
+            e0 += ck.ce[1] * (B1(B1c, 2, cy, cx) - B1(B1c, 2, cy - 1, cx)) - ck.ce[2] * (B1(B1c, 1, cy, cx) - B1(B1p, 1, cy, cx));
+          if (d1)
+            e1 += ck.ce[2] * (B1(B1c, 0, cy, cx) - B1(B1p, 0, cy, cx)) - ck.ce[0] * (B1(B1c, 2, cy, cx) - B1(B1c, 2, cy, cx - 1));
+          if (d2)
+            e2 += ck.ce[0] * (B1(B1c, 1, cy, cx) - B1(B1c, 1, cy, cx - 1)) - ck.ce[1] * (B1(B1c, 0, cy, cx) - B1(B1c, 0, cy - 1, cx));
+          if ((m2[q] & 8) && kw) {
+            const int64_t s = (int64_t)(i0 + x) + (int64_t)g.P0 * (j0 + y) + kstride * ze;
+            if (d0) out.c[0][s] = e0;
+            if (d1) out.c[1][s] = e1;
+            if (d2) out.c[2][s] = e2;
+          }
+          E2(E2c, 0, y, x) = e0;
+          E2(E2c, 1, y, x) = e1;
+          E2(E2c, 2, y, x) = e2;
+        }
+      }
+      __syncthreads();
+      // ---- phase 4: B2(z-2) on the own tile
+      if (p >= 4 && bown) {
+        const int zb = z - 2;
+        if (zb >= k0 && zb < k1) {
+          const int x = bx, y = by;
+          const int cx = x + 1, cy = y + 1;  // B1 region coordinates
+          const int64_t s = bsij + kstride * zb;
+          out.c[3][s] = B1(B1p, 0, cy, cx) + (ck.cb[2] * (E2(E2c, 1, y, x) - E2(E2p, 1, y, x)) -
+                                              ck.cb[1] * (E2(E2p, 2, y + 1, x) - E2(E2p, 2, y, x)));
+          out.c[4][s] = B1(B1p, 1, cy, cx) + (ck.cb[0] * (E2(E2p, 2, y, x + 1) - E2(E2p, 2, y, x)) -
+                                              ck.cb[2] * (E2(E2c, 0, y, x) - E2(E2p, 0, y, x)));
+          out.c[5][s] = B1(B1p, 2, cy, cx) + (ck.cb[1] * (E2(E2p, 0, y + 1, x) - E2(E2p, 0, y, x)) -
+                                              ck.cb[0] * (E2(E2p, 1, y, x + 1) - E2(E2p, 1, y, x)));
+        }
+      }
+#undef B0C
+#undef B0P
+#undef E0C
+#undef E1
+#undef B1
+#undef E2
+    }
+    gplane += P;
+    __syncthreads();
+  }
+}
+
 // ---- variant 3: B planes by TMA, E planes by register prefetch ------------
 // Same sweep and arithmetic as k_fused_tma, but each thread loads the old E
 // values of its <= 2 region points one plane ahead into registers (plain
@@ -622,7 +867,7 @@ __global__ void k_gather(YeeGeom g, bool face, double* __restrict__ dst, int64_t
 // One state-modifying kernel of the step sequence; the multi-slab paths
 // exchange ghost planes after every phase.
 struct Phase {
-  int kind;  // 0 b-kick(h1), 1 e-kick(h1), 2 fused e-kick(h1) + b-kick(h2)
+  int kind;  // 0 b-kick(h1), 1 e-kick(h1), 2 fused e-kick(h1) + b-kick(h2), 3 two of those
   double h1, h2;
 };
 
@@ -634,11 +879,19 @@ struct YeeDev {
   double d[3] = {1, 1, 1};
   double dt = 0, eps0 = 1, mu0 = 1, dv = 1;
   int prec = 8;
-  int variant = 2;
+  // fused-sweep variant: SFEEC_YEE_VARIANT overrides the default (A/B runs)
+  int variant = [] {
+    const char* v = std::getenv("SFEEC_YEE_VARIANT");
+    return v ? std::atoi(v) : 2;
+  }();
   // TMA descriptors of the two ping-pong buffers (B box, E box), PEC only
   CUtensorMap mapB[2], mapE[2];
   bool have_maps = false;
   int tma_blocks = 0, tma_blocks_b = 0;
+  // variant 4 (two steps per sweep): its own boxes
+  CUtensorMap mapB2[2], mapE2[2];
+  bool have_maps2 = false;
+  int tma_blocks2 = 0;
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, partials;
@@ -714,7 +967,7 @@ struct YeeDev {
     ++launches;
   }
 
-  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32;
+  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 4, kNT2 = 512;
 
   template <class T>
   void make_maps() {
@@ -754,6 +1007,67 @@ struct YeeDev {
     SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     tma_blocks = std::max(1, per_sm) * sms;
     have_maps = true;
+  }
+
+  template <class T>
+  void make_maps2() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      SFEEC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn)
+        throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t w = sizeof(T);
+    cuuint64_t dims[4] = {(cuuint64_t)g.S[0], (cuuint64_t)g.S[1], (cuuint64_t)g.S[2], 6};
+    cuuint64_t strides[3] = {(cuuint64_t)g.P0 * w, (cuuint64_t)g.P0 * g.S[1] * w,
+                             (cuuint64_t)g.npts() * w};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    using Cfg = TmaCfg2<T, kTX, kTY, kNS2>;
+    cuuint32_t boxB[4] = {(cuuint32_t)Cfg::kBW, kTY + 4, 1, 3};
+    cuuint32_t boxE[4] = {(cuuint32_t)Cfg::kBW, kTY + 3, 1, 3};
+    const CUtensorMapDataType dt_ = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                   : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    for (int b = 0; b < 2; ++b) {
+      void* ptr = buf[b].p;
+      for (int which = 0; which < 2; ++which) {
+        CUresult r = encode(which ? &mapE2[b] : &mapB2[b], dt_, 4, ptr, dims, strides,
+                            which ? boxE : boxB, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
+      }
+    }
+    auto kern = k_fused2_tma<T, kTX, kTY, kNS2, kNT2>;
+    SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+    int per_sm = 0, sms = 0;
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2, Cfg::kSmem));
+    SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    tma_blocks2 = std::max(1, per_sm) * sms;
+    have_maps2 = true;
+  }
+
+  // two fused steps over local planes [kbeg, kend): buf[cur] -> buf[cur^1]
+  template <class T>
+  void launch_range2(double h_e, double h_b, int kbeg, int kend) {
+    if (!have_maps2) make_maps2<T>();
+    const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
+    const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
+    const int n_units = ntx * nty * nchunks;
+    const int grid = std::min(n_units, tma_blocks2);
+    k_fused2_tma<T, kTX, kTY, kNS2, kNT2><<<grid, kNT2, TmaCfg2<T, kTX, kTY, kNS2>::kSmem, stream>>>(
+        mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
+        ntx, ntx * nty, n_units, kbeg, kend);
+    SFEEC_LAUNCH_CHECK();
+    ++launches;
+  }
+
+  template <class T>
+  void fused2_tma(double h_e, double h_b) {
+    launch_range2<T>(h_e, h_b, sweep_beg(), sweep_end());
+    cur ^= 1;
   }
 
   // planes swept by the fused kernel: [0, n) on one domain, [1, nzl + 1) on a slab
@@ -841,9 +1155,13 @@ struct YeeDev {
     std::vector<Phase> p;
     if (n <= 0) return p;
     const bool use_fused = variant >= 1 && g.bc == SFEEC_BC_PEC;
+    const bool two = variant == 4 && g.bc == SFEEC_BC_PEC && !slab();
     p.push_back({0, 0.5 * dt, 0});
     for (int64_t s = 0; s + 1 < n; ++s) {
-      if (use_fused) {
+      if (two && s + 2 < n) {  // two fused steps per sweep
+        p.push_back({3, dt, dt});
+        ++s;
+      } else if (use_fused) {
         p.push_back({2, dt, dt});
       } else {
         p.push_back({1, dt, 0});
@@ -861,6 +1179,8 @@ struct YeeDev {
       bkick<T>(p.h1);
     else if (p.kind == 1)
       ekick<T>(p.h1);
+    else if (p.kind == 3)
+      fused2_tma<T>(p.h1, p.h2);
     else if (variant >= 2 || slab())
       fused_tma<T>(p.h1, p.h2);
     else
@@ -1407,7 +1727,7 @@ int sfeec_yee_set_stream(sfeec_yee* h, void* s) {
 int sfeec_yee_set_variant(sfeec_yee* h, int variant) {
   return guarded([&] {
     require(h, "null handle");
-    require(variant >= 0 && variant <= 3, "variant must be 0, 1, 2 or 3");
+    require(variant >= 0 && variant <= 4, "variant must be 0..4");
     h->d.variant = variant;
   });
 }

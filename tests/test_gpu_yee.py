@@ -47,7 +47,7 @@ def _pec_case(nx, ny, nz, d, dt, steps, seed=3):
     return b0, e0, pb, pe, ph, port
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("dims", [(6, 5, 7), (33, 9, 40), (40, 17, 3), (64, 16, 65)])
 def test_pec_matches_oracle(variant, dims):
     d = (1.0, 0.8, 1.25)
@@ -67,7 +67,7 @@ def test_fused_equals_unfused_closely():
     dims, d = (37, 21, 70), (1.0, 1.0, 1.0)
     rng = np.random.default_rng(0)
     ys = []
-    for v in (0, 1, 2, 3):
+    for v in (0, 1, 2, 3, 4):
         y = S.YeeScheme(*dims, *d, 0.3, bc=L.BC_PEC)
         y.set_variant(v)
         if not ys:
@@ -75,8 +75,28 @@ def test_fused_equals_unfused_closely():
         y.load(b0, e0)
         y.advance(25)
         ys.append(y.fetch())
-    for k in (1, 2, 3):
+    for k in (1, 2, 3, 4):
         assert rel_l2(ys[k][0], ys[0][0]) <= 1e-14 and rel_l2(ys[k][1], ys[0][1]) <= 1e-14
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("steps", [1, 2, 3, 8, 11])
+def test_two_step_sweep_equals_single_step_sweeps(prec, steps):
+    """Variant 4 (two leapfrog steps per z-sweep, E1/B1/E2 kept on chip) runs
+    the same per-point expressions as variant 2: bitwise equal, for odd and
+    even step counts and ragged tiles / chunks."""
+    dims, d = (45, 19, 70), (1.0, 0.9, 1.1)
+    rng = np.random.default_rng(1)
+    out = {}
+    for v in (2, 4):
+        y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
+        y.set_variant(v)
+        if not out:
+            b0, e0 = rng.standard_normal(y.n_faces), rng.standard_normal(y.n_edges)
+        y.load(b0, e0)
+        y.advance(steps)
+        out[v] = y.fetch()
+    assert np.array_equal(out[2][0], out[4][0]) and np.array_equal(out[2][1], out[4][1])
 
 
 def test_fp32_tracks_fp64():
