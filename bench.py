@@ -468,10 +468,14 @@ def run_ours(args, rank, world, local_rank):
                      "step_bytes": R.step_bytes(), "step_achieved_gbs": step_gbs,
                      "peak_source": peak_src},
         "e2e": {"value": units * args.steps / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)),
-                "d2h_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)),
-                "job": f"set_state + advance({args.steps}) + get_state through the C ABI "
-                       "from/to pinned host buffers; bytes are per job"},
+                # the state crosses PCIe once per job (set_state ... get_state);
+                # per step that is the job's bytes / steps
+                "h2d_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)) // args.steps,
+                "d2h_bytes_per_step": int(getattr(R, "e2e_bytes", 8 * ndof)) // args.steps,
+                "h2d_bytes_per_job": int(getattr(R, "e2e_bytes", 8 * ndof)),
+                "d2h_bytes_per_job": int(getattr(R, "e2e_bytes", 8 * ndof)),
+                "job": f"set_state (pinned host -> HBM) + advance({args.steps}) + get_state "
+                       "(HBM -> pinned host) through the C ABI, one job timed by wall clock"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
