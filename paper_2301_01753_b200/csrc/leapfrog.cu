@@ -9,6 +9,7 @@
 //   strict      the reference's three sub-flows, one thread per row in CSR
 //               order, separate multiply/add -> bitwise equal to the CPU step.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -44,6 +45,8 @@ struct LeapfrogDev {
   double c2() const { return 1.0 / (eps0 * mu0); }
 
   ~LeapfrogDev() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -135,6 +138,60 @@ struct LeapfrogDev {
                    nu, dt);
   }
 
+  // CUDA graph of kGraphPairs merged [Ha(dt) He(dt)] pairs, replayed for the
+  // bulk of advance(n): small, launch-bound systems (config 1: ~7 us per
+  // kernel launched one by one) pay one graph launch per kGraphPairs x 4
+  // kernels. Rebuilt when dt changes; off while per-kernel timing is on or
+  // with SFEEC_GRAPHS=0.
+  static constexpr int kGraphPairs = 32;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  double graph_dt = -1;
+  int64_t graph_kernels = 0;
+
+  bool graphs_on() const {
+    const char* v = std::getenv("SFEEC_GRAPHS");
+    return !timing && !(v && std::atoi(v) == 0);
+  }
+  void build_graph() {
+    if (graph_exec) {
+      cudaGraphExecDestroy(graph_exec);
+      graph_exec = nullptr;
+    }
+    if (!cap_stream) SFEEC_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    cudaStream_t saved = stream;
+    const int64_t saved_launches = launches;
+    stream = cap_stream;
+    SFEEC_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kGraphPairs; ++k) {
+      flow_ha(dt);
+      flow_he(dt);
+    }
+    cudaGraph_t gph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cap_stream, &gph);
+    stream = saved;
+    graph_kernels = launches - saved_launches;
+    launches = saved_launches;
+    SFEEC_CUDA(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&graph_exec, gph, 0);
+    cudaGraphDestroy(gph);
+    SFEEC_CUDA(ei);
+    graph_dt = dt;
+  }
+  void pairs(int64_t m) {  // m x [Ha(dt) He(dt)]
+    if (m >= kGraphPairs && graphs_on()) {
+      if (!graph_exec || graph_dt != dt) build_graph();
+      for (; m >= kGraphPairs; m -= kGraphPairs) {
+        SFEEC_CUDA(cudaGraphLaunch(graph_exec, stream));
+        launches += graph_kernels;
+      }
+    }
+    for (; m > 0; --m) {
+      flow_ha(dt);
+      flow_he(dt);
+    }
+  }
+
   void advance(int64_t n) {
     launches = 0;
     if (n <= 0) return;
@@ -153,10 +210,9 @@ struct LeapfrogDev {
     } else {
       // merged Strang: He(h/2) [Ha(h) He(h)]^(n-1) Ha(h) He(h/2)
       flow_he(0.5 * dt);
-      for (int64_t s = 0; s < n; ++s) {
-        flow_ha(dt);
-        flow_he(s == n - 1 ? 0.5 * dt : dt);
-      }
+      pairs(n - 1);
+      flow_ha(dt);
+      flow_he(0.5 * dt);
     }
     for (int64_t s = 0; s < n; ++s) time = time + dt;  // dynamics.cpp:88, per step
   }
