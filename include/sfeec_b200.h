@@ -260,6 +260,14 @@ double sfeec_part_step_bytes(sfeec_part* h);
  * +-1/spacing), and the divergence D (cells x faces). Replaces
  * generate_cubical_lattice + derivative_matrix for Q1 (mesh_cubical.cpp:15-173,
  * operators.cpp:29-42), extended with PEC. */
+/* The consistent Q1- mass matrices of the same lattice (form 1: M1 over the
+ * edge DOFs, form 2: M2 over the faces): reference mass_matrix
+ * (operators.cpp:133-179) with the Q1 element (form_space.cpp:295-321) and the
+ * order-3 cube rule (quadrature.cpp:90-107), duplicates summed in the
+ * reference's triplet order -- bitwise the reference on periodic lattices.
+ * The cubical SFEEC (non-lumped) system is C, M2 and the SPAI of M1. */
+int sfeec_build_yee_mass(int nx, int ny, int nz, double dx, double dy, double dz, int bc,
+                         int form, sfeec_csr_owned* m);
 int sfeec_build_yee_curl(int nx, int ny, int nz, double dx, double dy, double dz, int bc,
                          sfeec_csr_owned* c, sfeec_csr_owned* div);
 /* Jittered Kuhn/Freudenthal tetrahedral mesh of the unit cube (n^3 cubes x 6

@@ -30,5 +30,6 @@ from .scheme import (  # noqa: F401
     tet_device_operators,
     tet_device_scheme,
     transpose,
+    yee_masses,
     yee_operators,
 )

@@ -143,6 +143,9 @@ _SIGS = {
     "sfeec_part_device_ptrs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "sfeec_part_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64, _PD]),
     "sfeec_part_step_bytes": (C.c_double, [_P]),
+    "sfeec_build_yee_mass": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(sfeec_csr_owned)]),
     "sfeec_build_yee_curl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),

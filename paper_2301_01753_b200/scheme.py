@@ -479,6 +479,17 @@ def yee_operators(nx, ny, nz, dx, dy, dz, bc=L.BC_PEC):
     return SparseOperator._from_owned(c), SparseOperator._from_owned(d)
 
 
+def yee_masses(nx, ny, nz, dx, dy, dz, bc=L.BC_PEC):
+    """(M1, M2): the consistent Q1- mass matrices of the lattice (reference
+    mass_matrix, operators.cpp:133-179), same numbering as yee_operators."""
+    out = []
+    for form in (1, 2):
+        m = L.sfeec_csr_owned()
+        L.check(L.lib().sfeec_build_yee_mass(nx, ny, nz, dx, dy, dz, bc, form, C.byref(m)))
+        out.append(SparseOperator._from_owned(m, True))
+    return tuple(out)
+
+
 class TetMesh:
     """Jittered Kuhn/Freudenthal tet mesh of the unit cube, PEC walls, first-
     order Whitney forms (host C++ builder; numbering contract in DESIGN.md)."""
