@@ -106,3 +106,28 @@ def test_config3_gauss_and_energy_history(tet128):
     assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
     assert (en.max() - en.min()) / en[0] <= 0.05
     assert s.cfl_number() == pytest.approx(1.0, rel=1e-9)
+
+
+@pytest.fixture(scope="module")
+def p2_32():
+    s = S.p2_device_scheme(32, 0.1, seed=2023, dt=1.0, with_div=True)
+    b0 = s.apply("c", inputs.gaussian(7, s._n1))
+    s.set_dt(configs.cfl_dt(s))
+    return s, b0, np.zeros(s._n1)
+
+
+def test_config4_system_first_steps_match_oracle(p2_32):
+    """The config-4 system (P2-, S(M1^2) SPAI) at 32^3 (N1 = 1.2M, nnz(Q) =
+    3.5e8): 3 production steps against the C oracle on the downloaded
+    operators, then Gauss law and a bounded energy over 200 steps."""
+    s, b0, e0 = p2_32
+    ops = S.p2_device_operators(32, 0.1, seed=2023)
+    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)  # noqa: E731
+    port = O.PortScheme(1, s.dt(), tup(ops["q_sym"]), tup(ops["c"]), tup(ops["m2"]),
+                        q_is_symmetric=True)
+    pb, pe, _ = port.steps(b0, e0, 3)
+    out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 3)
+    assert rel_l2(out.first, pb) <= 1e-12 and rel_l2(out.e, pe) <= 1e-12
+    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 200, 20)
+    assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
+    assert (en.max() - en.min()) / en[0] <= 0.10
