@@ -301,16 +301,16 @@ struct TmaCfg {
 // One __syncthreads per plane: E_new is triple-buffered and the TMA ring has
 // D + 3 stages, so the producer never overwrites a stage or an E_new buffer
 // that a lagging warp of the previous plane may still read.
-template <class T, int TX, int TY, int NS>
-__global__ void __launch_bounds__(TX* TY)
+template <class T, int TX, int TY, int NS, int NTH>
+__global__ void __launch_bounds__(NTH)
     k_fused_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                 YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                 int n_units, int kbeg, int kend) {
   using Cfg = TmaCfg<T, TX, TY, NS>;
   constexpr int D = Cfg::kD;
   constexpr int BWB = Cfg::kBWB, BWE = Cfg::kBWE, OFF = Cfg::kOff;
-  constexpr int NT = TX * TY, NE = (TX + 1) * (TY + 1);
-  static_assert(NE <= 2 * NT, "E region needs at most two passes");
+  constexpr int NT = NTH, NE = (TX + 1) * (TY + 1);
+  static_assert(NE <= 2 * NT && TX * TY <= NT, "E region needs at most two passes");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(TX* TY)
     li_[q] = pl[q] % (TX + 1);
     lj_[q] = pl[q] / (TX + 1);
   }
-  const bool has2 = tid + NT < NE;
-  const int bli = tid % TX, blj = tid / TX;  // own B point
+  const bool has1 = tid < NE, has2 = tid + NT < NE;
+  const int bli = tid % TX, blj = tid / TX;  // own B point (tid < TX * TY)
 
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
@@ -353,11 +353,11 @@ __global__ void __launch_bounds__(TX* TY)
       const int i = i0 + li_[q], j = j0 + lj_[q];
       const bool ix = i < n0, iy = i >= 1 && i <= n0 - 1;
       const bool jx = j < n1, jy = j >= 1 && j <= n1 - 1;
-      const bool own = li_[q] < TX && lj_[q] < TY && i < n0 && j < n1;
+      const bool own = li_[q] < TX && lj_[q] < TY && i < n0 && j < n1 && pl[q] < NE;
       m[q] = (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u) | (own ? 8u : 0u);
       sij[q] = (int64_t)i + (int64_t)g.P0 * j;
     }
-    const bool bown = i0 + bli < n0 && j0 + blj < n1;
+    const bool bown = tid < TX * TY && i0 + bli < n0 && j0 + blj < n1;
     const int64_t bsij = (int64_t)(i0 + bli) + (int64_t)g.P0 * (j0 + blj);
 
     auto issue = [&](int p) {
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(TX* TY)
       // E_new(kk) on [i0, i0+TX] x [j0, j0+TY]
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        if (q == 1 && !has2) break;
+        if ((q == 0 && !has1) || (q == 1 && !has2)) break;
         const int li = li_[q], lj = lj_[q];
         const int bi = li + OFF, bj = lj + 1;
         T e0 = EC(0, lj, li), e1 = EC(1, lj, li), e2 = EC(2, lj, li);
@@ -967,7 +967,10 @@ struct YeeDev {
     ++launches;
   }
 
-  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 4, kNT2 = 512;
+  // kNT1: threads of the one-step sweep -- (TX+1)(TY+1) = 297 E points, so 320
+  // threads cover the E region in one pass instead of 256 + 41
+  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 4, kNT2 = 512,
+                       kNT1 = 320;
 
   template <class T>
   void make_maps() {
@@ -1000,10 +1003,10 @@ struct YeeDev {
         if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
       }
     }
-    auto kern = k_fused_tma<T, kTX, kTY, kNS>;
+    auto kern = k_fused_tma<T, kTX, kTY, kNS, kNT1>;
     SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
     int per_sm = 0, sms = 0;
-    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTX * kTY, Cfg::kSmem));
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT1, Cfg::kSmem));
     SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     tma_blocks = std::max(1, per_sm) * sms;
     have_maps = true;
@@ -1121,7 +1124,7 @@ struct YeeDev {
       return;
     }
     const int grid = std::min(n_units, tma_blocks);
-    k_fused_tma<T, kTX, kTY, kNS><<<grid, kTX * kTY, Cfg::kSmem, stream>>>(
+    k_fused_tma<T, kTX, kTY, kNS, kNT1><<<grid, kNT1, Cfg::kSmem, stream>>>(
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
         ntx, ntx * nty, n_units, kbeg, kend);
     SFEEC_LAUNCH_CHECK();
