@@ -182,6 +182,9 @@ double sfeec_yee_step_bytes(sfeec_yee* h);
  * a slab is passed in its local numbering; sfeec_yee_slab_dof_map gives the
  * local -> global DOF ids. sfeec_yee_energy on a slab returns its own part. */
 int sfeec_nccl_unique_id(void* out128);
+/* Self-check of the run-time NCCL binding on one device: a 1-rank
+ * communicator, grouped send/recv of n doubles to self; max |error| out. */
+int sfeec_nccl_selftest(int device, int64_t n, double* max_err);
 int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
                           double eps0, double mu0, int precision, int rank, int nranks,
                           const void* nccl_id /* 128 bytes from rank 0 */, int device,

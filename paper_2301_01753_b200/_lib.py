@@ -100,6 +100,7 @@ _SIGS = {
     "sfeec_yee_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64]),
     "sfeec_yee_step_bytes": (C.c_double, [_P]),
     "sfeec_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "sfeec_nccl_selftest": (C.c_int, [C.c_int, C.c_int64, _PD]),
     "sfeec_yee_create_slab": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_double, C.c_double, C.c_double, C.c_double,
                                         C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,

@@ -1502,6 +1502,40 @@ int sfeec_nccl_unique_id(void* out128) {
   });
 }
 
+// Exercises the run-time NCCL binding (nccl_loader.hpp) on one device: a
+// 1-rank communicator, a grouped send/recv to self of n doubles on a stream,
+// the comparison, destroy. The multi-rank calls are the same entry points.
+int sfeec_nccl_selftest(int device, int64_t n, double* max_err) {
+  return guarded([&] {
+    require(n >= 1 && max_err, "bad argument");
+    select_device(device);
+    const Nccl& nc = Nccl::get();
+    ncclUniqueId id;
+    nc.check(nc.get_unique_id(&id), "ncclGetUniqueId");
+    ncclComm_t comm = nullptr;
+    nc.check(nc.comm_init_rank(&comm, 1, id, 0), "ncclCommInitRank");
+    cudaStream_t st;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<double> h((size_t)n), back((size_t)n);
+    for (int64_t i = 0; i < n; ++i) h[(size_t)i] = 0.5 * (double)i - 3.0;
+    DevBuf<double> x, y;
+    x.upload(h.data(), h.size(), st);
+    y.alloc((size_t)n);
+    y.zero(st);
+    nc.check(nc.group_start(), "ncclGroupStart");
+    nc.check(nc.send(x.p, (size_t)n, ncclFloat64, 0, comm, st), "ncclSend");
+    nc.check(nc.recv(y.p, (size_t)n, ncclFloat64, 0, comm, st), "ncclRecv");
+    nc.check(nc.group_end(), "ncclGroupEnd");
+    SFEEC_CUDA(cudaMemcpyAsync(back.data(), y.p, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st));
+    SFEEC_CUDA(cudaStreamSynchronize(st));
+    double err = 0;
+    for (int64_t i = 0; i < n; ++i) err = std::max(err, std::fabs(back[(size_t)i] - h[(size_t)i]));
+    *max_err = err;
+    cudaStreamDestroy(st);
+    nc.check(nc.comm_destroy(comm), "ncclCommDestroy");
+  });
+}
+
 int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
                           double eps0, double mu0, int precision, int rank, int nranks,
                           const void* nccl_id, int device, sfeec_yee** out) {

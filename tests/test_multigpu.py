@@ -321,3 +321,15 @@ def test_p2_device_slabs_bitwise_equal_single_device(world):
         p.fetch_into(b, e)
     assert np.array_equal(b, ref.first) and np.array_equal(e, ref.e)
     assert partition.energy_local(parts) == pytest.approx(one.energy(ref), rel=1e-13)
+
+
+@pytest.mark.gpu
+def test_nccl_binding_selftest():
+    """The run-time NCCL binding the slab paths use (nccl_loader.hpp): unique
+    id, communicator, grouped send/recv, destroy -- on one device (1 rank)."""
+    import ctypes as C
+    from paper_2301_01753_b200 import _lib as L
+    err = C.c_double(-1.0)
+    L.check(L.lib().sfeec_nccl_selftest(0, 1 << 20, C.byref(err)))
+    assert err.value == 0.0
+    assert len(S.nccl_unique_id()) == 128
