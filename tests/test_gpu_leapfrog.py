@@ -186,3 +186,37 @@ def test_device_matches_live_oracle_larger_pec():
     out, en, _ = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 100, 1)
     assert rel_l2(out.first, pf) <= TOL and rel_l2(out.e, pe) <= TOL
     assert np.max(np.abs(en - ph)) <= TOL * ph[0]
+
+
+@pytest.mark.parametrize("strang", [1, 0])
+def test_non_default_units_match_reference(strang):
+    """UnitSystem{eps0, mu0} != 1 (dynamics.hpp:9-18): c^2 = 1/(eps0 mu0) in the
+    e-kick and eps0 / mu0 weights in the energy -- strict mode bitwise the
+    reference step, production within 1e-12, energy and CFL to round-off."""
+    from paper_2301_01753_b200 import configs
+    sys_ = configs.tet_system(4, 0.1, seed=6)
+    b0, e0, _ = configs.initial_gaussian(sys_, seed=3)
+    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)  # noqa: E731
+    units = S.UnitSystem(eps0=2.5, mu0=0.4)
+    dt, steps = 0.02, 30
+    kind = S.SplitKind.Strang if strang else S.SplitKind.LieTrotter
+    if O.ref_available():
+        ref = O.RefScheme(strang, dt, tup(sys_.q), tup(sys_.c), tup(sys_.m2), eps0=2.5, mu0=0.4)
+        rb, re_, _, _ = ref.steps(True, b0, e0, steps)
+        r_energy = ref.energy(True, rb, re_)
+        r_cfl = ref.cfl()
+    else:
+        port = O.PortScheme(strang, dt, tup(sys_.q), tup(sys_.c), tup(sys_.m2), eps0=2.5, mu0=0.4)
+        rb, re_, _ = port.steps(b0, e0, steps)
+        r_energy = port.energy(rb, re_)
+        r_cfl = port.cfl()
+    for strict in (True, False):
+        s = S.SplitScheme(kind, dt, sys_.q, sys_.c, sys_.m2, units=units, warn_cfl=False,
+                          strict=strict)
+        out = s.advance(S.make_state(S.Formulation.BE, b0, e0), steps)
+        if strict:
+            assert np.array_equal(out.first, rb) and np.array_equal(out.e, re_)
+        else:
+            assert rel_l2(out.first, rb) <= TOL and rel_l2(out.e, re_) <= TOL
+        assert s.energy(out) == pytest.approx(r_energy, rel=1e-13)
+        assert s.cfl_number() == pytest.approx(r_cfl, rel=1e-10)
