@@ -312,8 +312,9 @@ __global__ void __launch_bounds__(NTH)
   constexpr int NT = NTH, NE = (TX + 1) * (TY + 1);
   static_assert(NE <= 2 * NT && TX * TY <= NT, "E region needs at most two passes");
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // 128-byte aligned start, as an offset into the shared array so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
@@ -488,8 +489,9 @@ __global__ void __launch_bounds__(NTH)
   constexpr int QN = (N1 + NT - 1) / NT;
   static_assert(NB <= N1 && N2 <= N1 && TX * TY <= NT, "pass counts");
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // 128-byte aligned start, as an offset into the shared array so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);
   T* sB1 = sE1 + 3 * Cfg::kE1;
   T* sE2 = sB1 + 3 * Cfg::kB1;
@@ -707,8 +709,9 @@ __global__ void __launch_bounds__(TX* TY)
   constexpr int NT = TX * TY, NE = (TX + 1) * (TY + 1);
   static_assert(NE <= 2 * NT, "E region needs at most two passes");
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // 128-byte aligned start, as an offset into the shared array so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
