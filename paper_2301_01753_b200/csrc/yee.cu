@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(NTH)
 // tile; the B0 / E0 boxes start at i0 - OFF (TMA's 16-byte alignment; OFF =
 // 16/sizeof(T) >= 2). Every point update is the same expression as in
 // k_fused_tma (yee_e_upd / yee_b_upd), so the result equals two single
-// sweeps. Three barriers per plane; NS = D + 2 TMA stages.
+// sweeps. Three barriers per plane; NS = D + 2 TMA stages; the E1, B1, E2
+// planes are double-buffered, so with NS = 3 two CTAs fit per SM (fp64).
 template <class T, int TX, int TY, int NS>
 struct TmaCfg2 {
   static constexpr int kOff = 16 / (int)sizeof(T);
@@ -462,7 +463,9 @@ struct TmaCfg2 {
   static constexpr int kXB = TX + 2, kYB = TY + 2;  // B1 region, origin (i0-1, j0-1)
   static constexpr int kX2 = TX + 1, kY2 = TY + 1;  // E2 region, origin (i0, j0)
   static constexpr int kE1 = 3 * kX1 * kY1, kB1 = 3 * kXB * kYB, kE2 = 3 * kX2 * kY2;
-  static constexpr int kBufBytes = 3 * (kE1 + kB1 + kE2) * (int)sizeof(T);
+  // E1, B1, E2 planes are double-buffered: each plane's last reader runs
+  // before the barrier that precedes the write of the plane two steps on
+  static constexpr int kBufBytes = 2 * (kE1 + kB1 + kE2) * (int)sizeof(T);
   static constexpr int kBarOff = (NS * kStage + kBufBytes + 15) / 16 * 16;
   static constexpr int kSmem = kBarOff + NS * 8 + 128;
   static constexpr int kD = NS - 2;  // prefetch distance in planes
@@ -493,8 +496,8 @@ __global__ void __launch_bounds__(NTH)
   // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);
-  T* sB1 = sE1 + 3 * Cfg::kE1;
-  T* sE2 = sB1 + 3 * Cfg::kB1;
+  T* sB1 = sE1 + 2 * Cfg::kE1;
+  T* sE2 = sB1 + 2 * Cfg::kB1;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -561,12 +564,12 @@ __global__ void __launch_bounds__(NTH)
       const T* __restrict__ B0p = reinterpret_cast<const T*>(base + ((gc + NS - 1) % NS) * Cfg::kStage);
       const T* __restrict__ E0c =
           reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage + Cfg::kBStride);
-      T* E1c = sE1 + (gc % 3) * Cfg::kE1;              // E1(z)
-      const T* E1p = sE1 + ((gc + 2) % 3) * Cfg::kE1;  // E1(z-1)
-      T* B1c = sB1 + ((gc + 2) % 3) * Cfg::kB1;        // B1(z-1)
-      const T* B1p = sB1 + ((gc + 1) % 3) * Cfg::kB1;  // B1(z-2)
-      T* E2c = sE2 + ((gc + 2) % 3) * Cfg::kE2;        // E2(z-1)
-      const T* E2p = sE2 + ((gc + 1) % 3) * Cfg::kE2;  // E2(z-2)
+      T* E1c = sE1 + (gc & 1) * Cfg::kE1;              // E1(z)
+      const T* E1p = sE1 + ((gc + 1) & 1) * Cfg::kE1;  // E1(z-1)
+      T* B1c = sB1 + ((gc + 1) & 1) * Cfg::kB1;        // B1(z-1)
+      const T* B1p = sB1 + (gc & 1) * Cfg::kB1;        // B1(z-2)
+      T* E2c = sE2 + ((gc + 1) & 1) * Cfg::kE2;        // E2(z-1)
+      const T* E2p = sE2 + (gc & 1) * Cfg::kE2;        // E2(z-2)
 #define B0C(c, y, x) B0c[((c) * (TY + 4) + (y)) * BW + (x)]
 #define B0P(c, y, x) B0p[((c) * (TY + 4) + (y)) * BW + (x)]
 #define E0C(c, y, x) E0c[((c) * (TY + 3) + (y)) * BW + (x)]
@@ -972,7 +975,7 @@ struct YeeDev {
 
   // kNT1: threads of the one-step sweep -- (TX+1)(TY+1) = 297 E points, so 320
   // threads cover the E region in one pass instead of 256 + 41
-  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 4, kNT2 = 512,
+  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 3, kNT2 = 416,
                        kNT1 = 320;
 
   template <class T>
