@@ -161,8 +161,8 @@ class YeeRunner:
         if world > 1:
             self.y, self.b0, self.e0, self.dt = yee_slab_setup(cfg["n"], cfg["precision"],
                                                                 device, rank, world, dist)
-            self.kernel_label = ("fused TMA sweep per z-slab + NCCL ghost-plane exchange "
-                                 "after every kernel")
+            self.kernel_label = ("two-step fused TMA sweep per z-slab (two ghost planes) + "
+                                 "NCCL ghost-plane exchange overlapped with the interior chunks")
         else:
             self.y, self.b0, self.e0, self.dt = yee_setup(cfg["n"], cfg["precision"], device)
         self.ndof = self.y.n_edges + self.y.n_faces
@@ -188,11 +188,19 @@ class YeeRunner:
         return ms.value, n.value
 
     def dominant(self, k_steps):
-        """(name, bytes per launch, avg ms per launch) of the fused sweep."""
+        """(name, algorithmic bytes per launch, avg ms per launch) of the fused
+        sweep. The timed launches cover the k_steps - 1 merged steps between
+        the opening b-half-kick and the closing e-kick + b-half-kick; a
+        two-step sweep (k_fused2_tma) advances two of them per launch, so its
+        algorithmic bytes per launch are two steps' worth."""
         self.timing(True)
         self.y.advance(k_steps)
         ms, n = self.timing(False)
-        return "k_fused_tma (e-kick + b-kick sweep)", self.y.step_bytes(), ms / max(n, 1)
+        n = max(n, 1)
+        per_launch = (k_steps - 1) / n
+        name = ("k_fused2_tma (two e-kick + b-kick pairs per z-sweep)" if per_launch > 1.5
+                else "k_fused_tma (e-kick + b-kick sweep)")
+        return name, self.y.step_bytes() * per_launch, ms / n
 
     def step_bytes(self):
         return self.y.step_bytes()
@@ -208,7 +216,9 @@ class YeeRunner:
         L.check(L.lib().sfeec_yee_get_state(self.y.handle, dptr(out_b), dptr(out_e), None))
         return time.perf_counter() - t0
 
-    kernel_label = "fused e-kick + b-kick z-sweep, TMA-pipelined (k_fused_tma)"
+    kernel_label = ("two leapfrog steps per TMA-pipelined z-sweep, intermediates in registers + "
+                    "shared memory (k_fused2_tma; SFEEC_YEE_VARIANT=2 selects the one-step "
+                    "k_fused_tma)")
 
 
 def tet_setup(cfg, device):

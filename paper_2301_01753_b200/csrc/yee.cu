@@ -463,9 +463,8 @@ struct TmaCfg2 {
   static constexpr int kXB = TX + 2, kYB = TY + 2;  // B1 region, origin (i0-1, j0-1)
   static constexpr int kX2 = TX + 1, kY2 = TY + 1;  // E2 region, origin (i0, j0)
   static constexpr int kE1 = 3 * kX1 * kY1, kB1 = 3 * kXB * kYB, kE2 = 3 * kX2 * kY2;
-  // E1, B1, E2 planes are double-buffered: each plane's last reader runs
-  // before the barrier that precedes the write of the plane two steps on
-  static constexpr int kBufBytes = 2 * (kE1 + kB1 + kE2) * (int)sizeof(T);
+  // E1 and E2 planes double-buffered, B1 single, all on the E1 region grid
+  static constexpr int kBufBytes = 5 * 3 * kX1 * kY1 * (int)sizeof(T);
   static constexpr int kBarOff = (NS * kStage + kBufBytes + 15) / 16 * 16;
   static constexpr int kSmem = kBarOff + NS * 8 + 128;
   static constexpr int kD = NS - 2;  // prefetch distance in planes
@@ -485,19 +484,17 @@ __global__ void __launch_bounds__(NTH)
                  int n_units, int kbeg, int kend) {
   using Cfg = TmaCfg2<T, TX, TY, NS>;
   constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
-  constexpr int NT = NTH;  // threads; regions are covered in QN passes
-  constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, XB = Cfg::kXB, YB = Cfg::kYB, X2 = Cfg::kX2,
-                Y2 = Cfg::kY2;
-  constexpr int N1 = X1 * Y1, NB = XB * YB, N2 = X2 * Y2;
-  constexpr int QN = (N1 + NT - 1) / NT;
-  static_assert(NB <= N1 && N2 <= N1 && TX * TY <= NT, "pass counts");
+  // one thread per point of the E1 region (origin (i0-1, j0-1)); the B1, E2
+  // and B2 regions are subsets in the same coordinates, so every thread keeps
+  // its own point's E1, B1, E2 of the current and previous plane in
+  // registers and only the x/y neighbours go through shared memory
+  constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, NP = X1 * Y1;
+  static_assert(NP <= NTH, "one region point per thread");
   extern __shared__ unsigned char smem_raw[];
-  // 128-byte aligned start, as an offset into the shared array so the
-  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);
-  T* sB1 = sE1 + 2 * Cfg::kE1;
-  T* sE2 = sB1 + 2 * Cfg::kB1;
+  T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);  // 2 planes x 3 comps x NP
+  T* sB1 = sE1 + 2 * 3 * NP;                                 // 1 plane
+  T* sE2 = sB1 + 3 * NP;                                     // 2 planes
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -510,39 +507,25 @@ __global__ void __launch_bounds__(NTH)
   uint32_t gplane = 0;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int64_t kstride = (int64_t)g.P0 * g.S[1];
-  // region coordinates of this thread's points (pass 0: tid, pass 1: tid + NT)
-  int x1[QN], y1[QN], xb[QN], yb[QN], x2[QN], y2[QN];
-#pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const int p = tid + q * NT;
-    x1[q] = p % X1;
-    y1[q] = p / X1;
-    xb[q] = p % XB;
-    yb[q] = p / XB;
-    x2[q] = p % X2;
-    y2[q] = p / X2;
-  }
-  const int bx = tid % TX, by = tid / TX;  // own B2 point (tid < TX * TY)
-  const bool bthr = tid < TX * TY;
+  const bool pt = tid < NP;
+  const int x = tid % X1, y = tid / X1;
+  const int me = tid;                           // own index in the region arrays
+  const int bi = x + OFF - 1, bj = y + 1, ej = y;  // own point in the B0 / E0 boxes
+  const bool inB1 = pt && x <= TX + 1 && y <= TY + 1;
+  const bool inE2 = pt && x >= 1 && x <= TX + 1 && y >= 1 && y <= TY + 1;
 
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
     const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
     const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
     const int P = k1 - k0 + 4;  // local planes p <-> z = k0 - 2 + p
-    uint32_t m1[QN], mb[QN], m2[QN];
-#pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int i1 = i0 - 1 + x1[q], j1 = j0 - 1 + y1[q];
-      m1[q] = tid + q * NT < N1 ? e_mask_xy(i1, j1, n0, n1) : 0u;
-      const int ib = i0 - 1 + xb[q], jb = j0 - 1 + yb[q];
-      mb[q] = (tid + q * NT < NB && ib >= 0 && ib < n0 && jb >= 0 && jb < n1) ? 1u : 0u;
-      const int i2 = i0 + x2[q], j2 = j0 + y2[q];
-      const bool own = x2[q] < TX && y2[q] < TY && i2 < n0 && j2 < n1;
-      m2[q] = tid + q * NT < N2 ? (e_mask_xy(i2, j2, n0, n1) | (own ? 8u : 0u)) : 0u;
-    }
-    const bool bown = bthr && i0 + bx < n0 && j0 + by < n1;
-    const int64_t bsij = (int64_t)(i0 + bx) + (int64_t)g.P0 * (j0 + by);
+    const int i = i0 - 1 + x, j = j0 - 1 + y;
+    const uint32_t m = pt ? e_mask_xy(i, j, n0, n1) : 0u;
+    const bool b1up = inB1 && i >= 0 && i < n0 && j >= 0 && j < n1;
+    const bool own = inE2 && x <= TX && y <= TY && i < n0 && j < n1;
+    const int64_t sij = (int64_t)i + (int64_t)g.P0 * j;
+    T e1c[3] = {0, 0, 0}, e1p[3] = {0, 0, 0}, b1c[3] = {0, 0, 0}, b1p[3] = {0, 0, 0};
+    T e2c[3] = {0, 0, 0}, e2p[3] = {0, 0, 0};
 
     auto issue = [&](int p) {
       const uint32_t gp = gplane + p;
@@ -564,119 +547,94 @@ __global__ void __launch_bounds__(NTH)
       const T* __restrict__ B0p = reinterpret_cast<const T*>(base + ((gc + NS - 1) % NS) * Cfg::kStage);
       const T* __restrict__ E0c =
           reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage + Cfg::kBStride);
-      T* E1c = sE1 + (gc & 1) * Cfg::kE1;              // E1(z)
-      const T* E1p = sE1 + ((gc + 1) & 1) * Cfg::kE1;  // E1(z-1)
-      T* B1c = sB1 + ((gc + 1) & 1) * Cfg::kB1;        // B1(z-1)
-      const T* B1p = sB1 + (gc & 1) * Cfg::kB1;        // B1(z-2)
-      T* E2c = sE2 + ((gc + 1) & 1) * Cfg::kE2;        // E2(z-1)
-      const T* E2p = sE2 + (gc & 1) * Cfg::kE2;        // E2(z-2)
-#define B0C(c, y, x) B0c[((c) * (TY + 4) + (y)) * BW + (x)]
-#define B0P(c, y, x) B0p[((c) * (TY + 4) + (y)) * BW + (x)]
-#define E0C(c, y, x) E0c[((c) * (TY + 3) + (y)) * BW + (x)]
-#define E1(buf, c, y, x) buf[((c) * Y1 + (y)) * X1 + (x)]
-#define B1(buf, c, y, x) buf[((c) * YB + (y)) * XB + (x)]
-#define E2(buf, c, y, x) buf[((c) * Y2 + (y)) * X2 + (x)]
-      // ---- phase 1: E1(z) on the E1 region (global i = i0-1+x, j = j0-1+y)
-      if (p >= 1) {
+      T* E1z = sE1 + (gc & 1) * 3 * NP;                 // E1(z)
+      const T* E1y = sE1 + ((gc + 1) & 1) * 3 * NP;     // E1(z-1)
+      T* E2y = sE2 + ((gc + 1) & 1) * 3 * NP;           // E2(z-1)
+      const T* E2x = sE2 + (gc & 1) * 3 * NP;           // E2(z-2)
+#define B0C(c, yy, xx) B0c[((c) * (TY + 4) + (yy)) * BW + (xx)]
+#define B0P(c, yy, xx) B0p[((c) * (TY + 4) + (yy)) * BW + (xx)]
+#define E0C(c, yy, xx) E0c[((c) * (TY + 3) + (yy)) * BW + (xx)]
+#define R(buf, c, idx) buf[(c) * NP + (idx)]
+      // ---- phase 1: E1(z) at the own point
+      if (p >= 1 && pt) {
         const int zg = z + g.kofs;
         const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
-#pragma unroll
-        for (int q = 0; q < QN; ++q) {
-          if (tid + q * NT >= N1) break;
-          const int x = x1[q], y = y1[q];
-          const int bi = x + OFF - 1, bj = y + 1;  // B0 box: x from i0-OFF, y from j0-2
-          const int ei = x + OFF - 1, ej = y;      // E0 box: x from i0-OFF, y from j0-1
-          T e0 = E0C(0, ej, ei), e1 = E0C(1, ej, ei), e2 = E0C(2, ej, ei);
-          if ((m1[q] & 1) && kin)
-            e0 += ck.ce[1] * (B0C(2, bj, bi) - B0C(2, bj - 1, bi)) - ck.ce[2] * (B0C(1, bj, bi) - B0P(1, bj, bi));
-          if ((m1[q] & 2) && kin)
-            e1 += ck.ce[2] * (B0C(0, bj, bi) - B0P(0, bj, bi)) - ck.ce[0] * (B0C(2, bj, bi) - B0C(2, bj, bi - 1));
-          if ((m1[q] & 4) && kz)
-            e2 += ck.ce[0] * (B0C(1, bj, bi) - B0C(1, bj, bi - 1)) - ck.ce[1] * (B0C(0, bj, bi) - B0C(0, bj - 1, bi));
-          E1(E1c, 0, y, x) = e0;
-          E1(E1c, 1, y, x) = e1;
-          E1(E1c, 2, y, x) = e2;
-        }
+        T e0 = E0C(0, ej, bi), e1 = E0C(1, ej, bi), e2 = E0C(2, ej, bi);
+        if ((m & 1) && kin)
+          e0 += ck.ce[1] * (B0C(2, bj, bi) - B0C(2, bj - 1, bi)) - ck.ce[2] * (B0C(1, bj, bi) - B0P(1, bj, bi));
+        if ((m & 2) && kin)
+          e1 += ck.ce[2] * (B0C(0, bj, bi) - B0P(0, bj, bi)) - ck.ce[0] * (B0C(2, bj, bi) - B0C(2, bj, bi - 1));
+        if ((m & 4) && kz)
+          e2 += ck.ce[0] * (B0C(1, bj, bi) - B0C(1, bj, bi - 1)) - ck.ce[1] * (B0C(0, bj, bi) - B0C(0, bj - 1, bi));
+        e1c[0] = e0;
+        e1c[1] = e1;
+        e1c[2] = e2;
+        R(E1z, 0, me) = e0;
+        R(E1z, 1, me) = e1;
+        R(E1z, 2, me) = e2;
       }
-      __syncthreads();
-      // ---- phase 2: B1(z-1) on the B1 region (global i = i0-1+x, j = j0-1+y)
-      if (p >= 2) {
-        const int zb = z - 1;
-        const int zg = zb + g.kofs;
-        const bool kb = zg >= 0 && zg < n2;
-#pragma unroll
-        for (int q = 0; q < QN; ++q) {
-          if (tid + q * NT >= NB) break;
-          const int x = xb[q], y = yb[q];
-          const int bi = x + OFF - 1, bj = y + 1;  // B0 box coordinates of (i, j)
-          T v0 = B0P(0, bj, bi), v1 = B0P(1, bj, bi), v2 = B0P(2, bj, bi);
-          if (mb[q] && kb) {  // E1 region coordinates of (i, j): (x, y)
-            v0 = v0 + (ck.cb[2] * (E1(E1c, 1, y, x) - E1(E1p, 1, y, x)) -
-                       ck.cb[1] * (E1(E1p, 2, y + 1, x) - E1(E1p, 2, y, x)));
-            v1 = v1 + (ck.cb[0] * (E1(E1p, 2, y, x + 1) - E1(E1p, 2, y, x)) -
-                       ck.cb[2] * (E1(E1c, 0, y, x) - E1(E1p, 0, y, x)));
-            v2 = v2 + (ck.cb[1] * (E1(E1p, 0, y + 1, x) - E1(E1p, 0, y, x)) -
-                       ck.cb[0] * (E1(E1p, 1, y, x + 1) - E1(E1p, 1, y, x)));
-          }
-          B1(B1c, 0, y, x) = v0;
-          B1(B1c, 1, y, x) = v1;
-          B1(B1c, 2, y, x) = v2;
+      __syncthreads();  // the B1 plane is free (last read by the previous phase 3)
+      // ---- phase 2: B1(z-1) at the own point (E1(z-1) neighbours from smem)
+      if (p >= 2 && inB1) {
+        const int zg = z - 1 + g.kofs;
+        T v0 = B0P(0, bj, bi), v1 = B0P(1, bj, bi), v2 = B0P(2, bj, bi);
+        if (b1up && zg >= 0 && zg < n2) {
+          v0 = v0 + (ck.cb[2] * (e1c[1] - e1p[1]) - ck.cb[1] * (R(E1y, 2, me + X1) - e1p[2]));
+          v1 = v1 + (ck.cb[0] * (R(E1y, 2, me + 1) - e1p[2]) - ck.cb[2] * (e1c[0] - e1p[0]));
+          v2 = v2 + (ck.cb[1] * (R(E1y, 0, me + X1) - e1p[0]) - ck.cb[0] * (R(E1y, 1, me + 1) - e1p[1]));
         }
+        b1c[0] = v0;
+        b1c[1] = v1;
+        b1c[2] = v2;
+        R(sB1, 0, me) = v0;
+        R(sB1, 1, me) = v1;
+        R(sB1, 2, me) = v2;
       }
-      __syncthreads();
-      // ---- phase 3: E2(z-1) on the E2 region (global i = i0+x, j = j0+y)
-      if (p >= 3) {
+      __syncthreads();  // B1(z-1) complete
+      // ---- phase 3: E2(z-1) at the own point (B1(z-1) neighbours from smem)
+      if (p >= 3 && inE2) {
         const int ze = z - 1;
         const int zg = ze + g.kofs;
         const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
-        const bool kw = ze >= k0 && ze < k1;
-#pragma unroll
-        for (int q = 0; q < QN; ++q) {
-          if (tid + q * NT >= N2) break;
-          const int x = x2[q], y = y2[q];
-          const int ex = x + 1, ey = y + 1;  // E1 region coordinates of (i, j)
-          const int cx = x + 1, cy = y + 1;  // B1 region coordinates of (i, j)
-          T e0 = E1(E1p, 0, ey, ex), e1 = E1(E1p, 1, ey, ex), e2 = E1(E1p, 2, ey, ex);
-          const bool d0 = (m2[q] & 1) && kin, d1 = (m2[q] & 2) && kin, d2 = (m2[q] & 4) && kz;
-          if (d0)
-            e0 += ck.ce[1] * (B1(B1c, 2, cy, cx) - B1(B1c, 2, cy - 1, cx)) - ck.ce[2] * (B1(B1c, 1, cy, cx) - B1(B1p, 1, cy, cx));
-          if (d1)
-            e1 += ck.ce[2] * (B1(B1c, 0, cy, cx) - B1(B1p, 0, cy, cx)) - ck.ce[0] * (B1(B1c, 2, cy, cx) - B1(B1c, 2, cy, cx - 1));
-          if (d2)
-            e2 += ck.ce[0] * (B1(B1c, 1, cy, cx) - B1(B1c, 1, cy, cx - 1)) - ck.ce[1] * (B1(B1c, 0, cy, cx) - B1(B1c, 0, cy - 1, cx));
-          if ((m2[q] & 8) && kw) {
-            const int64_t s = (int64_t)(i0 + x) + (int64_t)g.P0 * (j0 + y) + kstride * ze;
-            if (d0) out.c[0][s] = e0;
-            if (d1) out.c[1][s] = e1;
-            if (d2) out.c[2][s] = e2;
-          }
-          E2(E2c, 0, y, x) = e0;
-          E2(E2c, 1, y, x) = e1;
-          E2(E2c, 2, y, x) = e2;
+        T e0 = e1p[0], e1 = e1p[1], e2 = e1p[2];
+        const bool d0 = (m & 1) && kin, d1 = (m & 2) && kin, d2 = (m & 4) && kz;
+        if (d0) e0 += ck.ce[1] * (b1c[2] - R(sB1, 2, me - X1)) - ck.ce[2] * (b1c[1] - b1p[1]);
+        if (d1) e1 += ck.ce[2] * (b1c[0] - b1p[0]) - ck.ce[0] * (b1c[2] - R(sB1, 2, me - 1));
+        if (d2) e2 += ck.ce[0] * (b1c[1] - R(sB1, 1, me - 1)) - ck.ce[1] * (b1c[0] - R(sB1, 0, me - X1));
+        if (own && ze >= k0 && ze < k1) {
+          const int64_t s = sij + kstride * ze;
+          if (d0) out.c[0][s] = e0;
+          if (d1) out.c[1][s] = e1;
+          if (d2) out.c[2][s] = e2;
         }
+        e2c[0] = e0;
+        e2c[1] = e1;
+        e2c[2] = e2;
+        R(E2y, 0, me) = e0;
+        R(E2y, 1, me) = e1;
+        R(E2y, 2, me) = e2;
       }
-      __syncthreads();
-      // ---- phase 4: B2(z-2) on the own tile
-      if (p >= 4 && bown) {
+      // ---- phase 4: B2(z-2) on the own tile point (E2(z-2) neighbours, written
+      // in the previous iteration, from smem)
+      if (p >= 4 && own) {
         const int zb = z - 2;
         if (zb >= k0 && zb < k1) {
-          const int x = bx, y = by;
-          const int cx = x + 1, cy = y + 1;  // B1 region coordinates
-          const int64_t s = bsij + kstride * zb;
-          out.c[3][s] = B1(B1p, 0, cy, cx) + (ck.cb[2] * (E2(E2c, 1, y, x) - E2(E2p, 1, y, x)) -
-                                              ck.cb[1] * (E2(E2p, 2, y + 1, x) - E2(E2p, 2, y, x)));
-          out.c[4][s] = B1(B1p, 1, cy, cx) + (ck.cb[0] * (E2(E2p, 2, y, x + 1) - E2(E2p, 2, y, x)) -
-                                              ck.cb[2] * (E2(E2c, 0, y, x) - E2(E2p, 0, y, x)));
-          out.c[5][s] = B1(B1p, 2, cy, cx) + (ck.cb[1] * (E2(E2p, 0, y + 1, x) - E2(E2p, 0, y, x)) -
-                                              ck.cb[0] * (E2(E2p, 1, y, x + 1) - E2(E2p, 1, y, x)));
+          const int64_t s = sij + kstride * zb;
+          out.c[3][s] = b1p[0] + (ck.cb[2] * (e2c[1] - e2p[1]) - ck.cb[1] * (R(E2x, 2, me + X1) - e2p[2]));
+          out.c[4][s] = b1p[1] + (ck.cb[0] * (R(E2x, 2, me + 1) - e2p[2]) - ck.cb[2] * (e2c[0] - e2p[0]));
+          out.c[5][s] = b1p[2] + (ck.cb[1] * (R(E2x, 0, me + X1) - e2p[0]) - ck.cb[0] * (R(E2x, 1, me + 1) - e2p[1]));
         }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        e1p[c] = e1c[c];
+        b1p[c] = b1c[c];
+        e2p[c] = e2c[c];
       }
 #undef B0C
 #undef B0P
 #undef E0C
-#undef E1
-#undef B1
-#undef E2
+#undef R
     }
     gplane += P;
     __syncthreads();
@@ -885,10 +843,12 @@ struct YeeDev {
   double d[3] = {1, 1, 1};
   double dt = 0, eps0 = 1, mu0 = 1, dv = 1;
   int prec = 8;
-  // fused-sweep variant: SFEEC_YEE_VARIANT overrides the default (A/B runs)
+  // fused-sweep variant: SFEEC_YEE_VARIANT overrides the default (A/B runs).
+  // Default 4: two leapfrog steps per z-sweep (k_fused2_tma), measured fastest
+  // (256^3 fp64 0.219 vs 0.288 ms/step for the one-step sweep, variant 2)
   int variant = [] {
     const char* v = std::getenv("SFEEC_YEE_VARIANT");
-    return v ? std::atoi(v) : 2;
+    return v ? std::atoi(v) : 4;
   }();
   // TMA descriptors of the two ping-pong buffers (B box, E box), PEC only
   CUtensorMap mapB[2], mapE[2];
@@ -1080,8 +1040,9 @@ struct YeeDev {
   }
 
   // planes swept by the fused kernel: [0, n) on one domain, [1, nzl + 1) on a slab
-  int sweep_beg() const { return slab() ? 1 : 0; }
-  int sweep_end() const { return slab() ? g.S[2] - 1 : g.n[2]; }
+  int ghost() const { return slab() ? g.kown_lo : 0; }  // ghost planes per side
+  int sweep_beg() const { return slab() ? ghost() : 0; }
+  int sweep_end() const { return slab() ? g.S[2] - ghost() : g.n[2]; }
   int sweep_chunks() const { return (sweep_end() - sweep_beg() + kChunk - 1) / kChunk; }
 
   template <class T>
@@ -1090,17 +1051,29 @@ struct YeeDev {
     cur ^= 1;
   }
 
-  // Split sweep for overlapping the halo exchange: part 0 = the bottom and top
-  // z-chunks (they produce every plane a neighbour needs), part 1 = the rest.
-  // Neither flips the buffers.
+  // Split sweep for overlapping the halo exchange: part 0 = the z-chunks that
+  // produce the planes the neighbours need (the bottom and top `ghost()`
+  // owned planes), part 1 = the rest. two: the two-step sweep. Neither flips
+  // the buffers.
   template <class T>
-  void fused_part(double h_e, double h_b, int part) {
-    const int kb = sweep_beg(), ke = sweep_end(), nch = sweep_chunks();
+  void fused_part(double h_e, double h_b, int part, bool two = false) {
+    const int kb = sweep_beg(), ke = sweep_end(), G = ghost();
+    auto range = [&](int a, int b) {
+      if (b <= a) return;
+      if (two)
+        launch_range2<T>(h_e, h_b, a, b);
+      else
+        launch_range<T>(h_e, h_b, a, b);
+    };
+    const int lo_end = std::min(kb + kChunk, ke);
+    // first chunk of the top part: the chunk holding plane ke - G (chunks are
+    // aligned to kb), but never below the bottom chunk's end
+    const int hi_beg = std::max(lo_end, kb + ((ke - G - kb) / kChunk) * kChunk);
     if (part == 0) {
-      launch_range<T>(h_e, h_b, kb, std::min(kb + kChunk, ke));
-      if (nch >= 2) launch_range<T>(h_e, h_b, kb + (nch - 1) * kChunk, ke);
-    } else if (nch >= 3) {
-      launch_range<T>(h_e, h_b, kb + kChunk, kb + (nch - 1) * kChunk);
+      range(kb, lo_end);
+      range(hi_beg, ke);
+    } else {
+      range(lo_end, hi_beg);
     }
   }
 
@@ -1143,18 +1116,18 @@ struct YeeDev {
   // next kernel reads the ghosts. The exchange touches only ghost planes and
   // the boundary chunks' planes, the interior sweep only interior planes.
   template <class T>
-  void fused_overlapped(double h_e, double h_b) {
+  void fused_overlapped(double h_e, double h_b, bool two = false) {
     if (!comm_stream) {
       SFEEC_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
       SFEEC_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
       SFEEC_CUDA(cudaEventCreateWithFlags(&ev_xch, cudaEventDisableTiming));
     }
-    fused_part<T>(h_e, h_b, 0);
+    fused_part<T>(h_e, h_b, 0, two);
     SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
     SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
     exchange_nccl(cur ^ 1, comm_stream);
     SFEEC_CUDA(cudaEventRecord(ev_xch, comm_stream));
-    fused_part<T>(h_e, h_b, 1);
+    fused_part<T>(h_e, h_b, 1, two);
     SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
     cur ^= 1;
   }
@@ -1164,7 +1137,7 @@ struct YeeDev {
     std::vector<Phase> p;
     if (n <= 0) return p;
     const bool use_fused = variant >= 1 && g.bc == SFEEC_BC_PEC;
-    const bool two = variant == 4 && g.bc == SFEEC_BC_PEC && !slab();
+    const bool two = variant == 4 && g.bc == SFEEC_BC_PEC && (!slab() || ghost() >= 2);
     p.push_back({0, 0.5 * dt, 0});
     for (int64_t s = 0; s + 1 < n; ++s) {
       if (two && s + 2 < n) {  // two fused steps per sweep
@@ -1202,32 +1175,34 @@ struct YeeDev {
       run_t<float>(p);
   }
 
-  // ghost-plane exchange over NCCL (one process per GPU): local plane 1 (E and
-  // B) goes down into the lower neighbour's top ghost; the top owned B plane
-  // goes up into the upper neighbour's bottom ghost. Planes are contiguous in
-  // every component array, so no packing.
+  // ghost-plane exchange over NCCL (one process per GPU): the first G owned
+  // planes (E and B) go down into the lower neighbour's top ghosts; the top G
+  // owned planes go up into the upper neighbour's bottom ghosts (B only when
+  // G = 1: the one-step kernels never read E below). Each component's G
+  // planes are contiguous, so one message per component and direction.
   void exchange_nccl() { exchange_nccl(cur, stream); }
   void exchange_nccl(int bufsel, cudaStream_t es) {
     if (!slab() || !comm) return;
     const Nccl& nc = Nccl::get();
     const ncclDataType_t ty = prec == 8 ? ncclFloat64 : ncclFloat32;
-    const size_t cnt = (size_t)plane();
+    const int G = ghost();
+    const size_t cnt = (size_t)plane() * (size_t)G;
     char* base = buf[bufsel].p;
     cudaStream_t stream = es;
     auto at = [&](int comp, int pl) {
-      return base + ((size_t)comp * (size_t)g.npts() + (size_t)pl * cnt) * (size_t)prec;
+      return base + ((size_t)comp * (size_t)g.npts() + (size_t)pl * (size_t)plane()) * (size_t)prec;
     };
-    const int top_owned = g.S[2] - 2, top_ghost = g.S[2] - 1;
+    const int c_up = G == 1 ? 3 : 0;
     nc.check(nc.group_start(), "ncclGroupStart");
     if (rank > 0) {
-      for (int c = 0; c < 6; ++c) nc.check(nc.send(at(c, 1), cnt, ty, rank - 1, comm, stream), "ncclSend");
-      for (int c = 3; c < 6; ++c) nc.check(nc.recv(at(c, 0), cnt, ty, rank - 1, comm, stream), "ncclRecv");
+      for (int c = 0; c < 6; ++c) nc.check(nc.send(at(c, G), cnt, ty, rank - 1, comm, stream), "ncclSend");
+      for (int c = c_up; c < 6; ++c) nc.check(nc.recv(at(c, 0), cnt, ty, rank - 1, comm, stream), "ncclRecv");
     }
     if (rank < nranks - 1) {
       for (int c = 0; c < 6; ++c)
-        nc.check(nc.recv(at(c, top_ghost), cnt, ty, rank + 1, comm, stream), "ncclRecv");
-      for (int c = 3; c < 6; ++c)
-        nc.check(nc.send(at(c, top_owned), cnt, ty, rank + 1, comm, stream), "ncclSend");
+        nc.check(nc.recv(at(c, g.S[2] - G), cnt, ty, rank + 1, comm, stream), "ncclRecv");
+      for (int c = c_up; c < 6; ++c)
+        nc.check(nc.send(at(c, g.S[2] - 2 * G), cnt, ty, rank + 1, comm, stream), "ncclSend");
     }
     nc.check(nc.group_end(), "ncclGroupEnd");
   }
@@ -1241,11 +1216,11 @@ struct YeeDev {
     for (size_t i = 0; i < p.size(); ++i) {
       if (t && i == 1) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
       if (t && i + 2 == p.size()) SFEEC_CUDA(cudaEventRecord(ev[1], stream));
-      if (overlap && p[i].kind == 2) {
+      if (overlap && (p[i].kind == 2 || p[i].kind == 3)) {
         if (prec == 8)
-          fused_overlapped<double>(p[i].h1, p[i].h2);
+          fused_overlapped<double>(p[i].h1, p[i].h2, p[i].kind == 3);
         else
-          fused_overlapped<float>(p[i].h1, p[i].h2);
+          fused_overlapped<float>(p[i].h1, p[i].h2, p[i].kind == 3);
         continue;
       }
       run(p[i]);
@@ -1384,12 +1359,14 @@ struct YeeGroup {
   std::vector<std::unique_ptr<YeeDev>> s;
   YeeGeom global;
 
-  // flip = 1: exchange into the buffers being written (the split sweep)
+  // flip = 1: exchange into the buffers being written (the split sweep);
+  // the same planes and components as YeeDev::exchange_nccl
   void exchange(int flip = 0) {
     const int R = (int)s.size();
     for (int r = 0; r < R; ++r) {
       YeeDev& a = *s[(size_t)r];
-      const size_t bytes = (size_t)a.plane() * (size_t)a.prec;
+      const int G = a.ghost();
+      const size_t bytes = (size_t)a.plane() * (size_t)a.prec * (size_t)G;
       auto at = [&](YeeDev& d, int comp, int pl) {
         return d.buf[d.cur ^ flip].p +
                ((size_t)comp * (size_t)d.g.npts() + (size_t)pl * (size_t)d.plane()) * (size_t)d.prec;
@@ -1397,33 +1374,34 @@ struct YeeGroup {
       if (r > 0) {
         YeeDev& lo = *s[(size_t)r - 1];
         for (int c = 0; c < 6; ++c)
-          SFEEC_CUDA(cudaMemcpyAsync(at(lo, c, lo.g.S[2] - 1), at(a, c, 1), bytes,
+          SFEEC_CUDA(cudaMemcpyAsync(at(lo, c, lo.g.S[2] - G), at(a, c, G), bytes,
                                      cudaMemcpyDeviceToDevice, a.stream));
       }
       if (r < R - 1) {
         YeeDev& hi = *s[(size_t)r + 1];
-        for (int c = 3; c < 6; ++c)
-          SFEEC_CUDA(cudaMemcpyAsync(at(hi, c, 0), at(a, c, a.g.S[2] - 2), bytes,
+        for (int c = G == 1 ? 3 : 0; c < 6; ++c)
+          SFEEC_CUDA(cudaMemcpyAsync(at(hi, c, 0), at(a, c, a.g.S[2] - 2 * G), bytes,
                                      cudaMemcpyDeviceToDevice, a.stream));
       }
     }
   }
   void run_all(const Phase& p) {
-    if (p.kind == 2 && s[0]->variant >= 2) {
+    if ((p.kind == 2 || p.kind == 3) && s[0]->variant >= 2) {
       // the NCCL path's overlapped schedule, serialised: boundary chunks,
       // exchange into the new buffers, interior chunks, flip
+      const bool two = p.kind == 3;
       for (auto& d : s) {
         if (d->prec == 8)
-          d->fused_part<double>(p.h1, p.h2, 0);
+          d->fused_part<double>(p.h1, p.h2, 0, two);
         else
-          d->fused_part<float>(p.h1, p.h2, 0);
+          d->fused_part<float>(p.h1, p.h2, 0, two);
       }
       exchange(1);
       for (auto& d : s) {
         if (d->prec == 8)
-          d->fused_part<double>(p.h1, p.h2, 1);
+          d->fused_part<double>(p.h1, p.h2, 1, two);
         else
-          d->fused_part<float>(p.h1, p.h2, 1);
+          d->fused_part<float>(p.h1, p.h2, 1, two);
         d->cur ^= 1;
       }
       return;
@@ -1622,7 +1600,7 @@ void sfeec_yee_group_destroy(sfeec_yee_group* h) { delete h; }
 
 int sfeec_yee_group_set_variant(sfeec_yee_group* h, int variant) {
   return guarded([&] {
-    require(h && (variant == 0 || variant >= 2) && variant <= 3, "slabs support variants 0, 2 and 3");
+    require(h && (variant == 0 || variant >= 2) && variant <= 4, "slabs support variants 0, 2, 3 and 4");
     for (auto& d : h->g.s) d->variant = variant;
   });
 }

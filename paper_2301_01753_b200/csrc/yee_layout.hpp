@@ -116,14 +116,19 @@ inline YeeGeom make_yee_geom(int nx, int ny, int nz, int bc) {
 // Slab r of R of a PEC lattice with nz global cells (nz divisible by R):
 // local storage planes 0 (ghost below), 1..nzl (owned), nzl+1 (ghost above;
 // on the last slab this is the global top wall plane, owned and constant).
-inline YeeGeom make_yee_slab(int nx, int ny, int nz, int r, int R) {
+// ghost planes per side of a slab: 2, so the two-step sweep (two leapfrog
+// steps per pass, yee.cu k_fused2_tma) has its halo; the one-step kernels
+// read only the inner ghost plane
+inline constexpr int kYeeGhost = 2;
+
+inline YeeGeom make_yee_slab(int nx, int ny, int nz, int r, int R, int G = kYeeGhost) {
   YeeGeom g = make_yee_geom(nx, ny, nz, 1);
   const int nzl = nz / R;
-  g.S[2] = nzl + 2;
+  g.S[2] = nzl + 2 * G;
   g.np_alloc = ((int64_t)g.P0 * g.S[1] * g.S[2] + 31) / 32 * 32;
-  g.kofs = r * nzl - 1;
-  g.kown_lo = 1;
-  g.kown_hi = (r == R - 1) ? nzl + 2 : nzl + 1;
+  g.kofs = r * nzl - G;
+  g.kown_lo = G;
+  g.kown_hi = (r == R - 1) ? G + nzl + 1 : G + nzl;  // the last slab owns the top wall
   g.init_offsets();
   return g;
 }

@@ -67,20 +67,23 @@ def test_slab_maps_are_z_ordered_single_process(world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("variant", [2, 3, 0])
-def test_group_lockstep_bitwise_equals_single_domain(world, variant):
+@pytest.mark.parametrize("variant", [2, 3, 0, 4])
+@pytest.mark.parametrize("steps", [30, 31])
+def test_group_lockstep_bitwise_equals_single_domain(world, variant, steps):
+    """Slabs with two ghost planes, the NCCL path's split schedule (boundary
+    chunks, exchange, interior chunks); variant 4 = two steps per sweep."""
     dims, d = (37, 21, 70 * world), (1.0, 0.9, 1.1)  # 3 z-chunks per slab: boundary + interior
     rng = np.random.default_rng(world)
     one = S.YeeScheme(*dims, *d, 0.2, bc=1)
     one.set_variant(variant)
     b0, e0 = rng.standard_normal(one.n_faces), rng.standard_normal(one.n_edges)
     one.load(b0, e0)
-    one.advance(30)
+    one.advance(steps)
     b1, e1, _ = one.fetch()
     grp = S.YeeGroup(*dims, *d, 0.2, world)
     grp.set_variant(variant)
     grp.load(b0, e0)
-    grp.advance(30)
+    grp.advance(steps)
     b2, e2 = grp.fetch()
     assert np.array_equal(b1, b2) and np.array_equal(e1, e2)
     assert grp.energy() == pytest.approx(one.energy(), rel=1e-13)
