@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsfeec_b200.so")
+# SFEEC_B200_LIB: an alternative build of the same library (tuning A/B runs)
+LIB_PATH = os.environ.get("SFEEC_B200_LIB") or os.path.join(_HERE, "libsfeec_b200.so")
 
 SFEEC_OK, SFEEC_EINVAL, SFEEC_ECUDA, SFEEC_ENCCL, SFEEC_ENOMEM = range(5)
 SPLIT_LIE_TROTTER, SPLIT_STRANG = 0, 1

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -48,6 +49,16 @@ struct YeeCoef {
 namespace {
 
 constexpr int kThreads = 256;
+
+// One curl update x + (c1*d1 - c2*d2) with the rounding pinned (one mul, one
+// fma, one add), so every Yee kernel (one-step, fused, two-step) produces
+// bitwise the same point values whatever the compiler would contract.
+__device__ __forceinline__ double yee_upd(double x, double c1, double d1, double c2, double d2) {
+  return __dadd_rn(x, __fma_rn(c1, d1, -__dmul_rn(c2, d2)));
+}
+__device__ __forceinline__ float yee_upd(float x, float c1, float d1, float c2, float d2) {
+  return __fadd_rn(x, __fmaf_rn(c1, d1, -__fmul_rn(c2, d2)));
+}
 
 // DOF masks (PEC), yee_layout.hpp. k is the local storage plane; the masks
 // are evaluated at the global plane k + kofs, and only owned planes count.
@@ -100,15 +111,15 @@ __global__ void __launch_bounds__(kThreads) k_bkick(YeeGeom g, Fields<T> f, YeeC
     const T* ez = f.c[2];
     if (b_dof(g, 0, i, j, kk)) {
       const T ey0 = ey[s], ez0 = ez[s];
-      f.c[3][s] += k.cb[2] * (ey[g.sidx(i, j, kp)] - ey0) - k.cb[1] * (ez[g.sidx(i, jp, kk)] - ez0);
+      f.c[3][s] = yee_upd(f.c[3][s], k.cb[2], ey[g.sidx(i, j, kp)] - ey0, k.cb[1], ez[g.sidx(i, jp, kk)] - ez0);
     }
     if (b_dof(g, 1, i, j, kk)) {
       const T ez0 = ez[s], ex0 = ex[s];
-      f.c[4][s] += k.cb[0] * (ez[g.sidx(ip, j, kk)] - ez0) - k.cb[2] * (ex[g.sidx(i, j, kp)] - ex0);
+      f.c[4][s] = yee_upd(f.c[4][s], k.cb[0], ez[g.sidx(ip, j, kk)] - ez0, k.cb[2], ex[g.sidx(i, j, kp)] - ex0);
     }
     if (b_dof(g, 2, i, j, kk)) {
       const T ex0 = ex[s], ey0 = ey[s];
-      f.c[5][s] += k.cb[1] * (ex[g.sidx(i, jp, kk)] - ex0) - k.cb[0] * (ey[g.sidx(ip, j, kk)] - ey0);
+      f.c[5][s] = yee_upd(f.c[5][s], k.cb[1], ex[g.sidx(i, jp, kk)] - ex0, k.cb[0], ey[g.sidx(ip, j, kk)] - ey0);
     }
   }
 }
@@ -133,15 +144,15 @@ __global__ void __launch_bounds__(kThreads) k_ekick(YeeGeom g, Fields<T> f, YeeC
     const T* bz = f.c[5];
     if (e_dof(g, 0, i, j, kk)) {
       const T bz0 = bz[s], by0 = by[s];
-      f.c[0][s] += k.ce[1] * (bz0 - bz[g.sidx(i, jm, kk)]) - k.ce[2] * (by0 - by[g.sidx(i, j, km)]);
+      f.c[0][s] = yee_upd(f.c[0][s], k.ce[1], bz0 - bz[g.sidx(i, jm, kk)], k.ce[2], by0 - by[g.sidx(i, j, km)]);
     }
     if (e_dof(g, 1, i, j, kk)) {
       const T bx0 = bx[s], bz0 = bz[s];
-      f.c[1][s] += k.ce[2] * (bx0 - bx[g.sidx(i, j, km)]) - k.ce[0] * (bz0 - bz[g.sidx(im, j, kk)]);
+      f.c[1][s] = yee_upd(f.c[1][s], k.ce[2], bx0 - bx[g.sidx(i, j, km)], k.ce[0], bz0 - bz[g.sidx(im, j, kk)]);
     }
     if (e_dof(g, 2, i, j, kk)) {
       const T by0 = by[s], bx0 = bx[s];
-      f.c[2][s] += k.ce[0] * (by0 - by[g.sidx(im, j, kk)]) - k.ce[1] * (bx0 - bx[g.sidx(i, jm, kk)]);
+      f.c[2][s] = yee_upd(f.c[2][s], k.ce[0], by0 - by[g.sidx(im, j, kk)], k.ce[1], bx0 - bx[g.sidx(i, jm, kk)]);
     }
   }
 }
@@ -190,14 +201,11 @@ __global__ void __launch_bounds__(TX* TY)
       for (int c = 0; c < 3; ++c) e[c] = in_range ? in.c[c][s] : T(0);
       if (in_range) {
         if (e_dof(g, 0, i, j, kk))
-          e[0] += ck.ce[1] * (sB[cur][2][bj][bi] - sB[cur][2][bj - 1][bi]) -
-                  ck.ce[2] * (sB[cur][1][bj][bi] - sB[prev][1][bj][bi]);
+          e[0] = yee_upd(e[0], ck.ce[1], sB[cur][2][bj][bi] - sB[cur][2][bj - 1][bi], ck.ce[2], sB[cur][1][bj][bi] - sB[prev][1][bj][bi]);
         if (e_dof(g, 1, i, j, kk))
-          e[1] += ck.ce[2] * (sB[cur][0][bj][bi] - sB[prev][0][bj][bi]) -
-                  ck.ce[0] * (sB[cur][2][bj][bi] - sB[cur][2][bj][bi - 1]);
+          e[1] = yee_upd(e[1], ck.ce[2], sB[cur][0][bj][bi] - sB[prev][0][bj][bi], ck.ce[0], sB[cur][2][bj][bi] - sB[cur][2][bj][bi - 1]);
         if (e_dof(g, 2, i, j, kk))
-          e[2] += ck.ce[0] * (sB[cur][1][bj][bi] - sB[cur][1][bj][bi - 1]) -
-                  ck.ce[1] * (sB[cur][0][bj][bi] - sB[cur][0][bj - 1][bi]);
+          e[2] = yee_upd(e[2], ck.ce[0], sB[cur][1][bj][bi] - sB[cur][1][bj][bi - 1], ck.ce[1], sB[cur][0][bj][bi] - sB[cur][0][bj - 1][bi]);
         if (li < TX && lj < TY && kk < k1) {
 #pragma unroll
           for (int c = 0; c < 3; ++c)
@@ -216,17 +224,11 @@ __global__ void __launch_bounds__(TX* TY)
         const int64_t s = g.sidx(i, j, kb);
         const int bi = li + 1, bj = lj + 1;
         if (b_dof(g, 0, i, j, kb))
-          out.c[3][s] = sB[prev][0][bj][bi] +
-                        (ck.cb[2] * (sE[cur][1][lj][li] - sE[prev][1][lj][li]) -
-                         ck.cb[1] * (sE[prev][2][lj + 1][li] - sE[prev][2][lj][li]));
+          out.c[3][s] = yee_upd(sB[prev][0][bj][bi], ck.cb[2], sE[cur][1][lj][li] - sE[prev][1][lj][li], ck.cb[1], sE[prev][2][lj + 1][li] - sE[prev][2][lj][li]);
         if (b_dof(g, 1, i, j, kb))
-          out.c[4][s] = sB[prev][1][bj][bi] +
-                        (ck.cb[0] * (sE[prev][2][lj][li + 1] - sE[prev][2][lj][li]) -
-                         ck.cb[2] * (sE[cur][0][lj][li] - sE[prev][0][lj][li]));
+          out.c[4][s] = yee_upd(sB[prev][1][bj][bi], ck.cb[0], sE[prev][2][lj][li + 1] - sE[prev][2][lj][li], ck.cb[2], sE[cur][0][lj][li] - sE[prev][0][lj][li]);
         if (b_dof(g, 2, i, j, kb))
-          out.c[5][s] = sB[prev][2][bj][bi] +
-                        (ck.cb[1] * (sE[prev][0][lj + 1][li] - sE[prev][0][lj][li]) -
-                         ck.cb[0] * (sE[prev][1][lj][li + 1] - sE[prev][1][lj][li]));
+          out.c[5][s] = yee_upd(sB[prev][2][bj][bi], ck.cb[1], sE[prev][0][lj + 1][li] - sE[prev][0][lj][li], ck.cb[0], sE[prev][1][lj][li + 1] - sE[prev][1][lj][li]);
       }
     }
     __syncthreads();
@@ -398,11 +400,11 @@ __global__ void __launch_bounds__(NTH)
         T e0 = EC(0, lj, li), e1 = EC(1, lj, li), e2 = EC(2, lj, li);
         const bool d0 = (m[q] & 1) && kin, d1 = (m[q] & 2) && kin, d2 = (m[q] & 4) && kz;
         if (d0)
-          e0 += ck.ce[1] * (BC(2, bj, bi) - BC(2, bj - 1, bi)) - ck.ce[2] * (BC(1, bj, bi) - BP(1, bj, bi));
+          e0 = yee_upd(e0, ck.ce[1], BC(2, bj, bi) - BC(2, bj - 1, bi), ck.ce[2], BC(1, bj, bi) - BP(1, bj, bi));
         if (d1)
-          e1 += ck.ce[2] * (BC(0, bj, bi) - BP(0, bj, bi)) - ck.ce[0] * (BC(2, bj, bi) - BC(2, bj, bi - 1));
+          e1 = yee_upd(e1, ck.ce[2], BC(0, bj, bi) - BP(0, bj, bi), ck.ce[0], BC(2, bj, bi) - BC(2, bj, bi - 1));
         if (d2)
-          e2 += ck.ce[0] * (BC(1, bj, bi) - BC(1, bj, bi - 1)) - ck.ce[1] * (BC(0, bj, bi) - BC(0, bj - 1, bi));
+          e2 = yee_upd(e2, ck.ce[0], BC(1, bj, bi) - BC(1, bj, bi - 1), ck.ce[1], BC(0, bj, bi) - BC(0, bj - 1, bi));
         if ((m[q] & 8) && kw) {
           const int64_t s = sij[q] + kstride * kk;
           if (d0) out.c[0][s] = e0;
@@ -419,12 +421,9 @@ __global__ void __launch_bounds__(NTH)
         const int li = bli, lj = blj;
         const int64_t s = bsij + kstride * (kk - 1);
         const int bi = li + OFF, bj = lj + 1;
-        out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
-                                       ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
-        out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
-                                       ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
-        out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
-                                       ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
+        out.c[3][s] = yee_upd(BP(0, bj, bi), ck.cb[2], EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li), ck.cb[1], EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li));
+        out.c[4][s] = yee_upd(BP(1, bj, bi), ck.cb[0], EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li), ck.cb[2], EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li));
+        out.c[5][s] = yee_upd(BP(2, bj, bi), ck.cb[1], EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li), ck.cb[0], EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li));
       }
 #undef BC
 #undef BP
@@ -448,8 +447,10 @@ __global__ void __launch_bounds__(NTH)
 // tile; the B0 / E0 boxes start at i0 - OFF (TMA's 16-byte alignment; OFF =
 // 16/sizeof(T) >= 2). Every point update is the same expression as in
 // k_fused_tma (yee_e_upd / yee_b_upd), so the result equals two single
-// sweeps. Three barriers per plane; NS = D + 2 TMA stages; the E1, B1, E2
-// planes are double-buffered, so with NS = 3 two CTAs fit per SM (fp64).
+// sweeps. Two barriers per plane; NS = D + 1 TMA stages; the E1 and E2
+// planes are double-buffered, B1 single, so with NS = 3 two CTAs fit per SM
+// (fp64). One thread per E1-region point keeps that point's E1, B1, E2 and
+// old B of the current and previous plane in registers.
 template <class T, int TX, int TY, int NS>
 struct TmaCfg2 {
   static constexpr int kOff = 16 / (int)sizeof(T);
@@ -467,7 +468,10 @@ struct TmaCfg2 {
   static constexpr int kBufBytes = 5 * 3 * kX1 * kY1 * (int)sizeof(T);
   static constexpr int kBarOff = (NS * kStage + kBufBytes + 15) / 16 * 16;
   static constexpr int kSmem = kBarOff + NS * 8 + 128;
-  static constexpr int kD = NS - 2;  // prefetch distance in planes
+  // prefetch distance in planes: a stage is read only in phase 1 of its own
+  // plane (the own old B is carried to the next plane in registers), so the
+  // stage of plane p-1 is free once plane p starts
+  static constexpr int kD = NS - 1;
 };
 
 // E DOF mask bits of (i, j) (yee_layout.hpp): 1 Ex, 2 Ey, 4 Ez (z parts apart)
@@ -477,19 +481,22 @@ __device__ __forceinline__ uint32_t e_mask_xy(int i, int j, int n0, int n1) {
   return (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u);
 }
 
-template <class T, int TX, int TY, int NS, int NTH>
-__global__ void __launch_bounds__(NTH)
+template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB>
+__global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                  int n_units, int kbeg, int kend) {
   using Cfg = TmaCfg2<T, TX, TY, NS>;
   constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
-  // one thread per point of the E1 region (origin (i0-1, j0-1)); the B1, E2
-  // and B2 regions are subsets in the same coordinates, so every thread keeps
-  // its own point's E1, B1, E2 of the current and previous plane in
-  // registers and only the x/y neighbours go through shared memory
+  // NPT points of the E1 region (origin (i0-1, j0-1)) per thread: points
+  // tid + h*NH, h < NPT. The B1, E2 and B2 regions are subsets in the same
+  // coordinates, so a thread keeps its points' E1, B1, E2 and old B of the
+  // current and previous plane in registers; only the x/y neighbours go
+  // through shared memory. Several points per thread amortise the per-plane
+  // control (barrier waits, stage and buffer addressing) and add ILP.
   constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, NP = X1 * Y1;
-  static_assert(NP <= NTH, "one region point per thread");
+  constexpr int NH = (NP + NPT - 1) / NPT;
+  static_assert(NH <= NTH, "NPT region points per thread");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);  // 2 planes x 3 comps x NP
@@ -507,25 +514,48 @@ __global__ void __launch_bounds__(NTH)
   uint32_t gplane = 0;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int64_t kstride = (int64_t)g.P0 * g.S[1];
-  const bool pt = tid < NP;
-  const int x = tid % X1, y = tid / X1;
-  const int me = tid;                           // own index in the region arrays
-  const int bi = x + OFF - 1, bj = y + 1, ej = y;  // own point in the B0 / E0 boxes
-  const bool inB1 = pt && x <= TX + 1 && y <= TY + 1;
-  const bool inE2 = pt && x >= 1 && x <= TX + 1 && y >= 1 && y <= TY + 1;
+  // own points: region index me[h], box offsets (B0: row bj, col bi; E0: row
+  // ej, col bi), region membership
+  int me[NPT], xo[NPT], yo[NPT], ob[NPT], oe[NPT];
+  bool pt[NPT], inB1[NPT], inE2[NPT];
+#pragma unroll
+  for (int h = 0; h < NPT; ++h) {
+    me[h] = tid + h * NH;
+    pt[h] = tid < NH && me[h] < NP;
+    xo[h] = me[h] % X1;
+    yo[h] = me[h] / X1;
+    ob[h] = (yo[h] + 1) * BW + xo[h] + OFF - 1;
+    oe[h] = yo[h] * BW + xo[h] + OFF - 1;
+    inB1[h] = pt[h] && xo[h] <= TX + 1 && yo[h] <= TY + 1;
+    inE2[h] = pt[h] && xo[h] >= 1 && xo[h] <= TX + 1 && yo[h] >= 1 && yo[h] <= TY + 1;
+  }
+  const bool any = pt[0];  // point 0 exists whenever any does
+
+  // per-point state of one plane: E1, B1, E2 and the old B (B0). Two sets
+  // ping-pong (cur/prev) through a 2x unrolled plane loop, so no register
+  // moves rotate them.
+  struct Pt {
+    T e1[3], b1[3], e2[3], b0[3];
+  };
+  const T ce0 = ck.ce[0], ce1 = ck.ce[1], ce2 = ck.ce[2];
+  const T cb0 = ck.cb[0], cb1 = ck.cb[1], cb2 = ck.cb[2];
 
   for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
     const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
     const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
     const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
     const int P = k1 - k0 + 4;  // local planes p <-> z = k0 - 2 + p
-    const int i = i0 - 1 + x, j = j0 - 1 + y;
-    const uint32_t m = pt ? e_mask_xy(i, j, n0, n1) : 0u;
-    const bool b1up = inB1 && i >= 0 && i < n0 && j >= 0 && j < n1;
-    const bool own = inE2 && x <= TX && y <= TY && i < n0 && j < n1;
-    const int64_t sij = (int64_t)i + (int64_t)g.P0 * j;
-    T e1c[3] = {0, 0, 0}, e1p[3] = {0, 0, 0}, b1c[3] = {0, 0, 0}, b1p[3] = {0, 0, 0};
-    T e2c[3] = {0, 0, 0}, e2p[3] = {0, 0, 0};
+    uint32_t m[NPT];
+    bool b1up[NPT], own[NPT];
+    int64_t sij[NPT];
+#pragma unroll
+    for (int h = 0; h < NPT; ++h) {
+      const int i = i0 - 1 + xo[h], j = j0 - 1 + yo[h];
+      m[h] = pt[h] ? e_mask_xy(i, j, n0, n1) : 0u;
+      b1up[h] = inB1[h] && i >= 0 && i < n0 && j >= 0 && j < n1;
+      own[h] = inE2[h] && xo[h] <= TX && yo[h] <= TY && i < n0 && j < n1;
+      sij[h] = (int64_t)i + (int64_t)g.P0 * j;
+    }
 
     auto issue = [&](int p) {
       const uint32_t gp = gplane + p;
@@ -538,103 +568,129 @@ __global__ void __launch_bounds__(NTH)
     };
     if (tid == 0)
       for (int p = 0; p < D && p < P; ++p) issue(p);
-    for (int p = 0; p < P; ++p) {
+
+    // plane p of the unit (PAR = p & 1 selects the E1/E2 double buffers at
+    // compile time): C receives this plane's values, V holds the previous
+    // plane's
+    auto plane = [&](auto par, int p, Pt* C, const Pt* V) {
+      constexpr int PAR = decltype(par)::value;
       if (tid == 0 && p + D < P) issue(p + D);
       const uint32_t gc = gplane + p;
-      mbar_wait(&bars[gc % NS], (gc / NS) & 1);
+      const int st = gc % NS;
+      mbar_wait(&bars[st], (gc / NS) & 1);
       const int z = k0 - 2 + p;
-      const T* __restrict__ B0c = reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage);
-      const T* __restrict__ B0p = reinterpret_cast<const T*>(base + ((gc + NS - 1) % NS) * Cfg::kStage);
-      const T* __restrict__ E0c =
-          reinterpret_cast<const T*>(base + (gc % NS) * Cfg::kStage + Cfg::kBStride);
-      T* E1z = sE1 + (gc & 1) * 3 * NP;                 // E1(z)
-      const T* E1y = sE1 + ((gc + 1) & 1) * 3 * NP;     // E1(z-1)
-      T* E2y = sE2 + ((gc + 1) & 1) * 3 * NP;           // E2(z-1)
-      const T* E2x = sE2 + (gc & 1) * 3 * NP;           // E2(z-2)
-#define B0C(c, yy, xx) B0c[((c) * (TY + 4) + (yy)) * BW + (xx)]
-#define B0P(c, yy, xx) B0p[((c) * (TY + 4) + (yy)) * BW + (xx)]
-#define E0C(c, yy, xx) E0c[((c) * (TY + 3) + (yy)) * BW + (xx)]
+      const T* __restrict__ B0c = reinterpret_cast<const T*>(base + st * Cfg::kStage);
+      const T* __restrict__ E0c = reinterpret_cast<const T*>(base + st * Cfg::kStage + Cfg::kBStride);
+      T* E1z = sE1 + PAR * 3 * NP;            // E1(z)
+      const T* E1y = sE1 + (1 - PAR) * 3 * NP;  // E1(z-1)
+      T* E2y = sE2 + (1 - PAR) * 3 * NP;        // E2(z-1)
+      const T* E2x = sE2 + PAR * 3 * NP;        // E2(z-2)
+      constexpr int BC = (TY + 4) * BW, EC = (TY + 3) * BW;  // component strides in the boxes
 #define R(buf, c, idx) buf[(c) * NP + (idx)]
-      // ---- phase 1: E1(z) at the own point
-      if (p >= 1 && pt) {
+      // ---- phase 1: E1(z); the own B0(z) is kept for the next plane (it is
+      // B0(z-1) there)
+      if (any) {
         const int zg = z + g.kofs;
         const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
-        T e0 = E0C(0, ej, bi), e1 = E0C(1, ej, bi), e2 = E0C(2, ej, bi);
-        if ((m & 1) && kin)
-          e0 += ck.ce[1] * (B0C(2, bj, bi) - B0C(2, bj - 1, bi)) - ck.ce[2] * (B0C(1, bj, bi) - B0P(1, bj, bi));
-        if ((m & 2) && kin)
-          e1 += ck.ce[2] * (B0C(0, bj, bi) - B0P(0, bj, bi)) - ck.ce[0] * (B0C(2, bj, bi) - B0C(2, bj, bi - 1));
-        if ((m & 4) && kz)
-          e2 += ck.ce[0] * (B0C(1, bj, bi) - B0C(1, bj, bi - 1)) - ck.ce[1] * (B0C(0, bj, bi) - B0C(0, bj - 1, bi));
-        e1c[0] = e0;
-        e1c[1] = e1;
-        e1c[2] = e2;
-        R(E1z, 0, me) = e0;
-        R(E1z, 1, me) = e1;
-        R(E1z, 2, me) = e2;
-      }
-      __syncthreads();  // the B1 plane is free (last read by the previous phase 3)
-      // ---- phase 2: B1(z-1) at the own point (E1(z-1) neighbours from smem)
-      if (p >= 2 && inB1) {
-        const int zg = z - 1 + g.kofs;
-        T v0 = B0P(0, bj, bi), v1 = B0P(1, bj, bi), v2 = B0P(2, bj, bi);
-        if (b1up && zg >= 0 && zg < n2) {
-          v0 = v0 + (ck.cb[2] * (e1c[1] - e1p[1]) - ck.cb[1] * (R(E1y, 2, me + X1) - e1p[2]));
-          v1 = v1 + (ck.cb[0] * (R(E1y, 2, me + 1) - e1p[2]) - ck.cb[2] * (e1c[0] - e1p[0]));
-          v2 = v2 + (ck.cb[1] * (R(E1y, 0, me + X1) - e1p[0]) - ck.cb[0] * (R(E1y, 1, me + 1) - e1p[1]));
+#pragma unroll
+        for (int h = 0; h < NPT; ++h) {
+          if (!pt[h]) continue;
+          const T* b = B0c + ob[h];
+          C[h].b0[0] = b[0];
+          C[h].b0[1] = b[BC];
+          C[h].b0[2] = b[2 * BC];
+          if (p >= 1) {
+            const T* e = E0c + oe[h];
+            const T e0 = e[0], e1 = e[EC], e2 = e[2 * EC];
+            const T u0 = yee_upd(e0, ce1, C[h].b0[2] - b[2 * BC - BW], ce2, C[h].b0[1] - V[h].b0[1]);
+            const T u1 = yee_upd(e1, ce2, C[h].b0[0] - V[h].b0[0], ce0, C[h].b0[2] - b[2 * BC - 1]);
+            const T u2 = yee_upd(e2, ce0, C[h].b0[1] - b[BC - 1], ce1, C[h].b0[0] - b[-BW]);
+            C[h].e1[0] = (m[h] & 1) && kin ? u0 : e0;
+            C[h].e1[1] = (m[h] & 2) && kin ? u1 : e1;
+            C[h].e1[2] = (m[h] & 4) && kz ? u2 : e2;
+            R(E1z, 0, me[h]) = C[h].e1[0];
+            R(E1z, 1, me[h]) = C[h].e1[1];
+            R(E1z, 2, me[h]) = C[h].e1[2];
+          }
         }
-        b1c[0] = v0;
-        b1c[1] = v1;
-        b1c[2] = v2;
-        R(sB1, 0, me) = v0;
-        R(sB1, 1, me) = v1;
-        R(sB1, 2, me) = v2;
+      }
+      __syncthreads();  // E1(z) complete; the B1 plane is free
+      // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem). Points outside
+      // the B1 region compute too (their values are never read)
+      if (p >= 2 && any) {
+        const int zg = z - 1 + g.kofs;
+        const bool zin = zg >= 0 && zg < n2;
+#pragma unroll
+        for (int h = 0; h < NPT; ++h) {
+          if (!pt[h]) continue;
+          const int q = me[h];
+          const bool up = b1up[h] && zin;
+          const Pt& v = V[h];
+          const T u0 = yee_upd(v.b0[0], cb2, C[h].e1[1] - v.e1[1], cb1, R(E1y, 2, q + X1) - v.e1[2]);
+          const T u1 = yee_upd(v.b0[1], cb0, R(E1y, 2, q + 1) - v.e1[2], cb2, C[h].e1[0] - v.e1[0]);
+          const T u2 = yee_upd(v.b0[2], cb1, R(E1y, 0, q + X1) - v.e1[0], cb0, R(E1y, 1, q + 1) - v.e1[1]);
+          C[h].b1[0] = up ? u0 : v.b0[0];
+          C[h].b1[1] = up ? u1 : v.b0[1];
+          C[h].b1[2] = up ? u2 : v.b0[2];
+          R(sB1, 0, q) = C[h].b1[0];
+          R(sB1, 1, q) = C[h].b1[1];
+          R(sB1, 2, q) = C[h].b1[2];
+        }
       }
       __syncthreads();  // B1(z-1) complete
-      // ---- phase 3: E2(z-1) at the own point (B1(z-1) neighbours from smem)
-      if (p >= 3 && inE2) {
+      // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem); points outside
+      // the E2 region compute too (never read)
+      if (p >= 3 && any) {
         const int ze = z - 1;
         const int zg = ze + g.kofs;
         const bool kin = zg >= 1 && zg <= n2 - 1, kz = zg >= 0 && zg < n2;
-        T e0 = e1p[0], e1 = e1p[1], e2 = e1p[2];
-        const bool d0 = (m & 1) && kin, d1 = (m & 2) && kin, d2 = (m & 4) && kz;
-        if (d0) e0 += ck.ce[1] * (b1c[2] - R(sB1, 2, me - X1)) - ck.ce[2] * (b1c[1] - b1p[1]);
-        if (d1) e1 += ck.ce[2] * (b1c[0] - b1p[0]) - ck.ce[0] * (b1c[2] - R(sB1, 2, me - 1));
-        if (d2) e2 += ck.ce[0] * (b1c[1] - R(sB1, 1, me - 1)) - ck.ce[1] * (b1c[0] - R(sB1, 0, me - X1));
-        if (own && ze >= k0 && ze < k1) {
-          const int64_t s = sij + kstride * ze;
-          if (d0) out.c[0][s] = e0;
-          if (d1) out.c[1][s] = e1;
-          if (d2) out.c[2][s] = e2;
+        const bool zw = ze >= k0 && ze < k1;
+#pragma unroll
+        for (int h = 0; h < NPT; ++h) {
+          if (!pt[h]) continue;
+          const int q = me[h];
+          const Pt& v = V[h];
+          const bool d0 = (m[h] & 1) && kin, d1 = (m[h] & 2) && kin, d2 = (m[h] & 4) && kz;
+          const T u0 = yee_upd(v.e1[0], ce1, C[h].b1[2] - R(sB1, 2, q - X1), ce2, C[h].b1[1] - v.b1[1]);
+          const T u1 = yee_upd(v.e1[1], ce2, C[h].b1[0] - v.b1[0], ce0, C[h].b1[2] - R(sB1, 2, q - 1));
+          const T u2 = yee_upd(v.e1[2], ce0, C[h].b1[1] - R(sB1, 1, q - 1), ce1, C[h].b1[0] - R(sB1, 0, q - X1));
+          C[h].e2[0] = d0 ? u0 : v.e1[0];
+          C[h].e2[1] = d1 ? u1 : v.e1[1];
+          C[h].e2[2] = d2 ? u2 : v.e1[2];
+          if (own[h] && zw) {
+            const int64_t s = sij[h] + kstride * ze;
+            if (d0) out.c[0][s] = C[h].e2[0];
+            if (d1) out.c[1][s] = C[h].e2[1];
+            if (d2) out.c[2][s] = C[h].e2[2];
+          }
+          R(E2y, 0, q) = C[h].e2[0];
+          R(E2y, 1, q) = C[h].e2[1];
+          R(E2y, 2, q) = C[h].e2[2];
         }
-        e2c[0] = e0;
-        e2c[1] = e1;
-        e2c[2] = e2;
-        R(E2y, 0, me) = e0;
-        R(E2y, 1, me) = e1;
-        R(E2y, 2, me) = e2;
       }
-      // ---- phase 4: B2(z-2) on the own tile point (E2(z-2) neighbours, written
-      // in the previous iteration, from smem)
-      if (p >= 4 && own) {
+      // ---- phase 4: B2(z-2) on the own tile points (E2(z-2) neighbours,
+      // written in the previous plane, from smem)
+      if (p >= 4) {
         const int zb = z - 2;
         if (zb >= k0 && zb < k1) {
-          const int64_t s = sij + kstride * zb;
-          out.c[3][s] = b1p[0] + (ck.cb[2] * (e2c[1] - e2p[1]) - ck.cb[1] * (R(E2x, 2, me + X1) - e2p[2]));
-          out.c[4][s] = b1p[1] + (ck.cb[0] * (R(E2x, 2, me + 1) - e2p[2]) - ck.cb[2] * (e2c[0] - e2p[0]));
-          out.c[5][s] = b1p[2] + (ck.cb[1] * (R(E2x, 0, me + X1) - e2p[0]) - ck.cb[0] * (R(E2x, 1, me + 1) - e2p[1]));
+#pragma unroll
+          for (int h = 0; h < NPT; ++h) {
+            if (!own[h]) continue;
+            const int q = me[h];
+            const Pt& v = V[h];
+            const int64_t s = sij[h] + kstride * zb;
+            out.c[3][s] = yee_upd(v.b1[0], cb2, C[h].e2[1] - v.e2[1], cb1, R(E2x, 2, q + X1) - v.e2[2]);
+            out.c[4][s] = yee_upd(v.b1[1], cb0, R(E2x, 2, q + 1) - v.e2[2], cb2, C[h].e2[0] - v.e2[0]);
+            out.c[5][s] = yee_upd(v.b1[2], cb1, R(E2x, 0, q + X1) - v.e2[0], cb0, R(E2x, 1, q + 1) - v.e2[1]);
+          }
         }
       }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        e1p[c] = e1c[c];
-        b1p[c] = b1c[c];
-        e2p[c] = e2c[c];
-      }
-#undef B0C
-#undef B0P
-#undef E0C
 #undef R
+    };
+    Pt A[NPT], B[NPT];
+    for (int p = 0; p < P; p += 2) {
+      plane(std::integral_constant<int, 0>{}, p, A, B);
+      if (p + 1 < P) plane(std::integral_constant<int, 1>{}, p + 1, B, A);
     }
     gplane += P;
     __syncthreads();
@@ -761,11 +817,11 @@ __global__ void __launch_bounds__(TX* TY)
         T e0 = ec[q][0], e1 = ec[q][1], e2 = ec[q][2];
         const bool d0 = (m[q] & 1) && kin, d1 = (m[q] & 2) && kin, d2 = (m[q] & 4) && kz;
         if (d0)
-          e0 += ck.ce[1] * (BC(2, bj, bi) - BC(2, bj - 1, bi)) - ck.ce[2] * (BC(1, bj, bi) - BP(1, bj, bi));
+          e0 = yee_upd(e0, ck.ce[1], BC(2, bj, bi) - BC(2, bj - 1, bi), ck.ce[2], BC(1, bj, bi) - BP(1, bj, bi));
         if (d1)
-          e1 += ck.ce[2] * (BC(0, bj, bi) - BP(0, bj, bi)) - ck.ce[0] * (BC(2, bj, bi) - BC(2, bj, bi - 1));
+          e1 = yee_upd(e1, ck.ce[2], BC(0, bj, bi) - BP(0, bj, bi), ck.ce[0], BC(2, bj, bi) - BC(2, bj, bi - 1));
         if (d2)
-          e2 += ck.ce[0] * (BC(1, bj, bi) - BC(1, bj, bi - 1)) - ck.ce[1] * (BC(0, bj, bi) - BC(0, bj - 1, bi));
+          e2 = yee_upd(e2, ck.ce[0], BC(1, bj, bi) - BC(1, bj, bi - 1), ck.ce[1], BC(0, bj, bi) - BC(0, bj - 1, bi));
         if ((m[q] & 8) && kw) {
           const int64_t s = sij[q] + kstride * kk;
           if (d0) out.c[0][s] = e0;
@@ -781,12 +837,9 @@ __global__ void __launch_bounds__(TX* TY)
         const int li = bli, lj = blj;
         const int64_t s = bsij + kstride * (kk - 1);
         const int bi = li + OFF, bj = lj + 1;
-        out.c[3][s] = BP(0, bj, bi) + (ck.cb[2] * (EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li)) -
-                                       ck.cb[1] * (EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li)));
-        out.c[4][s] = BP(1, bj, bi) + (ck.cb[0] * (EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li)) -
-                                       ck.cb[2] * (EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li)));
-        out.c[5][s] = BP(2, bj, bi) + (ck.cb[1] * (EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li)) -
-                                       ck.cb[0] * (EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li)));
+        out.c[3][s] = yee_upd(BP(0, bj, bi), ck.cb[2], EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li), ck.cb[1], EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li));
+        out.c[4][s] = yee_upd(BP(1, bj, bi), ck.cb[0], EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li), ck.cb[2], EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li));
+        out.c[5][s] = yee_upd(BP(2, bj, bi), ck.cb[1], EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li), ck.cb[0], EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li));
       }
 #undef BC
 #undef BP
@@ -935,8 +988,27 @@ struct YeeDev {
 
   // kNT1: threads of the one-step sweep -- (TX+1)(TY+1) = 297 E points, so 320
   // threads cover the E region in one pass instead of 256 + 41
-  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNS2 = 3, kNT2 = 416,
-                       kNT1 = 320;
+  static constexpr int kTX = 32, kTY = 8, kNS = 5, kChunk = 32, kNT1 = 320;
+  // two-step sweep, per precision: tile kTX x kTY2, kNT2 threads (one per
+  // E1-region point, (kTX+3)(kTY2+3) of them), kNS2 TMA stages, kMB2 CTAs
+  // per SM (the register budget). Measured on 256^3 (tools/yee2_ab.sh).
+#ifndef YEE2_TY64
+#define YEE2_TY64 16
+#define YEE2_NT64 672
+#define YEE2_MB64 1
+#endif
+#ifndef YEE2_TY32
+#define YEE2_TY32 16
+#define YEE2_NT32 672
+#define YEE2_MB32 1
+#endif
+  static constexpr int kNS2 = 3, kNPT2 = 1;
+  template <class T>
+  static constexpr int kTY2 = sizeof(T) == 8 ? YEE2_TY64 : YEE2_TY32;
+  template <class T>
+  static constexpr int kNT2 = sizeof(T) == 8 ? YEE2_NT64 : YEE2_NT32;
+  template <class T>
+  static constexpr int kMB2 = sizeof(T) == 8 ? YEE2_MB64 : YEE2_MB32;
 
   template <class T>
   void make_maps() {
@@ -994,9 +1066,9 @@ struct YeeDev {
     cuuint64_t strides[3] = {(cuuint64_t)g.P0 * w, (cuuint64_t)g.P0 * g.S[1] * w,
                              (cuuint64_t)g.npts() * w};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    using Cfg = TmaCfg2<T, kTX, kTY, kNS2>;
-    cuuint32_t boxB[4] = {(cuuint32_t)Cfg::kBW, kTY + 4, 1, 3};
-    cuuint32_t boxE[4] = {(cuuint32_t)Cfg::kBW, kTY + 3, 1, 3};
+    using Cfg = TmaCfg2<T, kTX, kTY2<T>, kNS2>;
+    cuuint32_t boxB[4] = {(cuuint32_t)Cfg::kBW, kTY2<T> + 4, 1, 3};
+    cuuint32_t boxE[4] = {(cuuint32_t)Cfg::kBW, kTY2<T> + 3, 1, 3};
     const CUtensorMapDataType dt_ = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     for (int b = 0; b < 2; ++b) {
@@ -1009,10 +1081,10 @@ struct YeeDev {
         if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
       }
     }
-    auto kern = k_fused2_tma<T, kTX, kTY, kNS2, kNT2>;
+    auto kern = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>>;
     SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
     int per_sm = 0, sms = 0;
-    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2, Cfg::kSmem));
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2<T>, Cfg::kSmem));
     SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     tma_blocks2 = std::max(1, per_sm) * sms;
     have_maps2 = true;
@@ -1022,11 +1094,11 @@ struct YeeDev {
   template <class T>
   void launch_range2(double h_e, double h_b, int kbeg, int kend) {
     if (!have_maps2) make_maps2<T>();
-    const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
+    const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY2<T> - 1) / kTY2<T>;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
     const int grid = std::min(n_units, tma_blocks2);
-    k_fused2_tma<T, kTX, kTY, kNS2, kNT2><<<grid, kNT2, TmaCfg2<T, kTX, kTY, kNS2>::kSmem, stream>>>(
+    k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>><<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2>::kSmem, stream>>>(
         mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
         ntx, ntx * nty, n_units, kbeg, kend);
     SFEEC_LAUNCH_CHECK();
