@@ -334,6 +334,13 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
 int sfeec_tet_dev_operators(int n, double jitter, uint64_t seed, int device, sfeec_csr_owned* c,
                             sfeec_csr_owned* m2, sfeec_csr_owned* d, sfeec_csr_owned* q_sym,
                             sfeec_csr_owned* ct);
+/* device layout of a resident operator (0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D):
+ * info[7] = {layout (0 CSR, 1 signed, 2 fp64 values, 3 stencil), column-delta
+ * form, ELL, slices (ELL: 32-row groups), slices kept at int32 columns,
+ * stored entries incl. padding, nnz}; *bytes = what one application streams
+ * from the operator arrays in this layout (the algorithmic count of SURVEY.md
+ * 8(d) stays 12 B / nonzero whatever the layout). No reference counterpart. */
+int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes);
 /* y = A x with a resident operator of the handle: 0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D */
 int sfeec_dev_apply(sfeec_dev* h, int which, const double* x, double* y);
 /* apply_curl_of_curl (operators.cpp:268-290): y = Q_sym C^T M2 C a with the

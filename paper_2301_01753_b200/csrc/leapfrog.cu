@@ -662,6 +662,26 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
   });
 }
 
+int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes) {
+  return guarded([&] {
+    require(h, "null handle");
+    require(which >= 0 && which <= 4, "layout_info: which must be 0..4");
+    auto& d = h->d;
+    const DevOperator* ops[5] = {&d.q, &d.c, &d.ct, &d.m2, &d.div};
+    const DevOperator& a = *ops[which];
+    if (info) {
+      info[0] = (int64_t)a.layout;
+      info[1] = a.delta ? 1 : 0;
+      info[2] = a.ell ? 1 : 0;
+      info[3] = a.ell ? (a.rows + 31) / 32 : a.n_slices;
+      info[4] = a.n_full;
+      info[5] = a.sell_entries;
+      info[6] = a.nnz;
+    }
+    if (bytes) *bytes = a.stream_bytes();
+  });
+}
+
 // 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2); a
 // non-incidence C (P2-, config 4) streams 12 B per entry
 double sfeec_dev_step_bytes(sfeec_dev* h) {

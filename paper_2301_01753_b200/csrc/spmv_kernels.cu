@@ -3,6 +3,7 @@
 // (coalesced) streaming of the operator arrays, L1/L2 hits on the gathered
 // neighbour values, and enough loads in flight per SM.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 
@@ -316,6 +317,347 @@ __global__ void __launch_bounds__(kThreads)
   y[r] = ACC ? fma(alpha, res, y0) : res;
 }
 
+// ---- column-delta layouts (DSlice in spmv_kernels.cuh) --------------------
+// Entry code (uint16): sel << 15 | delta (values, delta <= 32766) or
+// sel << 15 | delta << 1 | negative (incidence, delta <= 16382); the column is
+// base_sel[k] + lane + delta. Two bases per entry cover a slice / group that
+// straddles two entity types (k-th neighbours in two id ranges). 0xffff pads.
+constexpr unsigned kDPad = 0xffffu;
+
+__device__ __forceinline__ unsigned dcode_of(uint2 d, int j) {
+  const unsigned w = j < 2 ? d.x : d.y;
+  return (j & 1) ? (w >> 16) : (w & 0xffffu);
+}
+__device__ __forceinline__ int bse(int4 b, int j) {
+  return j == 0 ? b.x : j == 1 ? b.y : j == 2 ? b.z : b.w;
+}
+
+// one chunk of 4 entries -> gathered x (0 for pads) and, for SIGNED, the sign
+template <bool SIGNED>
+__device__ __forceinline__ void dgather(int4 b0, int4 b1, uint2 d, int lane,
+                                        const double* __restrict__ x, double (&xv)[4],
+                                        bool (&neg)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const unsigned u = dcode_of(d, j);
+    const int off = SIGNED ? (int)((u >> 1) & 0x3fffu) : (int)(u & 0x7fffu);
+    const int base = (u >> 15) ? bse(b1, j) : bse(b0, j);
+    neg[j] = SIGNED && (u & 1u);
+    xv[j] = u != kDPad ? __ldg(x + (base + lane + off)) : 0.0;
+  }
+}
+
+// sliced column-delta layout, persistent warps (one per slice per round),
+// software-pipelined as k_sell_pipe: the base / code / value loads of chunk
+// c+1 are issued before the gathers of chunk c. Rows summed in CSR order.
+template <bool ACC, bool SIGNED, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_dsell(int64_t n_slices, const DSlice* __restrict__ meta, const int32_t* __restrict__ dbase,
+            const uint16_t* __restrict__ dcol, const double* __restrict__ val, double scale,
+            const double* __restrict__ x, double* __restrict__ y, double alpha) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_slices) return;
+  auto ld = [&](int64_t i) {
+    const int4* p = reinterpret_cast<const int4*>(meta + i);
+    const int4 a = __ldg(p), b = __ldg(p + 1);
+    DSlice m;
+    m.r0 = ((int64_t)(unsigned)a.y << 32) | (unsigned)a.x;
+    m.vptr = ((int64_t)(unsigned)a.w << 32) | (unsigned)a.z;
+    m.dptr = ((int64_t)(unsigned)b.y << 32) | (unsigned)b.x;
+    m.bptr = b.z;
+    m.nw = b.w;
+    return m;
+  };
+  DSlice m = ld(s);
+  while (true) {
+    const int64_t sn = s + nwarps;
+    DSlice mn;
+    if (sn < n_slices) mn = ld(sn);
+    const int w = m.nw & 0xfffff, nr = (m.nw >> 20) & 63;
+    const bool full = (m.nw >> 26) & 1;
+    if (lane < nr) {
+      const int64_t row = m.r0 + lane;
+      const double y0 = ACC ? y[row] : 0.0;
+      const double* vp = SIGNED ? nullptr : val + m.vptr + lane;
+      double acc = 0.0;
+      if (!full) {
+        const int4* bp = reinterpret_cast<const int4*>(dbase + m.bptr);
+        const uint2* dp = reinterpret_cast<const uint2*>(dcol + m.dptr) + lane;
+        int4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
+        uint2 d = __ldcs(dp);
+        double v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (!SIGNED && j < w) ? __ldcs(vp + (int64_t)j * nr) : 0.0;
+        for (int k0 = 0, c = 0; k0 < w; k0 += 4, ++c) {
+          int4 b0n = b0, b1n = b1;
+          uint2 dn = d;
+          double vn[4];
+          if (k0 + 4 < w) {
+            b0n = __ldg(bp + 2 * c + 2);
+            b1n = __ldg(bp + 2 * c + 3);
+            dn = __ldcs(dp + (int64_t)(c + 1) * nr);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            vn[j] = (!SIGNED && k0 + 4 + j < w) ? __ldcs(vp + (int64_t)(k0 + 4 + j) * nr) : 0.0;
+          double xv[4];
+          bool neg[4];
+          dgather<SIGNED>(b0, b1, d, lane, x, xv, neg);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (SIGNED)
+              acc += neg[j] ? -xv[j] : xv[j];
+            else
+              acc = fma(v[j], xv[j], acc);
+          }
+          b0 = b0n;
+          b1 = b1n;
+          d = dn;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = vn[j];
+        }
+      } else {
+        // int32 columns (the codes did not fit; rare), as k_sell
+        const int32_t* cp = reinterpret_cast<const int32_t*>(dcol + m.dptr) + lane;
+        for (int k0 = 0; k0 < w; k0 += 4) {
+          int32_t p[4];
+          double v[4], xv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool ok = k0 + j < w;
+            p[j] = ok ? __ldcs(cp + (int64_t)(k0 + j) * nr) : kPad;
+            v[j] = (!SIGNED && ok) ? __ldcs(vp + (int64_t)(k0 + j) * nr) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            xv[j] = p[j] != kPad ? __ldg(x + (SIGNED && p[j] < 0 ? ~p[j] : p[j])) : 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (SIGNED)
+              acc += p[j] < 0 ? -xv[j] : xv[j];
+            else
+              acc = fma(v[j], xv[j], acc);
+          }
+        }
+      }
+      const double r = SIGNED ? scale * acc : acc;
+      y[row] = ACC ? fma(alpha, r, y0) : r;
+    }
+    if (sn >= n_slices) break;
+    s = sn;
+    m = mn;
+  }
+}
+
+// ELL column-delta layout (narrow operators, width W <= 8): one thread per
+// row, 32-row groups; every load of a row is independent of the others (the
+// group's bases are warp broadcasts, its full-column index another).
+template <bool ACC, bool SIGNED, int W>
+__global__ void __launch_bounds__(kThreads)
+    k_dell(int64_t rows, const int32_t* __restrict__ dbase, const uint16_t* __restrict__ dcol,
+           const int32_t* __restrict__ dfull, const int32_t* __restrict__ fcol,
+           const double* __restrict__ val, double scale, const double* __restrict__ x,
+           double* __restrict__ y, double alpha) {
+  constexpr int NC = (W + 3) / 4;  // code chunks per row
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t g = r >> 5;
+  const int lane = threadIdx.x & 31;
+  const double y0 = ACC ? y[r] : 0.0;
+  const int fi = __ldg(dfull + g);
+  int4 b0[NC], b1[NC];
+  uint2 d[NC];
+  double v[W];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int4* bp = reinterpret_cast<const int4*>(dbase + g * 8 * NC) + 2 * c;
+    b0[c] = __ldg(bp);
+    b1[c] = __ldg(bp + 1);
+    d[c] = __ldcs(reinterpret_cast<const uint2*>(dcol + g * 128 * NC) + c * 32 + lane);
+  }
+  if (!SIGNED) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = __ldcs(val + g * 32 * W + k * 32 + lane);
+  }
+  double xv[4 * NC];
+  bool neg[4 * NC];
+  if (fi < 0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double xc[4];
+      bool nc[4];
+      dgather<SIGNED>(b0[c], b1[c], d[c], lane, x, xc, nc);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        xv[4 * c + j] = xc[j];
+        neg[4 * c + j] = nc[j];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int32_t p = __ldcs(fcol + (int64_t)fi * 32 * W + k * 32 + lane);
+      neg[k] = SIGNED && p < 0 && p != kPad;
+      xv[k] = p != kPad ? __ldg(x + (SIGNED && p < 0 ? ~p : p)) : 0.0;
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    if (SIGNED)
+      acc += neg[k] ? -xv[k] : xv[k];
+    else
+      acc = fma(v[k], xv[k], acc);
+  }
+  const double res = SIGNED ? scale * acc : acc;
+  y[r] = ACC ? fma(alpha, res, y0) : res;
+}
+
+// ---- delta layout builders ----
+// the two bases of entry k for the rows r0 .. r0+nr-1 (lane = row - r0):
+// b0 = min(col - lane) over the rows that have an entry k, b1 = the min of
+// those beyond b0 + lim; *fit = 0 if some row is beyond b1 + lim too
+__device__ __forceinline__ int2 dbase_entry(const int64_t* __restrict__ rp,
+                                            const int32_t* __restrict__ ci, int64_t r0, int nr,
+                                            int k, int lane, int lim, bool* fit) {
+  int v = INT_MAX;
+  if (lane < nr) {
+    const int64_t b = rp[r0 + lane], e = rp[r0 + lane + 1];
+    if (b + k < e) v = ci[b + k] - lane;
+  }
+  const int m0 = __reduce_min_sync(0xffffffffu, v);
+  if (m0 == INT_MAX) return make_int2(0, 0);  // no row has entry k
+  const bool in0 = (int64_t)v - m0 <= lim;
+  const int m1 = __reduce_min_sync(0xffffffffu, in0 ? INT_MAX : v);
+  if (m1 == INT_MAX) return make_int2(m0, m0);
+  const bool in1 = !in0 && (int64_t)v - m1 <= lim;
+  if (__any_sync(0xffffffffu, v != INT_MAX && !in0 && !in1)) *fit = false;
+  return make_int2(m0, m1);
+}
+
+// code of entry k of lane `lane` (kDPad for a pad slot)
+__device__ __forceinline__ uint16_t dcode(const int64_t* __restrict__ rp,
+                                          const int32_t* __restrict__ ci,
+                                          const double* __restrict__ cv, bool sg, int64_t row,
+                                          int k, int lane, int32_t b0, int32_t b1) {
+  const int64_t b = rp[row], e = rp[row + 1];
+  if (b + k >= e) return (uint16_t)kDPad;
+  const int lim = sg ? 16382 : 32766;
+  const int v = ci[b + k] - lane;
+  const unsigned sel = (int64_t)v - b0 <= lim ? 0u : 1u;
+  const unsigned dl = (unsigned)(v - (sel ? b1 : b0));
+  return (uint16_t)((sel << 15) | (sg ? (dl << 1) | (cv[b + k] < 0 ? 1u : 0u) : dl));
+}
+
+// pass 1 of the sliced form: bases of every slice + fit flags (warp per
+// slice); slice s, chunk c: b0 of entries 4c..4c+3 at sb[s] + 8c, b1 at +4
+__global__ void k_dsell_bases(int64_t n_slices, const int64_t* __restrict__ srow,
+                              const int32_t* __restrict__ sw, const int32_t* __restrict__ sb,
+                              const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              int lim, int32_t* __restrict__ base, uint8_t* __restrict__ fit) {
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl >= n_slices) return;
+  const int64_t r0 = srow[sl];
+  const int nr = (int)(srow[sl + 1] - r0), w = sw[sl];
+  bool ok = true;
+  for (int k = 0; k < ((w + 3) & ~3); ++k) {
+    const int2 bk = k < w ? dbase_entry(rp, ci, r0, nr, k, lane, lim, &ok) : make_int2(0, 0);
+    if (lane == 0) {
+      base[sb[sl] + 8 * (k >> 2) + (k & 3)] = bk.x;
+      base[sb[sl] + 8 * (k >> 2) + 4 + (k & 3)] = bk.y;
+    }
+  }
+  if (lane == 0) fit[sl] = ok ? 1 : 0;
+}
+
+// pass 2: codes (or int32 columns) and values, warp per slice
+__global__ void k_dsell_fill(int64_t n_slices, const DSlice* __restrict__ meta,
+                             const int32_t* __restrict__ base, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const double* __restrict__ cv,
+                             bool sg, uint16_t* __restrict__ dcol, double* __restrict__ sv) {
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl >= n_slices) return;
+  const DSlice m = meta[sl];
+  const int w = m.nw & 0xfffff, nr = (m.nw >> 20) & 63;
+  const bool full = (m.nw >> 26) & 1;
+  if (lane >= nr) return;
+  const int64_t row = m.r0 + lane, b = rp[row], e = rp[row + 1];
+  for (int k = 0; k < w; ++k) {
+    if (!sg) sv[m.vptr + (int64_t)k * nr + lane] = b + k < e ? cv[b + k] : 0.0;
+    if (full) {
+      int32_t* fc = reinterpret_cast<int32_t*>(dcol + m.dptr);
+      int32_t c = kPad;
+      if (b + k < e)
+        c = sg && cv[b + k] < 0 ? ~ci[b + k] : ci[b + k];
+      else if (!sg)
+        c = e > b ? ci[b] : 0;  // val 0, a column the row reads anyway
+      fc[(int64_t)k * nr + lane] = c;
+    }
+  }
+  if (!full)
+    for (int k = 0; k < ((w + 3) & ~3); ++k) {
+      const int32_t* bk = base + m.bptr + 8 * (k >> 2) + (k & 3);
+      dcol[m.dptr + (int64_t)(k >> 2) * 4 * nr + 4 * lane + (k & 3)] =
+          k < w ? dcode(rp, ci, cv, sg, row, k, lane, bk[0], bk[4]) : (uint16_t)kDPad;
+    }
+}
+
+// ELL form, pass 1: bases per 32-row group (warp per group), same chunk
+// layout as the sliced form at g * 2 * W4
+__global__ void k_dell_bases(int64_t rows, int w, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, int lim, int32_t* __restrict__ base,
+                             uint8_t* __restrict__ fit) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g * 32 >= rows) return;
+  const int nr = rows - g * 32 < 32 ? (int)(rows - g * 32) : 32;
+  const int w4 = (w + 3) & ~3;
+  bool ok = true;
+  for (int k = 0; k < w4; ++k) {
+    const int2 bk = k < w ? dbase_entry(rp, ci, g * 32, nr, k, lane, lim, &ok) : make_int2(0, 0);
+    if (lane == 0) {
+      base[g * 2 * w4 + 8 * (k >> 2) + (k & 3)] = bk.x;
+      base[g * 2 * w4 + 8 * (k >> 2) + 4 + (k & 3)] = bk.y;
+    }
+  }
+  if (lane == 0) fit[g] = ok ? 1 : 0;
+}
+
+// ELL form, pass 2: one thread per row
+__global__ void k_dell_fill(int64_t rows, int w, const int32_t* __restrict__ base,
+                            const int32_t* __restrict__ dfull, const int64_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, const double* __restrict__ cv,
+                            bool sg, uint16_t* __restrict__ dcol, int32_t* __restrict__ fcol,
+                            double* __restrict__ sv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t g = r >> 5;
+  const int lane = (int)(r & 31), w4 = (w + 3) & ~3;
+  const int64_t b = rp[r], e = rp[r + 1];
+  const int fi = dfull[g];
+  for (int k = 0; k < w4; ++k) {
+    const int64_t o = g * 32 * w4 + (int64_t)(k >> 2) * 128 + 4 * lane + (k & 3);
+    const int32_t* bk = base + g * 2 * w4 + 8 * (k >> 2) + (k & 3);
+    dcol[o] = (fi < 0 && k < w) ? dcode(rp, ci, cv, sg, r, k, lane, bk[0], bk[4])
+                                : (uint16_t)kDPad;
+  }
+  for (int k = 0; k < w; ++k) {
+    if (!sg) sv[g * 32 * w + k * 32 + lane] = b + k < e ? cv[b + k] : 0.0;
+    if (fi >= 0) {
+      int32_t c = kPad;
+      if (b + k < e)
+        c = sg && cv[b + k] < 0 ? ~ci[b + k] : ci[b + k];
+      else if (!sg)
+        c = e > b ? ci[b] : 0;
+      fcol[(int64_t)fi * 32 * w + k * 32 + lane] = c;
+    }
+  }
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double alpha,
                        int64_t n, int strict) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -344,6 +686,111 @@ inline unsigned blocks_for(int64_t threads) {
 static bool wide_rows(double avg) {
   const char* env = std::getenv("SFEEC_WIDE_CSR");
   return env && std::atoi(env) == 1 && avg >= 64.0;
+}
+
+// SFEEC_DELTA=1 selects the column-delta layouts. Off by default: measured on
+// B200 (tet128 K-Q 0.564 -> 0.612 ms, config 4 K-Q 6.96 -> 7.59 ms) the
+// 17% fewer bytes do not pay for the longer per-entry decode (ncu: 47% more
+// instructions, issue-bound); the narrow ELL operators gain 1-2%.
+static bool delta_enabled() {
+  const char* e = std::getenv("SFEEC_DELTA");
+  return e && std::atoi(e) == 1;
+}
+
+// the sliced delta form pays when its bytes (values + int16 deltas + int32
+// bases + 32 B metadata per slice) undercut the int32 form's (values + int32
+// columns + 20 B metadata per slice): not for short slices of short rows
+static bool dsell_pays(const std::vector<int64_t>& hrow, const std::vector<int32_t>& hw,
+                       bool sg) {
+  double b_delta = 0, b_int = 0;
+  const double vb = sg ? 0.0 : 8.0;
+  for (size_t i = 0; i < hw.size(); ++i) {
+    const double nr = (double)(hrow[i + 1] - hrow[i]), w = hw[i], w4 = (hw[i] + 3) & ~3;
+    b_delta += nr * w * vb + 2.0 * nr * w4 + 8.0 * w4 + 32.0;
+    b_int += nr * w * (vb + 4.0) + 20.0;
+  }
+  return b_delta < b_int;
+}
+
+void DevOperator::build_dsell(const int64_t* drp, const int32_t* dci, const double* dv,
+                              const std::vector<int64_t>& hrow, const std::vector<int32_t>& hw,
+                              cudaStream_t s) {
+  const bool sg = layout == kSigned;
+  n_slices = (int64_t)hw.size();
+  std::vector<int32_t> hb((size_t)n_slices);
+  int64_t nb = 0;
+  for (int64_t i = 0; i < n_slices; ++i) {
+    if (hw[(size_t)i] >= (1 << 20)) throw Error(SFEEC_EINVAL, "sliced delta layout: row too wide");
+    hb[(size_t)i] = (int32_t)nb;
+    nb += 2 * ((hw[(size_t)i] + 3) & ~3);
+  }
+  if (nb > INT32_MAX) throw Error(SFEEC_EINVAL, "sliced delta layout: too many base columns");
+  DevBuf<int64_t> srow;
+  DevBuf<int32_t> sw, sb;
+  srow.upload(hrow.data(), hrow.size(), s);
+  sw.upload(hw.data(), hw.size(), s);
+  sb.upload(hb.data(), hb.size(), s);
+  dbase.alloc((size_t)std::max<int64_t>(nb, 8));
+  DevBuf<uint8_t> fit;
+  fit.alloc((size_t)n_slices);
+  k_dsell_bases<<<blocks_for(n_slices * 32), kThreads, 0, s>>>(
+      n_slices, srow.p, sw.p, sb.p, drp, dci, sg ? 16382 : 32766, dbase.p, fit.p);
+  SFEEC_LAUNCH_CHECK();
+  std::vector<uint8_t> hf((size_t)n_slices);
+  SFEEC_CUDA(cudaMemcpyAsync(hf.data(), fit.p, hf.size(), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  std::vector<DSlice> hm((size_t)n_slices);
+  int64_t vp = 0, dp = 0;
+  n_full = 0;
+  for (int64_t i = 0; i < n_slices; ++i) {
+    const int64_t nr = hrow[(size_t)i + 1] - hrow[(size_t)i], w = hw[(size_t)i];
+    const bool full = hf[(size_t)i] == 0;
+    n_full += full;
+    hm[(size_t)i] = DSlice{hrow[(size_t)i], vp, dp, hb[(size_t)i],
+                           (int32_t)(w | (nr << 20) | ((int64_t)full << 26))};
+    vp += w * nr;
+    dp += full ? ((2 * w * nr + 3) & ~int64_t(3)) : ((w + 3) & ~int64_t(3)) * nr;
+  }
+  sell_entries = vp;
+  dslice.upload(hm.data(), hm.size(), s);
+  dcol.alloc((size_t)std::max<int64_t>(dp, 4));
+  if (!sg) sell_val.alloc((size_t)std::max<int64_t>(vp, 1));
+  k_dsell_fill<<<blocks_for(n_slices * 32), kThreads, 0, s>>>(
+      n_slices, dslice.p, dbase.p, drp, dci, dv, sg, dcol.p, sell_val.p);
+  SFEEC_LAUNCH_CHECK();
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  ell = false;
+  delta = true;
+}
+
+void DevOperator::build_dell(const int64_t* drp, const int32_t* dci, const double* dv, int w,
+                             cudaStream_t s) {
+  const bool sg = layout == kSigned;
+  const int64_t G = (rows + 31) / 32, w4 = (w + 3) & ~3;
+  dbase.alloc((size_t)(G * 2 * w4));
+  DevBuf<uint8_t> fit;
+  fit.alloc((size_t)G);
+  k_dell_bases<<<blocks_for(G * 32), kThreads, 0, s>>>(rows, w, drp, dci, sg ? 16382 : 32766,
+                                                        dbase.p, fit.p);
+  SFEEC_LAUNCH_CHECK();
+  std::vector<uint8_t> hf((size_t)G);
+  SFEEC_CUDA(cudaMemcpyAsync(hf.data(), fit.p, hf.size(), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> hfull((size_t)G);
+  n_full = 0;
+  for (int64_t g = 0; g < G; ++g) hfull[(size_t)g] = hf[(size_t)g] ? -1 : (int32_t)n_full++;
+  dfull.upload(hfull.data(), hfull.size(), s);
+  dcol.alloc((size_t)(G * 32 * w4));
+  if (!sg) sell_val.alloc((size_t)(G * 32 * w));
+  sell_col.alloc((size_t)std::max<int64_t>(1, n_full * 32 * w));
+  k_dell_fill<<<blocks_for(rows), kThreads, 0, s>>>(rows, w, dbase.p, dfull.p, drp, dci, dv, sg,
+                                                     dcol.p, sell_col.p, sell_val.p);
+  SFEEC_LAUNCH_CHECK();
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  ell = true;
+  ell_w = w;
+  sell_entries = G * 32 * w;
+  delta = true;
 }
 
 void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
@@ -410,6 +857,11 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
   int64_t wmax = 0;
   for (int64_t r = 0; r < rows; ++r) wmax = std::max(wmax, h.row_ptr[(size_t)r + 1] - h.row_ptr[(size_t)r]);
   const double ell_pad = (double)(rows * wmax) / (double)nnz;
+  if (wmax >= 1 && wmax <= 8 && ell_pad <= (layout == kSigned ? 1.3 : 1.1) && delta_enabled()) {
+    build_dell(rp.p, ci.p, val.p, (int)wmax, s);
+    drop_csr();
+    return;
+  }
   if (wmax >= 1 && wmax <= 8 && ell_pad <= (layout == kSigned ? 1.3 : 1.1)) {
     ell = true;
     ell_w = (int)wmax;
@@ -439,6 +891,11 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
     sell_col.upload(ec.data(), ec.size(), s);
     if (layout == kSell) sell_val.upload(evv.data(), evv.size(), s);
     SFEEC_CUDA(cudaStreamSynchronize(s));
+    drop_csr();
+    return;
+  }
+  if (delta_enabled() && dsell_pays(hrow, hw, layout == kSigned)) {
+    build_dsell(rp.p, ci.p, val.p, hrow, hw, s);
     drop_csr();
     return;
   }
@@ -610,6 +1067,17 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
   }
   const bool sg = layout == kSigned;
   const double ell_pad = (double)(rows * wmax) / (double)nnz;
+  const bool ell_ok = wmax >= 1 && wmax <= 8 && ell_pad <= (sg ? 1.3 : 1.1);
+  if (delta_enabled() && (ell_ok || dsell_pays(hrow, hw, sg))) {
+    if (ell_ok)
+      build_dell(d.rp.p, d.ci.p, d.val.p, (int)wmax, s);
+    else
+      build_dsell(d.rp.p, d.ci.p, d.val.p, hrow, hw, s);
+    d.rp.reset();
+    d.ci.reset();
+    d.val.reset();
+    return;
+  }
   if (wmax >= 1 && wmax <= 8 && ell_pad <= (sg ? 1.3 : 1.1)) {
     ell = true;
     ell_w = (int)wmax;
@@ -638,11 +1106,16 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
 }
 
 double DevOperator::stream_bytes() const {
+  if (delta && layout != kCsr)
+    return (layout == kSell ? 8.0 * (double)sell_val.n : 0.0) + 2.0 * (double)dcol.n +
+           4.0 * (double)dbase.n + (ell ? 4.0 * (double)(dfull.n + sell_col.n)
+                                        : (double)sizeof(DSlice) * (double)dslice.n);
+  const double meta = ell ? 0.0 : 20.0 * (double)n_slices;
   switch (layout) {
     case kSigned:
-      return 4.0 * (double)sell_entries;
+      return 4.0 * (double)sell_entries + meta;
     case kSell:
-      return 12.0 * (double)sell_entries;
+      return 12.0 * (double)sell_entries + meta;
     default:
       return 12.0 * (double)nnz + 8.0 * (double)(rows + 1);
   }
@@ -709,6 +1182,63 @@ static void launch_vec(const DevOperator& a, const double* x, double* y, double 
   }
 }
 
+template <bool ACC, bool SG>
+static void launch_delta_t(const DevOperator& a, const double* x, double* y, double alpha,
+                           cudaStream_t s) {
+  const double sc = SG ? a.scale : 1.0;
+  if (a.ell) {
+    const unsigned g = blocks_for(a.rows);
+#define SFEEC_DELL_W(W)                                                                     \
+  case W:                                                                                   \
+    k_dell<ACC, SG, W><<<g, kThreads, 0, s>>>(a.rows, a.dbase.p, a.dcol.p, a.dfull.p,      \
+                                              a.sell_col.p, a.sell_val.p, sc, x, y, alpha); \
+    break;
+    switch (a.ell_w) {
+      SFEEC_DELL_W(1)
+      SFEEC_DELL_W(2)
+      SFEEC_DELL_W(3)
+      SFEEC_DELL_W(4)
+      SFEEC_DELL_W(5)
+      SFEEC_DELL_W(6)
+      SFEEC_DELL_W(7)
+      SFEEC_DELL_W(8)
+      default:
+        throw Error(SFEEC_ECUDA, "bad ELL width");
+    }
+#undef SFEEC_DELL_W
+  } else {
+    // SFEEC_DSELL_MB: resident CTAs per SM (3: 85 registers, 4: 64)
+    const char* env = std::getenv("SFEEC_DSELL_MB");
+    const int mb = env ? std::atoi(env) : 4;
+    auto grid = [&](int m) {
+      return (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * m);
+    };
+    if (mb == 4)
+      k_dsell<ACC, SG, 4><<<grid(4), kThreads, 0, s>>>(a.n_slices, a.dslice.p, a.dbase.p,
+                                                       a.dcol.p, a.sell_val.p, sc, x, y, alpha);
+    else
+      k_dsell<ACC, SG, 3><<<grid(3), kThreads, 0, s>>>(a.n_slices, a.dslice.p, a.dbase.p,
+                                                       a.dcol.p, a.sell_val.p, sc, x, y, alpha);
+  }
+  SFEEC_LAUNCH_CHECK();
+}
+
+static void launch_delta(const DevOperator& a, const double* x, double* y, double alpha,
+                         bool accumulate, cudaStream_t s) {
+  const bool sg = a.layout == DevOperator::kSigned;
+  if (accumulate) {
+    if (sg)
+      launch_delta_t<true, true>(a, x, y, alpha, s);
+    else
+      launch_delta_t<true, false>(a, x, y, alpha, s);
+  } else {
+    if (sg)
+      launch_delta_t<false, true>(a, x, y, alpha, s);
+    else
+      launch_delta_t<false, false>(a, x, y, alpha, s);
+  }
+}
+
 void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
                  bool accumulate, cudaStream_t s) {
   if (a.rows == 0) return;
@@ -718,6 +1248,10 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   }
   if (a.layout == DevOperator::kStencil) {
     launch_stencil(*a.st, x, y, alpha, accumulate, s);
+    return;
+  }
+  if (a.delta && a.layout != DevOperator::kCsr) {
+    launch_delta(a, x, y, alpha, accumulate, s);
     return;
   }
   if (a.ell && a.layout != DevOperator::kCsr) {

@@ -2,6 +2,7 @@
 // (K-Q, K-Cb, K-M2, K-CTe in SURVEY.md 2.4).
 #pragma once
 #include <memory>
+#include <vector>
 
 #include "device_util.cuh"
 
@@ -20,6 +21,25 @@ namespace sfeec_b200 {
 //            (~col for negative) -> 4 B/entry instead of 12.
 //   kSell:   general values: fp64 value + int32 column per entry.
 struct StencilOp;
+
+// Column-delta forms of both layouts (SFEEC_DELTA=1; off by default, measured
+// slower: spmv_kernels.cu delta_enabled). Inside a slice (or a 32-row ELL group) entry k of lane l sits at
+// column base_sel[k] + l + delta: two int32 bases per (slice, entry), read by
+// the whole warp as broadcasts, plus a uint16 code per entry (sel bit + delta,
+// kSigned: sel + delta + negative bit). The tet numbering puts consecutive
+// rows at neighbouring vertices of one entity type, so the k-th neighbours of
+// a slice's rows are consecutive ids; the second base covers slices that
+// straddle two types. 10.1 B/entry instead of 12 (values), 2.1 instead of 4
+// (incidence). A slice whose codes do not fit keeps int32 columns ("full").
+// Codes are stored in chunks of 4 entries per lane (one 8-byte load per lane
+// per chunk).
+struct DSlice {
+  int64_t r0;    // first row
+  int64_t vptr;  // first value (entry k of lane l at vptr + k*nr + l)
+  int64_t dptr;  // first int16 of the deltas (or of the int32 columns of a full slice)
+  int32_t bptr;  // first base column (4-aligned)
+  int32_t nw;    // w | nr << 20 | full << 26
+};
 
 struct DevOperator {
   // kStencil: mesh-aware layout of the device-assembled tet operators
@@ -41,6 +61,15 @@ struct DevOperator {
   double scale = 1.0;         // kSigned: |value|
   bool ell = false;           // narrow operator stored as plain ELL (width ell_w)
   int ell_w = 0;
+  // column-delta form (see DSlice): sliced -> dslice; ELL -> 32-row groups,
+  // group g's bases at dbase[g*W4], deltas at dcol[g*32*W4], values at
+  // sell_val[g*32*W], dfull[g] = index of its int32 columns in sell_col or -1
+  bool delta = false;
+  int64_t n_full = 0;  // slices / groups that kept int32 columns
+  DevBuf<DSlice> dslice;
+  DevBuf<int32_t> dbase;
+  DevBuf<uint16_t> dcol;
+  DevBuf<int32_t> dfull;
 
   void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
   // production layouts make the CSR copy redundant: free it (halves the
@@ -71,6 +100,11 @@ struct DevOperator {
   void download_csr(int64_t* row_ptr, int32_t* col_idx, double* v, cudaStream_t s) const;
   // algorithmic bytes of one application in this layout (arrays streamed once)
   double stream_bytes() const;
+  // column-delta builders from a device CSR (kSell / kSigned decided)
+  void build_dsell(const int64_t* rp, const int32_t* ci, const double* v,
+                   const std::vector<int64_t>& hrow, const std::vector<int32_t>& hw,
+                   cudaStream_t s);
+  void build_dell(const int64_t* rp, const int32_t* ci, const double* v, int w, cudaStream_t s);
 };
 
 void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s);

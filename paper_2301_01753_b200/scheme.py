@@ -308,6 +308,16 @@ class SplitScheme:
         L.check(L.lib().sfeec_dev_apply(self._h, idx, L.dptr(x), L.dptr(y)))
         return y
 
+    def layout_info(self, which: str) -> dict:
+        """Device layout of a resident operator (sfeec_dev_layout_info)."""
+        idx = {"q_sym": 0, "c": 1, "ct": 2, "m2": 3, "div": 4}[which]
+        info, by = np.zeros(7, np.int64), C.c_double()
+        L.check(L.lib().sfeec_dev_layout_info(self._h, idx, L.i64ptr(info), C.byref(by)))
+        keys = ("layout", "delta", "ell", "slices", "full_slices", "entries", "nnz")
+        out = {k: int(v) for k, v in zip(keys, info)}
+        out["stream_bytes"] = by.value
+        return out
+
     def set_dt(self, dt: float) -> None:
         L.check(L.lib().sfeec_dev_set_dt(self._h, float(dt)))
         self._dt = float(dt)
