@@ -335,9 +335,10 @@ int sfeec_tet_dev_operators(int n, double jitter, uint64_t seed, int device, sfe
                             sfeec_csr_owned* m2, sfeec_csr_owned* d, sfeec_csr_owned* q_sym,
                             sfeec_csr_owned* ct);
 /* device layout of a resident operator (0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D):
- * info[7] = {layout (0 CSR, 1 signed, 2 fp64 values, 3 stencil), column-delta
+ * info[9] = {layout (0 CSR, 1 signed, 2 fp64 values, 3 stencil), column-delta
  * form, ELL, slices (ELL: 32-row groups), slices kept at int32 columns,
- * stored entries incl. padding, nnz}; *bytes = what one application streams
+ * stored entries incl. padding, nnz, windowed (shared-memory staged x),
+ * window units}; *bytes = what one application streams
  * from the operator arrays in this layout (the algorithmic count of SURVEY.md
  * 8(d) stays 12 B / nonzero whatever the layout). No reference counterpart. */
 int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes);

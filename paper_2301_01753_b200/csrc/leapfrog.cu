@@ -677,6 +677,8 @@ int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes)
       info[4] = a.n_full;
       info[5] = a.sell_entries;
       info[6] = a.nnz;
+      info[7] = a.win ? 1 : 0;
+      info[8] = a.win ? a.n_units : 0;
     }
     if (bytes) *bytes = a.stream_bytes();
   });

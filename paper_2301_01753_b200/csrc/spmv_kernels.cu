@@ -385,8 +385,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (!full) {
         const int4* bp = reinterpret_cast<const int4*>(dbase + m.bptr);
         const uint2* dp = reinterpret_cast<const uint2*>(dcol + m.dptr) + lane;
-        int4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
-        uint2 d = __ldcs(dp);
+        int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+        if (w > 0) {
+          b0 = __ldg(bp);
+          b1 = __ldg(bp + 1);
+        }
+        uint2 d = w > 0 ? __ldcs(dp) : make_uint2(0u, 0u);
         double v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = (!SIGNED && j < w) ? __ldcs(vp + (int64_t)j * nr) : 0.0;
@@ -825,7 +829,8 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
         ++e;
       }
       hw.push_back((int32_t)w);
-      hptr.push_back(hptr.back() + w * (e - r));
+      // slice starts 4-entry aligned (16 B of columns: bulk copies, k_sell_tma)
+      hptr.push_back(hptr.back() + ((w * (e - r) + 3) & ~int64_t(3)));
       hrow.push_back(e);
       r = e;
     }
@@ -848,6 +853,10 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
     layout = kSell;
   } else {
     SFEEC_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  if (win_enabled() && build_win(rp.p, ci.p, val.p, hrow, hw, s)) {
+    drop_csr();
     return;
   }
   // narrow operators (C: 3, C^T: <= 6, M2: 7 per row) go to plain ELL: one
@@ -899,9 +908,9 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
     drop_csr();
     return;
   }
-  std::vector<int32_t> hc((size_t)sell_entries, layout == kSigned ? kPad : 0);
+  std::vector<int32_t> hc((size_t)sell_entries + 4, layout == kSigned ? kPad : 0);
   std::vector<double> hv;
-  if (layout == kSell) hv.assign((size_t)sell_entries, 0.0);
+  if (layout == kSell) hv.assign((size_t)sell_entries + 4, 0.0);
 #pragma omp parallel for schedule(static)
   for (int64_t sl = 0; sl < n_slices; ++sl) {
     const int64_t r0 = hrow[(size_t)sl], nr = hrow[(size_t)sl + 1] - r0;
@@ -925,6 +934,7 @@ void DevOperator::upload(const HostCSR& h, bool strict_only, cudaStream_t s) {
       }
     }
   }
+  if (layout == kSell) prepare_sell_tma();
   slice_row.upload(hrow.data(), hrow.size(), s);
   slice_ptr.upload(hptr.data(), hptr.size(), s);
   slice_w.upload(hw.data(), hw.size(), s);
@@ -1045,7 +1055,8 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
         ++e;
       }
       hw.push_back((int32_t)w);
-      hptr.push_back(hptr.back() + w * (e - r));
+      // slice starts 4-entry aligned (16 B of columns: bulk copies, k_sell_tma)
+      hptr.push_back(hptr.back() + ((w * (e - r) + 3) & ~int64_t(3)));
       hrow.push_back(e);
       r = e;
     }
@@ -1067,6 +1078,12 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
   }
   const bool sg = layout == kSigned;
   const double ell_pad = (double)(rows * wmax) / (double)nnz;
+  if (win_enabled() && build_win(d.rp.p, d.ci.p, d.val.p, hrow, hw, s)) {
+    d.rp.reset();
+    d.ci.reset();
+    d.val.reset();
+    return;
+  }
   const bool ell_ok = wmax >= 1 && wmax <= 8 && ell_pad <= (sg ? 1.3 : 1.1);
   if (delta_enabled() && (ell_ok || dsell_pays(hrow, hw, sg))) {
     if (ell_ok)
@@ -1091,8 +1108,9 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
     slice_row.upload(hrow.data(), hrow.size(), s);
     slice_ptr.upload(hptr.data(), hptr.size(), s);
     slice_w.upload(hw.data(), hw.size(), s);
-    sell_col.alloc((size_t)sell_entries);
-    if (!sg) sell_val.alloc((size_t)sell_entries);
+    if (!sg) prepare_sell_tma();
+    sell_col.alloc((size_t)sell_entries + 4);  // + the alignment over-read of k_sell_tma
+    if (!sg) sell_val.alloc((size_t)sell_entries + 4);
     k_to_sell<<<blocks_for(n_slices * 32), kThreads, 0, s>>>(n_slices, sg, slice_row.p,
                                                              slice_ptr.p, slice_w.p, d.rp.p,
                                                              d.ci.p, d.val.p, sell_col.p,
@@ -1106,6 +1124,10 @@ void DevOperator::upload_device(DevCSR&& d, cudaStream_t s) {
 }
 
 double DevOperator::stream_bytes() const {
+  if (win && layout != kCsr)
+    return (layout == kSell ? 8.0 * (double)sell_val.n : 0.0) + 2.0 * (double)dcol.n +
+           (double)sizeof(DSlice) * (double)dslice.n +
+           (double)sizeof(WUnit) * (double)wunit.n + 8.0 * (double)wseg.n;
   if (delta && layout != kCsr)
     return (layout == kSell ? 8.0 * (double)sell_val.n : 0.0) + 2.0 * (double)dcol.n +
            4.0 * (double)dbase.n + (ell ? 4.0 * (double)(dfull.n + sell_col.n)
@@ -1250,6 +1272,10 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
     launch_stencil(*a.st, x, y, alpha, accumulate, s);
     return;
   }
+  if (a.win && a.layout != DevOperator::kCsr) {
+    launch_win(a, x, y, alpha, accumulate, s);
+    return;
+  }
   if (a.delta && a.layout != DevOperator::kCsr) {
     launch_delta(a, x, y, alpha, accumulate, s);
     return;
@@ -1336,7 +1362,9 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         SFEEC_SELL(false, true);
       break;
     case DevOperator::kSell:
-      if (variant >= 9 && variant <= 13) {
+      if (sell_tma_enabled() && !venv) {
+        launch_sell_tma(a, x, y, alpha, accumulate, s);
+      } else if (variant >= 9 && variant <= 13) {
 #define SFEEC_PIPE(CH, MB)                                                                        \
   do {                                                                                            \
     const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \

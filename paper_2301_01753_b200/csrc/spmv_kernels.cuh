@@ -33,6 +33,28 @@ struct StencilOp;
 // (incidence). A slice whose codes do not fit keeps int32 columns ("full").
 // Codes are stored in chunks of 4 entries per lane (one 8-byte load per lane
 // per chunk).
+// Windowed sliced layout ("win", the default where it fits): the rows are cut
+// into units of whole slices (~1-2k rows); the columns a unit touches, in
+// 32-column blocks, form its window (a few contiguous id ranges: the k-major
+// numbering puts a row's neighbours in 3 vertex planes x 3 vertex rows). A
+// persistent CTA per SM stages each unit's window of x in shared memory with
+// bulk async copies (cp.async.bulk, mbarrier completion; double-buffered, a
+// producer warp runs one unit ahead) while 8 consumer warps stream the
+// unit's slices: fp64 values plus a uint16 window index per entry (kSigned:
+// index << 1 | negative) -- 10 B/entry (values) or 2 B/entry (incidence)
+// instead of 12 / 4 -- and gather x from shared memory instead of L2.
+struct WUnit {
+  int64_t s0;       // first slice
+  int32_t ns;       // slices
+  int32_t seg0;     // first segment
+  int32_t nseg;     // segments
+  int32_t wsize;    // window size (doubles, a multiple of 32)
+  int32_t pad[2];
+};
+// segment: window columns [col, col + len) land at shared index dst, len =
+// next dst - dst (the unit's wsize for its last segment)
+constexpr int kWinCap = 14336;  // doubles per window buffer (112 KB)
+
 struct DSlice {
   int64_t r0;    // first row
   int64_t vptr;  // first value (entry k of lane l at vptr + k*nr + l)
@@ -70,6 +92,14 @@ struct DevOperator {
   DevBuf<int32_t> dbase;
   DevBuf<uint16_t> dcol;
   DevBuf<int32_t> dfull;
+  // windowed layout (see WUnit): dslice (codes at dptr, chunks of 8 entries
+  // per lane), dcol, sell_val, plus the units and their segments
+  bool win = false;
+  int64_t n_units = 0;
+  int64_t win_rows = 0;   // target rows per unit the build settled on
+  bool win_narrow = false;  // every slice <= 8 wide: codes entry-major, no chunks
+  DevBuf<WUnit> wunit;
+  DevBuf<int2> wseg;      // {first column, shared index}
 
   void upload(const HostCSR& h, bool strict_only, cudaStream_t s);
   // production layouts make the CSR copy redundant: free it (halves the
@@ -105,7 +135,22 @@ struct DevOperator {
                    const std::vector<int64_t>& hrow, const std::vector<int32_t>& hw,
                    cudaStream_t s);
   void build_dell(const int64_t* rp, const int32_t* ci, const double* v, int w, cudaStream_t s);
+  // windowed layout from a device CSR; false (nothing changed) when some
+  // unit's window cannot fit kWinCap even at the smallest unit size
+  bool build_win(const int64_t* rp, const int32_t* ci, const double* v,
+                 const std::vector<int64_t>& hrow, const std::vector<int32_t>& hw,
+                 cudaStream_t s);
 };
+
+// the windowed kernel (window_spmv.cu)
+void launch_win(const DevOperator& a, const double* x, double* y, double alpha, bool accumulate,
+                cudaStream_t s);
+bool win_enabled();
+// the TMA-streamed sliced kernel (stream_spmv.cu; fp64 sliced operators)
+void launch_sell_tma(const DevOperator& a, const double* x, double* y, double alpha,
+                     bool accumulate, cudaStream_t s);
+bool sell_tma_enabled();
+void prepare_sell_tma();
 
 void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s);
 void launch_spmv_axpy_strict(const DevOperator& a, const double* x, double* y, double alpha,

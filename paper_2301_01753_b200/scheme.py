@@ -311,9 +311,10 @@ class SplitScheme:
     def layout_info(self, which: str) -> dict:
         """Device layout of a resident operator (sfeec_dev_layout_info)."""
         idx = {"q_sym": 0, "c": 1, "ct": 2, "m2": 3, "div": 4}[which]
-        info, by = np.zeros(7, np.int64), C.c_double()
+        info, by = np.zeros(9, np.int64), C.c_double()
         L.check(L.lib().sfeec_dev_layout_info(self._h, idx, L.i64ptr(info), C.byref(by)))
-        keys = ("layout", "delta", "ell", "slices", "full_slices", "entries", "nnz")
+        keys = ("layout", "delta", "ell", "slices", "full_slices", "entries", "nnz", "win",
+                "units")
         out = {k: int(v) for k, v in zip(keys, info)}
         out["stream_bytes"] = by.value
         return out
