@@ -913,7 +913,7 @@ struct YeeDev {
   int tma_blocks2 = 0;
   DevBuf<char> buf[2];
   int cur = 0;
-  DevBuf<double> stage, partials;
+  DevBuf<double> stage, stage_b, partials;  // host-state staging (e / b), reductions
   double time = 0;
   int64_t launches = 0;
   int64_t n_edges = 0, n_faces = 0;
@@ -1363,13 +1363,14 @@ struct YeeDev {
   }
 
   void set_state(const double* b, const double* e) {
-    DevBuf<double> db;
-    db.alloc((size_t)n_faces);
-    SFEEC_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * (size_t)n_faces, cudaMemcpyHostToDevice,
-                               stream));
+    // persistent staging: no allocation on the host-state path
+    if (stage_b.n < (size_t)std::max<int64_t>(1, n_faces))
+      stage_b.alloc((size_t)std::max<int64_t>(1, n_faces));
+    SFEEC_CUDA(cudaMemcpyAsync(stage_b.p, b, sizeof(double) * (size_t)n_faces,
+                               cudaMemcpyHostToDevice, stream));
     SFEEC_CUDA(cudaMemcpyAsync(stage.p, e, sizeof(double) * (size_t)n_edges,
                                cudaMemcpyHostToDevice, stream));
-    set_state_dev(db.p, stage.p);
+    set_state_dev(stage_b.p, stage.p);
     // ghosts of both buffers: exchange once per buffer
     exchange_nccl();
     cur ^= 1;

@@ -155,7 +155,7 @@ class TetPart:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and callable(getattr(L, "lib", None)):  # (module globals go at shutdown)
             L.lib().sfeec_part_destroy(h)
             self._h = None
 

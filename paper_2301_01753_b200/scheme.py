@@ -176,7 +176,7 @@ class SplitScheme:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and callable(getattr(L, "lib", None)):  # (module globals go at shutdown)
             L.lib().sfeec_dev_destroy(h)
             self._h = None
 
@@ -359,7 +359,7 @@ class YeeScheme:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and callable(getattr(L, "lib", None)):  # (module globals go at shutdown)
             L.lib().sfeec_yee_destroy(h)
             self._h = None
 
@@ -457,7 +457,7 @@ class YeeGroup:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and callable(getattr(L, "lib", None)):  # (module globals go at shutdown)
             L.lib().sfeec_yee_group_destroy(h)
             self._h = None
 
@@ -516,7 +516,7 @@ class TetMesh:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and callable(getattr(L, "lib", None)):  # (module globals go at shutdown)
             L.lib().sfeec_tetmesh_destroy(h)
             self._h = None
 
