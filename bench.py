@@ -158,7 +158,7 @@ class YeeRunner:
     def __init__(self, cfg, device, rank=0, world=1, dist=None):
         from paper_2301_01753_b200 import _lib as L
         self.L = L
-        if world > 1:
+        if dist is not None:
             self.y, self.b0, self.e0, self.dt = yee_slab_setup(cfg["n"], cfg["precision"],
                                                                 device, rank, world, dist)
             self.kernel_label = ("two-step fused TMA sweep per z-slab (two ghost planes) + "
@@ -318,7 +318,7 @@ class TetSlabRunner:
         from paper_2301_01753_b200 import inputs, partition
         t0 = time.perf_counter()
         ids = [None]
-        if world > 1:
+        if dist is not None:
             ids = [S.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(ids, src=0)
         self.p = partition.TetPart.from_device(cfg["n"], cfg["jitter"], 2023, rank, world,
@@ -401,12 +401,12 @@ def run_ours(args, rank, world, local_rank):
     cfg = CONFIGS[args.config]
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if cfg["kind"] == "yee":
         R = YeeRunner(cfg, local_rank, rank, world, dist)
-    elif world > 1 or args.partitioned:
+    elif dist is not None or args.partitioned:
         R = TetSlabRunner(cfg, local_rank, rank, world, dist)
     else:
         R = TetRunner(cfg, local_rank)
@@ -499,7 +499,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_sample(args.config, budget_s=args.cpu_budget)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 
@@ -589,14 +589,30 @@ def run_reference(args, rank, world):
                     "d2h_bytes_per_step": 0}}
     if cfg.get("precision") == 4:
         line["config"]["note"] = "the reference is fp64 only"
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def dptr(t):
     return ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # everything else that writes to fd 1 (NCCL's version banner, library
+    # prints) goes to stderr, so stdout carries exactly the JSON line
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
@@ -606,6 +622,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="tet configs at N=1: run the z-slab partition path (one slab)")
+    ap.add_argument("--dist", action="store_true",
+                    help="the multi-GPU code path (NCCL process group, slab runners, "
+                         "max-over-ranks) even at world size 1, e.g. under torchrun with "
+                         "one process")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)
     args = ap.parse_args()
