@@ -129,6 +129,10 @@ int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e);
 int64_t sfeec_dev_last_launches(sfeec_dev* h);
 /* algorithmic HBM bytes of one merged leapfrog step */
 double sfeec_dev_step_bytes(sfeec_dev* h);
+/* which leapfrog half-steps run as one fused wavefront kernel (wave.cu):
+ * bit 0 He (K-Q + K-Cb), bit 1 Ha (K-M2 + K-CTe); 0 with SFEEC_WAVE=0, in
+ * strict mode, the AE formulation or unsupported operator layouts */
+int sfeec_dev_fused(sfeec_dev* h);
 /* change dt (the scheme is otherwise unchanged; the cached CFL number is
  * rescaled) -- used to set dt = 0.5 * dt_CFL after sfeec_dev_cfl_number */
 int sfeec_dev_set_dt(sfeec_dev* h, double dt);

@@ -102,8 +102,29 @@ struct LeapfrogDev {
     ++launches;
   }
 
+  // fused producer -> consumer wavefront kernels (wave.cu): He = K-Q + K-Cb,
+  // Ha = K-M2 + K-CTe; built before any graph capture (the plan build
+  // synchronises), used in production BE mode when SFEEC_WAVE != 0
+  WavePlan wave_he, wave_ha;
+  void prepare_wave() {
+    if (strict() || form != SFEEC_FORM_BE || !wave_enabled()) return;
+    if (!wave_he.built && build_wave_plan(q, c, wave_he, stream)) t1.zero(stream);
+    if (!wave_ha.built && build_wave_plan(m2, ct, wave_ha, stream)) t2.zero(stream);
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+  }
+  bool wave_on(const WavePlan& w) const {
+    return w.ok && !strict() && form == SFEEC_FORM_BE && wave_enabled();
+  }
+
   // dynamics.cpp:47-55
   void flow_he(double h) {
+    if (wave_on(wave_he)) {  // b -= h C (Q e), one kernel
+      tic(q);
+      launch_wave(wave_he, q, c, e.p, t1.p, first.p, -h, stream);
+      toc();
+      ++launches;
+      return;
+    }
     apply(q, e.p, t1.p);
     if (form == SFEEC_FORM_AE) {
       axpy_vec(first.p, t1.p, -h, n1);
@@ -122,6 +143,12 @@ struct LeapfrogDev {
     if (form == SFEEC_FORM_AE) {
       apply(c, first.p, t3.p);
       b = t3.p;
+    } else if (wave_on(wave_ha)) {  // e += f C^T (M2 b), one kernel
+      tic(m2);
+      launch_wave(wave_ha, m2, ct, b, t2.p, e.p, f, stream);
+      toc();
+      ++launches;
+      return;
     }
     apply(m2, b, t2.p);
     apply_axpy(ct, t2.p, e.p, f);
@@ -196,6 +223,7 @@ struct LeapfrogDev {
     launches = 0;
     if (n <= 0) return;
     check_cfl_once();
+    prepare_wave();
     if (strict() || kind == SFEEC_SPLIT_LIE_TROTTER || form == SFEEC_FORM_AE) {
       for (int64_t s = 0; s < n; ++s) {
         if (kind == SFEEC_SPLIT_STRANG) {
@@ -657,6 +685,10 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
       bytes[2] = ctb * d.ct.nnz + 8.0 * d.n2 + 16.0 * d.n1; // e += f C^T u
       bytes[3] = 12.0 * d.m2.nnz + 16.0 * d.n2;  // u = M2 b
       bytes[4] = 0;
+      // fused pairs (t, u stay intermediates): b -= h C (Q e); e += f C^T (M2 b)
+      if (d.wave_on(d.wave_he)) bytes[0] = 12.0 * d.q.nnz + 8.0 * d.n1 + cb * d.c.nnz + 16.0 * d.n2;
+      if (d.wave_on(d.wave_ha))
+        bytes[3] = 12.0 * d.m2.nnz + 8.0 * d.n2 + ctb * d.ct.nnz + 16.0 * d.n1;
     }
     d.timing = enable != 0;
   });
@@ -682,6 +714,19 @@ int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes)
     }
     if (bytes) *bytes = a.stream_bytes();
   });
+}
+
+// bit 0: He (K-Q + K-Cb) runs as one wavefront kernel, bit 1: Ha (K-M2 + K-CTe)
+int sfeec_dev_fused(sfeec_dev* h) {
+  if (!h) return 0;
+  int r = 0;
+  guarded([&] {
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    d.prepare_wave();
+    r = (d.wave_on(d.wave_he) ? 1 : 0) | (d.wave_on(d.wave_ha) ? 2 : 0);
+  });
+  return r;
 }
 
 // 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2); a

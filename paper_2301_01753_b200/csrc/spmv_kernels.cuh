@@ -152,6 +152,25 @@ void launch_sell_tma(const DevOperator& a, const double* x, double* y, double al
 bool sell_tma_enabled();
 void prepare_sell_tma();
 
+// Fused producer -> consumer pair (wave.cu): t = P x, then y += alpha C t in
+// one persistent wavefront kernel (P sliced or ELL fp64, C ELL). A plan is
+// built once per operator pair; ok == false means the layouts are not
+// supported and the caller runs the two kernels.
+struct WavePlan {
+  bool built = false, ok = false;
+  DevBuf<int4> items;
+  int n_items = 0;
+  int64_t n_prod = 0;
+  DevBuf<int> sync;  // ticket + per-producer-item flags, cleared per launch
+  unsigned grid = 0;
+  int batch = 1;  // items per ticket
+  void* kernel = nullptr;
+};
+bool wave_enabled();  // SFEEC_WAVE=1 (default off: measured slower, wave.cu)
+bool build_wave_plan(const DevOperator& p, const DevOperator& c, WavePlan& plan, cudaStream_t s);
+void launch_wave(const WavePlan& plan, const DevOperator& p, const DevOperator& c,
+                 const double* x, double* t, double* y, double alpha, cudaStream_t s);
+
 void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaStream_t s);
 void launch_spmv_axpy_strict(const DevOperator& a, const double* x, double* y, double alpha,
                              cudaStream_t s);

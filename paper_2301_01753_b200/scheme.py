@@ -326,6 +326,11 @@ class SplitScheme:
     def last_launches(self) -> int:
         return int(L.lib().sfeec_dev_last_launches(self._h))
 
+    def fused(self) -> int:
+        """Bit 0: He (K-Q + K-Cb) runs as one wavefront kernel (wave.cu);
+        bit 1: Ha (K-M2 + K-CTe). 0 with SFEEC_WAVE=0 or unsupported layouts."""
+        return int(L.lib().sfeec_dev_fused(self._h))
+
     KERNEL_CLASSES = ("K-Q", "K-Cb", "K-CTe", "K-M2", "other")
 
     def kernel_timing(self, enable: bool = True) -> dict:
