@@ -228,6 +228,99 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---- sliced layout, software-pipelined + L2 bulk prefetch -----------------
+// As k_sell_pipe, and lane 0 issues cp.async.bulk.prefetch.L2 for the column
+// and value arrays of the warp's NEXT slice (its first kPfCols entries per
+// row) while the current one streams, plus, inside wide slices (config 4's
+// ~300/row), the next kPfCols columns every kPfCols: the HBM requests run a
+// slice ahead of the loads with no registers held for them, and the loads
+// then hit L2.
+constexpr int kPfCols = 32;
+
+__device__ __forceinline__ void l2_prefetch_bytes(const char* base, int64_t b0, int64_t b1,
+                                                  int64_t bmax) {
+  b0 &= ~int64_t(15);
+  b1 = min((b1 + 15) & ~int64_t(15), bmax & ~int64_t(15));
+  if (b1 > b0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + b0),
+                 "r"((unsigned)(b1 - b0))
+                 : "memory");
+}
+// entries [e0, e1) of the sliced column / value arrays (n entries in all)
+__device__ __forceinline__ void l2_prefetch_entries(const int32_t* col, const double* val,
+                                                    int64_t e0, int64_t e1, int64_t n) {
+  l2_prefetch_bytes(reinterpret_cast<const char*>(col), 4 * e0, 4 * e1, 4 * n);
+  l2_prefetch_bytes(reinterpret_cast<const char*>(val), 8 * e0, 8 * e1, 8 * n);
+}
+
+template <bool ACC, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_sell_pf(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
+              const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
+              const double* __restrict__ val, const double* __restrict__ x,
+              double* __restrict__ y, double alpha, int64_t n_entries) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_slices) return;
+  SliceMeta m = load_meta(srow, sptr, sw, s);
+  SliceMeta mn;
+  if (s + nwarps < n_slices) mn = load_meta(srow, sptr, sw, s + nwarps);
+  if (lane == 0)
+    l2_prefetch_entries(col, val, m.ptr, m.ptr + (int64_t)min(m.w, kPfCols) * m.nr, n_entries);
+  while (true) {
+    const int64_t sn = s + nwarps;
+    SliceMeta mnn;
+    if (sn + nwarps < n_slices) mnn = load_meta(srow, sptr, sw, sn + nwarps);
+    if (lane == 0 && sn < n_slices)
+      l2_prefetch_entries(col, val, mn.ptr, mn.ptr + (int64_t)min(mn.w, kPfCols) * mn.nr,
+                          n_entries);
+    if (lane < m.nr) {
+      const int64_t row = m.r0 + lane;
+      const double y0 = ACC ? y[row] : 0.0;
+      const int64_t base = m.ptr + lane;
+      double acc = 0.0;
+      int32_t p[CH];
+      double v[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const bool ok = j < m.w;
+        const int64_t o = base + (int64_t)j * m.nr;
+        p[j] = ok ? __ldcs(col + o) : kPad;
+        v[j] = ok ? __ldcs(val + o) : 0.0;
+      }
+      for (int k0 = 0; k0 < m.w; k0 += CH) {
+        if (lane == 0 && (k0 % kPfCols) == 0 && k0 + kPfCols < m.w)
+          l2_prefetch_entries(col, val, m.ptr + (int64_t)(k0 + kPfCols) * m.nr,
+                              m.ptr + (int64_t)min(k0 + 2 * kPfCols, m.w) * m.nr, n_entries);
+        int32_t pn[CH];
+        double vn[CH], xv[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const bool ok = k0 + CH + j < m.w;
+          const int64_t o = base + (int64_t)(k0 + CH + j) * m.nr;
+          pn[j] = ok ? __ldcs(col + o) : kPad;
+          vn[j] = ok ? __ldcs(val + o) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) xv[j] = p[j] != kPad ? __ldg(x + p[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) acc = fma(v[j], xv[j], acc);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          p[j] = pn[j];
+          v[j] = vn[j];
+        }
+      }
+      y[row] = ACC ? fma(alpha, acc, y0) : acc;
+    }
+    if (sn >= n_slices) break;
+    s = sn;
+    m = mn;
+    mn = mnn;
+  }
+}
+
 // ---- sliced layout, two lanes per row (wide rows, e.g. Q_sym ~16/row) -----
 // A warp takes half a slice pair: lanes 2i, 2i+1 share row i of 16 rows and
 // take alternate entries, so each lane holds <= CH entries of a <= 2*CH row
@@ -1364,6 +1457,24 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
     case DevOperator::kSell:
       if (sell_tma_enabled() && !venv) {
         launch_sell_tma(a, x, y, alpha, accumulate, s);
+      } else if (variant >= 14 && variant <= 16) {
+#define SFEEC_PF(CH, MB)                                                                          \
+  do {                                                                                            \
+    const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \
+    if (accumulate)                                                                               \
+      k_sell_pf<true, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,   \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, (int64_t)std::min(a.sell_col.n, a.sell_val.n));           \
+    else                                                                                          \
+      k_sell_pf<false, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,  \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, (int64_t)std::min(a.sell_col.n, a.sell_val.n));           \
+  } while (0)
+        if (variant == 15)
+          SFEEC_PF(2, 4);
+        else if (variant == 16)
+          SFEEC_PF(4, 3);
+        else
+          SFEEC_PF(4, 4);
+#undef SFEEC_PF
       } else if (variant >= 9 && variant <= 13) {
 #define SFEEC_PIPE(CH, MB)                                                                        \
   do {                                                                                            \

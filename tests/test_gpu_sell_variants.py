@@ -1,0 +1,35 @@
+"""GPU: the sliced SpMV variants selectable by SFEEC_SELL_VARIANT (register
+pipelined k_sell_pipe = 9..13, + L2 bulk prefetch k_sell_pf = 14..16) give
+bitwise the same rows (same per-row FMA order) on the tet operators."""
+import numpy as np
+import pytest
+
+import paper_2301_01753_b200 as S
+from tests.test_gpu_delta import layout_env
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("variant", [14, 15, 16])
+def test_prefetch_variants_bitwise(variant):
+    s = S.tet_device_scheme(16, 0.1, 3, dt=0.01)
+    rng = np.random.default_rng(variant)
+    x = rng.standard_normal(s._n1)
+    ref = s.apply("q_sym", x)
+    with layout_env(SFEEC_SELL_VARIANT=variant):
+        out = s.apply("q_sym", x)
+        st = S.make_state(S.Formulation.BE, rng.standard_normal(s._n2), rng.standard_normal(s._n1))
+        a = s.advance(st, 9)
+    assert np.array_equal(out, ref)
+    b = s.advance(st, 9)
+    assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
+
+
+def test_prefetch_wide_rows_bitwise():
+    """config 4's S(M1^2) Q: ~300 entries per row, in-slice prefetches"""
+    s = S.p2_device_scheme(3, 0.1, 2, dt=0.005)
+    x = np.random.default_rng(1).standard_normal(s._n1)
+    ref = s.apply("q_sym", x)
+    with layout_env(SFEEC_SELL_VARIANT=14):
+        out = s.apply("q_sym", x)
+    assert np.array_equal(out, ref)
