@@ -81,13 +81,24 @@ struct LeapfrogDev {
     ev_used.clear();
   }
 
+  // Alternating row order (SFEEC_ALT_DIR): in the step chain M2 -> C^T -> Q
+  // -> C each kernel reads the vector the previous one wrote; running M2 and
+  // Q in descending row order makes each kernel start on the rows its
+  // producer wrote last, which are still in the 126 MB L2. Rows are
+  // computed identically either way.
+  bool alt_dir() const {
+    const char* v = std::getenv("SFEEC_ALT_DIR");
+    return v && std::atoi(v) != 0;
+  }
+  bool reversed(const DevOperator& a) const { return (&a == &m2 || &a == &q) && alt_dir(); }
+
   // y = A x
   void apply(const DevOperator& a, const double* x, double* y) {
     tic(a);
     if (strict())
       launch_spmv_strict(a, x, y, stream);
     else
-      launch_spmv(a, x, y, 0.0, false, stream);
+      launch_spmv(a, x, y, 0.0, false, stream, reversed(a));
     toc();
     ++launches;
   }
@@ -97,7 +108,7 @@ struct LeapfrogDev {
     if (strict())
       launch_spmv_axpy_strict(a, x, y, alpha, stream);
     else
-      launch_spmv(a, x, y, alpha, true, stream);
+      launch_spmv(a, x, y, alpha, true, stream, reversed(a));
     toc();
     ++launches;
   }

@@ -176,16 +176,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
     k_sell_pipe(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
                 const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ x,
-                double* __restrict__ y, double alpha) {
+                double* __restrict__ y, double alpha, int rev) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
-  SliceMeta m = load_meta(srow, sptr, sw, s);
+  // rev: slices in descending order (the previous kernel's last-written rows,
+  // still in L2, come first); every row's arithmetic is unchanged
+  const int64_t last = n_slices - 1;
+  SliceMeta m = load_meta(srow, sptr, sw, rev ? last - s : s);
   while (true) {
     const int64_t sn = s + nwarps;
     SliceMeta mn;
-    if (sn < n_slices) mn = load_meta(srow, sptr, sw, sn);
+    if (sn < n_slices) mn = load_meta(srow, sptr, sw, rev ? last - sn : sn);
     if (lane < m.nr) {
       const int64_t row = m.r0 + lane;
       const double y0 = ACC ? y[row] : 0.0;
@@ -380,9 +383,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
 template <bool ACC, bool SIGNED, int W>
 __global__ void __launch_bounds__(kThreads)
     k_ell(int64_t rows, const int32_t* __restrict__ col, const double* __restrict__ val,
-          double scale, const double* __restrict__ x, double* __restrict__ y, double alpha) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
+          double scale, const double* __restrict__ x, double* __restrict__ y, double alpha,
+          int rev) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= rows) return;
+  const int64_t r = rev ? rows - 1 - g : g;  // rev: descending rows (see k_sell_pipe)
   const double y0 = ACC ? y[r] : 0.0;
   int32_t p[W];
   double v[W], xv[W];
@@ -1355,7 +1360,8 @@ static void launch_delta(const DevOperator& a, const double* x, double* y, doubl
 }
 
 void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
-                 bool accumulate, cudaStream_t s) {
+                 bool accumulate, cudaStream_t s, bool reverse) {
+  const int rev = reverse ? 1 : 0;  // k_ell / k_sell_pipe only; the others ignore it
   if (a.rows == 0) return;
   if (a.nnz == 0) {
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
@@ -1380,14 +1386,14 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   case W:                                                                                    \
     if (sg) {                                                                                \
       if (accumulate)                                                                        \
-        k_ell<true, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha); \
+        k_ell<true, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
       else                                                                                   \
-        k_ell<false, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha); \
+        k_ell<false, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
     } else {                                                                                 \
       if (accumulate)                                                                        \
-        k_ell<true, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha); \
+        k_ell<true, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
       else                                                                                   \
-        k_ell<false, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha); \
+        k_ell<false, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
     }                                                                                        \
     break;
     switch (a.ell_w) {
@@ -1481,10 +1487,10 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
     const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \
     if (accumulate)                                                                               \
       k_sell_pipe<true, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p, \
-          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);                             \
     else                                                                                          \
       k_sell_pipe<false, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,\
-          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha);                                  \
+          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);                             \
   } while (0)
         if (variant == 10)
           SFEEC_PIPE(2, 4);

@@ -175,8 +175,10 @@ void launch_spmv_strict(const DevOperator& a, const double* x, double* y, cudaSt
 void launch_spmv_axpy_strict(const DevOperator& a, const double* x, double* y, double alpha,
                              cudaStream_t s);
 // accumulate ? y += alpha * A x : y = A x
+// reverse: rows in descending order (k_ell, k_sell_pipe), so a kernel starts
+// on the rows the previous kernel wrote last (still in L2); results unchanged
 void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
-                 bool accumulate, cudaStream_t s);
+                 bool accumulate, cudaStream_t s, bool reverse = false);
 // y += alpha * x   (strict: y + (alpha*x) with separate rounding)
 void launch_axpy(double* y, const double* x, double alpha, int64_t n, bool strict,
                  cudaStream_t s);

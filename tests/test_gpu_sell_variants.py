@@ -33,3 +33,15 @@ def test_prefetch_wide_rows_bitwise():
     with layout_env(SFEEC_SELL_VARIANT=14):
         out = s.apply("q_sym", x)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("n", [16, 24])
+def test_alternating_row_order_bitwise(n):
+    """SFEEC_ALT_DIR=1 runs M2 and Q in descending row order: same rows."""
+    s = S.tet_device_scheme(n, 0.1, 3, dt=0.01)
+    rng = np.random.default_rng(n)
+    st = S.make_state(S.Formulation.BE, rng.standard_normal(s._n2), rng.standard_normal(s._n1))
+    a = s.advance(st, 40)
+    with layout_env(SFEEC_ALT_DIR=1):
+        b = s.advance(st, 40)
+    assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
