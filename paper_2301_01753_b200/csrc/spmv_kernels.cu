@@ -17,6 +17,58 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int32_t kPad = 0x7fffffff;  // padding slot in the signed sliced layout
 
+// Streaming (evict-first) loads of the operator arrays with an optional L2
+// prefetch-size hint: PF 0 = plain ld.global.cs, 1 = .L2::128B, 2 = .L2::256B
+// (on a miss the L2 fetches the whole 128/256-byte block, so the next
+// warp-wide chunk of the same stream is already on its way). Values unchanged.
+template <int PF>
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  if constexpr ((PF & 3) == 0) {
+    return __ldcs(p);
+  } else {
+    int32_t v;
+    if constexpr ((PF & 3) == 1)
+      asm volatile("ld.global.cs.L2::128B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    else
+      asm volatile("ld.global.cs.L2::256B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+  }
+}
+template <int PF>
+__device__ __forceinline__ double ld_stream(const double* p) {
+  if constexpr ((PF & 3) == 0) {
+    return __ldcs(p);
+  } else {
+    double v;
+    if constexpr ((PF & 3) == 1)
+      asm volatile("ld.global.cs.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    else
+      asm volatile("ld.global.cs.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+}
+
+// Gather of the input vector: PF bit 2 adds an L2 evict_last policy, so the
+// gathered x (re-read by neighbouring rows) outlives the evict-first operator
+// streams in L2. PF & 3 is the stream prefetch size (ld_stream).
+template <int PF>
+__device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
+  if constexpr ((PF & 4) == 0) {
+    return __ldg(p);
+  } else {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+  }
+}
+template <int PF>
+__device__ __forceinline__ uint64_t gather_policy() {
+  uint64_t pol = 0;
+  if constexpr ((PF & 4) != 0)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // ---- strict: reference-order, no FMA ------------------------------------
 // sparse.cpp:98-103: acc += val*x in stored order; then the flow's axpy
 // (dynamics.cpp:50,53,66) as a separate multiply and add.
@@ -171,13 +223,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // As k_sell (fp64 values), but the column/value loads of chunk c+1 are issued
 // before the gathers of chunk c, so a chunk costs one gather round trip and
 // the streaming loads overlap it.
-template <bool ACC, int CH, int MINB>
+template <bool ACC, int CH, int MINB, int PF = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_sell_pipe(int64_t n_slices, const int64_t* __restrict__ srow, const int64_t* __restrict__ sptr,
                 const int32_t* __restrict__ sw, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ x,
                 double* __restrict__ y, double alpha, int rev) {
   const int lane = threadIdx.x & 31;
+  const uint64_t pol = gather_policy<PF>();
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= n_slices) return;
@@ -200,8 +253,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int j = 0; j < CH; ++j) {
         const bool ok = j < m.w;
         const int64_t o = base + (int64_t)j * m.nr;
-        p[j] = ok ? __ldcs(col + o) : kPad;
-        v[j] = ok ? __ldcs(val + o) : 0.0;
+        p[j] = ok ? ld_stream<PF>(col + o) : kPad;
+        v[j] = ok ? ld_stream<PF>(val + o) : 0.0;
       }
       for (int k0 = 0; k0 < m.w; k0 += CH) {
         int32_t pn[CH];
@@ -210,11 +263,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int j = 0; j < CH; ++j) {
           const bool ok = k0 + CH + j < m.w;
           const int64_t o = base + (int64_t)(k0 + CH + j) * m.nr;
-          pn[j] = ok ? __ldcs(col + o) : kPad;
-          vn[j] = ok ? __ldcs(val + o) : 0.0;
+          pn[j] = ok ? ld_stream<PF>(col + o) : kPad;
+          vn[j] = ok ? ld_stream<PF>(val + o) : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < CH; ++j) xv[j] = p[j] != kPad ? __ldg(x + p[j]) : 0.0;
+        for (int j = 0; j < CH; ++j) xv[j] = p[j] != kPad ? ld_gather<PF>(x + p[j], pol) : 0.0;
 #pragma unroll
         for (int j = 0; j < CH; ++j) acc = fma(v[j], xv[j], acc);
 #pragma unroll
@@ -380,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 }
 
 // ---- plain ELL for narrow operators: one thread per row ------------------
-template <bool ACC, bool SIGNED, int W>
+template <bool ACC, bool SIGNED, int W, int PF = 0>
 __global__ void __launch_bounds__(kThreads)
     k_ell(int64_t rows, const int32_t* __restrict__ col, const double* __restrict__ val,
           double scale, const double* __restrict__ x, double* __restrict__ y, double alpha,
@@ -389,19 +442,20 @@ __global__ void __launch_bounds__(kThreads)
   if (g >= rows) return;
   const int64_t r = rev ? rows - 1 - g : g;  // rev: descending rows (see k_sell_pipe)
   const double y0 = ACC ? y[r] : 0.0;
+  const uint64_t pol = gather_policy<PF>();
   int32_t p[W];
   double v[W], xv[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) {
-    p[k] = __ldcs(col + (int64_t)k * rows + r);
-    if (!SIGNED) v[k] = __ldcs(val + (int64_t)k * rows + r);
+    p[k] = ld_stream<PF>(col + (int64_t)k * rows + r);
+    if (!SIGNED) v[k] = ld_stream<PF>(val + (int64_t)k * rows + r);
   }
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     if (SIGNED)
-      xv[k] = p[k] != kPad ? __ldg(x + (p[k] < 0 ? ~p[k] : p[k])) : 0.0;
+      xv[k] = p[k] != kPad ? ld_gather<PF>(x + (p[k] < 0 ? ~p[k] : p[k]), pol) : 0.0;
     else
-      xv[k] = __ldg(x + p[k]);
+      xv[k] = ld_gather<PF>(x + p[k], pol);
   }
   double acc = 0.0;
 #pragma unroll
@@ -1359,9 +1413,18 @@ static void launch_delta(const DevOperator& a, const double* x, double* y, doubl
   }
 }
 
+// SFEEC_L2PF: L2 hints in k_ell and the default k_sell_pipe: bits 0-1 the
+// prefetch size of the operator streams (1 = 128 B, 2 = 256 B), bit 2 an
+// evict_last policy on the gathered x (valid: 0, 1, 2, 4, 6); results unchanged
+static int l2_prefetch_size() {
+  const char* e = std::getenv("SFEEC_L2PF");
+  return e ? std::atoi(e) : 0;
+}
+
 void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
                  bool accumulate, cudaStream_t s, bool reverse) {
   const int rev = reverse ? 1 : 0;  // k_ell / k_sell_pipe only; the others ignore it
+  const int l2pf = l2_prefetch_size();  // k_ell / k_sell_pipe streaming-load hint
   if (a.rows == 0) return;
   if (a.nnz == 0) {
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
@@ -1382,18 +1445,30 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   if (a.ell && a.layout != DevOperator::kCsr) {
     const unsigned g = blocks_for(a.rows);
     const bool sg = a.layout == DevOperator::kSigned;
+#define SFEEC_ELL_PF(W, PF)                                                                   \
+  if (sg) {                                                                                  \
+    if (accumulate)                                                                          \
+      k_ell<true, true, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
+    else                                                                                     \
+      k_ell<false, true, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
+  } else {                                                                                   \
+    if (accumulate)                                                                          \
+      k_ell<true, false, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
+    else                                                                                     \
+      k_ell<false, false, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
+  }
 #define SFEEC_ELL_W(W)                                                                       \
   case W:                                                                                    \
-    if (sg) {                                                                                \
-      if (accumulate)                                                                        \
-        k_ell<true, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
-      else                                                                                   \
-        k_ell<false, true, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
+    if (l2pf == 1) {                                                                         \
+      SFEEC_ELL_PF(W, 1)                                                                     \
+    } else if (l2pf == 2) {                                                                  \
+      SFEEC_ELL_PF(W, 2)                                                                     \
+    } else if (l2pf == 4) {                                                                  \
+      SFEEC_ELL_PF(W, 4)                                                                     \
+    } else if (l2pf == 6) {                                                                  \
+      SFEEC_ELL_PF(W, 6)                                                                     \
     } else {                                                                                 \
-      if (accumulate)                                                                        \
-        k_ell<true, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
-      else                                                                                   \
-        k_ell<false, false, W><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
+      SFEEC_ELL_PF(W, 0)                                                                     \
     }                                                                                        \
     break;
     switch (a.ell_w) {
@@ -1409,6 +1484,7 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
         throw Error(SFEEC_ECUDA, "bad ELL width");
     }
 #undef SFEEC_ELL_W
+#undef SFEEC_ELL_PF
     SFEEC_LAUNCH_CHECK();
     return;
   }
@@ -1482,16 +1558,17 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
           SFEEC_PF(4, 4);
 #undef SFEEC_PF
       } else if (variant >= 9 && variant <= 13) {
-#define SFEEC_PIPE(CH, MB)                                                                        \
+#define SFEEC_PIPE_PF(CH, MB, PF)                                                                 \
   do {                                                                                            \
     const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \
     if (accumulate)                                                                               \
-      k_sell_pipe<true, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p, \
-          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);                             \
+      k_sell_pipe<true, CH, MB, PF><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,            \
+          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);              \
     else                                                                                          \
-      k_sell_pipe<false, CH, MB><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p, a.slice_ptr.p,\
-          a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);                             \
+      k_sell_pipe<false, CH, MB, PF><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,           \
+          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);              \
   } while (0)
+#define SFEEC_PIPE(CH, MB) SFEEC_PIPE_PF(CH, MB, 0)
         if (variant == 10)
           SFEEC_PIPE(2, 4);
         else if (variant == 11)
@@ -1500,9 +1577,18 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
           SFEEC_PIPE(2, 8);
         else if (variant == 13)
           SFEEC_PIPE(3, 6);
+        else if (l2pf == 1)
+          SFEEC_PIPE_PF(4, 4, 1);
+        else if (l2pf == 2)
+          SFEEC_PIPE_PF(4, 4, 2);
+        else if (l2pf == 4)
+          SFEEC_PIPE_PF(4, 4, 4);
+        else if (l2pf == 6)
+          SFEEC_PIPE_PF(4, 4, 6);
         else
           SFEEC_PIPE(4, 4);
 #undef SFEEC_PIPE
+#undef SFEEC_PIPE_PF
       } else if (variant >= 5) {
 #define SFEEC_TPR2(CH, MB)                                                                   \
   do {                                                                                       \

@@ -45,3 +45,21 @@ def test_alternating_row_order_bitwise(n):
     with layout_env(SFEEC_ALT_DIR=1):
         b = s.advance(st, 40)
     assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
+
+
+@pytest.mark.parametrize("pf", [1, 2, 4, 6])
+def test_l2_prefetch_size_hint_bitwise(pf):
+    """SFEEC_L2PF=1/2 adds .L2::128B/.L2::256B to the operator streams of
+    k_ell and k_sell_pipe: same loads, same rows, same steps."""
+    s = S.tet_device_scheme(16, 0.1, 3, dt=0.01)
+    rng = np.random.default_rng(pf)
+    x, z = rng.standard_normal(s._n1), rng.standard_normal(s._n2)
+    ref = [s.apply(w, v) for w, v in (("q_sym", x), ("c", x), ("ct", z), ("m2", z))]
+    st = S.make_state(S.Formulation.BE, rng.standard_normal(s._n2), rng.standard_normal(s._n1))
+    a = s.advance(st, 9)
+    with layout_env(SFEEC_L2PF=pf):
+        out = [s.apply(w, v) for w, v in (("q_sym", x), ("c", x), ("ct", z), ("m2", z))]
+        b = s.advance(st, 9)
+    for o, r in zip(out, ref):
+        assert np.array_equal(o, r)
+    assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
