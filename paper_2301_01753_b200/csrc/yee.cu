@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(NTH)
 // planes are double-buffered, B1 single, so with NS = 3 two CTAs fit per SM
 // (fp64). One thread per E1-region point keeps that point's E1, B1, E2 and
 // old B of the current and previous plane in registers.
-template <class T, int TX, int TY, int NS>
+template <class T, int TX, int TY, int NS, int NB1 = 1>
 struct TmaCfg2 {
   static constexpr int kOff = 16 / (int)sizeof(T);
   static constexpr int kBW = (((TX + 2 + kOff) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
@@ -464,8 +464,9 @@ struct TmaCfg2 {
   static constexpr int kXB = TX + 2, kYB = TY + 2;  // B1 region, origin (i0-1, j0-1)
   static constexpr int kX2 = TX + 1, kY2 = TY + 1;  // E2 region, origin (i0, j0)
   static constexpr int kE1 = 3 * kX1 * kY1, kB1 = 3 * kXB * kYB, kE2 = 3 * kX2 * kY2;
-  // E1 and E2 planes double-buffered, B1 single, all on the E1 region grid
-  static constexpr int kBufBytes = 5 * 3 * kX1 * kY1 * (int)sizeof(T);
+  // E1 and E2 planes double-buffered, B1 single (NB1 = 1) or double (NB1 =
+  // 2), all on the E1 region grid
+  static constexpr int kBufBytes = (4 + NB1) * 3 * kX1 * kY1 * (int)sizeof(T);
   static constexpr int kBarOff = (NS * kStage + kBufBytes + 15) / 16 * 16;
   static constexpr int kSmem = kBarOff + NS * 8 + 128;
   // prefetch distance in planes: a stage is read only in phase 1 of its own
@@ -481,12 +482,17 @@ __device__ __forceinline__ uint32_t e_mask_xy(int i, int j, int n0, int n1) {
   return (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u);
 }
 
-template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB>
+// NB1 = 2 double-buffers the B1 plane: phase 2 of plane p+1 then writes the
+// other buffer than the one phase 3 of plane p reads, and the only other
+// reason for the barrier between phases 1 and 2 (E1(z-1) neighbours) is
+// already covered by the previous plane's barrier, so each plane needs one
+// barrier instead of two. Same arithmetic, bitwise the same result.
+template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1>
 __global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                  int n_units, int kbeg, int kend) {
-  using Cfg = TmaCfg2<T, TX, TY, NS>;
+  using Cfg = TmaCfg2<T, TX, TY, NS, NB1>;
   constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
   // NPT points of the E1 region (origin (i0-1, j0-1)) per thread: points
   // tid + h*NH, h < NPT. The B1, E2 and B2 regions are subsets in the same
@@ -500,8 +506,8 @@ __global__ void __launch_bounds__(NTH, MINB)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   T* sE1 = reinterpret_cast<T*>(base + NS * Cfg::kStage);  // 2 planes x 3 comps x NP
-  T* sB1 = sE1 + 2 * 3 * NP;                                 // 1 plane
-  T* sE2 = sB1 + 3 * NP;                                     // 2 planes
+  T* sB1 = sE1 + 2 * 3 * NP;                                 // NB1 planes
+  T* sE2 = sB1 + NB1 * 3 * NP;                               // 2 planes
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -584,6 +590,7 @@ __global__ void __launch_bounds__(NTH, MINB)
       T* E1z = sE1 + PAR * 3 * NP;            // E1(z)
       const T* E1y = sE1 + (1 - PAR) * 3 * NP;  // E1(z-1)
       T* E2y = sE2 + (1 - PAR) * 3 * NP;        // E2(z-1)
+      T* B1p = sB1 + (NB1 == 2 ? PAR : 0) * 3 * NP;  // B1(z-1)
       const T* E2x = sE2 + PAR * 3 * NP;        // E2(z-2)
       constexpr int BC = (TY + 4) * BW, EC = (TY + 3) * BW;  // component strides in the boxes
 #define R(buf, c, idx) buf[(c) * NP + (idx)]
@@ -614,7 +621,7 @@ __global__ void __launch_bounds__(NTH, MINB)
           }
         }
       }
-      __syncthreads();  // E1(z) complete; the B1 plane is free
+      if constexpr (NB1 == 1) __syncthreads();  // the B1 plane is free
       // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem). Points outside
       // the B1 region compute too (their values are never read)
       if (p >= 2 && any) {
@@ -632,9 +639,9 @@ __global__ void __launch_bounds__(NTH, MINB)
           C[h].b1[0] = up ? u0 : v.b0[0];
           C[h].b1[1] = up ? u1 : v.b0[1];
           C[h].b1[2] = up ? u2 : v.b0[2];
-          R(sB1, 0, q) = C[h].b1[0];
-          R(sB1, 1, q) = C[h].b1[1];
-          R(sB1, 2, q) = C[h].b1[2];
+          R(B1p, 0, q) = C[h].b1[0];
+          R(B1p, 1, q) = C[h].b1[1];
+          R(B1p, 2, q) = C[h].b1[2];
         }
       }
       __syncthreads();  // B1(z-1) complete
@@ -651,9 +658,9 @@ __global__ void __launch_bounds__(NTH, MINB)
           const int q = me[h];
           const Pt& v = V[h];
           const bool d0 = (m[h] & 1) && kin, d1 = (m[h] & 2) && kin, d2 = (m[h] & 4) && kz;
-          const T u0 = yee_upd(v.e1[0], ce1, C[h].b1[2] - R(sB1, 2, q - X1), ce2, C[h].b1[1] - v.b1[1]);
-          const T u1 = yee_upd(v.e1[1], ce2, C[h].b1[0] - v.b1[0], ce0, C[h].b1[2] - R(sB1, 2, q - 1));
-          const T u2 = yee_upd(v.e1[2], ce0, C[h].b1[1] - R(sB1, 1, q - 1), ce1, C[h].b1[0] - R(sB1, 0, q - X1));
+          const T u0 = yee_upd(v.e1[0], ce1, C[h].b1[2] - R(B1p, 2, q - X1), ce2, C[h].b1[1] - v.b1[1]);
+          const T u1 = yee_upd(v.e1[1], ce2, C[h].b1[0] - v.b1[0], ce0, C[h].b1[2] - R(B1p, 2, q - 1));
+          const T u2 = yee_upd(v.e1[2], ce0, C[h].b1[1] - R(B1p, 1, q - 1), ce1, C[h].b1[0] - R(B1p, 0, q - X1));
           C[h].e2[0] = d0 ? u0 : v.e1[0];
           C[h].e2[1] = d1 ? u1 : v.e1[1];
           C[h].e2[2] = d2 ? u2 : v.e1[2];
@@ -911,6 +918,7 @@ struct YeeDev {
   CUtensorMap mapB2[2], mapE2[2];
   bool have_maps2 = false;
   int tma_blocks2 = 0;
+  int nb1 = 2;  // B1 buffers of the two-step sweep (SFEEC_YEE_B1=1: the two-barrier form)
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, stage_b, partials;  // host-state staging (e / b), reductions
@@ -1081,10 +1089,16 @@ struct YeeDev {
         if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
       }
     }
-    auto kern = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>>;
-    SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+    const char* e1 = std::getenv("SFEEC_YEE_B1");
+    nb1 = e1 && std::atoi(e1) == 1 ? 1 : 2;
+    using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
+    auto kern1 = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1>;
+    auto kern2 = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2>;
+    auto kern = nb1 == 2 ? kern2 : kern1;
+    const int smem = nb1 == 2 ? Cfg2::kSmem : Cfg::kSmem;
+    SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0, sms = 0;
-    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2<T>, Cfg::kSmem));
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2<T>, smem));
     SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     tma_blocks2 = std::max(1, per_sm) * sms;
     have_maps2 = true;
@@ -1098,9 +1112,16 @@ struct YeeDev {
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
     const int grid = std::min(n_units, tma_blocks2);
-    k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>><<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2>::kSmem, stream>>>(
-        mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
-        ntx, ntx * nty, n_units, kbeg, kend);
+    if (nb1 == 2)
+      k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2>
+          <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>::kSmem, stream>>>(
+              mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
+              kChunk, ntx, ntx * nty, n_units, kbeg, kend);
+    else
+      k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1>
+          <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, 1>::kSmem, stream>>>(
+              mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
+              kChunk, ntx, ntx * nty, n_units, kbeg, kend);
     SFEEC_LAUNCH_CHECK();
     ++launches;
   }

@@ -131,3 +131,31 @@ def test_zero_and_identity_flows():
     y.flow_ha(0.0)
     b, e, _ = y.fetch()
     assert np.array_equal(b, b0) and np.array_equal(e, e0)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_two_step_sweep_one_barrier_form_bitwise(prec):
+    """The default two-step sweep double-buffers the B1 plane and syncs once
+    per plane; SFEEC_YEE_B1=1 is the two-barrier form: bitwise equal, also
+    on the lockstep slab group (ghost planes, chunked boundary/interior)."""
+    import os
+    from tests.test_gpu_delta import layout_env
+    dims, d = (45, 19, 70), (1.0, 0.9, 1.1)
+    rng = np.random.default_rng(5)
+    out = {}
+    for nb1 in ("1", "2"):
+        with layout_env(SFEEC_YEE_B1=nb1):
+            y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
+            y.set_variant(4)
+            if not out:
+                b0, e0 = rng.standard_normal(y.n_faces), rng.standard_normal(y.n_edges)
+            y.load(b0, e0)
+            y.advance(9)
+            g = S.YeeGroup(*dims, *d, 0.25, 2, precision=prec)
+            g.set_variant(4)
+            g.load(b0, e0)
+            g.advance(9)
+            out[nb1] = y.fetch()[:2] + g.fetch()[:2]
+    assert os.environ.get("SFEEC_YEE_B1") is None
+    for a, b in zip(out["1"], out["2"]):
+        assert np.array_equal(a, b)
