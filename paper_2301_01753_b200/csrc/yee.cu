@@ -487,7 +487,51 @@ __device__ __forceinline__ uint32_t e_mask_xy(int i, int j, int n0, int n1) {
 // reason for the barrier between phases 1 and 2 (E1(z-1) neighbours) is
 // already covered by the previous plane's barrier, so each plane needs one
 // barrier instead of two. Same arithmetic, bitwise the same result.
-template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1>
+// ORD = 1 orders the E1-region points so that the TX x TY own tile comes
+// first, one warp per tile row (TX = 32), then the rims the E2, B1 and E1
+// regions add. Phases 2-4 run only on their region's points (the others'
+// values are never read), so the idle rim warps skip them, and the own-point
+// stores are whole 32-wide rows. ORD = 0 is the row-major map over the E1
+// region, every phase on every point. Same point updates either way.
+template <int TX, int TY>
+__device__ __forceinline__ void region_point(int t, int& x, int& y) {
+  constexpr int kOwn = TX * TY;
+  constexpr int kE2 = kOwn + TY + (TX + 1);       // + column TX+1, row TY+1
+  constexpr int kB1 = kE2 + (TY + 2) + (TX + 1);  // + column 0, row 0
+  if (t < kOwn) {
+    x = 1 + t % TX;
+    y = 1 + t / TX;
+  } else if (t < kE2) {
+    const int u = t - kOwn;
+    if (u < TY) {
+      x = TX + 1;
+      y = 1 + u;
+    } else {
+      x = 1 + (u - TY);
+      y = TY + 1;
+    }
+  } else if (t < kB1) {
+    const int u = t - kE2;
+    if (u < TY + 2) {
+      x = 0;
+      y = u;
+    } else {
+      x = 1 + (u - (TY + 2));
+      y = 0;
+    }
+  } else {  // E1 rim: column TX+2 (y 0..TY+2), row TY+2 (x 0..TX+1)
+    const int u = t - kB1;
+    if (u < TY + 3) {
+      x = TX + 2;
+      y = u;
+    } else {
+      x = u - (TY + 3);
+      y = TY + 2;
+    }
+  }
+}
+
+template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1, int ORD = 0>
 __global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
@@ -526,10 +570,15 @@ __global__ void __launch_bounds__(NTH, MINB)
   bool pt[NPT], inB1[NPT], inE2[NPT];
 #pragma unroll
   for (int h = 0; h < NPT; ++h) {
-    me[h] = tid + h * NH;
-    pt[h] = tid < NH && me[h] < NP;
-    xo[h] = me[h] % X1;
-    yo[h] = me[h] / X1;
+    const int t = tid + h * NH;
+    pt[h] = tid < NH && t < NP;
+    if constexpr (ORD == 0) {  // row-major over the E1 region
+      xo[h] = t % X1;
+      yo[h] = t / X1;
+    } else {  // own tile rows, then the E2, B1 and E1 rims (region_point)
+      region_point<TX, TY>(t, xo[h], yo[h]);
+    }
+    me[h] = yo[h] * X1 + xo[h];  // shared-memory index on the E1 region grid
     ob[h] = (yo[h] + 1) * BW + xo[h] + OFF - 1;
     oe[h] = yo[h] * BW + xo[h] + OFF - 1;
     inB1[h] = pt[h] && xo[h] <= TX + 1 && yo[h] <= TY + 1;
@@ -629,7 +678,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         const bool zin = zg >= 0 && zg < n2;
 #pragma unroll
         for (int h = 0; h < NPT; ++h) {
-          if (!pt[h]) continue;
+          if (ORD == 0 ? !pt[h] : !inB1[h]) continue;
           const int q = me[h];
           const bool up = b1up[h] && zin;
           const Pt& v = V[h];
@@ -654,7 +703,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         const bool zw = ze >= k0 && ze < k1;
 #pragma unroll
         for (int h = 0; h < NPT; ++h) {
-          if (!pt[h]) continue;
+          if (ORD == 0 ? !pt[h] : !inE2[h]) continue;
           const int q = me[h];
           const Pt& v = V[h];
           const bool d0 = (m[h] & 1) && kin, d1 = (m[h] & 2) && kin, d2 = (m[h] & 4) && kz;
@@ -919,6 +968,7 @@ struct YeeDev {
   bool have_maps2 = false;
   int tma_blocks2 = 0;
   int nb1 = 2;  // B1 buffers of the two-step sweep (SFEEC_YEE_B1=1: the two-barrier form)
+  int ord = 1;  // tile-first point order (SFEEC_YEE_ORD=0: row-major, every phase on every point)
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, stage_b, partials;  // host-state staging (e / b), reductions
@@ -1091,10 +1141,13 @@ struct YeeDev {
     }
     const char* e1 = std::getenv("SFEEC_YEE_B1");
     nb1 = e1 && std::atoi(e1) == 1 ? 1 : 2;
+    const char* eo = std::getenv("SFEEC_YEE_ORD");
+    ord = eo && std::atoi(eo) == 0 ? 0 : 1;
     using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
-    auto kern1 = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1>;
-    auto kern2 = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2>;
-    auto kern = nb1 == 2 ? kern2 : kern1;
+    auto kern = nb1 == 2 ? (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1>
+                                : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 0>)
+                         : (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 1>
+                                : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 0>);
     const int smem = nb1 == 2 ? Cfg2::kSmem : Cfg::kSmem;
     SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0, sms = 0;
@@ -1112,16 +1165,20 @@ struct YeeDev {
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
     const int grid = std::min(n_units, tma_blocks2);
-    if (nb1 == 2)
-      k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2>
-          <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>::kSmem, stream>>>(
-              mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
-              kChunk, ntx, ntx * nty, n_units, kbeg, kend);
+#define SFEEC_K2(NB1, ORD)                                                                   \
+  k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD>                     \
+      <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream>>>(                \
+          mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),   \
+          kChunk, ntx, ntx * nty, n_units, kbeg, kend)
+    if (nb1 == 2 && ord)
+      SFEEC_K2(2, 1);
+    else if (nb1 == 2)
+      SFEEC_K2(2, 0);
+    else if (ord)
+      SFEEC_K2(1, 1);
     else
-      k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1>
-          <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, 1>::kSmem, stream>>>(
-              mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
-              kChunk, ntx, ntx * nty, n_units, kbeg, kend);
+      SFEEC_K2(1, 0);
+#undef SFEEC_K2
     SFEEC_LAUNCH_CHECK();
     ++launches;
   }

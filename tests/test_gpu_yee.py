@@ -134,17 +134,19 @@ def test_zero_and_identity_flows():
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_two_step_sweep_one_barrier_form_bitwise(prec):
-    """The default two-step sweep double-buffers the B1 plane and syncs once
-    per plane; SFEEC_YEE_B1=1 is the two-barrier form: bitwise equal, also
-    on the lockstep slab group (ghost planes, chunked boundary/interior)."""
+def test_two_step_sweep_forms_bitwise(prec):
+    """Two-step sweep forms: SFEEC_YEE_B1=1 (two barriers per plane, single
+    B1 buffer) or 2 (one barrier, default) x SFEEC_YEE_ORD=0 (row-major
+    points, every phase on every point) or 1 (tile-first order, rim warps
+    skip phases 2-4, default): bitwise equal, on one domain and on the
+    lockstep slab group (ghost planes, chunked boundary/interior)."""
     import os
     from tests.test_gpu_delta import layout_env
     dims, d = (45, 19, 70), (1.0, 0.9, 1.1)
     rng = np.random.default_rng(5)
     out = {}
-    for nb1 in ("1", "2"):
-        with layout_env(SFEEC_YEE_B1=nb1):
+    for form in (("1", "0"), ("2", "0"), ("1", "1"), ("2", "1")):
+        with layout_env(SFEEC_YEE_B1=form[0], SFEEC_YEE_ORD=form[1]):
             y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
             y.set_variant(4)
             if not out:
@@ -155,7 +157,9 @@ def test_two_step_sweep_one_barrier_form_bitwise(prec):
             g.set_variant(4)
             g.load(b0, e0)
             g.advance(9)
-            out[nb1] = y.fetch()[:2] + g.fetch()[:2]
-    assert os.environ.get("SFEEC_YEE_B1") is None
-    for a, b in zip(out["1"], out["2"]):
-        assert np.array_equal(a, b)
+            out[form] = y.fetch()[:2] + g.fetch()[:2]
+    assert os.environ.get("SFEEC_YEE_B1") is None and os.environ.get("SFEEC_YEE_ORD") is None
+    ref = out[("1", "0")]
+    for form, o in out.items():
+        for a, b in zip(ref, o):
+            assert np.array_equal(a, b), form
