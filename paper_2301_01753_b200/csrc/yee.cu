@@ -545,7 +545,9 @@ __global__ void __launch_bounds__(NTH, MINB)
   // through shared memory. Several points per thread amortise the per-plane
   // control (barrier waits, stage and buffer addressing) and add ILP.
   constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, NP = X1 * Y1;
-  constexpr int NH = (NP + NPT - 1) / NPT;
+  // (ORD = 1 rounds the stride up to whole warps, so every h keeps the
+  // one-tile-row-per-warp layout)
+  constexpr int NH = ORD == 0 ? (NP + NPT - 1) / NPT : ((NP + NPT - 1) / NPT + 31) / 32 * 32;
   static_assert(NH <= NTH, "NPT region points per thread");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1060,7 +1062,13 @@ struct YeeDev {
 #define YEE2_NT32 672
 #define YEE2_MB32 1
 #endif
-  static constexpr int kNS2 = 3, kNPT2 = 1;
+#ifndef YEE2_NPT
+#define YEE2_NPT 1
+#endif
+#ifndef YEE2_NS
+#define YEE2_NS 3
+#endif
+  static constexpr int kNS2 = YEE2_NS, kNPT2 = YEE2_NPT;
   template <class T>
   static constexpr int kTY2 = sizeof(T) == 8 ? YEE2_TY64 : YEE2_TY32;
   template <class T>
