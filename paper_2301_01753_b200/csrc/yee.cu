@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <type_traits>
 #include <vector>
@@ -535,7 +536,8 @@ template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 =
 __global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
-                 int n_units, int kbeg, int kend) {
+                 int n_units, int kbeg, int kend, const int4* __restrict__ sched,
+                 const int* __restrict__ cta_ptr) {
   using Cfg = TmaCfg2<T, TX, TY, NS, NB1>;
   constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
   // NPT points of the E1 region (origin (i0-1, j0-1)) per thread: points
@@ -597,10 +599,25 @@ __global__ void __launch_bounds__(NTH, MINB)
   const T ce0 = ck.ce[0], ce1 = ck.ce[1], ce2 = ck.ce[2];
   const T cb0 = ck.cb[0], cb1 = ck.cb[1], cb2 = ck.cb[2];
 
-  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
-    const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
+  // units: (tile, z-chunk) round-robin over the CTAs, or, with a schedule,
+  // the CTA's own list of (tile, k0, k1) (Yee2Sched)
+  const int u_beg = sched ? cta_ptr[blockIdx.x] : (int)blockIdx.x;
+  const int u_end = sched ? cta_ptr[blockIdx.x + 1] : n_units;
+  const int u_step = sched ? 1 : (int)gridDim.x;
+  for (int unit = u_beg; unit < u_end; unit += u_step) {
+    int tile, k0, k1;
+    if (sched) {
+      const int4 w = sched[unit];
+      tile = w.x;
+      k0 = w.y;
+      k1 = w.z;
+    } else {
+      const int chunk = unit / n_tiles;
+      tile = unit - chunk * n_tiles;
+      k0 = kbeg + chunk * kchunk;
+      k1 = min(k0 + kchunk, kend);
+    }
     const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
-    const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
     const int P = k1 - k0 + 4;  // local planes p <-> z = k0 - 2 + p
     uint32_t m[NPT];
     bool b1up[NPT], own[NPT];
@@ -946,6 +963,60 @@ struct Phase {
   double h1, h2;
 };
 
+// Unit schedule of the two-step sweep over planes [kbeg, kend) of `ntiles`
+// tile columns on `ncta` persistent CTAs. A unit over planes [k0, k1) costs
+// k1 - k0 + 4 plane iterations (two halo planes each side), so the
+// round-robin 32-plane chunks spend 4/32 of the sweep on z halos. When there
+// are fewer tile columns than CTAs, each of the first `ntiles` CTAs instead
+// takes the bottom [kbeg, kbeg + Z) of one column in one unit -- all of them
+// march through z together, so x/y neighbours share their halo rows in L2 --
+// and the remaining CTAs take the tops [kbeg + Z, kend), m columns each, with
+// Z chosen so both kinds of CTA run the same number of plane iterations.
+// Otherwise (or for short ranges) it is the round-robin chunking.
+struct Yee2Sched {
+  DevBuf<int4> units;
+  DevBuf<int> cta_ptr;
+  int grid = 0;
+};
+
+inline Yee2Sched make_yee2_sched(int ntiles, int kbeg, int kend, int ncta, int kchunk = 32) {
+  std::vector<int4> u;
+  std::vector<int> ptr(1, 0);
+  const int L = kend - kbeg, R = ncta - ntiles;
+  if (R > 0 && L >= 16) {
+    const int m = (ntiles + R - 1) / R;
+    // Z + 4 = m (L - Z + 4)
+    int Z = (int)std::lround((double)(m * (L + 4) - 4) / (double)(m + 1));
+    Z = std::max(1, std::min(Z, L));
+    for (int t = 0; t < ntiles; ++t) {
+      u.push_back(make_int4(t, kbeg, kbeg + Z, 0));
+      ptr.push_back((int)u.size());
+    }
+    if (Z < L)
+      for (int r = 0; r < R; ++r) {
+        for (int t = r; t < ntiles; t += R) u.push_back(make_int4(t, kbeg + Z, kend, 0));
+        if ((int)u.size() > ptr.back()) ptr.push_back((int)u.size());
+      }
+  } else {
+    const int nch = (L + kchunk - 1) / kchunk, n = ntiles * nch;
+    const int grid = std::max(1, std::min(n, ncta));
+    for (int b = 0; b < grid; ++b) {
+      for (int w = b; w < n; w += grid) {
+        const int c = w / ntiles, t = w - c * ntiles;
+        u.push_back(make_int4(t, kbeg + c * kchunk, std::min(kbeg + (c + 1) * kchunk, kend), 0));
+      }
+      ptr.push_back((int)u.size());
+    }
+  }
+  Yee2Sched s;
+  s.grid = (int)ptr.size() - 1;
+  s.units.alloc(std::max<size_t>(1, u.size()));
+  s.cta_ptr.alloc(ptr.size());
+  SFEEC_CUDA(cudaMemcpy(s.units.p, u.data(), sizeof(int4) * u.size(), cudaMemcpyHostToDevice));
+  SFEEC_CUDA(cudaMemcpy(s.cta_ptr.p, ptr.data(), sizeof(int) * ptr.size(), cudaMemcpyHostToDevice));
+  return s;
+}
+
 struct YeeDev {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -971,6 +1042,15 @@ struct YeeDev {
   int tma_blocks2 = 0;
   int nb1 = 2;  // B1 buffers of the two-step sweep (SFEEC_YEE_B1=1: the two-barrier form)
   int ord = 1;  // tile-first point order (SFEEC_YEE_ORD=0: row-major, every phase on every point)
+  // balanced unit schedule of the two-step sweep (SFEEC_YEE_SCHED=0: round-robin z-chunks)
+  bool sched2 = true;
+  std::map<std::pair<int, int>, Yee2Sched> scheds2;
+  const Yee2Sched& schedule2(int ntiles, int kbeg, int kend) {
+    auto key = std::make_pair(kbeg, kend);
+    auto it = scheds2.find(key);
+    if (it == scheds2.end()) it = scheds2.emplace(key, make_yee2_sched(ntiles, kbeg, kend, tma_blocks2)).first;
+    return it->second;
+  }
   DevBuf<char> buf[2];
   int cur = 0;
   DevBuf<double> stage, stage_b, partials;  // host-state staging (e / b), reductions
@@ -1151,6 +1231,8 @@ struct YeeDev {
     nb1 = e1 && std::atoi(e1) == 1 ? 1 : 2;
     const char* eo = std::getenv("SFEEC_YEE_ORD");
     ord = eo && std::atoi(eo) == 0 ? 0 : 1;
+    const char* es = std::getenv("SFEEC_YEE_SCHED");
+    sched2 = !(es && std::atoi(es) == 0);
     using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
     auto kern = nb1 == 2 ? (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1>
                                 : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 0>)
@@ -1172,12 +1254,14 @@ struct YeeDev {
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY2<T> - 1) / kTY2<T>;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
-    const int grid = std::min(n_units, tma_blocks2);
+    const Yee2Sched* sc = sched2 ? &schedule2(ntx * nty, kbeg, kend) : nullptr;
+    const int grid = sc ? sc->grid : std::min(n_units, tma_blocks2);
 #define SFEEC_K2(NB1, ORD)                                                                   \
   k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD>                     \
       <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream>>>(                \
           mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),   \
-          kChunk, ntx, ntx * nty, n_units, kbeg, kend)
+          kChunk, ntx, ntx * nty, n_units, kbeg, kend, sc ? sc->units.p : nullptr,             \
+          sc ? sc->cta_ptr.p : nullptr)
     if (nb1 == 2 && ord)
       SFEEC_K2(2, 1);
     else if (nb1 == 2)

@@ -138,15 +138,17 @@ def test_two_step_sweep_forms_bitwise(prec):
     """Two-step sweep forms: SFEEC_YEE_B1=1 (two barriers per plane, single
     B1 buffer) or 2 (one barrier, default) x SFEEC_YEE_ORD=0 (row-major
     points, every phase on every point) or 1 (tile-first order, rim warps
-    skip phases 2-4, default): bitwise equal, on one domain and on the
-    lockstep slab group (ghost planes, chunked boundary/interior)."""
+    skip phases 2-4, default) x SFEEC_YEE_SCHED=0 (round-robin z-chunks) or
+    1 (balanced column/top schedule, default): bitwise equal, on one domain
+    and on the lockstep slab group (ghost planes, chunked boundary/interior)."""
     import os
     from tests.test_gpu_delta import layout_env
     dims, d = (45, 19, 70), (1.0, 0.9, 1.1)
     rng = np.random.default_rng(5)
     out = {}
-    for form in (("1", "0"), ("2", "0"), ("1", "1"), ("2", "1")):
-        with layout_env(SFEEC_YEE_B1=form[0], SFEEC_YEE_ORD=form[1]):
+    for form in (("1", "0", "0"), ("2", "0", "0"), ("1", "1", "0"), ("2", "1", "0"),
+                 ("2", "1", "1")):
+        with layout_env(SFEEC_YEE_B1=form[0], SFEEC_YEE_ORD=form[1], SFEEC_YEE_SCHED=form[2]):
             y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
             y.set_variant(4)
             if not out:
@@ -159,7 +161,7 @@ def test_two_step_sweep_forms_bitwise(prec):
             g.advance(9)
             out[form] = y.fetch()[:2] + g.fetch()[:2]
     assert os.environ.get("SFEEC_YEE_B1") is None and os.environ.get("SFEEC_YEE_ORD") is None
-    ref = out[("1", "0")]
+    ref = out[("1", "0", "0")]
     for form, o in out.items():
         for a, b in zip(ref, o):
             assert np.array_equal(a, b), form
