@@ -532,7 +532,8 @@ __device__ __forceinline__ void region_point(int t, int& x, int& y) {
   }
 }
 
-template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1, int ORD = 0>
+template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1, int ORD = 0,
+          int PF1 = 0>
 __global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
@@ -646,12 +647,18 @@ __global__ void __launch_bounds__(NTH, MINB)
     // plane p of the unit (PAR = p & 1 selects the E1/E2 double buffers at
     // compile time): C receives this plane's values, V holds the previous
     // plane's
+    // PF1: plane p+1's TMA issue, stage wait and the own old B / old E of
+    // the stage are done right after plane p's barrier, so those loads are in
+    // flight during phases 3-4 of plane p (pf holds them until phase 1)
+    T pf[NPT][6];
     auto plane = [&](auto par, int p, Pt* C, const Pt* V) {
       constexpr int PAR = decltype(par)::value;
-      if (tid == 0 && p + D < P) issue(p + D);
       const uint32_t gc = gplane + p;
       const int st = gc % NS;
-      mbar_wait(&bars[st], (gc / NS) & 1);
+      if (!PF1 || p == 0) {
+        if (tid == 0 && p + D < P) issue(p + D);
+        mbar_wait(&bars[st], (gc / NS) & 1);
+      }
       const int z = k0 - 2 + p;
       const T* __restrict__ B0c = reinterpret_cast<const T*>(base + st * Cfg::kStage);
       const T* __restrict__ E0c = reinterpret_cast<const T*>(base + st * Cfg::kStage + Cfg::kBStride);
@@ -671,12 +678,19 @@ __global__ void __launch_bounds__(NTH, MINB)
         for (int h = 0; h < NPT; ++h) {
           if (!pt[h]) continue;
           const T* b = B0c + ob[h];
-          C[h].b0[0] = b[0];
-          C[h].b0[1] = b[BC];
-          C[h].b0[2] = b[2 * BC];
+          if (PF1 && p > 0) {
+            C[h].b0[0] = pf[h][0];
+            C[h].b0[1] = pf[h][1];
+            C[h].b0[2] = pf[h][2];
+          } else {
+            C[h].b0[0] = b[0];
+            C[h].b0[1] = b[BC];
+            C[h].b0[2] = b[2 * BC];
+          }
           if (p >= 1) {
             const T* e = E0c + oe[h];
-            const T e0 = e[0], e1 = e[EC], e2 = e[2 * EC];
+            const T e0 = PF1 ? pf[h][3] : e[0], e1 = PF1 ? pf[h][4] : e[EC],
+                    e2 = PF1 ? pf[h][5] : e[2 * EC];
             const T u0 = yee_upd(e0, ce1, C[h].b0[2] - b[2 * BC - BW], ce2, C[h].b0[1] - V[h].b0[1]);
             const T u1 = yee_upd(e1, ce2, C[h].b0[0] - V[h].b0[0], ce0, C[h].b0[2] - b[2 * BC - 1]);
             const T u2 = yee_upd(e2, ce0, C[h].b0[1] - b[BC - 1], ce1, C[h].b0[0] - b[-BW]);
@@ -713,6 +727,28 @@ __global__ void __launch_bounds__(NTH, MINB)
         }
       }
       __syncthreads();  // B1(z-1) complete
+      if constexpr (PF1) {
+        if (p + 1 < P) {
+          if (tid == 0 && p + 1 + D < P) issue(p + 1 + D);
+          const uint32_t gn = gc + 1;
+          const int sn = gn % NS;
+          mbar_wait(&bars[sn], (gn / NS) & 1);
+          const T* B0n = reinterpret_cast<const T*>(base + sn * Cfg::kStage);
+          const T* E0n = reinterpret_cast<const T*>(base + sn * Cfg::kStage + Cfg::kBStride);
+#pragma unroll
+          for (int h = 0; h < NPT; ++h) {
+            if (!pt[h]) continue;
+            const T* b = B0n + ob[h];
+            pf[h][0] = b[0];
+            pf[h][1] = b[BC];
+            pf[h][2] = b[2 * BC];
+            const T* e = E0n + oe[h];
+            pf[h][3] = e[0];
+            pf[h][4] = e[EC];
+            pf[h][5] = e[2 * EC];
+          }
+        }
+      }
       // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem); points outside
       // the E2 region compute too (never read)
       if (p >= 3 && any) {
@@ -1042,6 +1078,8 @@ struct YeeDev {
   int tma_blocks2 = 0;
   int nb1 = 2;  // B1 buffers of the two-step sweep (SFEEC_YEE_B1=1: the two-barrier form)
   int ord = 1;  // tile-first point order (SFEEC_YEE_ORD=0: row-major, every phase on every point)
+  // stage prefetch one plane ahead (SFEEC_YEE_PF1=1; needs nb1 = 2, ord = 1)
+  bool pf1 = false;
   // balanced unit schedule of the two-step sweep (SFEEC_YEE_SCHED=0: round-robin z-chunks)
   bool sched2 = true;
   std::map<std::pair<int, int>, Yee2Sched> scheds2;
@@ -1234,7 +1272,10 @@ struct YeeDev {
     const char* es = std::getenv("SFEEC_YEE_SCHED");
     sched2 = !(es && std::atoi(es) == 0);
     using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
-    auto kern = nb1 == 2 ? (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1>
+    const char* ep = std::getenv("SFEEC_YEE_PF1");
+    pf1 = ep && std::atoi(ep) == 1 && nb1 == 2 && ord;
+    auto kern = pf1 ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1, 1>
+              : nb1 == 2 ? (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1>
                                 : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 0>)
                          : (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 1>
                                 : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 0>);
@@ -1256,20 +1297,22 @@ struct YeeDev {
     const int n_units = ntx * nty * nchunks;
     const Yee2Sched* sc = sched2 ? &schedule2(ntx * nty, kbeg, kend) : nullptr;
     const int grid = sc ? sc->grid : std::min(n_units, tma_blocks2);
-#define SFEEC_K2(NB1, ORD)                                                                   \
-  k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD>                     \
+#define SFEEC_K2(NB1, ORD, PF)                                                               \
+  k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD, PF>                 \
       <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream>>>(                \
           mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),   \
           kChunk, ntx, ntx * nty, n_units, kbeg, kend, sc ? sc->units.p : nullptr,             \
           sc ? sc->cta_ptr.p : nullptr)
-    if (nb1 == 2 && ord)
-      SFEEC_K2(2, 1);
+    if (pf1)
+      SFEEC_K2(2, 1, 1);
+    else if (nb1 == 2 && ord)
+      SFEEC_K2(2, 1, 0);
     else if (nb1 == 2)
-      SFEEC_K2(2, 0);
+      SFEEC_K2(2, 0, 0);
     else if (ord)
-      SFEEC_K2(1, 1);
+      SFEEC_K2(1, 1, 0);
     else
-      SFEEC_K2(1, 0);
+      SFEEC_K2(1, 0, 0);
 #undef SFEEC_K2
     SFEEC_LAUNCH_CHECK();
     ++launches;

@@ -147,8 +147,9 @@ def test_two_step_sweep_forms_bitwise(prec):
     rng = np.random.default_rng(5)
     out = {}
     for form in (("1", "0", "0"), ("2", "0", "0"), ("1", "1", "0"), ("2", "1", "0"),
-                 ("2", "1", "1")):
-        with layout_env(SFEEC_YEE_B1=form[0], SFEEC_YEE_ORD=form[1], SFEEC_YEE_SCHED=form[2]):
+                 ("2", "1", "1"), ("2", "1", "1", "1")):
+        with layout_env(SFEEC_YEE_B1=form[0], SFEEC_YEE_ORD=form[1], SFEEC_YEE_SCHED=form[2],
+                        SFEEC_YEE_PF1=form[3] if len(form) > 3 else "0"):
             y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
             y.set_variant(4)
             if not out:
@@ -161,6 +162,7 @@ def test_two_step_sweep_forms_bitwise(prec):
             g.advance(9)
             out[form] = y.fetch()[:2] + g.fetch()[:2]
     assert os.environ.get("SFEEC_YEE_B1") is None and os.environ.get("SFEEC_YEE_ORD") is None
+    assert os.environ.get("SFEEC_YEE_PF1") is None
     ref = out[("1", "0", "0")]
     for form, o in out.items():
         for a, b in zip(ref, o):
