@@ -704,8 +704,8 @@ __global__ void __launch_bounds__(NTH, MINB)
         }
       }
       if constexpr (NB1 == 1) __syncthreads();  // the B1 plane is free
-      // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem). Points outside
-      // the B1 region compute too (their values are never read)
+      // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem). With ORD = 0
+      // points outside the B1 region compute too (their values are never read)
       if (p >= 2 && any) {
         const int zg = z - 1 + g.kofs;
         const bool zin = zg >= 0 && zg < n2;
@@ -749,8 +749,8 @@ __global__ void __launch_bounds__(NTH, MINB)
           }
         }
       }
-      // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem); points outside
-      // the E2 region compute too (never read)
+      // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem); with ORD = 0
+      // points outside the E2 region compute too (never read)
       if (p >= 3 && any) {
         const int ze = z - 1;
         const int zg = ze + g.kofs;
