@@ -1105,10 +1105,23 @@ struct YeeDev {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;  // overlapped halo exchange
   cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
+  // host-state copies: a copy stream, so one vector's scatter / gather runs
+  // while the other crosses PCIe
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_cp[3] = {nullptr, nullptr, nullptr};
+
+  void make_copy_stream() {
+    if (copy_stream) return;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ev_cp) SFEEC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
 
   ~YeeDev() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev_cp)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_bnd) cudaEventDestroy(ev_bnd);
     if (ev_xch) cudaEventDestroy(ev_xch);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -1553,12 +1566,16 @@ struct YeeDev {
   }
 
   // device scatter of the (b, e) DOF vectors (already in `stage` buffers)
-  void set_state_dev(const double* b_dev, const double* e_dev) {
+  // (ready_b / ready_e: optional events the b / e staging copies record)
+  void set_state_dev(const double* b_dev, const double* e_dev, cudaEvent_t ready_b = nullptr,
+                     cudaEvent_t ready_e = nullptr) {
     buf[0].zero(stream);
     buf[1].zero(stream);
     cur = 0;
-    for (int face = 0; face < 2; ++face) {
+    for (int face = 1; face >= 0; --face) {
       const int64_t n = face ? n_faces : n_edges;
+      const cudaEvent_t ready = face ? ready_b : ready_e;
+      if (ready) SFEEC_CUDA(cudaStreamWaitEvent(stream, ready, 0));
       if (!n) continue;
       unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
       // both ping-pong buffers: the fused sweep never rewrites the constant
@@ -1579,11 +1596,18 @@ struct YeeDev {
     // persistent staging: no allocation on the host-state path
     if (stage_b.n < (size_t)std::max<int64_t>(1, n_faces))
       stage_b.alloc((size_t)std::max<int64_t>(1, n_faces));
+    make_copy_stream();
+    // b then e over PCIe on the copy stream; the buffer clears and b's scatter
+    // run on the compute stream while e is still crossing
+    SFEEC_CUDA(cudaEventRecord(ev_cp[2], stream));  // earlier work on the stage buffers
+    SFEEC_CUDA(cudaStreamWaitEvent(copy_stream, ev_cp[2], 0));
     SFEEC_CUDA(cudaMemcpyAsync(stage_b.p, b, sizeof(double) * (size_t)n_faces,
-                               cudaMemcpyHostToDevice, stream));
+                               cudaMemcpyHostToDevice, copy_stream));
+    SFEEC_CUDA(cudaEventRecord(ev_cp[0], copy_stream));
     SFEEC_CUDA(cudaMemcpyAsync(stage.p, e, sizeof(double) * (size_t)n_edges,
-                               cudaMemcpyHostToDevice, stream));
-    set_state_dev(stage_b.p, stage.p);
+                               cudaMemcpyHostToDevice, copy_stream));
+    SFEEC_CUDA(cudaEventRecord(ev_cp[1], copy_stream));
+    set_state_dev(stage_b.p, stage.p, ev_cp[0], ev_cp[1]);
     // ghosts of both buffers: exchange once per buffer
     exchange_nccl();
     cur ^= 1;
@@ -1593,19 +1617,28 @@ struct YeeDev {
   }
 
   void get_state(double* b, double* e) {
+    // e gathered into `stage`, b into `stage_b`: b's gather runs while e
+    // crosses PCIe on the copy stream
+    if (stage_b.n < (size_t)std::max<int64_t>(1, n_faces))
+      stage_b.alloc((size_t)std::max<int64_t>(1, n_faces));
+    make_copy_stream();
     for (int face = 0; face < 2; ++face) {
       double* dst = face ? b : e;
       const int64_t n = face ? n_faces : n_edges;
       if (!dst || !n) continue;
+      double* st = face ? stage_b.p : stage.p;
       unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
       if (prec == 8)
-        k_gather<double><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<double>(cur));
+        k_gather<double><<<blocks, 256, 0, stream>>>(g, face, st, n, fields<double>(cur));
       else
-        k_gather<float><<<blocks, 256, 0, stream>>>(g, face, stage.p, n, fields<float>(cur));
+        k_gather<float><<<blocks, 256, 0, stream>>>(g, face, st, n, fields<float>(cur));
       SFEEC_LAUNCH_CHECK();
-      SFEEC_CUDA(cudaMemcpyAsync(dst, stage.p, sizeof(double) * (size_t)n,
-                                 cudaMemcpyDeviceToHost, stream));
+      SFEEC_CUDA(cudaEventRecord(ev_cp[face], stream));
+      SFEEC_CUDA(cudaStreamWaitEvent(copy_stream, ev_cp[face], 0));
+      SFEEC_CUDA(cudaMemcpyAsync(dst, st, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
+                                 copy_stream));
     }
+    SFEEC_CUDA(cudaStreamSynchronize(copy_stream));
     SFEEC_CUDA(cudaStreamSynchronize(stream));
   }
 

@@ -31,3 +31,18 @@ for rep in range(3):
     print(f"set_state {1e3*(t1-t0):.2f} ms  advance({k}) {1e3*(t2-t1):.2f} ms  "
           f"get_state {1e3*(t3-t2):.2f} ms  total {1e3*(t3-t0):.2f} ms  "
           f"bytes each way {8*(R.b0.size+R.e0.size)/1e6:.0f} MB", flush=True)
+# PCIe ceiling: plain pinned copies of the same byte count
+nbytes = 8 * (R.b0.size + R.e0.size)
+h = torch.empty(nbytes // 8, dtype=torch.float64).pin_memory()
+d = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    h.copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"plain H2D {1e3*(t1-t0):.2f} ms ({nbytes/(t1-t0)/1e9:.1f} GB/s)  "
+          f"D2H {1e3*(t2-t1):.2f} ms ({nbytes/(t2-t1)/1e9:.1f} GB/s)", flush=True)
