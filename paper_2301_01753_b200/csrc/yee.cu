@@ -51,15 +51,27 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// One curl update x + (c1*d1 - c2*d2) with the rounding pinned (one mul, one
-// fma, one add), so every Yee kernel (one-step, fused, two-step) produces
-// bitwise the same point values whatever the compiler would contract.
+// One curl update x + c1*d1 - c2*d2 with the rounding pinned, so every Yee
+// kernel (one-step, fused, two-step) produces bitwise the same point values
+// whatever the compiler would contract.
+#ifndef YEE_UPD_MUL
+// two chained FMAs, x + c1 d1 - c2 d2 = fma(c1, d1, fma(-c2, d2, x)): two
+// FP64 operations and two dependent latencies per update
+__device__ __forceinline__ double yee_upd(double x, double c1, double d1, double c2, double d2) {
+  return __fma_rn(c1, d1, __fma_rn(-c2, d2, x));
+}
+__device__ __forceinline__ float yee_upd(float x, float c1, float d1, float c2, float d2) {
+  return __fmaf_rn(c1, d1, __fmaf_rn(-c2, d2, x));
+}
+#else
+// previous form: x + (c1 d1 - c2 d2), one mul, one fma, one add
 __device__ __forceinline__ double yee_upd(double x, double c1, double d1, double c2, double d2) {
   return __dadd_rn(x, __fma_rn(c1, d1, -__dmul_rn(c2, d2)));
 }
 __device__ __forceinline__ float yee_upd(float x, float c1, float d1, float c2, float d2) {
   return __fadd_rn(x, __fmaf_rn(c1, d1, -__fmul_rn(c2, d2)));
 }
+#endif
 
 // DOF masks (PEC), yee_layout.hpp. k is the local storage plane; the masks
 // are evaluated at the global plane k + kofs, and only owned planes count.
