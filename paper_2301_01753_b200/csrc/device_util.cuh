@@ -20,6 +20,37 @@ namespace sfeec_b200 {
 
 #define SFEEC_LAUNCH_CHECK() SFEEC_CUDA(cudaGetLastError())
 
+// Programmatic dependent launch (PDL). A kernel launched with launch_pdl may
+// start while the previous kernel in the stream is still finishing: it runs
+// its prologue (barrier init, index math), then pdl_wait() blocks until the
+// previous grid has completed and its writes are visible. pdl_trigger() lets
+// the next PDL kernel be scheduled once every CTA of this grid has issued it
+// (or exited). Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SFEEC_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // One CTA-resident persistent grid worth of blocks for grid-stride kernels:
 // 148 SMs x 8.
 constexpr int kReduceBlocks = 148 * 8;

@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // still in L2, come first); every row's arithmetic is unchanged
   const int64_t last = n_slices - 1;
   SliceMeta m = load_meta(srow, sptr, sw, rev ? last - s : s);
+  pdl_wait();  // PDL: x and y come from the previous kernels
+  pdl_trigger();
   while (true) {
     const int64_t sn = s + nwarps;
     SliceMeta mn;
@@ -441,7 +443,6 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= rows) return;
   const int64_t r = rev ? rows - 1 - g : g;  // rev: descending rows (see k_sell_pipe)
-  const double y0 = ACC ? y[r] : 0.0;
   const uint64_t pol = gather_policy<PF>();
   int32_t p[W];
   double v[W], xv[W];
@@ -450,6 +451,11 @@ __global__ void __launch_bounds__(kThreads)
     p[k] = ld_stream<PF>(col + (int64_t)k * rows + r);
     if (!SIGNED) v[k] = ld_stream<PF>(val + (int64_t)k * rows + r);
   }
+  // PDL: the operator stream above does not depend on the previous kernel;
+  // x and y do (no-ops without a programmatic launch)
+  pdl_wait();
+  pdl_trigger();
+  const double y0 = ACC ? y[r] : 0.0;
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     if (SIGNED)
@@ -1416,6 +1422,15 @@ static void launch_delta(const DevOperator& a, const double* x, double* y, doubl
 // SFEEC_L2PF: L2 hints in k_ell and the default k_sell_pipe: bits 0-1 the
 // prefetch size of the operator streams (1 = 128 B, 2 = 256 B), bit 2 an
 // evict_last policy on the gathered x (valid: 0, 1, 2, 4, 6); results unchanged
+// k_ell and k_sell_pipe are launched as programmatic dependents
+// (device_util.cuh), so each one's launch and operator prefetch overlap the
+// previous kernel's tail; results unchanged. Measured: tet16 (launch-bound)
+// 0.0109 -> 0.0090 ms/step, tet128 +0.3%. SFEEC_PDL=0 turns it off.
+static bool pdl_enabled() {
+  const char* e = std::getenv("SFEEC_PDL");
+  return !(e && std::atoi(e) == 0);
+}
+
 static int l2_prefetch_size() {
   const char* e = std::getenv("SFEEC_L2PF");
   return e ? std::atoi(e) : 0;
@@ -1425,6 +1440,7 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
                  bool accumulate, cudaStream_t s, bool reverse) {
   const int rev = reverse ? 1 : 0;  // k_ell / k_sell_pipe only; the others ignore it
   const int l2pf = l2_prefetch_size();  // k_ell / k_sell_pipe streaming-load hint
+  const bool pdl = pdl_enabled();        // k_ell / k_sell_pipe programmatic launches
   if (a.rows == 0) return;
   if (a.nnz == 0) {
     if (!accumulate) SFEEC_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)a.rows, s));
@@ -1448,14 +1464,14 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
 #define SFEEC_ELL_PF(W, PF)                                                                   \
   if (sg) {                                                                                  \
     if (accumulate)                                                                          \
-      k_ell<true, true, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
+      launch_pdl(pdl, k_ell<true, true, W, PF>, dim3(g), dim3(kThreads), 0, s, a.rows, a.sell_col.p, (const double*)nullptr, a.scale, x, y, alpha, rev); \
     else                                                                                     \
-      k_ell<false, true, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, nullptr, a.scale, x, y, alpha, rev); \
+      launch_pdl(pdl, k_ell<false, true, W, PF>, dim3(g), dim3(kThreads), 0, s, a.rows, a.sell_col.p, (const double*)nullptr, a.scale, x, y, alpha, rev); \
   } else {                                                                                   \
     if (accumulate)                                                                          \
-      k_ell<true, false, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
+      launch_pdl(pdl, k_ell<true, false, W, PF>, dim3(g), dim3(kThreads), 0, s, a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
     else                                                                                     \
-      k_ell<false, false, W, PF><<<g, kThreads, 0, s>>>(a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
+      launch_pdl(pdl, k_ell<false, false, W, PF>, dim3(g), dim3(kThreads), 0, s, a.rows, a.sell_col.p, a.sell_val.p, 1.0, x, y, alpha, rev); \
   }
 #define SFEEC_ELL_W(W)                                                                       \
   case W:                                                                                    \
@@ -1562,11 +1578,11 @@ void launch_spmv(const DevOperator& a, const double* x, double* y, double alpha,
   do {                                                                                            \
     const unsigned g9 = (unsigned)std::min<int64_t>(blocks_for(a.n_slices * 32), 148 * MB);       \
     if (accumulate)                                                                               \
-      k_sell_pipe<true, CH, MB, PF><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,            \
-          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);              \
+      launch_pdl(pdl, k_sell_pipe<true, CH, MB, PF>, dim3(g9), dim3(kThreads), 0, s, a.n_slices,  \
+          a.slice_row.p, a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev); \
     else                                                                                          \
-      k_sell_pipe<false, CH, MB, PF><<<g9, kThreads, 0, s>>>(a.n_slices, a.slice_row.p,           \
-          a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev);              \
+      launch_pdl(pdl, k_sell_pipe<false, CH, MB, PF>, dim3(g9), dim3(kThreads), 0, s, a.n_slices, \
+          a.slice_row.p, a.slice_ptr.p, a.slice_w.p, a.sell_col.p, a.sell_val.p, x, y, alpha, rev); \
   } while (0)
 #define SFEEC_PIPE(CH, MB) SFEEC_PIPE_PF(CH, MB, 0)
         if (variant == 10)

@@ -602,6 +602,10 @@ __global__ void __launch_bounds__(NTH, MINB)
     inE2[h] = pt[h] && xo[h] >= 1 && xo[h] <= TX + 1 && yo[h] >= 1 && yo[h] <= TY + 1;
   }
   const bool any = pt[0];  // point 0 exists whenever any does
+  // PDL: everything above is prologue; the previous sweep's output is read
+  // from here on (a no-op without a programmatic launch)
+  pdl_wait();
+  pdl_trigger();
 
   // per-point state of one plane: E1, B1, E2 and the old B (B0). Two sets
   // ping-pong (cur/prev) through a 2x unrolled plane loop, so no register
@@ -1092,6 +1096,8 @@ struct YeeDev {
   int ord = 1;  // tile-first point order (SFEEC_YEE_ORD=0: row-major, every phase on every point)
   // stage prefetch one plane ahead (SFEEC_YEE_PF1=1; needs nb1 = 2, ord = 1)
   bool pf1 = false;
+  // programmatic dependent launch of the two-step sweeps (SFEEC_PDL=0: off)
+  bool pdl = true;
   // balanced unit schedule of the two-step sweep (SFEEC_YEE_SCHED=0: round-robin z-chunks)
   bool sched2 = true;
   std::map<std::pair<int, int>, Yee2Sched> scheds2;
@@ -1296,6 +1302,8 @@ struct YeeDev {
     ord = eo && std::atoi(eo) == 0 ? 0 : 1;
     const char* es = std::getenv("SFEEC_YEE_SCHED");
     sched2 = !(es && std::atoi(es) == 0);
+    const char* epd = std::getenv("SFEEC_PDL");
+    pdl = !(epd && std::atoi(epd) == 0);
     using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
     const char* ep = std::getenv("SFEEC_YEE_PF1");
     pf1 = ep && std::atoi(ep) == 1 && nb1 == 2 && ord;
@@ -1323,11 +1331,11 @@ struct YeeDev {
     const Yee2Sched* sc = sched2 ? &schedule2(ntx * nty, kbeg, kend) : nullptr;
     const int grid = sc ? sc->grid : std::min(n_units, tma_blocks2);
 #define SFEEC_K2(NB1, ORD, PF)                                                               \
-  k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD, PF>                 \
-      <<<grid, kNT2<T>, TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream>>>(                \
-          mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),   \
-          kChunk, ntx, ntx * nty, n_units, kbeg, kend, sc ? sc->units.p : nullptr,             \
-          sc ? sc->cta_ptr.p : nullptr)
+  launch_pdl(pdl, k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD, PF>, \
+             dim3(grid), dim3(kNT2<T>), TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream,   \
+             mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1),                                  \
+             coef<T>(h_e / (eps0 * mu0), h_b), kChunk, ntx, ntx * nty, n_units, kbeg, kend,  \
+             sc ? sc->units.p : nullptr, sc ? sc->cta_ptr.p : nullptr)
     if (pf1)
       SFEEC_K2(2, 1, 1);
     else if (nb1 == 2 && ord)

@@ -63,3 +63,20 @@ def test_l2_prefetch_size_hint_bitwise(pf):
     for o, r in zip(out, ref):
         assert np.array_equal(o, r)
     assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_programmatic_dependent_launch_bitwise(graphs):
+    """SFEEC_PDL=1 launches k_ell / k_sell_pipe as programmatic dependents
+    (prologue and operator loads overlap the previous kernel's tail, data
+    reads after griddepcontrol.wait): the same steps, with and without the
+    CUDA-graph replay."""
+    rng = np.random.default_rng(11)
+    with layout_env(SFEEC_GRAPHS=graphs):
+        s = S.tet_device_scheme(16, 0.1, 3, dt=0.01)
+        st = S.make_state(S.Formulation.BE, rng.standard_normal(s._n2), rng.standard_normal(s._n1))
+        a = s.advance(st, 70)
+        with layout_env(SFEEC_PDL=1):
+            s2 = S.tet_device_scheme(16, 0.1, 3, dt=0.01)
+            b = s2.advance(st, 70)
+    assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)

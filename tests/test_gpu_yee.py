@@ -167,3 +167,23 @@ def test_two_step_sweep_forms_bitwise(prec):
     for form, o in out.items():
         for a, b in zip(ref, o):
             assert np.array_equal(a, b), form
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_two_step_sweep_pdl_bitwise(prec):
+    """SFEEC_PDL=1: back-to-back two-step sweeps as programmatic dependent
+    launches (each waits on griddepcontrol before its first TMA load)."""
+    from tests.test_gpu_delta import layout_env
+    dims, d = (45, 19, 70), (1.0, 0.9, 1.1)
+    rng = np.random.default_rng(9)
+    out = []
+    for pdl in ("0", "1"):  # off, on (the default)
+        with layout_env(SFEEC_PDL=pdl):
+            y = S.YeeScheme(*dims, *d, 0.25, bc=L.BC_PEC, precision=prec)
+            y.set_variant(4)
+            if not out:
+                b0, e0 = rng.standard_normal(y.n_faces), rng.standard_normal(y.n_edges)
+            y.load(b0, e0)
+            y.advance(23)
+            out.append(y.fetch()[:2])
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
