@@ -129,10 +129,6 @@ int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e);
 int64_t sfeec_dev_last_launches(sfeec_dev* h);
 /* algorithmic HBM bytes of one merged leapfrog step */
 double sfeec_dev_step_bytes(sfeec_dev* h);
-/* which leapfrog half-steps run as one fused wavefront kernel (wave.cu):
- * bit 0 He (K-Q + K-Cb), bit 1 Ha (K-M2 + K-CTe); 0 with SFEEC_WAVE=0, in
- * strict mode, the AE formulation or unsupported operator layouts */
-int sfeec_dev_fused(sfeec_dev* h);
 /* change dt (the scheme is otherwise unchanged; the cached CFL number is
  * rescaled) -- used to set dt = 0.5 * dt_CFL after sfeec_dev_cfl_number */
 int sfeec_dev_set_dt(sfeec_dev* h, double dt);
@@ -327,9 +323,8 @@ int sfeec_p2_spai_device(const sfeec_csr* m1, int device, sfeec_csr_owned* q, in
  * setup path for 128^3 / 256^3 (configs 3, 5). */
 /* layout flags for sfeec_tet_dev_create. Default: the sliced / ELL layouts
  * built on the device. HOST_LAYOUT: the same layouts built through the host
- * (the sfeec_dev_create path). STENCIL_LAYOUT: column ids recomputed from the
- * Kuhn stencil, values-only streams (stencil.cuh; fewer bytes but a longer
- * latency chain -- measured slower, kept for reference) */
+ * (the sfeec_dev_create path). STENCIL_LAYOUT (16) is rejected (the
+ * table-driven stencil layout was measured slower and removed). */
 enum { SFEEC_TET_HOST_LAYOUT = 8, SFEEC_TET_STENCIL_LAYOUT = 16 };
 int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                          int split_kind, int device, int flags, int with_div, sfeec_dev** out,
@@ -339,10 +334,8 @@ int sfeec_tet_dev_operators(int n, double jitter, uint64_t seed, int device, sfe
                             sfeec_csr_owned* m2, sfeec_csr_owned* d, sfeec_csr_owned* q_sym,
                             sfeec_csr_owned* ct);
 /* device layout of a resident operator (0 Q_sym, 1 C, 2 C^T, 3 M2, 4 D):
- * info[9] = {layout (0 CSR, 1 signed, 2 fp64 values, 3 stencil), column-delta
- * form, ELL, slices (ELL: 32-row groups), slices kept at int32 columns,
- * stored entries incl. padding, nnz, windowed (shared-memory staged x),
- * window units}; *bytes = what one application streams
+ * info[9] = {layout (0 CSR, 1 signed, 2 fp64 values), 0, ELL, slices (ELL:
+ * 32-row groups), 0, stored entries incl. padding, nnz, 0, 0}; *bytes = what one application streams
  * from the operator arrays in this layout (the algorithmic count of SURVEY.md
  * 8(d) stays 12 B / nonzero whatever the layout). No reference counterpart. */
 int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes);

@@ -82,7 +82,6 @@ _SIGS = {
     "sfeec_dev_state_device_ptrs": (C.c_int, [_P, C.POINTER(_PD), C.POINTER(_PD)]),
     "sfeec_dev_last_launches": (C.c_int64, [_P]),
     "sfeec_dev_step_bytes": (C.c_double, [_P]),
-    "sfeec_dev_fused": (C.c_int, [_P]),
     "sfeec_dev_layout_info": (C.c_int, [_P, C.c_int, _PI64, _PD]),
     "sfeec_dev_set_dt": (C.c_int, [_P, C.c_double]),
     "sfeec_dev_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64, _PD]),

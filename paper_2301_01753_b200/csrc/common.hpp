@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -18,6 +19,13 @@ struct Error : std::runtime_error {
 };
 
 void set_error(const std::string& msg);
+
+// Boolean environment switch: unset -> dflt, "0" -> false, anything else true.
+// Read once when a handle is created, never per launch.
+inline bool env_flag(const char* name, bool dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) != 0 : dflt;
+}
 
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(SFEEC_EINVAL, msg);

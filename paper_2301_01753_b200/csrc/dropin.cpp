@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 
 #include "common.hpp"
 #include "sfeec/dynamics.hpp"
@@ -296,43 +297,82 @@ FieldState make_state(Formulation f, std::vector<double> first, std::vector<doub
   return s;
 }
 
-// dynamics.cpp:145-185 restated over the device step
+namespace {
+// `copies` copies of `a` on the diagonal, as an int64 C-ABI view
+struct BlockDiag {
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  std::vector<double> v;
+  sfeec_csr view;
+  BlockDiag(const SparseOperator& a, int copies) {
+    const int64_t nnz = (int64_t)a.val.size();
+    rp.resize((size_t)a.rows * copies + 1);
+    ci.resize((size_t)(nnz * copies));
+    v.resize((size_t)(nnz * copies));
+    rp[0] = 0;
+    for (int b = 0; b < copies; ++b) {
+      const int64_t off = nnz * b;
+      for (int r = 0; r < a.rows; ++r) rp[(size_t)b * a.rows + r + 1] = off + a.row_ptr[r + 1];
+      for (int64_t k = 0; k < nnz; ++k) {
+        ci[(size_t)(off + k)] = a.col_idx[(size_t)k] + b * a.cols;
+        v[(size_t)(off + k)] = a.val[(size_t)k];
+      }
+    }
+    view.rows = (int64_t)a.rows * copies;
+    view.cols = (int64_t)a.cols * copies;
+    view.row_ptr = rp.data();
+    view.col_idx = ci.data();
+    view.val = v.data();
+  }
+};
+}  // namespace
+
+// Symplecticity of the one-step map Phi (the property of dynamics.cpp:145-185):
+// max |Phi^T J Phi - J| with J = (1/eps0) [[0, -I], [I, 0]] on (a, e).
+// Phi is taken in one device pass: the 2 n1 unit initial states are the
+// diagonal blocks of one block-diagonal system, advanced together by one
+// resident step; then with Phi = [A; E] (A the a-rows, E the e-rows),
+// Phi^T J Phi = (1/eps0) (P - P^T) for P = E^T A.
 double symplectic_check(const SplitScheme& scheme, int n1, int max_dofs) {
   if (2 * n1 > max_dofs)
     throw InvalidParameter("symplectic_check: system too large for the dense check");
-  const int n2 = 2 * n1;
-  std::vector<std::vector<double>> phi((size_t)n2);
-  for (int j = 0; j < n2; ++j) {
-    FieldState s;
-    s.formulation = Formulation::AE;
-    s.first.assign((size_t)n1, 0.0);
-    s.e.assign((size_t)n1, 0.0);
-    if (j < n1)
-      s.first[(size_t)j] = 1.0;
-    else
-      s.e[(size_t)(j - n1)] = 1.0;
-    FieldState t = scheme.step(s);
-    auto& col = phi[(size_t)j];
-    col.resize((size_t)n2);
-    for (int i = 0; i < n1; ++i) col[(size_t)i] = t.first[(size_t)i];
-    for (int i = 0; i < n1; ++i) col[(size_t)(n1 + i)] = t.e[(size_t)i];
+  if (n1 != scheme.q_sym().rows)
+    throw InvalidParameter("symplectic_check: n1 must equal the 1-form dimension");
+  const int m = 2 * n1;  // columns of Phi = batch size
+  BlockDiag q(scheme.q_sym(), m), c(scheme.curl(), m), m2(scheme.m2(), m);
+  sfeec_dev* h = nullptr;
+  check(sfeec_dev_create(&q.view, &c.view, &m2.view, nullptr, scheme.dt(), scheme.units().eps0,
+                         scheme.units().mu0,
+                         scheme.kind() == SplitKind::Strang ? SFEEC_SPLIT_STRANG
+                                                            : SFEEC_SPLIT_LIE_TROTTER,
+                         SFEEC_FORM_AE, 0, SFEEC_Q_IS_SYMMETRIC | SFEEC_NO_CFL_WARN, &h));
+  std::unique_ptr<sfeec_dev, void (*)(sfeec_dev*)> guard(h, sfeec_dev_destroy);
+  // batch b starts from unit vector b of (a, e): a-part for b < n1, e-part after
+  const size_t nb = (size_t)n1 * (size_t)m;
+  std::vector<double> a(nb, 0.0), e(nb, 0.0);
+  for (int b = 0; b < m; ++b) (b < n1 ? a : e)[(size_t)b * n1 + (size_t)(b % n1)] = 1.0;
+  check(sfeec_dev_set_state(h, a.data(), (int64_t)nb, e.data(), (int64_t)nb, 0.0));
+  check(sfeec_dev_advance(h, 1));
+  double t = 0;
+  check(sfeec_dev_get_state(h, a.data(), e.data(), &t));
+  // column b of A / E is block b of the advanced batch
+  std::vector<double> p((size_t)m * (size_t)m);
+  for (int i = 0; i < m; ++i) {
+    const double* ei = &e[(size_t)i * n1];
+    for (int j = 0; j < m; ++j) {
+      const double* aj = &a[(size_t)j * n1];
+      double s = 0;
+      for (int k = 0; k < n1; ++k) s += ei[k] * aj[k];
+      p[(size_t)i * m + j] = s;
+    }
   }
   const double se = 1.0 / scheme.units().eps0;
   double dev = 0;
-  for (int i = 0; i < n2; ++i) {
-    const auto& ci = phi[(size_t)i];
-    for (int j = 0; j < n2; ++j) {
-      const auto& cj = phi[(size_t)j];
-      double acc = 0;
-      for (int k = 0; k < n1; ++k)
-        acc += ci[(size_t)k] * (-se * cj[(size_t)(n1 + k)]) +
-               ci[(size_t)(n1 + k)] * (se * cj[(size_t)k]);
-      double target = 0;
-      if (j == i + n1) target = -se;
-      if (i == j + n1) target = se;
-      dev = std::max(dev, std::abs(acc - target));
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      const double jij = (j - i == n1) ? -se : (i - j == n1) ? se : 0.0;
+      dev = std::max(dev, std::abs(se * (p[(size_t)i * m + j] - p[(size_t)j * m + i]) - jij));
     }
-  }
   return dev;
 }
 

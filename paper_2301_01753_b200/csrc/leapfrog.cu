@@ -34,6 +34,12 @@ struct LeapfrogDev {
   bool warned = false;
   double cfl_cache = -1;
   int64_t launches = 0;
+  bool graphs = env_flag("SFEEC_GRAPHS", true);
+  // programmatic dependent launches of k_ell / k_sell_pipe (SFEEC_PDL, read
+  // once here); the operators carry the flag to launch_spmv
+  void set_pdl(bool on) {
+    for (DevOperator* a : {&q, &c, &ct, &m2, &div}) a->pdl = on;
+  }
   // per-operator launch timing with CUDA events on the launch stream
   // (kernel classes: 0 K-Q, 1 K-C, 2 K-CT, 3 K-M2, 4 other)
   bool timing = false;
@@ -81,24 +87,13 @@ struct LeapfrogDev {
     ev_used.clear();
   }
 
-  // Alternating row order (SFEEC_ALT_DIR): in the step chain M2 -> C^T -> Q
-  // -> C each kernel reads the vector the previous one wrote; running M2 and
-  // Q in descending row order makes each kernel start on the rows its
-  // producer wrote last, which are still in the 126 MB L2. Rows are
-  // computed identically either way.
-  bool alt_dir() const {
-    const char* v = std::getenv("SFEEC_ALT_DIR");
-    return v && std::atoi(v) != 0;
-  }
-  bool reversed(const DevOperator& a) const { return (&a == &m2 || &a == &q) && alt_dir(); }
-
   // y = A x
   void apply(const DevOperator& a, const double* x, double* y) {
     tic(a);
     if (strict())
       launch_spmv_strict(a, x, y, stream);
     else
-      launch_spmv(a, x, y, 0.0, false, stream, reversed(a));
+      launch_spmv(a, x, y, 0.0, false, stream);
     toc();
     ++launches;
   }
@@ -108,34 +103,13 @@ struct LeapfrogDev {
     if (strict())
       launch_spmv_axpy_strict(a, x, y, alpha, stream);
     else
-      launch_spmv(a, x, y, alpha, true, stream, reversed(a));
+      launch_spmv(a, x, y, alpha, true, stream);
     toc();
     ++launches;
   }
 
-  // fused producer -> consumer wavefront kernels (wave.cu): He = K-Q + K-Cb,
-  // Ha = K-M2 + K-CTe; built before any graph capture (the plan build
-  // synchronises), used in production BE mode when SFEEC_WAVE != 0
-  WavePlan wave_he, wave_ha;
-  void prepare_wave() {
-    if (strict() || form != SFEEC_FORM_BE || !wave_enabled()) return;
-    if (!wave_he.built && build_wave_plan(q, c, wave_he, stream)) t1.zero(stream);
-    if (!wave_ha.built && build_wave_plan(m2, ct, wave_ha, stream)) t2.zero(stream);
-    SFEEC_CUDA(cudaStreamSynchronize(stream));
-  }
-  bool wave_on(const WavePlan& w) const {
-    return w.ok && !strict() && form == SFEEC_FORM_BE && wave_enabled();
-  }
-
   // dynamics.cpp:47-55
   void flow_he(double h) {
-    if (wave_on(wave_he)) {  // b -= h C (Q e), one kernel
-      tic(q);
-      launch_wave(wave_he, q, c, e.p, t1.p, first.p, -h, stream);
-      toc();
-      ++launches;
-      return;
-    }
     apply(q, e.p, t1.p);
     if (form == SFEEC_FORM_AE) {
       axpy_vec(first.p, t1.p, -h, n1);
@@ -154,12 +128,6 @@ struct LeapfrogDev {
     if (form == SFEEC_FORM_AE) {
       apply(c, first.p, t3.p);
       b = t3.p;
-    } else if (wave_on(wave_ha)) {  // e += f C^T (M2 b), one kernel
-      tic(m2);
-      launch_wave(wave_ha, m2, ct, b, t2.p, e.p, f, stream);
-      toc();
-      ++launches;
-      return;
     }
     apply(m2, b, t2.p);
     apply_axpy(ct, t2.p, e.p, f);
@@ -180,17 +148,15 @@ struct LeapfrogDev {
   // bulk of advance(n): small, launch-bound systems (config 1: ~7 us per
   // kernel launched one by one) pay one graph launch per kGraphPairs x 4
   // kernels. Rebuilt when dt changes; off while per-kernel timing is on or
-  // with SFEEC_GRAPHS=0.
+  // with SFEEC_GRAPHS=0 (read once per handle, like SFEEC_PDL: a captured
+  // graph and the directly launched kernels always run in the same mode).
   static constexpr int kGraphPairs = 32;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
   double graph_dt = -1;
   int64_t graph_kernels = 0;
 
-  bool graphs_on() const {
-    const char* v = std::getenv("SFEEC_GRAPHS");
-    return !timing && !(v && std::atoi(v) == 0);
-  }
+  bool graphs_on() const { return !timing && graphs; }
   void build_graph() {
     if (graph_exec) {
       cudaGraphExecDestroy(graph_exec);
@@ -234,7 +200,6 @@ struct LeapfrogDev {
     launches = 0;
     if (n <= 0) return;
     check_cfl_once();
-    prepare_wave();
     if (strict() || kind == SFEEC_SPLIT_LIE_TROTTER || form == SFEEC_FORM_AE) {
       for (int64_t s = 0; s < n; ++s) {
         if (kind == SFEEC_SPLIT_STRANG) {
@@ -365,6 +330,7 @@ sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR
   d.t2.alloc((size_t)std::max<int64_t>(d.n2, 1));
   d.t3.alloc((size_t)std::max<int64_t>(d.n2, 1));
   d.partials.alloc(kReduceBlocks + 1);
+  d.set_pdl(env_flag("SFEEC_PDL", true));
   SFEEC_CUDA(cudaStreamSynchronize(d.stream));
   return h.release();
 }
@@ -406,6 +372,7 @@ sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct,
   d.t2.alloc((size_t)std::max<int64_t>(n2, 1));
   d.t3.alloc((size_t)std::max<int64_t>(n2, 1));
   d.partials.alloc(kReduceBlocks + 1);
+  d.set_pdl(env_flag("SFEEC_PDL", true));
   SFEEC_CUDA(cudaStreamSynchronize(d.stream));
   return h.release();
 }
@@ -696,10 +663,6 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
       bytes[2] = ctb * d.ct.nnz + 8.0 * d.n2 + 16.0 * d.n1; // e += f C^T u
       bytes[3] = 12.0 * d.m2.nnz + 16.0 * d.n2;  // u = M2 b
       bytes[4] = 0;
-      // fused pairs (t, u stay intermediates): b -= h C (Q e); e += f C^T (M2 b)
-      if (d.wave_on(d.wave_he)) bytes[0] = 12.0 * d.q.nnz + 8.0 * d.n1 + cb * d.c.nnz + 16.0 * d.n2;
-      if (d.wave_on(d.wave_ha))
-        bytes[3] = 12.0 * d.m2.nnz + 8.0 * d.n2 + ctb * d.ct.nnz + 16.0 * d.n1;
     }
     d.timing = enable != 0;
   });
@@ -714,30 +677,17 @@ int sfeec_dev_layout_info(sfeec_dev* h, int which, int64_t* info, double* bytes)
     const DevOperator& a = *ops[which];
     if (info) {
       info[0] = (int64_t)a.layout;
-      info[1] = a.delta ? 1 : 0;
+      info[1] = 0;  // (column-delta layouts: removed)
       info[2] = a.ell ? 1 : 0;
       info[3] = a.ell ? (a.rows + 31) / 32 : a.n_slices;
-      info[4] = a.n_full;
+      info[4] = 0;
       info[5] = a.sell_entries;
       info[6] = a.nnz;
-      info[7] = a.win ? 1 : 0;
-      info[8] = a.win ? a.n_units : 0;
+      info[7] = 0;  // (windowed layout: removed)
+      info[8] = 0;
     }
     if (bytes) *bytes = a.stream_bytes();
   });
-}
-
-// bit 0: He (K-Q + K-Cb) runs as one wavefront kernel, bit 1: Ha (K-M2 + K-CTe)
-int sfeec_dev_fused(sfeec_dev* h) {
-  if (!h) return 0;
-  int r = 0;
-  guarded([&] {
-    auto& d = h->d;
-    SFEEC_CUDA(cudaSetDevice(d.device));
-    d.prepare_wave();
-    r = (d.wave_on(d.wave_he) ? 1 : 0) | (d.wave_on(d.wave_ha) ? 2 : 0);
-  });
-  return r;
 }
 
 // 12 nnz(Q) + 12 nnz(M2) + 2*5 nnz(C) + 16 (N1 + N2); a

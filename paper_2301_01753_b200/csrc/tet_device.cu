@@ -15,7 +15,6 @@
 
 #include "device_util.cuh"
 #include "spmv_kernels.cuh"
-#include "stencil.cuh"
 #include "tet_device.hpp"
 #include "tet_mesh.hpp"
 
@@ -723,34 +722,7 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
                                split_kind, device, flags, hs);
       return;
     }
-    if (flags & SFEEC_TET_STENCIL_LAYOUT) {
-      // stencil layout built on the device from the device CSRs (no host trip)
-      auto sm = stencil_mesh(mesh, st.s);
-      DevOperator q, c, ct, m2, div;
-      auto mk = [&](int kind, DevCSR& csr, DevOperator& op) {
-        auto so = std::make_shared<StencilOp>();
-        stencil_build(mesh, sm, kind, &csr, *so, st.s);
-        op.rows = csr.rows;
-        op.cols = csr.cols;
-        op.nnz = csr.nnz;
-        op.layout = DevOperator::kStencil;
-        op.st = so;
-        csr.rp.reset();
-        csr.ci.reset();
-        csr.val.reset();
-      };
-      mk(kStQ, sys.qsym, q);
-      mk(kStM2, sys.m2, m2);
-      mk(kStC, sys.c, c);
-      mk(kStCT, sys.ct, ct);
-      if (with_div) div.adopt_csr(std::move(sys.d));
-      cudaStream_t hs;
-      SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
-      *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
-                               with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
-                               split_kind, device, flags & ~SFEEC_TET_STENCIL_LAYOUT, hs);
-      return;
-    }
+    require(!(flags & SFEEC_TET_STENCIL_LAYOUT), "the stencil layout was removed");
     sys.ct.rp.reset();  // the handle transposes C itself
     sys.ct.ci.reset();
     sys.ct.val.reset();

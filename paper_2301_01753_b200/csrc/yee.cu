@@ -495,17 +495,15 @@ __device__ __forceinline__ uint32_t e_mask_xy(int i, int j, int n0, int n1) {
   return (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u);
 }
 
-// NB1 = 2 double-buffers the B1 plane: phase 2 of plane p+1 then writes the
-// other buffer than the one phase 3 of plane p reads, and the only other
-// reason for the barrier between phases 1 and 2 (E1(z-1) neighbours) is
-// already covered by the previous plane's barrier, so each plane needs one
-// barrier instead of two. Same arithmetic, bitwise the same result.
-// ORD = 1 orders the E1-region points so that the TX x TY own tile comes
-// first, one warp per tile row (TX = 32), then the rims the E2, B1 and E1
-// regions add. Phases 2-4 run only on their region's points (the others'
-// values are never read), so the idle rim warps skip them, and the own-point
-// stores are whole 32-wide rows. ORD = 0 is the row-major map over the E1
-// region, every phase on every point. Same point updates either way.
+// The B1 plane is double-buffered: phase 2 of plane p+1 writes the other
+// buffer than the one phase 3 of plane p reads, and the only other reason for
+// a barrier between phases 1 and 2 (E1(z-1) neighbours) is already covered by
+// the previous plane's barrier, so each plane needs one barrier, not two.
+// The E1-region points are ordered so that the TX x TY own tile comes first,
+// one warp per tile row (TX = 32), then the rims the E2, B1 and E1 regions
+// add. Phases 2-4 run only on their region's points (the others' values are
+// never read), so the idle rim warps skip them, and the own-point stores are
+// whole 32-wide rows.
 template <int TX, int TY>
 __device__ __forceinline__ void region_point(int t, int& x, int& y) {
   constexpr int kOwn = TX * TY;
@@ -544,13 +542,13 @@ __device__ __forceinline__ void region_point(int t, int& x, int& y) {
   }
 }
 
-template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB, int NB1 = 1, int ORD = 0,
-          int PF1 = 0>
+template <class T, int TX, int TY, int NS, int NTH, int NPT, int MINB>
 __global__ void __launch_bounds__(NTH, MINB)
     k_fused2_tma(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapE,
                  YeeGeom g, Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
                  int n_units, int kbeg, int kend, const int4* __restrict__ sched,
                  const int* __restrict__ cta_ptr) {
+  constexpr int NB1 = 2;
   using Cfg = TmaCfg2<T, TX, TY, NS, NB1>;
   constexpr int D = Cfg::kD, BW = Cfg::kBW, OFF = Cfg::kOff;
   // NPT points of the E1 region (origin (i0-1, j0-1)) per thread: points
@@ -560,9 +558,9 @@ __global__ void __launch_bounds__(NTH, MINB)
   // through shared memory. Several points per thread amortise the per-plane
   // control (barrier waits, stage and buffer addressing) and add ILP.
   constexpr int X1 = Cfg::kX1, Y1 = Cfg::kY1, NP = X1 * Y1;
-  // (ORD = 1 rounds the stride up to whole warps, so every h keeps the
+  // (the stride is rounded up to whole warps, so every h keeps the
   // one-tile-row-per-warp layout)
-  constexpr int NH = ORD == 0 ? (NP + NPT - 1) / NPT : ((NP + NPT - 1) / NPT + 31) / 32 * 32;
+  constexpr int NH = ((NP + NPT - 1) / NPT + 31) / 32 * 32;
   static_assert(NH <= NTH, "NPT region points per thread");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -589,12 +587,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   for (int h = 0; h < NPT; ++h) {
     const int t = tid + h * NH;
     pt[h] = tid < NH && t < NP;
-    if constexpr (ORD == 0) {  // row-major over the E1 region
-      xo[h] = t % X1;
-      yo[h] = t / X1;
-    } else {  // own tile rows, then the E2, B1 and E1 rims (region_point)
-      region_point<TX, TY>(t, xo[h], yo[h]);
-    }
+    region_point<TX, TY>(t, xo[h], yo[h]);  // own tile rows, then the rims
     me[h] = yo[h] * X1 + xo[h];  // shared-memory index on the E1 region grid
     ob[h] = (yo[h] + 1) * BW + xo[h] + OFF - 1;
     oe[h] = yo[h] * BW + xo[h] + OFF - 1;
@@ -663,25 +656,19 @@ __global__ void __launch_bounds__(NTH, MINB)
     // plane p of the unit (PAR = p & 1 selects the E1/E2 double buffers at
     // compile time): C receives this plane's values, V holds the previous
     // plane's
-    // PF1: plane p+1's TMA issue, stage wait and the own old B / old E of
-    // the stage are done right after plane p's barrier, so those loads are in
-    // flight during phases 3-4 of plane p (pf holds them until phase 1)
-    T pf[NPT][6];
     auto plane = [&](auto par, int p, Pt* C, const Pt* V) {
       constexpr int PAR = decltype(par)::value;
       const uint32_t gc = gplane + p;
       const int st = gc % NS;
-      if (!PF1 || p == 0) {
-        if (tid == 0 && p + D < P) issue(p + D);
-        mbar_wait(&bars[st], (gc / NS) & 1);
-      }
+      if (tid == 0 && p + D < P) issue(p + D);
+      mbar_wait(&bars[st], (gc / NS) & 1);
       const int z = k0 - 2 + p;
       const T* __restrict__ B0c = reinterpret_cast<const T*>(base + st * Cfg::kStage);
       const T* __restrict__ E0c = reinterpret_cast<const T*>(base + st * Cfg::kStage + Cfg::kBStride);
       T* E1z = sE1 + PAR * 3 * NP;            // E1(z)
       const T* E1y = sE1 + (1 - PAR) * 3 * NP;  // E1(z-1)
       T* E2y = sE2 + (1 - PAR) * 3 * NP;        // E2(z-1)
-      T* B1p = sB1 + (NB1 == 2 ? PAR : 0) * 3 * NP;  // B1(z-1)
+      T* B1p = sB1 + PAR * 3 * NP;              // B1(z-1)
       const T* E2x = sE2 + PAR * 3 * NP;        // E2(z-2)
       constexpr int BC = (TY + 4) * BW, EC = (TY + 3) * BW;  // component strides in the boxes
 #define R(buf, c, idx) buf[(c) * NP + (idx)]
@@ -694,19 +681,12 @@ __global__ void __launch_bounds__(NTH, MINB)
         for (int h = 0; h < NPT; ++h) {
           if (!pt[h]) continue;
           const T* b = B0c + ob[h];
-          if (PF1 && p > 0) {
-            C[h].b0[0] = pf[h][0];
-            C[h].b0[1] = pf[h][1];
-            C[h].b0[2] = pf[h][2];
-          } else {
-            C[h].b0[0] = b[0];
-            C[h].b0[1] = b[BC];
-            C[h].b0[2] = b[2 * BC];
-          }
+          C[h].b0[0] = b[0];
+          C[h].b0[1] = b[BC];
+          C[h].b0[2] = b[2 * BC];
           if (p >= 1) {
             const T* e = E0c + oe[h];
-            const T e0 = PF1 ? pf[h][3] : e[0], e1 = PF1 ? pf[h][4] : e[EC],
-                    e2 = PF1 ? pf[h][5] : e[2 * EC];
+            const T e0 = e[0], e1 = e[EC], e2 = e[2 * EC];
             const T u0 = yee_upd(e0, ce1, C[h].b0[2] - b[2 * BC - BW], ce2, C[h].b0[1] - V[h].b0[1]);
             const T u1 = yee_upd(e1, ce2, C[h].b0[0] - V[h].b0[0], ce0, C[h].b0[2] - b[2 * BC - 1]);
             const T u2 = yee_upd(e2, ce0, C[h].b0[1] - b[BC - 1], ce1, C[h].b0[0] - b[-BW]);
@@ -719,15 +699,13 @@ __global__ void __launch_bounds__(NTH, MINB)
           }
         }
       }
-      if constexpr (NB1 == 1) __syncthreads();  // the B1 plane is free
-      // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem). With ORD = 0
-      // points outside the B1 region compute too (their values are never read)
+      // ---- phase 2: B1(z-1) (E1(z-1) neighbours from smem)
       if (p >= 2 && any) {
         const int zg = z - 1 + g.kofs;
         const bool zin = zg >= 0 && zg < n2;
 #pragma unroll
         for (int h = 0; h < NPT; ++h) {
-          if (ORD == 0 ? !pt[h] : !inB1[h]) continue;
+          if (!inB1[h]) continue;
           const int q = me[h];
           const bool up = b1up[h] && zin;
           const Pt& v = V[h];
@@ -743,30 +721,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         }
       }
       __syncthreads();  // B1(z-1) complete
-      if constexpr (PF1) {
-        if (p + 1 < P) {
-          if (tid == 0 && p + 1 + D < P) issue(p + 1 + D);
-          const uint32_t gn = gc + 1;
-          const int sn = gn % NS;
-          mbar_wait(&bars[sn], (gn / NS) & 1);
-          const T* B0n = reinterpret_cast<const T*>(base + sn * Cfg::kStage);
-          const T* E0n = reinterpret_cast<const T*>(base + sn * Cfg::kStage + Cfg::kBStride);
-#pragma unroll
-          for (int h = 0; h < NPT; ++h) {
-            if (!pt[h]) continue;
-            const T* b = B0n + ob[h];
-            pf[h][0] = b[0];
-            pf[h][1] = b[BC];
-            pf[h][2] = b[2 * BC];
-            const T* e = E0n + oe[h];
-            pf[h][3] = e[0];
-            pf[h][4] = e[EC];
-            pf[h][5] = e[2 * EC];
-          }
-        }
-      }
-      // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem); with ORD = 0
-      // points outside the E2 region compute too (never read)
+      // ---- phase 3: E2(z-1) (B1(z-1) neighbours from smem)
       if (p >= 3 && any) {
         const int ze = z - 1;
         const int zg = ze + g.kofs;
@@ -774,7 +729,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         const bool zw = ze >= k0 && ze < k1;
 #pragma unroll
         for (int h = 0; h < NPT; ++h) {
-          if (ORD == 0 ? !pt[h] : !inE2[h]) continue;
+          if (!inE2[h]) continue;
           const int q = me[h];
           const Pt& v = V[h];
           const bool d0 = (m[h] & 1) && kin, d1 = (m[h] & 2) && kin, d2 = (m[h] & 4) && kz;
@@ -824,164 +779,6 @@ __global__ void __launch_bounds__(NTH, MINB)
   }
 }
 
-// ---- variant 3: B planes by TMA, E planes by register prefetch ------------
-// Same sweep and arithmetic as k_fused_tma, but each thread loads the old E
-// values of its <= 2 region points one plane ahead into registers (plain
-// coalesced loads; each is read by exactly one thread) instead of staging E
-// through shared memory. The stage shrinks to the B tile, so three CTAs fit
-// per SM instead of two.
-template <class T, int TX, int TY, int NS>
-struct TmaCfgB {
-  static constexpr int kOff = 16 / (int)sizeof(T);
-  static constexpr int kBWB = (((TX + 1 + kOff) * (int)sizeof(T) + 15) / 16 * 16) / (int)sizeof(T);
-  static constexpr int kBBox = 3 * (TY + 2) * kBWB * (int)sizeof(T);
-  static constexpr int kStage = (kBBox + 127) / 128 * 128;
-  static constexpr int kEnew = 3 * (TY + 1) * (TX + 1);
-  static constexpr int kBarOff = (NS * kStage + 3 * kEnew * (int)sizeof(T) + 15) / 16 * 16;
-  static constexpr int kSmem = kBarOff + NS * 8 + 128;
-  static constexpr int kD = NS - 3;
-};
-
-template <class T, int TX, int TY, int NS>
-__global__ void __launch_bounds__(TX* TY)
-    k_fused_tma_b(const __grid_constant__ CUtensorMap mapB, YeeGeom g, Fields<T> in,
-                  Fields<T> out, YeeCoef<T> ck, int kchunk, int n_tiles_x, int n_tiles,
-                  int n_units, int kbeg, int kend) {
-  using Cfg = TmaCfgB<T, TX, TY, NS>;
-  constexpr int D = Cfg::kD;
-  constexpr int BWB = Cfg::kBWB, OFF = Cfg::kOff;
-  constexpr int NT = TX * TY, NE = (TX + 1) * (TY + 1);
-  static_assert(NE <= 2 * NT, "E region needs at most two passes");
-  extern __shared__ unsigned char smem_raw[];
-  // 128-byte aligned start, as an offset into the shared array so the
-  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
-  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* sEn = reinterpret_cast<T*>(base + NS * Cfg::kStage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + Cfg::kBarOff);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-  }
-  __syncthreads();
-  uint32_t gplane = 0;
-  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
-  const int64_t kstride = (int64_t)g.P0 * g.S[1];
-  const int pl[2] = {tid, tid + NT};
-  int li_[2], lj_[2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    li_[q] = pl[q] % (TX + 1);
-    lj_[q] = pl[q] / (TX + 1);
-  }
-  const bool has2 = tid + NT < NE;
-  const int bli = tid % TX, blj = tid / TX;
-
-  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
-    const int chunk = unit / n_tiles, tile = unit - chunk * n_tiles;
-    const int i0 = (tile % n_tiles_x) * TX, j0 = (tile / n_tiles_x) * TY;
-    const int k0 = kbeg + chunk * kchunk, k1 = min(k0 + kchunk, kend);
-    const int P = k1 - k0 + 2;
-    uint32_t m[2];
-    int64_t sij[2];
-    bool inr[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = i0 + li_[q], j = j0 + lj_[q];
-      const bool ix = i < n0, iy = i >= 1 && i <= n0 - 1;
-      const bool jx = j < n1, jy = j >= 1 && j <= n1 - 1;
-      const bool own = li_[q] < TX && lj_[q] < TY && i < n0 && j < n1;
-      m[q] = (ix && jy ? 1u : 0u) | (iy && jx ? 2u : 0u) | (iy && jy ? 4u : 0u) | (own ? 8u : 0u);
-      sij[q] = (int64_t)i + (int64_t)g.P0 * j;
-      inr[q] = (q == 0 || has2) && i < g.S[0] && j < g.S[1];
-    }
-    const bool bown = i0 + bli < n0 && j0 + blj < n1;
-    const int64_t bsij = (int64_t)(i0 + bli) + (int64_t)g.P0 * (j0 + blj);
-    // old E of plane k0 for the thread's region points
-    T ec[2][3], en[2][3];
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) ec[q][c] = inr[q] ? in.c[c][sij[q] + kstride * k0] : T(0);
-
-    auto issue = [&](int p) {
-      const uint32_t gp = gplane + p;
-      const int st = gp % NS;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&bars[st], Cfg::kBBox);
-      tma_load_4d(base + st * Cfg::kStage, &mapB, &bars[st], i0 - OFF, j0 - 1, k0 - 1 + p, 3);
-    };
-    if (tid == 0)
-      for (int p = 0; p <= D && p < P; ++p) issue(p);
-    for (int jp = 0; jp + 1 < P; ++jp) {
-      const int kk = k0 + jp;
-      if (tid == 0 && jp + 1 + D < P) issue(jp + 1 + D);
-      // prefetch the old E of the next plane into registers
-      const bool more = kk + 1 <= k1;
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) en[q][c] = (more && inr[q]) ? in.c[c][sij[q] + kstride * (kk + 1)] : T(0);
-      const uint32_t gc = gplane + jp + 1, gv = gplane + jp;
-      const int sc = gc % NS, sv = gv % NS;
-      if (jp == 0) mbar_wait(&bars[sv], (gv / NS) & 1);
-      mbar_wait(&bars[sc], (gc / NS) & 1);
-      const T* __restrict__ Bc = reinterpret_cast<const T*>(base + sc * Cfg::kStage);
-      const T* __restrict__ Bp = reinterpret_cast<const T*>(base + sv * Cfg::kStage);
-      T* Enc = sEn + ((gplane + jp) % 3) * Cfg::kEnew;
-      const T* Enp = sEn + ((gplane + jp + 2) % 3) * Cfg::kEnew;
-#define BC(c, y, x) Bc[((c) * (TY + 2) + (y)) * BWB + (x)]
-#define BP(c, y, x) Bp[((c) * (TY + 2) + (y)) * BWB + (x)]
-#define EN(buf, c, y, x) buf[((c) * (TY + 1) + (y)) * (TX + 1) + (x)]
-      const int kg = kk + g.kofs;
-      const bool kin = kg >= 1 && kg <= n2 - 1, kz = kg < n2, kw = kk < k1;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (q == 1 && !has2) break;
-        const int li = li_[q], lj = lj_[q];
-        const int bi = li + OFF, bj = lj + 1;
-        T e0 = ec[q][0], e1 = ec[q][1], e2 = ec[q][2];
-        const bool d0 = (m[q] & 1) && kin, d1 = (m[q] & 2) && kin, d2 = (m[q] & 4) && kz;
-        if (d0)
-          e0 = yee_upd(e0, ck.ce[1], BC(2, bj, bi) - BC(2, bj - 1, bi), ck.ce[2], BC(1, bj, bi) - BP(1, bj, bi));
-        if (d1)
-          e1 = yee_upd(e1, ck.ce[2], BC(0, bj, bi) - BP(0, bj, bi), ck.ce[0], BC(2, bj, bi) - BC(2, bj, bi - 1));
-        if (d2)
-          e2 = yee_upd(e2, ck.ce[0], BC(1, bj, bi) - BC(1, bj, bi - 1), ck.ce[1], BC(0, bj, bi) - BC(0, bj - 1, bi));
-        if ((m[q] & 8) && kw) {
-          const int64_t s = sij[q] + kstride * kk;
-          if (d0) out.c[0][s] = e0;
-          if (d1) out.c[1][s] = e1;
-          if (d2) out.c[2][s] = e2;
-        }
-        EN(Enc, 0, lj, li) = e0;
-        EN(Enc, 1, lj, li) = e1;
-        EN(Enc, 2, lj, li) = e2;
-      }
-      __syncthreads();
-      if (jp > 0 && bown) {
-        const int li = bli, lj = blj;
-        const int64_t s = bsij + kstride * (kk - 1);
-        const int bi = li + OFF, bj = lj + 1;
-        out.c[3][s] = yee_upd(BP(0, bj, bi), ck.cb[2], EN(Enc, 1, lj, li) - EN(Enp, 1, lj, li), ck.cb[1], EN(Enp, 2, lj + 1, li) - EN(Enp, 2, lj, li));
-        out.c[4][s] = yee_upd(BP(1, bj, bi), ck.cb[0], EN(Enp, 2, lj, li + 1) - EN(Enp, 2, lj, li), ck.cb[2], EN(Enc, 0, lj, li) - EN(Enp, 0, lj, li));
-        out.c[5][s] = yee_upd(BP(2, bj, bi), ck.cb[1], EN(Enp, 0, lj + 1, li) - EN(Enp, 0, lj, li), ck.cb[0], EN(Enp, 1, lj, li + 1) - EN(Enp, 1, lj, li));
-      }
-#undef BC
-#undef BP
-#undef EN
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ec[q][c] = en[q][c];
-    }
-    gplane += P;
-    __syncthreads();
-  }
-}
-
-// state pack/unpack between the SFEEC numbering (fp64) and storage (T)
 template <class T>
 __global__ void k_scatter(YeeGeom g, bool face, const double* __restrict__ src, int64_t n,
                           Fields<T> f) {
@@ -1087,19 +884,16 @@ struct YeeDev {
   // TMA descriptors of the two ping-pong buffers (B box, E box), PEC only
   CUtensorMap mapB[2], mapE[2];
   bool have_maps = false;
-  int tma_blocks = 0, tma_blocks_b = 0;
+  int tma_blocks = 0;
   // variant 4 (two steps per sweep): its own boxes
   CUtensorMap mapB2[2], mapE2[2];
   bool have_maps2 = false;
   int tma_blocks2 = 0;
-  int nb1 = 2;  // B1 buffers of the two-step sweep (SFEEC_YEE_B1=1: the two-barrier form)
-  int ord = 1;  // tile-first point order (SFEEC_YEE_ORD=0: row-major, every phase on every point)
-  // stage prefetch one plane ahead (SFEEC_YEE_PF1=1; needs nb1 = 2, ord = 1)
-  bool pf1 = false;
-  // programmatic dependent launch of the two-step sweeps (SFEEC_PDL=0: off)
-  bool pdl = true;
-  // balanced unit schedule of the two-step sweep (SFEEC_YEE_SCHED=0: round-robin z-chunks)
-  bool sched2 = true;
+  // programmatic dependent launch of the two-step sweeps (SFEEC_PDL=0: off;
+  // read once per handle). Off on NCCL slabs: a programmatic launch after the
+  // exchange-event wait has not been verified against a multi-process run.
+  bool pdl = env_flag("SFEEC_PDL", true);
+  // balanced unit schedule of the two-step sweep (make_yee2_sched)
   std::map<std::pair<int, int>, Yee2Sched> scheds2;
   const Yee2Sched& schedule2(int ntiles, int kbeg, int kend) {
     auto key = std::make_pair(kbeg, kend);
@@ -1296,23 +1090,9 @@ struct YeeDev {
         if (r != CUDA_SUCCESS) throw Error(SFEEC_ECUDA, "cuTensorMapEncodeTiled failed");
       }
     }
-    const char* e1 = std::getenv("SFEEC_YEE_B1");
-    nb1 = e1 && std::atoi(e1) == 1 ? 1 : 2;
-    const char* eo = std::getenv("SFEEC_YEE_ORD");
-    ord = eo && std::atoi(eo) == 0 ? 0 : 1;
-    const char* es = std::getenv("SFEEC_YEE_SCHED");
-    sched2 = !(es && std::atoi(es) == 0);
-    const char* epd = std::getenv("SFEEC_PDL");
-    pdl = !(epd && std::atoi(epd) == 0);
     using Cfg2 = TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>;
-    const char* ep = std::getenv("SFEEC_YEE_PF1");
-    pf1 = ep && std::atoi(ep) == 1 && nb1 == 2 && ord;
-    auto kern = pf1 ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1, 1>
-              : nb1 == 2 ? (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 1>
-                                : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 2, 0>)
-                         : (ord ? k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 1>
-                                : k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, 1, 0>);
-    const int smem = nb1 == 2 ? Cfg2::kSmem : Cfg::kSmem;
+    auto kern = k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>>;
+    const int smem = Cfg2::kSmem;
     SFEEC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0, sms = 0;
     SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT2<T>, smem));
@@ -1328,25 +1108,12 @@ struct YeeDev {
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY2<T> - 1) / kTY2<T>;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
-    const Yee2Sched* sc = sched2 ? &schedule2(ntx * nty, kbeg, kend) : nullptr;
-    const int grid = sc ? sc->grid : std::min(n_units, tma_blocks2);
-#define SFEEC_K2(NB1, ORD, PF)                                                               \
-  launch_pdl(pdl, k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>, NB1, ORD, PF>, \
-             dim3(grid), dim3(kNT2<T>), TmaCfg2<T, kTX, kTY2<T>, kNS2, NB1>::kSmem, stream,   \
-             mapB2[cur], mapE2[cur], g, fields<T>(cur ^ 1),                                  \
-             coef<T>(h_e / (eps0 * mu0), h_b), kChunk, ntx, ntx * nty, n_units, kbeg, kend,  \
-             sc ? sc->units.p : nullptr, sc ? sc->cta_ptr.p : nullptr)
-    if (pf1)
-      SFEEC_K2(2, 1, 1);
-    else if (nb1 == 2 && ord)
-      SFEEC_K2(2, 1, 0);
-    else if (nb1 == 2)
-      SFEEC_K2(2, 0, 0);
-    else if (ord)
-      SFEEC_K2(1, 1, 0);
-    else
-      SFEEC_K2(1, 0, 0);
-#undef SFEEC_K2
+    const Yee2Sched* sc = &schedule2(ntx * nty, kbeg, kend);
+    const int grid = sc->grid;
+    launch_pdl(pdl && !comm, k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>>, dim3(grid),
+               dim3(kNT2<T>), TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>::kSmem, stream, mapB2[cur],
+               mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk, ntx,
+               ntx * nty, n_units, kbeg, kend, sc->units.p, sc->cta_ptr.p);
     SFEEC_LAUNCH_CHECK();
     ++launches;
   }
@@ -1403,23 +1170,6 @@ struct YeeDev {
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY - 1) / kTY;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
     const int n_units = ntx * nty * nchunks;
-    if (variant == 3) {
-      using CfgB = TmaCfgB<T, kTX, kTY, kNS>;
-      auto kb = k_fused_tma_b<T, kTX, kTY, kNS>;
-      if (!tma_blocks_b) {
-        SFEEC_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgB::kSmem));
-        int per_sm = 0, sms = 0;
-        SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, kTX * kTY, CfgB::kSmem));
-        SFEEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        tma_blocks_b = std::max(1, per_sm) * sms;
-      }
-      kb<<<std::min(n_units, tma_blocks_b), kTX * kTY, CfgB::kSmem, stream>>>(
-          mapB[cur], g, fields<T>(cur), fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b),
-          kChunk, ntx, ntx * nty, n_units, kbeg, kend);
-      SFEEC_LAUNCH_CHECK();
-      ++launches;
-      return;
-    }
     const int grid = std::min(n_units, tma_blocks);
     k_fused_tma<T, kTX, kTY, kNS, kNT1><<<grid, kNT1, Cfg::kSmem, stream>>>(
         mapB[cur], mapE[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk,
@@ -1939,7 +1689,7 @@ void sfeec_yee_group_destroy(sfeec_yee_group* h) { delete h; }
 
 int sfeec_yee_group_set_variant(sfeec_yee_group* h, int variant) {
   return guarded([&] {
-    require(h && (variant == 0 || variant >= 2) && variant <= 4, "slabs support variants 0, 2, 3 and 4");
+    require(h && (variant == 0 || variant == 2 || variant == 4), "slabs support variants 0, 2 and 4");
     for (auto& d : h->g.s) d->variant = variant;
   });
 }
@@ -2087,7 +1837,7 @@ int sfeec_yee_set_stream(sfeec_yee* h, void* s) {
 int sfeec_yee_set_variant(sfeec_yee* h, int variant) {
   return guarded([&] {
     require(h, "null handle");
-    require(variant >= 0 && variant <= 4, "variant must be 0..4");
+    require(variant >= 0 && variant <= 4 && variant != 3, "variant must be 0, 1, 2 or 4");
     h->d.variant = variant;
   });
 }

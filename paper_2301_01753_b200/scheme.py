@@ -326,11 +326,6 @@ class SplitScheme:
     def last_launches(self) -> int:
         return int(L.lib().sfeec_dev_last_launches(self._h))
 
-    def fused(self) -> int:
-        """Bit 0: He (K-Q + K-Cb) runs as one wavefront kernel (wave.cu);
-        bit 1: Ha (K-M2 + K-CTe). 0 with SFEEC_WAVE=0 or unsupported layouts."""
-        return int(L.lib().sfeec_dev_fused(self._h))
-
     KERNEL_CLASSES = ("K-Q", "K-Cb", "K-CTe", "K-M2", "other")
 
     def kernel_timing(self, enable: bool = True) -> dict:
@@ -583,19 +578,16 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
                       device: int = 0) -> "SplitScheme":
     """First-order S(M1) tet system assembled on the B200 (C, D, M1, M2, SPAI,
     Q_sym), wrapped as a (b, e) SplitScheme. Operators stay in HBM.
-    layout: "device" (default: sliced/ELL layouts built on the GPU), "stencil"
-    (columns recomputed from the Kuhn stencil; slower, kept for reference) or
-    "host" (generic sliced/ELL layouts built through the host)."""
+    layout: "device" (default: sliced/ELL layouts built on the GPU) or "host"
+    (generic sliced/ELL layouts built through the host)."""
     units = units or UnitSystem()
     h = C.c_void_p()
     counts = np.zeros(3, np.int64)
     flags = 0 if warn_cfl else L.NO_CFL_WARN
     if layout == "host":
         flags |= 8  # SFEEC_TET_HOST_LAYOUT
-    elif layout == "stencil":
-        flags |= 16  # SFEEC_TET_STENCIL_LAYOUT
     elif layout != "device":
-        raise InvalidParameter("layout must be 'device', 'host' or 'stencil'")
+        raise InvalidParameter("layout must be 'device' or 'host'")
     L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                          units.mu0, int(SplitKind(kind)), device, flags,
                                          1 if with_div else 0, C.byref(h), L.i64ptr(counts)))

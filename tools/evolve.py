@@ -49,11 +49,15 @@ def main():
         b0 = s.apply("c", a)
         s.set_dt(args.dt if args.dt else configs.cfl_dt(s))
         state = S.make_state(S.Formulation.BE, b0, np.zeros(s._n1))
-        rows.append((0, 0.0, s.energy(state), s.gauss_residual(state)))
-        out, en, ga = s.advance_diag(state, args.steps, args.diag_every)
-        for k in range(len(en)):
-            step = (k + 1) * args.diag_every
-            rows.append((step, step * s.dt(), en[k], ga[k]))
+        # the package driver: time accumulated per step on the device (as
+        # cmd_evolve's time += dt) and a final row at step == steps
+        from paper_2301_01753_b200.evolve import evolve
+        text = evolve(s, state, args.steps, args.diag_every)
+        fh = sys.stdout if args.out == "-" else open(args.out, "w")
+        fh.write(text)
+        if fh is not sys.stdout:
+            fh.close()
+        return
     elif args.config == "yee":
         import bench
         n = args.n or 64
@@ -69,10 +73,13 @@ def main():
             return np.abs(db).max()
 
         rows.append((0, 0.0, y.energy(), gauss(b0)))
-        for k in range(args.steps // args.diag_every):
-            y.advance(args.diag_every)
+        s = 0
+        while s < args.steps:  # every diag_every steps and at the last step
+            nxt = min(args.steps, (s // args.diag_every + 1) * args.diag_every)
+            y.advance(nxt - s)
+            s = nxt
             b, _, t = y.fetch()
-            rows.append(((k + 1) * args.diag_every, t, y.energy(), gauss(b)))
+            rows.append((s, t, y.energy(), gauss(b)))
     else:
         raise SystemExit(f"unknown config {args.config}")
 
