@@ -390,6 +390,12 @@ void part_finish(PartDev& d, const void* nccl_id) {
     std::memcpy(&id, nccl_id, sizeof(id));
     Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, d.nranks, id, d.rank), "ncclCommInitRank");
   }
+  // PDL stays off on NCCL slabs (a programmatic launch after the exchange
+  // event wait is not verified against a multi-process run); SFEEC_PDL=0
+  // turns it off everywhere
+  const bool pdl = env_flag("SFEEC_PDL", true) && !d.comm;
+  for (SplitOp* o : {&d.q, &d.c, &d.ct, &d.m2})
+    for (auto& p : o->part) p.pdl = pdl;
 }
 
 // partition.py plane_splits / entity_plane_offsets / slab_system: the rank's
