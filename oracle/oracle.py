@@ -304,8 +304,48 @@ def port_lib():
         l.or_rng_fill_uniform.argtypes = [C.c_uint64, C.c_double, C.c_double, _PD, C.c_int64]
         l.or_yee_advance_e.argtypes = [C.c_int] * 3 + [_PD, _PD, _PD, C.c_double, C.c_double]
         l.or_yee_advance_b.argtypes = [C.c_int] * 3 + [_PD, _PD, _PD, C.c_double]
+        l.to_build.restype = C.c_int
+        l.to_build.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int] + \
+            [C.POINTER(to_csr)] * 5 + [_PI64]
+        l.to_free.argtypes = [C.POINTER(to_csr)]
         _port = l
     return _port
+
+
+class to_csr(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
+                ("rp", _PI64), ("ci", _PI32), ("v", _PD)]
+
+
+TET_OPERATORS = ("c", "d", "m1", "m2", "q_sym")
+
+
+def tet_c_operators(n, jitter, seed, want=("c", "m2", "q_sym")):
+    """The 3-D Kuhn tet operators from the C restatement (oracle/tet_oracle.c):
+    dict name -> (rows, cols, row_ptr, col_idx, val), plus "counts" =
+    (N1, N2, T, SPAI columns that failed the pivot test). Test / reference-arm
+    infrastructure only."""
+    l = port_lib()
+    mask = sum(1 << TET_OPERATORS.index(w) for w in want)
+    outs = [to_csr() for _ in TET_OPERATORS]
+    counts = np.zeros(4, np.int64)
+    rc = l.to_build(int(n), float(jitter), int(seed), mask, *[C.byref(o) for o in outs],
+                    counts.ctypes.data_as(_PI64))
+    res = {"counts": tuple(int(x) for x in counts)}
+    try:
+        if rc != 0:
+            raise MemoryError("tet_oracle: allocation failed or bad arguments")
+        for name, o in zip(TET_OPERATORS, outs):
+            if name not in want:
+                continue
+            rp = np.ctypeslib.as_array(o.rp, (o.rows + 1,)).copy()
+            ci = np.ctypeslib.as_array(o.ci, (max(o.nnz, 1),))[:o.nnz].copy()
+            va = np.ctypeslib.as_array(o.v, (max(o.nnz, 1),))[:o.nnz].copy()
+            res[name] = (int(o.rows), int(o.cols), rp, ci, va)
+    finally:
+        for o in outs:
+            l.to_free(C.byref(o))
+    return res
 
 
 class _Csr:
