@@ -2,20 +2,24 @@
 """Benchmark of the B200 SFEEC leapfrog (BASELINE.json metric:
 "edge+face DOF-updates/sec per leapfrog step; achieved HBM GB/s vs peak").
 
-Default workload = BASELINE.json configs[1]: Yee special case, 256^3 cubical
-cells, lumped masses, PEC walls, Courant 0.5, fp64; E0 = 0, B0 = C A with
-seeded Gaussian A. A "step" is one leapfrog step over all N1 + N2 DOFs.
+Default workload = BASELINE.json configs[4], the largest single-GPU config:
+256^3 cubes x 6 Kuhn tets (100.7M tets), jitter 0.1h, first-order Whitney
+forms, S(M1) SPAI, PEC walls, 8 seeded Gaussian pulses in A, B0 = C A, E0 = 0,
+dt = 0.5 CFL, fp64. A "step" is one leapfrog step over all N1 + N2 DOFs
+(318.6M).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config yee256|yee256_f32|tet16|tet64|tet128|tet256]
+                  [--config tet256|tet128|tet16|yee256|yee256_f32|p2_64|...]
 
 Other configs: tet16 = configs[0] (16^3 x 6 tets, S(M1) SPAI, jitter 0.1),
-tet128 = configs[2] (128^3 x 6 tets, jitter 0.15, Gaussian pulse), tet256.
+yee256 = configs[1] (Yee/lumped-mass 256^3, PEC, Courant 0.5), tet128 =
+configs[2] (128^3 x 6 tets, jitter 0.15, Gaussian pulse), p2_64 = configs[3].
 Under torchrun (N > 1) the Yee configs run one 256^3 block per rank stacked in
 z (weak scaling); the tet configs split the one mesh into N z-slabs (strong
 scaling).
 `--impl reference` times the reference CPU step (oracle/_ref: the unmodified
-reference SplitScheme::step, dynamics.cpp:69-90) on the host cores.
+reference SplitScheme::step, dynamics.cpp:69-90) on the host cores, on
+operators built without the product library (_ref_operators).
 """
 from __future__ import annotations
 
@@ -37,10 +41,10 @@ METRIC = "edge+face DOF-updates/sec per leapfrog step; achieved HBM GB/s vs peak
 UNIT = "DOF-updates/s"
 
 CONFIGS = {
-    "yee256": dict(kind="yee", n=256, precision=8, dtype="f64", ref_n=128,
+    "yee256": dict(kind="yee", n=256, precision=8, dtype="f64", ref_n=256,
                    desc="BASELINE configs[1] Yee/lumped-mass SFEEC, 256^3 cells, PEC, "
                         "Courant 0.5"),
-    "yee256_f32": dict(kind="yee", n=256, precision=4, dtype="f32", ref_n=128,
+    "yee256_f32": dict(kind="yee", n=256, precision=4, dtype="f32", ref_n=256,
                        desc="BASELINE configs[1] Yee/lumped-mass SFEEC in fp32, 256^3 cells, "
                             "PEC, Courant 0.5"),
     "tet16": dict(kind="tet", n=16, jitter=0.1, init="gaussian", dtype="f64", ref_n=16,
@@ -48,16 +52,16 @@ CONFIGS = {
                        "SPAI, PEC, dt = 0.5 CFL"),
     "tet64": dict(kind="tet", n=64, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
                   desc="64^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) SPAI, PEC, pulse"),
-    "tet128": dict(kind="tet", n=128, jitter=0.15, init="pulse", dtype="f64", ref_n=64,
+    "tet128": dict(kind="tet", n=128, jitter=0.15, init="pulse", dtype="f64", ref_n=128,
                    desc="BASELINE configs[2]: 128^3 x 6 Kuhn tets, jitter 0.15h, P1-, S(M1) "
                         "SPAI, PEC, Gaussian pulse width 0.1, dt = 0.5 CFL"),
-    "p2_64": dict(kind="p2", n=64, jitter=0.1, init="gaussian", dtype="f64", ref_n=10,
+    "p2_64": dict(kind="p2", n=64, jitter=0.1, init="gaussian", dtype="f64", ref_n=3,
                   desc="BASELINE configs[3]: 64^3 x 6 Kuhn tets, jitter 0.1h, P2-, S(M1^2) "
                        "(2-ring) SPAI, PEC, dt = 0.5 CFL"),
-    "p2_32": dict(kind="p2", n=32, jitter=0.1, init="gaussian", dtype="f64", ref_n=10,
+    "p2_32": dict(kind="p2", n=32, jitter=0.1, init="gaussian", dtype="f64", ref_n=3,
                   desc="32^3 x 6 Kuhn tets, jitter 0.1h, P2-, S(M1^2) SPAI, PEC (smaller "
                        "config-4 system)"),
-    "tet256": dict(kind="tet", n=256, jitter=0.1, init="pulse", npulses=8, dtype="f64", ref_n=64,
+    "tet256": dict(kind="tet", n=256, jitter=0.1, init="pulse", npulses=8, dtype="f64", ref_n=128,
                    desc="BASELINE configs[4]: 256^3 x 6 Kuhn tets (100.7M tets), jitter 0.1h, "
                         "P1-, S(M1) SPAI, PEC, 8 Gaussian pulses, dt = 0.5 CFL"),
 }
@@ -239,13 +243,10 @@ def tet_setup(cfg, device):
         return (s._n1, s._n2), s, b0, np.zeros(s._n1), time.perf_counter() - t0
     s = S.tet_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
                             device=device)
-    mesh = S.TetMesh(cfg["n"], cfg["jitter"], 2023)  # host geometry for the initial A
-    xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
     if cfg["init"] == "gaussian":
         a = inputs.gaussian(7, s._n1)
-    else:
-        a = inputs.pulse_one_form(xyz, ev, 7, 0.1, cfg.get("npulses", 1))
-    del xyz, ev, mesh
+    else:  # host C++ projection of the pulses (sfeec_tetmesh_pulse)
+        a = S.TetMesh(cfg["n"], cfg["jitter"], 2023).pulse(7, 0.1, cfg.get("npulses", 1))
     b0 = s.apply("c", a)
     s.set_dt(configs.cfl_dt(s))
     setup_s = time.perf_counter() - t0
@@ -341,10 +342,8 @@ class TetSlabRunner:
         if cfg["init"] == "gaussian":
             a = inputs.gaussian_ids(7, np.arange(eg[0], eg[0] + er[0]))
         else:
-            mesh = S.TetMesh(cfg["n"], cfg["jitter"], 2023)
-            xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
-            a = inputs.pulse_one_form(xyz, ev[eg[0]:eg[0] + er[0]], 7, 0.1, cfg.get("npulses", 1))
-            del xyz, ev, mesh
+            a = S.TetMesh(cfg["n"], cfg["jitter"], 2023).pulse(7, 0.1, cfg.get("npulses", 1),
+                                                               eg[0], eg[0] + er[0])
         self.b0 = self.p.apply("c", a)                 # owned faces of C A
         self.e0 = np.zeros(eg[2] - eg[1])
         self.n1, self.n2 = ls.n1, ls.n2
@@ -472,7 +471,12 @@ def run_ours(args, rank, world, local_rank):
         e2e_s = float(t[0])
 
     peak, peak_src = hbm_peak()
-    achieved = kbytes / (k_avg_ms * 1e-3) / 1e9
+    # roofline of the dominant kernel: DRAM bytes per launch (ncu, committed
+    # under profiles/) over the CUDA-event launch time; the algorithmic count
+    # (SURVEY.md 8(d) bytes per launch) over the same time beside it
+    alg_achieved = kbytes / (k_avg_ms * 1e-3) / 1e9
+    traffic = committed_traffic(args.config)
+    achieved = traffic / (k_avg_ms * 1e-3) / 1e9 if traffic else alg_achieved
     ndof = R.ndof
     value = units * args.steps / (ms * 1e-3)
     step_gbs = R.step_bytes() / (ms / args.steps * 1e-3) / 1e9
@@ -497,7 +501,11 @@ def run_ours(args, rank, world, local_rank):
                          else "working set fits in L2 (latency-bound parity config)",
                    "kernel": R.kernel_label},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": committed_traffic(args.config),
+                     "frac": achieved / peak, "traffic": traffic,
+                     "basis": ("ncu dram__bytes_read+write per launch (profiles/traffic.json) / "
+                               "CUDA-event average launch time" if traffic else
+                               "algorithmic bytes per launch / CUDA-event average launch time"),
+                     "algorithmic_achieved": alg_achieved, "algorithmic_frac": alg_achieved / peak,
                      "kernel": kname, "bytes_per_launch": kbytes, "kernel_avg_ms": k_avg_ms,
                      "step_bytes": R.step_bytes(), "step_achieved_gbs": step_gbs,
                      "peak_source": peak_src},
@@ -549,61 +557,104 @@ def committed_traffic(config):
 
 
 def _ref_operators(config):
-    """(q, c, m2, b0, e0, label) for the reference CPU arm at the sample size."""
-    import paper_2301_01753_b200 as S
+    """(q, c, m2, b0, e0, dt, label, same_config) for the reference CPU arm,
+    built WITHOUT the product library (that arm must not map it): the
+    reference's own periodic cubical lattice (mesh_cubical.cpp + the Q1 curl,
+    through oracle/_ref) for Yee, the C restatement oracle/tet_oracle.c for
+    first-order tets, the numpy restatement oracle/p2_oracle.py for P2-."""
+    from oracle import oracle as O
     cfg = CONFIGS[config]
     n = cfg["ref_n"]
-    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)
     if cfg["kind"] == "yee":
-        from paper_2301_01753_b200 import inputs
-        from paper_2301_01753_b200.configs import spmv
+        # yee_equivalence_check's lumped system (yee.cpp:95-121) on the
+        # reference's periodic n^3 lattice: same per-DOF operators as the PEC
+        # workload (7-point curl pairs, diagonal Q and M2), no walls
         h = 1.0 / n
-        c, _ = S.yee_operators(n, n, n, h, h, h, bc=1)
+        c = O.ref_cubical_curl(n, n, n, h, h, h)
+        n1, n2 = c[1], c[0]
         dv = h ** 3
-        n1, n2 = c.cols, c.rows
         q = (n1, n1, np.arange(n1 + 1), np.arange(n1, dtype=np.int32), np.full(n1, 1.0 / dv))
         m2 = (n2, n2, np.arange(n2 + 1), np.arange(n2, dtype=np.int32), np.full(n2, dv))
-        a = inputs.gaussian(20260101, n1)
-        return q, tup(c), m2, spmv(c, a), np.zeros(n1), 0.5 / (np.sqrt(3.0) * n), \
-            f"{n}^3 PEC Yee lattice (lumped masses)"
-    from paper_2301_01753_b200 import configs
+        a = O.port_uniform(20260101, n1)
+        return (q, c, m2, O.port_spmv(c, a), np.zeros(n1), 0.5 / (np.sqrt(3.0) * n),
+                f"{n}^3 periodic cubical lattice of the reference (mesh_cubical.cpp), lumped "
+                "masses", n == cfg["n"])
     if cfg["kind"] == "p2":
-        from paper_2301_01753_b200 import inputs
-        from paper_2301_01753_b200.configs import spmv
-        mesh = S.TetMesh(n, cfg["jitter"], 2023)
-        c, m1, m2 = mesh.p2_operator("c"), mesh.p2_operator("m1"), mesh.p2_operator("m2")
-        q, _ = S.spai_approximate_inverse(m1, "m1sq")
-        a = inputs.gaussian(7, c.cols)
-        return tup(q), tup(c), tup(m2), spmv(c, a), np.zeros(c.cols), 1e-3, \
-            f"{n}^3 x 6 Kuhn tets (P2-, S(M1^2) SPAI)"
-    sys_ = configs.tet_system(n, cfg["jitter"], seed=2023)
-    b0, e0, _ = (configs.initial_gaussian(sys_, seed=7) if cfg["init"] == "gaussian"
-                 else configs.initial_pulse(sys_, seed=7))
-    return tup(sys_.q), tup(sys_.c), tup(sys_.m2), b0, e0, 1e-3, \
-        f"{n}^3 x 6 Kuhn tets (P1-, S(M1) SPAI)"
+        from oracle.p2_oracle import OracleP2
+        from oracle.tetmesh_oracle import OracleTetMesh, pattern, spai_lstsq
+
+        def csr(rows, ncols):
+            rp = np.cumsum([0] + [len(r) for r in rows]).astype(np.int64)
+            return (len(rows), ncols, rp, np.array([c for r in rows for c, _ in r], np.int32),
+                    np.array([v for r in rows for _, v in r]))
+        P = OracleP2(OracleTetMesh(n, cfg["jitter"], 2023))
+        c, m1, m2 = (csr(P.curl_rows(), P.n1), csr(P.mass_rows(1), P.n1),
+                     csr(P.mass_rows(2), P.n2))
+        pat = pattern(m1, "m1sq")  # S(M1^2), spai.cpp:31-72
+        cols = spai_lstsq(m1, pat)
+        qr = np.concatenate([np.asarray(p_, np.int64) for p_ in pat])
+        qc = np.repeat(np.arange(P.n1), [len(p_) for p_ in pat])
+        order = np.lexsort((qc, qr))
+        q = (P.n1, P.n1, np.searchsorted(qr[order], np.arange(P.n1 + 1)).astype(np.int64),
+             qc[order].astype(np.int32), np.concatenate(cols)[order])
+        a = O.port_uniform(7, P.n1)
+        return (q, c, m2, O.port_spmv(c, a), np.zeros(P.n1), 1e-3,
+                f"{n}^3 x 6 Kuhn tets (P2-, S(M1^2) SPAI; operators from the numpy "
+                "restatement oracle/p2_oracle.py)", n == cfg["n"])
+    r = O.tet_c_operators(n, cfg["jitter"], 2023)
+    c = r["c"]
+    a = O.port_uniform(7, c[1])
+    return (r["q_sym"], c, r["m2"], O.port_spmv(c, a), np.zeros(c[1]), 1e-3,
+            f"{n}^3 x 6 Kuhn tets (P1-, S(M1) SPAI; operators from the C restatement "
+            "oracle/tet_oracle.c)", n == cfg["n"])
 
 
-def cpu_reference_sample(config, budget_s=20.0, max_steps=1000):
+def _omp_threads(k):
+    """Set the OpenMP thread count of this process (libgomp, shared by the
+    reference library)."""
+    import ctypes as C
+    C.CDLL("libgomp.so.1").omp_set_num_threads(int(k))
+
+
+def cpu_reference_sample(config, budget_s=20.0, max_steps=1000, threads=None):
     """The reference SplitScheme::step (oracle/_ref, unmodified reference
-    sources) on the same per-DOF workload, timed on the host cores."""
+    sources) on the same per-DOF workload, timed on the host cores: with all
+    host threads (`value`) and with one (`value_1thread`)."""
     from oracle import oracle as O
+    cores = os.cpu_count()
     if not O.ref_available():
-        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+        return {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": "oracle/_ref missing"}
-    q, c, m2, b, e, dt, label = _ref_operators(config)
+    t0 = time.perf_counter()
+    q, c, m2, b, e, dt, label, same = _ref_operators(config)
     ref = O.RefScheme(1, dt, q, c, m2)
+    setup_s = time.perf_counter() - t0
     n1, n2 = c[1], c[0]
-    b, e, _, _ = ref.steps(True, b, e, 1)  # warm-up
-    steps, secs = 0, 0.0
-    while secs < budget_s and steps < max_steps:
-        b, e, _, _ = ref.steps(True, b, e, 1)
-        secs += ref.last_seconds
-        steps += 1
-    return {"value": (n1 + n2) * steps / secs, "unit": UNIT, "cores": os.cpu_count(),
-            "kind": "reference",
-            "sample": f"{steps} x reference SplitScheme::step (Strang, BE) on the {label} "
-                      f"(N1+N2={n1 + n2}), wall clock, OpenMP threads = all {os.cpu_count()} "
-                      "host cores; same per-DOF operator structure as the GPU workload"}
+
+    def timed(nthreads, budget):
+        nonlocal b, e
+        _omp_threads(nthreads)
+        b, e, _, _ = ref.steps(True, b, e, 1)  # warm-up
+        steps, secs = 0, 0.0
+        while secs < budget and steps < max_steps:
+            b, e, _, _ = ref.steps(True, b, e, 1)
+            secs += ref.last_seconds
+            steps += 1
+        return (n1 + n2) * steps / secs, steps, secs
+
+    v_all, k_all, s_all = timed(threads or cores, budget_s)
+    v_one, k_one, s_one = timed(1, max(budget_s / 2, 5.0))
+    _omp_threads(cores)
+    return {"value": v_all, "unit": UNIT, "cores": threads or cores, "kind": "reference",
+            "value_1thread": v_one,
+            "same_config": bool(same),
+            "sample": f"{k_all} x reference SplitScheme::step (Strang, BE) on the {label} "
+                      f"(N1+N2={n1 + n2}), wall clock {s_all:.1f} s, OpenMP threads = "
+                      f"{threads or cores}; and {k_one} steps ({s_one:.1f} s) on 1 thread"
+                      + ("" if same else "; the workload's own size is infeasible for the "
+                         "reference (int32 triplet overflow in symmetric_part at 256^3, "
+                         "BASELINE.md 5), so this is the largest feasible size, compared "
+                         "per DOF") + f"; operator setup {setup_s:.0f} s untimed"}
 
 
 def run_reference(args, rank, world):
@@ -652,7 +703,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="yee256")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="tet256")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="tet configs at N=1: run the z-slab partition path (one slab)")

@@ -289,6 +289,11 @@ int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_ve
                            int64_t* face_vertices, int64_t* tet_vertices);
 /* which: 0 C (faces x interior edges, +-1), 1 M1 (interior edges), 2 M2
  * (faces), 3 D (tets x faces, +-1) */
+/* Gaussian-pulse initial potential on the DOF edges [e0, e1) (configs 3 and 5;
+ * DESIGN.md 6.4): a_e = int_e sum_k exp(-|x - x0_k|^2 / (2 sigma^2)) p_k . dx by
+ * 3-point Gauss-Legendre; x0, p: 3 * npulses each. Host (OpenMP). */
+int sfeec_tetmesh_pulse(const sfeec_tetmesh* h, int npulses, const double* x0, const double* p,
+                        double sigma, int64_t e0, int64_t e1, double* out);
 int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
 /* Second-order trimmed forms P2^- on the same mesh (BASELINE config 4; the
  * reference's P2^- is 2-D only, form_space.cpp:41-166 -- the 3-D element

@@ -386,6 +386,50 @@ int sfeec_tetmesh_counts(const sfeec_tetmesh* h, int64_t* n_vertices, int64_t* n
   });
 }
 
+// Canonical projection of a sum of Gaussian pulses onto the DOF edges
+// [e0, e1): a_e = int_e A . dx with A = sum_k exp(-|x - x0_k|^2 / (2 sigma^2))
+// p_k, 3-point Gauss-Legendre along the edge (the P1 integral DOF of the
+// reference form_space.cpp:410-429). The pulse parameters come from
+// inputs.pulse_params; inputs.pulse_one_form is the numpy statement of the
+// same sum (tests compare the two).
+int sfeec_tetmesh_pulse(const sfeec_tetmesh* h, int npulses, const double* x0, const double* p,
+                        double sigma, int64_t e0, int64_t e1, double* out) {
+  return guarded([&] {
+    require(h && out && (npulses == 0 || (x0 && p)), "null argument");
+    const TetMesh& m = h->m;
+    require(e0 >= 0 && e0 <= e1 && e1 <= m.n_edges, "pulse: edge range out of bounds");
+    const double q = std::sqrt(0.6);
+    const double gs[3] = {0.5 - 0.5 * q, 0.5, 0.5 + 0.5 * q};
+    const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    const double inv = 1.0 / (2.0 * sigma * sigma);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      int64_t v[2];
+      m.edge_vertices(e, v);
+      double xa[3], d[3];
+      for (int c = 0; c < 3; ++c) {
+        xa[c] = m.xyz[(size_t)(3 * v[0] + c)];
+        d[c] = m.xyz[(size_t)(3 * v[1] + c)] - xa[c];
+      }
+      double a = 0.0;
+      for (int k = 0; k < npulses; ++k) {
+        const double* c0 = x0 + 3 * k;
+        const double* pk = p + 3 * k;
+        const double tang = (d[0] * pk[0] + d[1] * pk[1]) + d[2] * pk[2];
+        for (int s = 0; s < 3; ++s) {
+          double r2 = 0.0;
+          for (int c = 0; c < 3; ++c) {
+            const double x = (xa[c] + gs[s] * d[c]) - c0[c];
+            r2 += x * x;
+          }
+          a += gw[s] * std::exp(-r2 * inv) * tang;
+        }
+      }
+      out[e - e0] = a;
+    }
+  });
+}
+
 int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_vertices,
                            int64_t* face_vertices, int64_t* tet_vertices) {
   return guarded([&] {

@@ -532,6 +532,20 @@ class TetMesh:
                                                L.i64ptr(tv) if tets else None))
         return xyz, ev, fv, tv
 
+    def pulse(self, seed: int, sigma: float = 0.1, npulses: int = 1, e0: int = 0,
+              e1: int | None = None) -> np.ndarray:
+        """Gaussian-pulse potential on DOF edges [e0, e1) (host C++, OpenMP):
+        the same sum as inputs.pulse_one_form, without the geometry arrays."""
+        from .inputs import pulse_params
+        e1 = self.n_edges if e1 is None else int(e1)
+        pp = pulse_params(seed, npulses)
+        x0 = np.ascontiguousarray([x for x, _ in pp], np.float64).reshape(-1)
+        pv = np.ascontiguousarray([q for _, q in pp], np.float64).reshape(-1)
+        out = np.zeros(max(e1 - int(e0), 0))
+        L.check(L.lib().sfeec_tetmesh_pulse(self._h, int(npulses), L.dptr(x0), L.dptr(pv),
+                                            float(sigma), int(e0), e1, L.dptr(out)))
+        return out
+
     def _op(self, which, symmetric=False) -> SparseOperator:
         out = L.sfeec_csr_owned()
         L.check(L.lib().sfeec_tetmesh_operator(self._h, which, C.byref(out)))

@@ -123,3 +123,16 @@ def test_pec_numbering_roundtrip_and_orientation():
     assert row == want
     # boundary face x = 0 has no interior edges
     assert c.row_ptr[face_id(0, 0, 1, 1) + 1] == c.row_ptr[face_id(0, 0, 1, 1)]
+
+
+@pytest.mark.parametrize("n,npulses", [(6, 1), (9, 8)])
+def test_host_pulse_projection_matches_numpy(n, npulses):
+    """sfeec_tetmesh_pulse (host C++) = inputs.pulse_one_form (numpy), to
+    rounding; edge sub-ranges are slices of the whole."""
+    from paper_2301_01753_b200 import inputs
+    m = S.TetMesh(n, 0.1, 2023)
+    xyz, ev, _, _ = m.geometry(faces=False, tets=False)
+    want = inputs.pulse_one_form(xyz, ev, 7, 0.1, npulses)
+    got = m.pulse(7, 0.1, npulses)
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+    assert np.array_equal(m.pulse(7, 0.1, npulses, 10, 200), got[10:200])
