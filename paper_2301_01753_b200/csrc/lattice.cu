@@ -1,0 +1,374 @@
+// Kuhn-lattice kernels of the first-order leapfrog (lattice.cuh, DESIGN.md
+// 3.4): one thread per vertex computes all edge (7) or face (12) rows of its
+// vertex. Every stencil is unrolled at compile time from lattice_tables.hpp,
+// so each neighbour read is a constant offset from the thread's position:
+// 32 lanes = 32 consecutive positions of a padded row -> coalesced loads of
+// the coefficient and field arrays, no index streams.
+//
+// Summation order per row = the slot order (dk, dj, type, di), which is the
+// ascending column order of the k-major numbering for rows away from the
+// 32-vertex x-block edges: those rows are summed exactly like the sliced /
+// ELL kernels (spmv_kernels.cu) sum their CSR rows.
+#include <utility>
+#include <vector>
+
+#include "lattice.cuh"
+#include "lattice_tables.hpp"
+
+namespace sfeec_b200 {
+
+namespace {
+
+constexpr int kLT = 256;  // threads per block (positions of one padded plane)
+
+SFEEC_HD constexpr int et(int t, int d) {
+  constexpr int v[7][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, 1, 0},
+                           {0, 1, 1}, {1, 0, 1}, {1, 1, 1}};
+  return v[t][d];
+}
+// second (largest) edge type of face type f (kFT[f][1])
+SFEEC_HD constexpr int ft_hi(int f) {
+  constexpr int v[12] = {3, 3, 4, 4, 5, 5, 6, 6, 6, 6, 6, 6};
+  return v[f];
+}
+
+// operator policies over the generated tables
+struct QOp {
+  static constexpr int kTypes = lat::kQTypes;
+  static constexpr int kArrays = lat::kQArrays;
+  SFEEC_HD static constexpr lat::Slot tab(int s) { return lat::kQTab(s); }
+  SFEEC_HD static constexpr int slot_off(int t) { return lat::kQSlotOff(t); }
+  SFEEC_HD static constexpr int canon_off(int t) { return lat::kQCanonOff(t); }
+};
+struct MOp {
+  static constexpr int kTypes = lat::kMTypes;
+  static constexpr int kArrays = lat::kMArrays;
+  SFEEC_HD static constexpr lat::Slot tab(int s) { return lat::kMTab(s); }
+  SFEEC_HD static constexpr int slot_off(int t) { return lat::kMSlotOff(t); }
+  SFEEC_HD static constexpr int canon_off(int t) { return lat::kMCanonOff(t); }
+};
+
+__device__ __forceinline__ int64_t offset_of(const LatGeom& g, int di, int dj, int dk) {
+  return di + (int64_t)g.S * dj + g.PS * dk;
+}
+
+// this thread's vertex (i, j, k) and lattice position; false off the cube
+__device__ __forceinline__ bool my_vertex(const LatGeom& g, int& i, int& j, int& k,
+                                          int64_t& idx) {
+  const int p = blockIdx.x * kLT + threadIdx.x;
+  if (p >= g.PS) return false;
+  k = blockIdx.y;
+  j = p / g.S - 1;
+  i = p - (j + 1) * g.S - 1;
+  idx = g.PS * (k + 1) + p;
+  return i >= 0 && i <= g.n && j >= 0 && j <= g.n;
+}
+
+// edge (v, t) is a DOF: inside the cube and not on a wall it lies in (PEC)
+template <int T>
+__device__ __forceinline__ bool edge_dof(int i, int j, int k, int n) {
+  const int c[3] = {i, j, k};
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    ok = ok && c[d] + et(T, d) <= n;
+    if (et(T, d) == 0) ok = ok && c[d] != 0 && c[d] != n;
+  }
+  return ok;
+}
+// face (v, f) exists: its farthest vertex is inside the cube
+template <int F>
+__device__ __forceinline__ bool face_ok(int i, int j, int k, int n) {
+  return i + et(ft_hi(F), 0) <= n && j + et(ft_hi(F), 1) <= n && k + et(ft_hi(F), 2) <= n;
+}
+
+// ---- symmetric stencil rows (Q_sym, M2) ------------------------------------
+template <class Op, int S>
+__device__ __forceinline__ void sym_term(double& acc, const double* __restrict__ coef,
+                                         const double* __restrict__ x, int64_t idx,
+                                         const LatGeom& g) {
+  constexpr lat::Slot sl = Op::tab(S);
+  const int64_t off = offset_of(g, sl.di, sl.dj, sl.dk);
+  const double c =
+      __ldg(coef + (int64_t)(Op::canon_off(sl.st) + sl.si) * g.NP + idx + (sl.mirror ? off : 0));
+  acc = fma(c, __ldg(x + (int64_t)sl.t * g.NP + idx + off), acc);
+}
+template <class Op, int T, int... I>
+__device__ __forceinline__ double sym_row(std::integer_sequence<int, I...>,
+                                          const double* __restrict__ coef,
+                                          const double* __restrict__ x, int64_t idx,
+                                          const LatGeom& g) {
+  double acc = 0.0;
+  (sym_term<Op, Op::slot_off(T) + I>(acc, coef, x, idx, g), ...);
+  return acc;
+}
+template <class Op, int T>
+__device__ __forceinline__ double sym_row(const double* __restrict__ coef,
+                                          const double* __restrict__ x, int64_t idx,
+                                          const LatGeom& g) {
+  return sym_row<Op, T>(std::make_integer_sequence<int, Op::slot_off(T + 1) - Op::slot_off(T)>{},
+                        coef, x, idx, g);
+}
+
+// t = Q_sym e on the DOF edges of one vertex (7 rows)
+template <int... Ts>
+__device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, const LatGeom& g,
+                                         int i, int j, int k, int64_t idx,
+                                         const double* __restrict__ qc,
+                                         const double* __restrict__ E, double* __restrict__ T) {
+  const double r[sizeof...(Ts)] = {sym_row<QOp, Ts>(qc, E, idx, g)...};
+  ((edge_dof<Ts>(i, j, k, g.n) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
+}
+__global__ void __launch_bounds__(kLT) k_lat_q(LatGeom g, const double* __restrict__ qc,
+                                               const double* __restrict__ E,
+                                               double* __restrict__ T) {
+  int i, j, k;
+  int64_t idx;
+  if (!my_vertex(g, i, j, k, idx)) return;
+  q_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, qc, E, T);
+}
+
+// u = M2 b on the faces of one vertex (12 rows)
+template <int... Fs>
+__device__ __forceinline__ void m2_vertex(std::integer_sequence<int, Fs...>, const LatGeom& g,
+                                          int i, int j, int k, int64_t idx,
+                                          const double* __restrict__ mc,
+                                          const double* __restrict__ B, double* __restrict__ U) {
+  const double r[sizeof...(Fs)] = {sym_row<MOp, Fs>(mc, B, idx, g)...};
+  ((face_ok<Fs>(i, j, k, g.n) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
+}
+__global__ void __launch_bounds__(kLT) k_lat_m2(LatGeom g, const double* __restrict__ mc,
+                                                const double* __restrict__ B,
+                                                double* __restrict__ U) {
+  int i, j, k;
+  int64_t idx;
+  if (!my_vertex(g, i, j, k, idx)) return;
+  m2_vertex(std::make_integer_sequence<int, 12>{}, g, i, j, k, idx, mc, B, U);
+}
+
+// ---- incidence rows (C, C^T): signed sums, then y = fma(alpha, sum, y) ----
+template <bool TRANS, int S>
+__device__ __forceinline__ void inc_term(double& acc, const double* __restrict__ x, int64_t idx,
+                                         const LatGeom& g) {
+  constexpr lat::CSlot sl = TRANS ? lat::kCTTab(S) : lat::kCTab(S);
+  const double v = __ldg(x + (int64_t)sl.t * g.NP + idx + offset_of(g, sl.di, sl.dj, sl.dk));
+  acc += sl.sign > 0 ? v : -v;
+}
+template <bool TRANS, int BASE, int... I>
+__device__ __forceinline__ double inc_row(std::integer_sequence<int, I...>,
+                                          const double* __restrict__ x, int64_t idx,
+                                          const LatGeom& g) {
+  double acc = 0.0;
+  (inc_term<TRANS, BASE + I>(acc, x, idx, g), ...);
+  return acc;
+}
+// b -= h C t on the faces of one vertex
+template <int... Fs>
+__device__ __forceinline__ void cb_vertex(std::integer_sequence<int, Fs...>, const LatGeom& g,
+                                          int i, int j, int k, int64_t idx, double alpha,
+                                          const double* __restrict__ T, double* __restrict__ B) {
+  const double r[sizeof...(Fs)] = {
+      inc_row<false, 3 * Fs>(std::make_integer_sequence<int, 3>{}, T, idx, g)...};
+  ((face_ok<Fs>(i, j, k, g.n)
+        ? (void)(B[(int64_t)Fs * g.NP + idx] = fma(alpha, r[Fs], B[(int64_t)Fs * g.NP + idx]))
+        : (void)0),
+   ...);
+}
+__global__ void __launch_bounds__(kLT) k_lat_cb(LatGeom g, double alpha,
+                                                const double* __restrict__ T,
+                                                double* __restrict__ B) {
+  int i, j, k;
+  int64_t idx;
+  if (!my_vertex(g, i, j, k, idx)) return;
+  cb_vertex(std::make_integer_sequence<int, 12>{}, g, i, j, k, idx, alpha, T, B);
+}
+// e += f C^T u on the DOF edges of one vertex
+template <int... Ts>
+__device__ __forceinline__ void cte_vertex(std::integer_sequence<int, Ts...>, const LatGeom& g,
+                                           int i, int j, int k, int64_t idx, double alpha,
+                                           const double* __restrict__ U, double* __restrict__ E) {
+  const double r[sizeof...(Ts)] = {inc_row<true, lat::kCTOff(Ts)>(
+      std::make_integer_sequence<int, lat::kCTOff(Ts + 1) - lat::kCTOff(Ts)>{}, U, idx, g)...};
+  ((edge_dof<Ts>(i, j, k, g.n)
+        ? (void)(E[(int64_t)Ts * g.NP + idx] = fma(alpha, r[Ts], E[(int64_t)Ts * g.NP + idx]))
+        : (void)0),
+   ...);
+}
+__global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, double alpha,
+                                                 const double* __restrict__ U,
+                                                 double* __restrict__ E) {
+  int i, j, k;
+  int64_t idx;
+  if (!my_vertex(g, i, j, k, idx)) return;
+  cte_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, alpha, U, E);
+}
+
+// ---- setup: coefficient arrays from a CSR of the k-major numbering -----------
+// Entry (r, c) of row type t at offset off: the slot of t's stencil with
+// (type(c), off); canonical slots store the value at the row's position.
+template <class Op, int T, int... I>
+__device__ __forceinline__ bool fill_match(std::integer_sequence<int, I...>, int t2,
+                                           int64_t off, const LatGeom& g, double v,
+                                           double* __restrict__ coef, int64_t idx) {
+  bool found = false;
+  (
+      [&] {
+        constexpr lat::Slot sl = Op::tab(Op::slot_off(T) + I);
+        if (!found && sl.t == t2 && off == offset_of(g, sl.di, sl.dj, sl.dk)) {
+          found = true;
+          if (!sl.mirror) coef[(int64_t)(Op::canon_off(T) + sl.si) * g.NP + idx] = v;
+        }
+      }(),
+      ...);
+  return found;
+}
+template <class Op, int... Ts>
+__device__ __forceinline__ bool fill_dispatch(std::integer_sequence<int, Ts...>, int t, int t2,
+                                              int64_t off, const LatGeom& g, double v,
+                                              double* __restrict__ coef, int64_t idx) {
+  bool found = false;
+  ((t == Ts ? (void)(found = fill_match<Op, Ts>(
+                         std::make_integer_sequence<int, Op::slot_off(Ts + 1) - Op::slot_off(Ts)>{},
+                         t2, off, g, v, coef, idx))
+            : (void)0),
+   ...);
+  return found;
+}
+template <class Op>
+__global__ void k_lat_fill(int64_t rows, const int64_t* __restrict__ rp,
+                           const int32_t* __restrict__ ci, const double* __restrict__ val,
+                           const int64_t* __restrict__ pos, LatGeom g, double* __restrict__ coef,
+                           int* __restrict__ bad) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t p = pos[r];
+  const int t = (int)(p / g.NP);
+  const int64_t idx = p - (int64_t)t * g.NP;
+  for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
+    const int64_t pc = pos[ci[q]];
+    const int t2 = (int)(pc / g.NP);
+    const int64_t off = (pc - (int64_t)t2 * g.NP) - idx;
+    if (!fill_dispatch<Op>(std::make_integer_sequence<int, Op::kTypes>{}, t, t2, off, g, val[q],
+                           coef, idx))
+      atomicExch(bad, 1);
+  }
+}
+
+__global__ void k_lat_scatter(int64_t n, const int64_t* __restrict__ pos,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) dst[pos[r]] = src[r];
+}
+__global__ void k_lat_gather(int64_t n, const int64_t* __restrict__ pos,
+                             const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) dst[r] = src[pos[r]];
+}
+
+inline unsigned blocks(int64_t n) { return (unsigned)((n + kLT - 1) / kLT); }
+
+}  // namespace
+
+void Lattice::build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2,
+                    cudaStream_t s) {
+  g.init(mesh.n);
+  n1 = mesh.n_edges;
+  n2 = mesh.n_faces;
+  require(qsym.rows == n1 && m2.rows == n2, "lattice: operator dimensions do not match the mesh");
+  {  // DOF -> lattice position (component * NP + vertex position)
+    std::vector<int64_t> ep((size_t)n1), fp((size_t)n2);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n1; ++r) {
+      int c[3];
+      mesh.coords(mesh.edge_v[(size_t)r], c);
+      ep[(size_t)r] = (int64_t)mesh.edge_t[(size_t)r] * g.NP + g.pos(c[0], c[1], c[2]);
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n2; ++r) {
+      int c[3];
+      mesh.coords(mesh.face_v[(size_t)r], c);
+      fp[(size_t)r] = (int64_t)mesh.face_t[(size_t)r] * g.NP + g.pos(c[0], c[1], c[2]);
+    }
+    epos.upload(ep.data(), ep.size(), s);
+    fpos.upload(fp.data(), fp.size(), s);
+    SFEEC_CUDA(cudaStreamSynchronize(s));  // the host vectors die here
+  }
+  qc.alloc((size_t)(lat::kQArrays * g.NP));
+  mc.alloc((size_t)(lat::kMArrays * g.NP));
+  qc.zero(s);
+  mc.zero(s);
+  DevBuf<int> bad;
+  bad.alloc(1);
+  bad.zero(s);
+  if (n1)
+    k_lat_fill<QOp><<<blocks(n1), kLT, 0, s>>>(n1, qsym.rp.p, qsym.ci.p, qsym.val.p, epos.p, g,
+                                                qc.p, bad.p);
+  if (n2)
+    k_lat_fill<MOp><<<blocks(n2), kLT, 0, s>>>(n2, m2.rp.p, m2.ci.p, m2.val.p, fpos.p, g, mc.p,
+                                               bad.p);
+  SFEEC_LAUNCH_CHECK();
+  int hbad = 0;
+  SFEEC_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  require(hbad == 0, "lattice: an operator entry lies outside the Kuhn-lattice stencil");
+  for (auto* b : {&E, &T}) {
+    b->alloc((size_t)(7 * g.NP));
+    b->zero(s);
+  }
+  for (auto* b : {&B, &U}) {
+    b->alloc((size_t)(12 * g.NP));
+    b->zero(s);
+  }
+  SFEEC_CUDA(cudaStreamSynchronize(s));
+  valid = newer = false;
+}
+
+void Lattice::scatter(const double* b, const double* e, cudaStream_t s) {
+  if (n2) k_lat_scatter<<<blocks(n2), kLT, 0, s>>>(n2, fpos.p, b, B.p);
+  if (n1) k_lat_scatter<<<blocks(n1), kLT, 0, s>>>(n1, epos.p, e, E.p);
+  SFEEC_LAUNCH_CHECK();
+}
+
+void Lattice::gather(double* b, double* e, cudaStream_t s) const {
+  if (n2) k_lat_gather<<<blocks(n2), kLT, 0, s>>>(n2, fpos.p, B.p, b);
+  if (n1) k_lat_gather<<<blocks(n1), kLT, 0, s>>>(n1, epos.p, E.p, e);
+  SFEEC_LAUNCH_CHECK();
+}
+
+void Lattice::apply_q(cudaStream_t s) const {
+  k_lat_q<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+  SFEEC_LAUNCH_CHECK();
+}
+void Lattice::apply_cb(double h, cudaStream_t s) const {
+  k_lat_cb<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, -h, T.p, B.p);
+  SFEEC_LAUNCH_CHECK();
+}
+void Lattice::apply_m2(cudaStream_t s) const {
+  k_lat_m2<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+  SFEEC_LAUNCH_CHECK();
+}
+void Lattice::apply_cte(double f, cudaStream_t s) const {
+  k_lat_cte<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, f, U.p, E.p);
+  SFEEC_LAUNCH_CHECK();
+}
+
+// bytes per launch (each array read once, each output written once; the
+// padded halo is not counted): V vertices, 8 B per value
+double Lattice::bytes_q() const {
+  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
+  return 8.0 * (lat::kQArrays * V + 7.0 * V + (double)n1);
+}
+double Lattice::bytes_cb() const {
+  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
+  return 8.0 * (7.0 * V + 2.0 * (double)n2);
+}
+double Lattice::bytes_m2() const {
+  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
+  return 8.0 * (lat::kMArrays * V + 12.0 * V + (double)n2);
+}
+double Lattice::bytes_cte() const {
+  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
+  return 8.0 * (12.0 * V + 2.0 * (double)n1);
+}
+
+}  // namespace sfeec_b200

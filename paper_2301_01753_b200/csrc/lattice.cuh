@@ -1,0 +1,72 @@
+// Kuhn-lattice layout of the first-order tet leapfrog (configs 1, 3, 5;
+// DESIGN.md 3.4). The DOFs of the k-major numbering live in vertex-lattice
+// component arrays instead: e and t as 7 arrays (edge types), b and u as 12
+// (face types), each over the (n+3)^3 padded vertex box (one zero halo layer,
+// so every stencil read stays in bounds). Non-DOF slots (PEC wall edges,
+// faces outside the cube) hold 0 and are never written.
+//
+// Q_sym and M2 are stored as per-vertex coefficient arrays, one per
+// "canonical" stencil slot (lattice_tables.hpp): both operators are exactly
+// symmetric, so each off-diagonal pair is stored once and the transposed slot
+// reads it at the neighbour's position. C and C^T are structural (+-1 by the
+// ascending-vertex orientation) and stream nothing. Column indices are not
+// stored at all: the lattice position of a neighbour is its row's position
+// plus a constant offset. Per vertex and step: 61 Q and 48 M2 coefficients
+// (8 B each) instead of 115 + 84 entries at 12 B in the CSR/sliced layouts.
+#pragma once
+#include <memory>
+
+#include "device_util.cuh"
+#include "tet_mesh.hpp"
+
+namespace sfeec_b200 {
+
+struct LatGeom {
+  int n = 0;        // cubes per axis (vertices 0..n)
+  int S = 0;        // padded vertices per axis (n + 3)
+  int64_t PS = 0;   // padded plane (S * S)
+  int64_t NP = 0;   // padded box (S^3): the component stride
+  int64_t org = 0;  // position of vertex (0, 0, 0)
+  void init(int n_) {
+    n = n_;
+    S = n + 3;
+    PS = (int64_t)S * S;
+    NP = PS * S;
+    org = PS + S + 1;
+  }
+  int64_t pos(int i, int j, int k) const { return org + i + (int64_t)S * j + PS * k; }
+};
+
+struct Lattice {
+  LatGeom g;
+  int64_t n1 = 0, n2 = 0;
+  DevBuf<double> qc;         // kQArrays * NP: canonical Q_sym coefficients
+  DevBuf<double> mc;         // kMArrays * NP: canonical M2 coefficients
+  DevBuf<double> E, T, B, U;  // 7, 7, 12, 12 components * NP
+  DevBuf<int64_t> epos, fpos;  // DOF id -> component * NP + position
+  bool pdl = true;
+  // state bookkeeping of the owning handle: `valid` = E/B hold the handle's
+  // state (or a newer one), `newer` = the DOF vectors are stale
+  bool valid = false, newer = false;
+
+  // coefficient arrays from the device CSRs of the k-major numbering (the
+  // CSRs are read, not consumed); throws if an entry falls outside the
+  // interior stencil (it cannot for the Kuhn mesh)
+  void build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2, cudaStream_t s);
+  // DOF vectors <-> lattice state
+  void scatter(const double* b, const double* e, cudaStream_t s);
+  void gather(double* b, double* e, cudaStream_t s) const;
+  // the four step kernels
+  void apply_q(cudaStream_t s) const;               // T = Q_sym E
+  void apply_cb(double h, cudaStream_t s) const;    // B -= h C T
+  void apply_m2(cudaStream_t s) const;              // U = M2 B
+  void apply_cte(double f, cudaStream_t s) const;   // E += f C^T U
+  // bytes each kernel moves (arrays read once, outputs written once)
+  double bytes_q() const;
+  double bytes_cb() const;
+  double bytes_m2() const;
+  double bytes_cte() const;
+  double step_bytes() const { return bytes_q() + bytes_cb() + bytes_m2() + bytes_cte(); }
+};
+
+}  // namespace sfeec_b200

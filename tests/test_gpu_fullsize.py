@@ -1,15 +1,26 @@
-"""GPU parity at BASELINE.json's full sizes, where the CPU oracle cannot run
-every step: size-independent properties of the scheme plus a few oracle steps.
+"""GPU parity at BASELINE.json's stated sizes: the shipped default kernels run
+against the CPU oracle (the C port of SplitScheme::step, bitwise the
+unmodified reference on the same operators; dynamics.cpp:69-102) for as many
+steps as the oracle finishes in about a minute, plus size-independent
+properties over the configs' full step counts.
 
-config 2 (Yee 256^3, PEC, 1000 steps): Gauss law D b = 0 kept to round-off,
-symplectic energy bounded, fused TMA sweep == unfused kernels, fp32 tracks
-fp64. config 3 (128^3 x 6 tets, device-assembled S(M1) system): 5 production
-steps against the C oracle on the downloaded operators (<= 1e-12), the Gauss
-residual and the energy history over 200 steps.
+  config 2  Yee 256^3 PEC fp64, the default two-step TMA sweep: 20 steps vs
+            the port (final state and energy history), bitwise vs the one-step
+            sweep, 1e-14 vs the unfused kick kernels; Gauss law and energy band
+            over 1000 steps; fp32 vs fp64.
+  config 3  128^3 x 6 tets: the device operators vs the C restatement of the
+            construction (oracle/tet_oracle.c), 500 production steps vs the
+            port with the energy history every 100 steps.
+  config 4  64^3 P2-, S(M1^2): 3 steps vs the port on the downloaded operators.
+  config 5  256^3 x 6 tets: C and M2 vs the C restatement, 3 steps vs the
+            port, Gauss law and energy over 100 steps.
+Tolerances: 1e-12 relative L2 on e and b, 1e-12 relative on energies
+(BASELINE.json north_star).
 """
+import gc
+
 import numpy as np
 import pytest
-import scipy.sparse as sp
 
 import paper_2301_01753_b200 as S
 from paper_2301_01753_b200 import configs, inputs
@@ -18,24 +29,84 @@ from tests.conftest import rel_l2
 
 pytestmark = pytest.mark.gpu
 
-
-def _csr(a):
-    return sp.csr_matrix((a.val, a.col_idx, a.row_ptr), shape=(a.rows, a.cols))
+TOL = 1e-12
 
 
+def tup(a):
+    return (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)
+
+
+def _gauss(d, b):
+    rows = np.repeat(np.arange(d.rows), np.diff(d.row_ptr))
+    db = np.zeros(d.rows)
+    np.add.at(db, rows, d.val * b[d.col_idx])
+    return np.abs(db).max()
+
+
+# ---- config 2: Yee 256^3 ------------------------------------------------------
 @pytest.fixture(scope="module")
 def yee256():
     import bench
     y, b0, e0, dt = bench.yee_setup(256, 8, 0)
     h = 1.0 / 256
-    _, d = S.yee_operators(256, 256, 256, h, h, h)
-    return y, b0, e0, dt, _csr(d)
+    c, d = S.yee_operators(256, 256, 256, h, h, h, bc=1)
+    return y, b0, e0, dt, c, d
 
 
-def test_config2_gauss_law_and_energy_over_1000_steps(yee256):
-    y, b0, e0, dt, d = yee256
+@pytest.fixture
+def yee_default(yee256):
+    """the shipped variant (two-step sweep) restored after each test"""
+    y = yee256[0]
+    y.set_variant(4)
+    yield yee256
+    y.set_variant(4)
+
+
+def test_config2_default_sweep_matches_oracle_20_steps(yee_default):
+    y, b0, e0, dt, c, _ = yee_default
+    dv = (1.0 / 256) ** 3
+    n1, n2 = c.cols, c.rows
+    q = S.scaled_identity(n1, 1.0 / dv)
+    m2 = S.scaled_identity(n2, dv)
+    port = O.PortScheme(1, dt, tup(q), tup(c), tup(m2), q_is_symmetric=True)
+    pb, pe, hist = b0, e0, []
+    for _ in range(4):  # 4 x 5 steps: energy history every 5 steps
+        pb, pe, _ = port.steps(pb, pe, 5)
+        hist.append(port.energy(pb, pe))
+    y.load(b0, e0)
+    dev_hist = []
+    for _ in range(4):
+        y.advance(5)  # each advance: half-kick, two-step sweeps, closing kicks
+        dev_hist.append(y.energy())
+    b, e, t = y.fetch()
+    assert rel_l2(b, pb) <= TOL and rel_l2(e, pe) <= TOL
+    assert np.allclose(dev_hist, hist, rtol=TOL, atol=0)
+    assert t == pytest.approx(20 * dt, rel=1e-14)
+    # one 20-step advance (9 two-step sweeps) lands on the same state
+    y.load(b0, e0)
+    y.advance(20)
+    b20, e20, _ = y.fetch()
+    assert rel_l2(b20, pb) <= TOL and rel_l2(e20, pe) <= TOL
+
+
+def test_config2_default_sweep_vs_one_step_and_unfused(yee_default):
+    """variant 4 (default) is bitwise variant 2 (one-step TMA sweep) and
+    within 1e-14 of variant 0 (unfused kick kernels), at 256^3 over 21 steps"""
+    y, b0, e0, _, _, _ = yee_default
+    out = {}
+    for v in (4, 2, 0):
+        y.set_variant(v)
+        y.load(b0, e0)
+        y.advance(21)
+        out[v] = y.fetch()[:2]
+    assert np.array_equal(out[4][0], out[2][0]) and np.array_equal(out[4][1], out[2][1])
+    assert rel_l2(out[4][0], out[0][0]) <= 1e-14 and rel_l2(out[4][1], out[0][1]) <= 1e-14
+
+
+def test_config2_gauss_law_and_energy_over_1000_steps(yee_default):
+    y, b0, e0, dt, _, d = yee_default
     scale = np.abs(b0).max()
-    assert np.abs(d @ b0).max() <= 1e-9 * scale * 256  # B0 = C A is divergence free
+    assert _gauss(d, b0) <= 1e-9 * scale * 256  # B0 = C A is divergence free
     y.load(b0, e0)
     energies = [y.energy()]
     for _ in range(10):
@@ -43,7 +114,7 @@ def test_config2_gauss_law_and_energy_over_1000_steps(yee256):
         energies.append(y.energy())
     b, e, t = y.fetch()
     assert t == pytest.approx(1000 * dt, rel=1e-12)
-    assert np.abs(d @ b).max() <= 1e-9 * scale * 256
+    assert _gauss(d, b) <= 1e-9 * scale * 256
     en = np.array(energies)
     # symplectic: the energy stays in a band (test_dynamics.cpp:342-368). The
     # white-noise B0 = C A puts its energy at grid-scale frequencies, where the
@@ -54,20 +125,8 @@ def test_config2_gauss_law_and_energy_over_1000_steps(yee256):
     assert (en[1:].max() - en[1:].min()) / en[1] <= 1e-3
 
 
-def test_config2_fused_sweep_equals_unfused_at_full_size(yee256):
-    y, b0, e0, dt, _ = yee256
-    out = []
-    for v in (2, 0):
-        y.set_variant(v)
-        y.load(b0, e0)
-        y.advance(20)
-        out.append(y.fetch())
-    y.set_variant(2)
-    assert rel_l2(out[0][0], out[1][0]) <= 1e-14 and rel_l2(out[0][1], out[1][1]) <= 1e-14
-
-
-def test_config2_fp32_tracks_fp64(yee256):
-    y, b0, e0, dt, _ = yee256
+def test_config2_fp32_tracks_fp64(yee_default):
+    y, b0, e0, dt, _, _ = yee_default
     h = 1.0 / 256
     y32 = S.YeeScheme(256, 256, 256, h, h, h, dt, bc=1, precision=4)
     for s in (y, y32):
@@ -75,59 +134,105 @@ def test_config2_fp32_tracks_fp64(yee256):
         s.advance(200)
     b64, e64, _ = y.fetch()
     b32, e32, _ = y32.fetch()
+    del y32
     assert rel_l2(b32, b64) <= 1e-4 and rel_l2(e32, e64) <= 1e-4
 
 
+# ---- config 3: 128^3 x 6 tets -------------------------------------------------
 @pytest.fixture(scope="module")
-def tet128():
+def tet128_ops():
+    ops = S.tet_device_operators(128, 0.15, seed=2023)
+    return {k: tup(v) for k, v in ops.items()}
+
+
+def test_config3_device_operators_match_c_restatement(tet128_ops):
+    """Connectivity, signs, patterns and M2 values bitwise; Q_sym (SPAI by a
+    different factorisation) to rounding."""
+    r = O.tet_c_operators(128, 0.15, 2023)
+    assert r["counts"][3] == 0  # no SPAI column failed the pivot test
+    for name in ("c", "m2"):
+        a, b = tet128_ops[name], r[name]
+        assert a[:2] == b[:2], name
+        for k in (2, 3, 4):
+            assert np.array_equal(a[k], b[k]), name
+    a, b = tet128_ops["q_sym"], r["q_sym"]
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+    assert np.abs(a[4] - b[4]).max() <= 1e-12 * np.abs(b[4]).max()
+
+
+def test_config3_500_steps_match_oracle_with_energy(tet128_ops):
     s = S.tet_device_scheme(128, 0.15, seed=2023, dt=1.0, with_div=True)
-    mesh = S.TetMesh(128, 0.15, 2023)
-    xyz, ev, _, _ = mesh.geometry(faces=False, tets=False)
-    a = inputs.pulse_one_form(xyz, ev, 7)
+    a = S.TetMesh(128, 0.15, 2023).pulse(7, 0.1, 1)
     b0 = s.apply("c", a)
     s.set_dt(configs.cfl_dt(s))
-    return s, b0, np.zeros(s._n1)
-
-
-def test_config3_first_steps_match_oracle(tet128):
-    s, b0, e0 = tet128
-    ops = S.tet_device_operators(128, 0.15, seed=2023)
-    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)
-    port = O.PortScheme(1, s.dt(), tup(ops["q_sym"]), tup(ops["c"]), tup(ops["m2"]),
-                        q_is_symmetric=True)
-    pb, pe, _ = port.steps(b0, e0, 5)
-    out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 5)
-    assert rel_l2(out.first, pb) <= 1e-12 and rel_l2(out.e, pe) <= 1e-12
-
-
-def test_config3_gauss_and_energy_history(tet128):
-    s, b0, e0 = tet128
-    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 200, 20)
-    assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
-    assert (en.max() - en.min()) / en[0] <= 0.05
     assert s.cfl_number() == pytest.approx(1.0, rel=1e-9)
+    e0 = np.zeros(s._n1)
+    ops = tet128_ops
+    port = O.PortScheme(1, s.dt(), ops["q_sym"], ops["c"], ops["m2"], q_is_symmetric=True)
+    pb, pe, hist = b0, e0, [port.energy(b0, e0)]
+    for _ in range(5):
+        pb, pe, _ = port.steps(pb, pe, 100)
+        hist.append(port.energy(pb, pe))
+    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 500, 100)
+    assert rel_l2(out.first, pb) <= TOL and rel_l2(out.e, pe) <= TOL
+    assert np.allclose(en, hist[1:], rtol=TOL, atol=0)
+    assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
+    # the smooth pulse: energy conserved to the modified-energy band
+    assert (max(hist) - min(hist)) / hist[0] <= 1e-3
 
 
-@pytest.fixture(scope="module")
-def p2_32():
-    s = S.p2_device_scheme(32, 0.1, seed=2023, dt=1.0, with_div=True)
+# ---- config 4: 64^3 P2-, S(M1^2) ----------------------------------------------
+def test_config4_first_steps_match_oracle_at_64():
+    ops = S.p2_device_operators(64, 0.1, seed=2023)  # assembled, downloaded, freed
+    ops = {k: tup(v) for k, v in ops.items()}
+    gc.collect()
+    s = S.p2_device_scheme(64, 0.1, seed=2023, dt=1.0, with_div=True)
+    assert s._n1 == 9_838_976 and s._n2 == 14_229_504  # SURVEY.md Appendix A
+    assert ops["q_sym"][3].size == 3_029_483_248
     b0 = s.apply("c", inputs.gaussian(7, s._n1))
     s.set_dt(configs.cfl_dt(s))
-    return s, b0, np.zeros(s._n1)
-
-
-def test_config4_system_first_steps_match_oracle(p2_32):
-    """The config-4 system (P2-, S(M1^2) SPAI) at 32^3 (N1 = 1.2M, nnz(Q) =
-    3.5e8): 3 production steps against the C oracle on the downloaded
-    operators, then Gauss law and a bounded energy over 200 steps."""
-    s, b0, e0 = p2_32
-    ops = S.p2_device_operators(32, 0.1, seed=2023)
-    tup = lambda a: (a.rows, a.cols, a.row_ptr, a.col_idx, a.val)  # noqa: E731
-    port = O.PortScheme(1, s.dt(), tup(ops["q_sym"]), tup(ops["c"]), tup(ops["m2"]),
-                        q_is_symmetric=True)
+    e0 = np.zeros(s._n1)
+    port = O.PortScheme(1, s.dt(), ops["q_sym"], ops["c"], ops["m2"], q_is_symmetric=True)
+    del ops
     pb, pe, _ = port.steps(b0, e0, 3)
+    ph = port.energy(pb, pe)
     out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 3)
-    assert rel_l2(out.first, pb) <= 1e-12 and rel_l2(out.e, pe) <= 1e-12
-    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 200, 20)
+    assert rel_l2(out.first, pb) <= TOL and rel_l2(out.e, pe) <= TOL
+    assert s.energy(out) == pytest.approx(ph, rel=TOL)
+    assert s.gauss_residual(out) <= 1e-12 * np.abs(b0).max()
+    del s, port
+    gc.collect()
+
+
+# ---- config 5: 256^3 x 6 tets -------------------------------------------------
+def test_config5_first_steps_match_oracle_at_256():
+    n = 256
+    ops = S.tet_device_operators(n, 0.1, seed=2023)
+    ops = {k: tup(v) for k, v in ops.items() if k in ("q_sym", "c", "m2")}
+    gc.collect()
+    # construction: incidence and M2 bitwise the C restatement (Q_sym is
+    # checked at 128^3; the 256^3 SPAI restatement would need ~100 GB of host)
+    r = O.tet_c_operators(n, 0.1, 2023, want=("c", "m2"))
+    assert r["counts"][:3] == (116_851_456, 201_719_808, 100_663_296)
+    for name in ("c", "m2"):
+        for k in (2, 3, 4):
+            assert np.array_equal(ops[name][k], r[name][k]), name
+    del r
+    gc.collect()
+    assert ops["q_sym"][3].size == 1_912_324_816  # SURVEY.md Appendix A
+    s = S.tet_device_scheme(n, 0.1, seed=2023, dt=1.0, with_div=True)
+    b0 = s.apply("c", S.TetMesh(n, 0.1, 2023).pulse(7, 0.1, 8))
+    s.set_dt(configs.cfl_dt(s))
+    e0 = np.zeros(s._n1)
+    port = O.PortScheme(1, s.dt(), ops["q_sym"], ops["c"], ops["m2"], q_is_symmetric=True)
+    del ops
+    pb, pe, _ = port.steps(b0, e0, 3)
+    ph = port.energy(pb, pe)
+    out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 3)
+    assert rel_l2(out.first, pb) <= TOL and rel_l2(out.e, pe) <= TOL
+    assert s.energy(out) == pytest.approx(ph, rel=TOL)
+    del port
+    gc.collect()
+    out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 100, 25)
     assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
-    assert (en.max() - en.min()) / en[0] <= 0.10
+    assert (en.max() - en.min()) / en[0] <= 1e-3
