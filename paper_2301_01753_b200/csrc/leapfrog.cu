@@ -14,7 +14,9 @@
 #include <cstring>
 #include <memory>
 
+#include "dev_handle.hpp"
 #include "device_util.cuh"
+#include "lattice.cuh"
 #include "spmv_kernels.cuh"
 
 namespace sfeec_b200 {
@@ -48,6 +50,22 @@ struct LeapfrogDev {
   double class_ms[5] = {0, 0, 0, 0, 0};
   int64_t class_launches[5] = {0, 0, 0, 0, 0};
   bool strict() const { return (flags & SFEEC_STRICT) != 0; }
+
+  // Kuhn-lattice layout (lattice.cuh) of a device-assembled first-order tet
+  // system: advance() runs the step on the lattice state; every other entry
+  // point works on the DOF vectors, gathered back when the lattice is newer
+  std::unique_ptr<Lattice> lat;
+  bool use_lat = false;  // inside advance(): the flows run on the lattice
+  bool lat_on() const { return lat && !strict() && form == SFEEC_FORM_BE; }
+  void sync_dof() {
+    if (lat && lat->newer) {
+      lat->gather(first.p, e.p, stream);
+      lat->newer = false;
+    }
+  }
+  void dof_changed() {
+    if (lat) lat->valid = lat->newer = false;
+  }
   double c2() const { return 1.0 / (eps0 * mu0); }
 
   ~LeapfrogDev() {
@@ -60,7 +78,8 @@ struct LeapfrogDev {
   int op_class(const DevOperator& a) const {
     return &a == &q ? 0 : &a == &c ? 1 : &a == &ct ? 2 : &a == &m2 ? 3 : 4;
   }
-  void tic(const DevOperator& a) {
+  void tic(const DevOperator& a) { tic_class(op_class(a)); }
+  void tic_class(int cls) {
     if (!timing) return;
     const size_t i = ev_used.size() * 2;
     while (ev_pool.size() < i + 2) {
@@ -68,7 +87,7 @@ struct LeapfrogDev {
       SFEEC_CUDA(cudaEventCreate(&e));
       ev_pool.push_back(e);
     }
-    ev_used.push_back({op_class(a), i});
+    ev_used.push_back({cls, i});
     SFEEC_CUDA(cudaEventRecord(ev_pool[i], stream));
   }
   void toc() {
@@ -110,6 +129,16 @@ struct LeapfrogDev {
 
   // dynamics.cpp:47-55
   void flow_he(double h) {
+    if (use_lat) {  // t = Q e, b -= h C t on the lattice
+      tic_class(0);
+      lat->apply_q(stream);
+      toc();
+      tic_class(1);
+      lat->apply_cb(h, stream);
+      toc();
+      launches += 2;
+      return;
+    }
     apply(q, e.p, t1.p);
     if (form == SFEEC_FORM_AE) {
       axpy_vec(first.p, t1.p, -h, n1);
@@ -124,6 +153,16 @@ struct LeapfrogDev {
   // dynamics.cpp:57-67
   void flow_ha(double h) {
     const double f = h * c2();
+    if (use_lat) {  // u = M2 b, e += f C^T u on the lattice
+      tic_class(3);
+      lat->apply_m2(stream);
+      toc();
+      tic_class(2);
+      lat->apply_cte(f, stream);
+      toc();
+      launches += 2;
+      return;
+    }
     const double* b = first.p;
     if (form == SFEEC_FORM_AE) {
       apply(c, first.p, t3.p);
@@ -200,6 +239,23 @@ struct LeapfrogDev {
     launches = 0;
     if (n <= 0) return;
     check_cfl_once();
+    if (lat_on()) {
+      if (!lat->valid) lat->scatter(first.p, e.p, stream);
+      lat->valid = true;
+      use_lat = true;
+      struct Off {
+        bool& f;
+        ~Off() { f = false; }
+      } off{use_lat};
+      advance_flows(n);
+      lat->newer = true;
+    } else {
+      advance_flows(n);
+    }
+    for (int64_t s = 0; s < n; ++s) time = time + dt;  // dynamics.cpp:88, per step
+  }
+
+  void advance_flows(int64_t n) {
     if (strict() || kind == SFEEC_SPLIT_LIE_TROTTER || form == SFEEC_FORM_AE) {
       for (int64_t s = 0; s < n; ++s) {
         if (kind == SFEEC_SPLIT_STRANG) {
@@ -218,11 +274,11 @@ struct LeapfrogDev {
       flow_ha(dt);
       flow_he(0.5 * dt);
     }
-    for (int64_t s = 0; s < n; ++s) time = time + dt;  // dynamics.cpp:88, per step
   }
 
   // dynamics.cpp:92-102
   double energy() {
+    sync_dof();
     apply(q, e.p, t1.p);
     double he = device_dot(e.p, t1.p, n1, partials.p, stream);
     const double* b = first.p;
@@ -239,6 +295,7 @@ struct LeapfrogDev {
   double gauss_residual() {
     require(form == SFEEC_FORM_BE, "gauss_residual: (b, e) formulation required");
     if (!has_div) return 0.0;
+    sync_dof();
     DevBuf<double> db;
     db.alloc((size_t)div.rows);
     apply(div, first.p, db.p);
@@ -339,7 +396,8 @@ sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR
 // device-assembled tet system in stencil layout). Production mode only.
 sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
                              DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
-                             double mu0, int split_kind, int device, int flags, cudaStream_t s) {
+                             double mu0, int split_kind, int device, int flags, cudaStream_t s,
+                             std::unique_ptr<Lattice> lat) {  // (dev_handle.hpp)
   require(!(flags & SFEEC_STRICT), "strict mode needs CSR operators (use the host builders)");
   select_device(device);
   auto h = std::make_unique<sfeec_dev>();
@@ -364,6 +422,7 @@ sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct,
   d.n1 = n1;
   d.n2 = n2;
   d.n_first = n2;
+  d.lat = std::move(lat);
   d.first.alloc((size_t)n2);
   d.first.zero(d.stream);
   d.e.alloc((size_t)n1);
@@ -423,6 +482,7 @@ int sfeec_dev_set_state(sfeec_dev* h, const double* first, int64_t n_first, cons
       SFEEC_CUDA(cudaMemcpyAsync(d.e.p, e, sizeof(double) * (size_t)n_e,
                                  cudaMemcpyHostToDevice, d.stream));
     SFEEC_CUDA(cudaStreamSynchronize(d.stream));
+    d.dof_changed();
     d.time = time;
   });
 }
@@ -432,6 +492,7 @@ int sfeec_dev_get_state(sfeec_dev* h, double* first, double* e, double* time) {
     require(h, "null handle");
     auto& d = h->d;
     SFEEC_CUDA(cudaSetDevice(d.device));
+    d.sync_dof();
     if (first && d.n_first)
       SFEEC_CUDA(cudaMemcpyAsync(first, d.first.p, sizeof(double) * (size_t)d.n_first,
                                  cudaMemcpyDeviceToHost, d.stream));
@@ -479,7 +540,9 @@ int sfeec_dev_flow_he(sfeec_dev* h, double dt) {
   return guarded([&] {
     require(h, "null handle");
     SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.sync_dof();
     h->d.flow_he(dt);
+    h->d.dof_changed();
     SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
   });
 }
@@ -488,7 +551,9 @@ int sfeec_dev_flow_ha(sfeec_dev* h, double dt) {
   return guarded([&] {
     require(h, "null handle");
     SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.sync_dof();
     h->d.flow_ha(dt);
+    h->d.dof_changed();
     SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
   });
 }
@@ -549,6 +614,10 @@ int sfeec_dev_set_stream(sfeec_dev* h, void* s) {
 int sfeec_dev_state_device_ptrs(sfeec_dev* h, double** first, double** e) {
   return guarded([&] {
     require(h, "null handle");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.sync_dof();  // the caller may read or write the DOF vectors
+    SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+    h->d.dof_changed();
     if (first) *first = h->d.first.p;
     if (e) *e = h->d.e.p;
   });
@@ -654,7 +723,13 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
     // algorithmic bytes per launch of each class (SURVEY.md 8(d) accounting:
     // 12 B per fp64 nonzero, 5 B per incidence entry (int8 sign + int32
     // column), 8 B per vector element read or written)
-    if (bytes) {
+    if (bytes && d.lat_on()) {  // what the lattice kernels move (lattice.cu)
+      bytes[0] = d.lat->bytes_q();
+      bytes[1] = d.lat->bytes_cb();
+      bytes[2] = d.lat->bytes_cte();
+      bytes[3] = d.lat->bytes_m2();
+      bytes[4] = 0;
+    } else if (bytes) {
       // an incidence C (+-1) streams 5 B per entry, a general one (P2-) 12 B
       const double cb = d.c.layout == DevOperator::kSigned ? 5.0 : 12.0;
       const double ctb = d.ct.layout == DevOperator::kSigned ? 5.0 : 12.0;

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <vector>
 
+#include "dev_handle.hpp"
 #include "device_util.cuh"
 #include "p2_device.hpp"
 #include "spmv_kernels.cuh"
@@ -479,9 +480,6 @@ void build_p2_system_device(const TetMesh& mesh, const P2Dofs& dofs, bool want_d
 
 using namespace sfeec_b200;
 
-sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
-                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
-                             double mu0, int split_kind, int device, int flags, cudaStream_t s);
 
 namespace {
 

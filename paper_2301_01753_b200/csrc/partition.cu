@@ -20,6 +20,7 @@
 #include <memory>
 #include <vector>
 
+#include "dev_handle.hpp"
 #include "device_util.cuh"
 #include "nccl_loader.hpp"
 #include "spmv_kernels.cuh"
@@ -313,9 +314,6 @@ struct sfeec_part {
   PartDev d;
 };
 
-sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
-                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
-                             double mu0, int split_kind, int device, int flags, cudaStream_t s);
 
 namespace {
 

@@ -13,6 +13,7 @@
 #include <memory>
 #include <vector>
 
+#include "dev_handle.hpp"
 #include "device_util.cuh"
 #include "spmv_kernels.cuh"
 #include "tet_device.hpp"
@@ -642,12 +643,6 @@ void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out,
 
 using namespace sfeec_b200;
 
-sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR* hdiv, double dt,
-                              double eps0, double mu0, int split_kind, int formulation,
-                              int device, int flags);
-sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
-                             DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
-                             double mu0, int split_kind, int device, int flags, cudaStream_t s);
 
 namespace {
 
@@ -709,6 +704,14 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
     if (!(flags & SFEEC_TET_HOST_LAYOUT) && !(flags & SFEEC_TET_STENCIL_LAYOUT)) {
       // default: the sliced / ELL layouts built on the device from the device
       // CSRs (only row pointers visit the host)
+      // plus, by default, the Kuhn-lattice form of Q_sym and M2 that
+      // advance() runs on (lattice.cuh; SFEEC_TET_NO_LATTICE keeps the
+      // sliced / ELL kernels for the step as well)
+      std::unique_ptr<Lattice> lat;
+      if (!(flags & SFEEC_TET_NO_LATTICE) && !(flags & SFEEC_STRICT)) {
+        lat = std::make_unique<Lattice>();
+        lat->build(mesh, sys.qsym, sys.m2, st.s);
+      }
       DevOperator q, c, ct, m2, div;
       q.upload_device(std::move(sys.qsym), st.s);
       m2.upload_device(std::move(sys.m2), st.s);
@@ -719,7 +722,8 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
       *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
                                with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
-                               split_kind, device, flags, hs);
+                               split_kind, device, flags & ~SFEEC_TET_NO_LATTICE, hs,
+                               std::move(lat));
       return;
     }
     require(!(flags & SFEEC_TET_STENCIL_LAYOUT), "the stencil layout was removed");

@@ -249,6 +249,21 @@ class SplitScheme:
         L.check(L.lib().sfeec_dev_advance(self._h, int(nsteps)))
         return self.fetch()
 
+    # resident-state forms: no host round trip of the state
+    def advance_resident(self, nsteps: int) -> None:
+        L.check(L.lib().sfeec_dev_advance(self._h, int(nsteps)))
+
+    def energy_resident(self) -> float:
+        out = C.c_double()
+        L.check(L.lib().sfeec_dev_energy(self._h, C.byref(out)))
+        return out.value
+
+    def flow_he_resident(self, dt: float) -> None:
+        L.check(L.lib().sfeec_dev_flow_he(self._h, float(dt)))
+
+    def flow_ha_resident(self, dt: float) -> None:
+        L.check(L.lib().sfeec_dev_flow_ha(self._h, float(dt)))
+
     def advance_diag(self, s: FieldState, nsteps: int, diag_every: int = 1):
         """advance + energy and Gauss residual after every diag_every steps."""
         self.load(s)
@@ -592,16 +607,21 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
                       device: int = 0) -> "SplitScheme":
     """First-order S(M1) tet system assembled on the B200 (C, D, M1, M2, SPAI,
     Q_sym), wrapped as a (b, e) SplitScheme. Operators stay in HBM.
-    layout: "device" (default: sliced/ELL layouts built on the GPU) or "host"
-    (generic sliced/ELL layouts built through the host)."""
+    layout: "device" (default: advance() runs on the Kuhn-lattice layout --
+    per-vertex coefficient arrays, no index streams; the
+    other entry points use sliced/ELL operators built on the GPU), "sell"
+    (sliced/ELL kernels for the step too) or "host" (generic sliced/ELL
+    layouts built through the host)."""
     units = units or UnitSystem()
     h = C.c_void_p()
     counts = np.zeros(3, np.int64)
     flags = 0 if warn_cfl else L.NO_CFL_WARN
     if layout == "host":
         flags |= 8  # SFEEC_TET_HOST_LAYOUT
+    elif layout == "sell":
+        flags |= 32  # SFEEC_TET_NO_LATTICE
     elif layout != "device":
-        raise InvalidParameter("layout must be 'device' or 'host'")
+        raise InvalidParameter("layout must be 'device', 'sell' or 'host'")
     L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                          units.mu0, int(SplitKind(kind)), device, flags,
                                          1 if with_div else 0, C.byref(h), L.i64ptr(counts)))
