@@ -9,6 +9,7 @@
 // ascending column order of the k-major numbering for rows away from the
 // 32-vertex x-block edges: those rows are summed exactly like the sliced /
 // ELL kernels (spmv_kernels.cu) sum their CSR rows.
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -119,7 +120,8 @@ __device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, cons
   const double r[sizeof...(Ts)] = {sym_row<QOp, Ts>(qc, E, idx, g)...};
   ((edge_dof<Ts>(i, j, k, g.n) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
 }
-__global__ void __launch_bounds__(kLT) k_lat_q(LatGeom g, const double* __restrict__ qc,
+template <int MINB>
+__global__ void __launch_bounds__(kLT, MINB) k_lat_q(LatGeom g, const double* __restrict__ qc,
                                                const double* __restrict__ E,
                                                double* __restrict__ T) {
   int i, j, k;
@@ -137,7 +139,8 @@ __device__ __forceinline__ void m2_vertex(std::integer_sequence<int, Fs...>, con
   const double r[sizeof...(Fs)] = {sym_row<MOp, Fs>(mc, B, idx, g)...};
   ((face_ok<Fs>(i, j, k, g.n) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
 }
-__global__ void __launch_bounds__(kLT) k_lat_m2(LatGeom g, const double* __restrict__ mc,
+template <int MINB>
+__global__ void __launch_bounds__(kLT, MINB) k_lat_m2(LatGeom g, const double* __restrict__ mc,
                                                 const double* __restrict__ B,
                                                 double* __restrict__ U) {
   int i, j, k;
@@ -203,6 +206,90 @@ __global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, double alpha,
   cte_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, alpha, U, E);
 }
 
+// ---- warp-per-row-type forms: a block is one warp per entity type over the
+// same 32 x CH positions, so a thread computes one row (~40 registers, full
+// occupancy) and the block's warps share the gathered neighbours in L1 -----
+template <int... Ts, class F>
+__device__ __forceinline__ void on_type(int w, std::integer_sequence<int, Ts...>, F&& f) {
+  ((w == Ts ? f(std::integral_constant<int, Ts>{}) : (void)0), ...);
+}
+struct QRowW {
+  const double* __restrict__ qc;
+  const double* __restrict__ E;
+  double* __restrict__ T;
+  static constexpr int kTypes = 7, kMinBlocks = 6;
+  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
+                                             int64_t idx) const {
+    on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
+      constexpr int t = decltype(tc)::value;
+      if (edge_dof<t>(i, j, k, g.n)) T[(int64_t)t * g.NP + idx] = sym_row<QOp, t>(qc, E, idx, g);
+    });
+  }
+};
+struct M2RowW {
+  const double* __restrict__ mc;
+  const double* __restrict__ B;
+  double* __restrict__ U;
+  static constexpr int kTypes = 12, kMinBlocks = 4;
+  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
+                                             int64_t idx) const {
+    on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
+      constexpr int f = decltype(fc)::value;
+      if (face_ok<f>(i, j, k, g.n)) U[(int64_t)f * g.NP + idx] = sym_row<MOp, f>(mc, B, idx, g);
+    });
+  }
+};
+struct CbRowW {
+  double alpha;
+  const double* __restrict__ T;
+  double* __restrict__ B;
+  static constexpr int kTypes = 12, kMinBlocks = 4;
+  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
+                                             int64_t idx) const {
+    on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
+      constexpr int f = decltype(fc)::value;
+      if (face_ok<f>(i, j, k, g.n)) {
+        const double r = inc_row<false, 3 * f>(std::make_integer_sequence<int, 3>{}, T, idx, g);
+        double* b = B + (int64_t)f * g.NP + idx;
+        *b = fma(alpha, r, *b);
+      }
+    });
+  }
+};
+struct CteRowW {
+  double alpha;
+  const double* __restrict__ U;
+  double* __restrict__ E;
+  static constexpr int kTypes = 7, kMinBlocks = 8;
+  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
+                                             int64_t idx) const {
+    on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
+      constexpr int t = decltype(tc)::value;
+      if (edge_dof<t>(i, j, k, g.n)) {
+        const double r = inc_row<true, lat::kCTOff(t)>(
+            std::make_integer_sequence<int, lat::kCTOff(t + 1) - lat::kCTOff(t)>{}, U, idx, g);
+        double* e = E + (int64_t)t * g.NP + idx;
+        *e = fma(alpha, r, *e);
+      }
+    });
+  }
+};
+constexpr int kWCH = 4;  // 32-position chunks per block
+template <class Row>
+__global__ void __launch_bounds__(Row::kTypes * 32, Row::kMinBlocks) k_lat_w(LatGeom g, Row row) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.y;
+#pragma unroll 1
+  for (int c = 0; c < kWCH; ++c) {
+    const int p = (blockIdx.x * kWCH + c) * 32 + lane;
+    if (p >= g.PS) return;
+    const int j = p / g.S - 1;
+    const int i = p - (j + 1) * g.S - 1;
+    if (i < 0 || i > g.n || j < 0 || j > g.n) continue;
+    row(g, w, i, j, k, g.PS * (k + 1) + p);
+  }
+}
+
 // ---- setup: coefficient arrays from a CSR of the k-major numbering -----------
 // Entry (r, c) of row type t at offset off: the slot of t's stencil with
 // (type(c), off); canonical slots store the value at the row's position.
@@ -266,6 +353,9 @@ __global__ void k_lat_gather(int64_t n, const int64_t* __restrict__ pos,
 }
 
 inline unsigned blocks(int64_t n) { return (unsigned)((n + kLT - 1) / kLT); }
+inline dim3 wgrid(const LatGeom& g) {
+  return dim3((unsigned)((g.PS + 32 * kWCH - 1) / (32 * kWCH)), g.n + 1);
+}
 
 }  // namespace
 
@@ -321,6 +411,8 @@ void Lattice::build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2,
   }
   SFEEC_CUDA(cudaStreamSynchronize(s));
   valid = newer = false;
+  const char* v = std::getenv("SFEEC_LAT_VARIANT");  // A/B of the kernel forms
+  variant = v ? std::atoi(v) : 0;
 }
 
 void Lattice::scatter(const double* b, const double* e, cudaStream_t s) {
@@ -335,20 +427,41 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
   SFEEC_LAUNCH_CHECK();
 }
 
+// variant 0: one thread per vertex (all its rows); 1: one warp per row type
 void Lattice::apply_q(cudaStream_t s) const {
-  k_lat_q<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+  if (variant == 1)
+    k_lat_w<QRowW><<<wgrid(g), 7 * 32, 0, s>>>(g, QRowW{qc.p, E.p, T.p});
+  else if (variant == 2)
+    k_lat_q<3><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+  else if (variant == 3)
+    k_lat_q<4><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+  else
+    k_lat_q<2><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cb(double h, cudaStream_t s) const {
-  k_lat_cb<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, -h, T.p, B.p);
+  if (variant == 1)
+    k_lat_w<CbRowW><<<wgrid(g), 12 * 32, 0, s>>>(g, CbRowW{-h, T.p, B.p});
+  else
+    k_lat_cb<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, -h, T.p, B.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_m2(cudaStream_t s) const {
-  k_lat_m2<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+  if (variant == 1)
+    k_lat_w<M2RowW><<<wgrid(g), 12 * 32, 0, s>>>(g, M2RowW{mc.p, B.p, U.p});
+  else if (variant == 2)
+    k_lat_m2<3><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+  else if (variant == 3)
+    k_lat_m2<4><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+  else
+    k_lat_m2<2><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cte(double f, cudaStream_t s) const {
-  k_lat_cte<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, f, U.p, E.p);
+  if (variant == 1)
+    k_lat_w<CteRowW><<<wgrid(g), 7 * 32, 0, s>>>(g, CteRowW{f, U.p, E.p});
+  else
+    k_lat_cte<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, f, U.p, E.p);
   SFEEC_LAUNCH_CHECK();
 }
 

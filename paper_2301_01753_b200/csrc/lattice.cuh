@@ -45,6 +45,7 @@ struct Lattice {
   DevBuf<double> E, T, B, U;  // 7, 7, 12, 12 components * NP
   DevBuf<int64_t> epos, fpos;  // DOF id -> component * NP + position
   bool pdl = true;
+  int variant = 0;  // kernel form (lattice.cu apply_*)
   // state bookkeeping of the owning handle: `valid` = E/B hold the handle's
   // state (or a newer one), `newer` = the DOF vectors are stale
   bool valid = false, newer = false;

@@ -50,7 +50,8 @@ def test_lattice_state_sync_between_calls():
     rng = np.random.default_rng(2)
     st = S.make_state(S.Formulation.BE, rng.standard_normal(lat._n2),
                       rng.standard_normal(lat._n1))
-    whole = lat.advance(st, 30)
+    # two advance() calls (each opens and closes with a half-kick)
+    whole = lat.advance(lat.advance(st, 10), 20)
     lat.load(st)
     lat.advance_resident(10)
     e10 = lat.energy_resident()       # gathers, lattice stays valid
@@ -60,8 +61,8 @@ def test_lattice_state_sync_between_calls():
     assert np.array_equal(two.first, whole.first) and np.array_equal(two.e, whole.e)
     assert e10 == pytest.approx(lat.energy(mid), rel=0)
     # a reload after lattice steps replaces the lattice state
-    lat.load(st)
-    again = lat.advance(st, 30)
+    lat.advance_resident(3)
+    again = lat.advance(lat.advance(st, 10), 20)
     assert np.array_equal(again.first, whole.first)
     # half-flows through the ABI run on the DOF vectors of the lattice state
     lat.load(st)

@@ -1,0 +1,9 @@
+# A/B of lattice kernel variants on tet256: python bench.py with SFEEC_LAT_VARIANT=v
+mkdir -p gpurun_out
+SFEEC_LAT_VARIANT=1 timeout 600 python -m pytest tests/test_gpu_lattice.py -x -q > gpurun_out/lat_tests_v1.log 2>&1; echo "tests v1 rc=$?"; tail -2 gpurun_out/lat_tests_v1.log
+for v in ${VARIANTS:-0 1 0 1}; do
+  SFEEC_LAT_VARIANT=$v timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --config ${CFG:-tet256} > gpurun_out/ab_v$v.json 2> gpurun_out/ab_v$v.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ab_v$v.json')); r=d['roofline']['per_kernel']
+print('v$v', round(d['ms_per_step'],4), {k: round(x['avg_ms'],4) for k,x in r.items()}, d['clocks']['sm_mhz'])"
+done
