@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <ostream>
+#include <sstream>
 
 #include "common.hpp"
 #include "sfeec/dynamics.hpp"
@@ -131,6 +133,37 @@ double max_asymmetry(const SparseOperator& a) {
     auto vs = a.row_vals(r);
     for (size_t k = 0; k < cs.size(); ++k) m = std::max(m, std::abs(vs[k] - a.at(cs[k], r)));
   }
+  return m;
+}
+
+void write_coordinate_list(std::ostream& os, const SparseOperator& a) {
+  // rows ascending, stored (ascending) column order within a row
+  char line[80];
+  for (int r = 0; r < a.rows; ++r)
+    for (int k = a.row_ptr[(size_t)r]; k < a.row_ptr[(size_t)r + 1]; ++k) {
+      const int n = std::snprintf(line, sizeof(line), "%d %d %.17g\n", r,
+                                  a.col_idx[(size_t)k], a.val[(size_t)k]);
+      os.write(line, n);
+    }
+}
+
+std::string to_coordinate_list(const SparseOperator& a) {
+  std::ostringstream os;
+  write_coordinate_list(os, a);
+  return os.str();
+}
+
+SparseOperator read_coordinate_list(std::istream& is, int rows, int cols) {
+  std::vector<Triplet> entries;
+  int hi_r = -1, hi_c = -1;
+  for (Triplet t; is >> t.r >> t.c >> t.v;) {  // until the first unparsable token
+    hi_r = std::max(hi_r, t.r);
+    hi_c = std::max(hi_c, t.c);
+    entries.push_back(t);
+  }
+  SparseOperator m = operator_from_triplets(rows < 0 ? hi_r + 1 : rows,
+                                            cols < 0 ? hi_c + 1 : cols, std::move(entries));
+  m.symmetric = m.rows == m.cols && max_asymmetry(m) == 0.0;
   return m;
 }
 

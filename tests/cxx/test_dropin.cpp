@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "sfeec/dynamics.hpp"
@@ -59,10 +61,47 @@ static Lattice pec_lattice(int nx, int ny, int nz, double dx, double dy, double 
   return {from_owned(c), from_owned(d)};
 }
 
+// host-side API: core.hpp's Rng is the reference splitmix64 stream, and the
+// coordinate-list export / import round-trips (test_operators.cpp:294-320)
+static void host_checks() {
+  {
+    Rng r(42);
+    std::vector<double> want = uniform(42, 5), got;
+    for (int k = 0; k < 5; ++k) got.push_back(r.uniform(-1, 1));
+    CHECK(got == want);
+  }
+  std::vector<Triplet> tri;
+  for (int r = 0; r < 7; ++r)
+    for (int c = 0; c < 7; ++c)
+      if ((r + c) % 3 != 1) tri.push_back({r, c, 1.0 / (1.0 + r + c) + (r == c)});
+  SparseOperator m = operator_from_triplets(7, 7, tri);
+  const std::string text = to_coordinate_list(m);
+  std::istringstream is(text);
+  int pr = -1, pc = -1, r, c;
+  double v;
+  while (is >> r >> c >> v) {  // sorted by (row, col)
+    CHECK(r > pr || (r == pr && c > pc));
+    pr = r;
+    pc = c;
+  }
+  std::istringstream is2(text);
+  SparseOperator m2 = read_coordinate_list(is2);
+  CHECK(m2.rows == 7 && m2.cols == 7 && m2.nnz() == m.nnz() && m2.symmetric);
+  CHECK(m2.val == m.val && m2.col_idx == m.col_idx && m2.row_ptr == m.row_ptr);
+  std::ostringstream os;
+  write_coordinate_list(os, m2);
+  CHECK(os.str() == text);
+  std::istringstream is3("0 1 2.5\n2 0 -1\n");  // explicit shape, not symmetric
+  SparseOperator m3 = read_coordinate_list(is3, 4, 3);
+  CHECK(m3.rows == 4 && m3.cols == 3 && m3.nnz() == 2 && !m3.symmetric);
+}
+
 int main() {
+  host_checks();
   if (sfeec_device_count() == 0) {
-    std::puts("no GPU: skipped");
-    return 0;
+    std::puts(failures ? "host checks FAILED; no GPU: device checks skipped"
+                       : "no GPU: skipped");
+    return failures ? 1 : 0;
   }
   // ---- sub-flow closed forms (test_dynamics.cpp:67-94) --------------------
   {
