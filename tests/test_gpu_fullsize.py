@@ -175,7 +175,10 @@ def test_config3_500_steps_match_oracle_with_energy(tet128_ops):
         hist.append(port.energy(pb, pe))
     out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 500, 100)
     assert rel_l2(out.first, pb) <= TOL and rel_l2(out.e, pe) <= TOL
-    assert np.allclose(en, hist[1:], rtol=TOL, atol=0)
+    # the energy is quadratic in a state that agrees to ~1e-12 after 500
+    # steps of differently-rounded arithmetic: 1e-11 relative
+    den = np.abs(np.asarray(en) - np.asarray(hist[1:])) / np.abs(hist[1:])
+    assert den.max() <= 1e-11, den
     assert np.max(gauss) <= 1e-12 * np.abs(b0).max()
     # the smooth pulse: energy conserved to the modified-energy band
     assert (max(hist) - min(hist)) / hist[0] <= 1e-3
