@@ -294,6 +294,16 @@ int sfeec_tetmesh_geometry(const sfeec_tetmesh* h, double* xyz, int64_t* edge_ve
  * 3-point Gauss-Legendre; x0, p: 3 * npulses each. Host (OpenMP). */
 int sfeec_tetmesh_pulse(const sfeec_tetmesh* h, int npulses, const double* x0, const double* p,
                         double sigma, int64_t e0, int64_t e1, double* out);
+/* The Fig. 3 accuracy pipeline (reference operators.cpp:181-257 l2_error,
+ * convergence.cpp:107-116) for the PEC cube's TE cavity family: kind 0 =
+ * A_m = sin(m pi y) sin(m pi z) dx, kind 1 = curl curl A_m = 2 (m pi)^2 A_m.
+ * project_cavity: canonical projection of A_m onto the DOF edges (integral
+ * DOFs, 4-point Gauss-Legendre; host). l2_error: abs_rel = {||w_h - f||,
+ * ||w_h - f|| / ||f||} over the mesh, w on the DOF edges (host buffer),
+ * computed on the device (64-point collapsed Gauss rule per tet). */
+int sfeec_tetmesh_project_cavity(const sfeec_tetmesh* h, int mode, double* out);
+int sfeec_tet_l2_error(const sfeec_tetmesh* h, const double* w, int kind, int mode, int device,
+                       double* abs_rel);
 int sfeec_tetmesh_operator(const sfeec_tetmesh* h, int which, sfeec_csr_owned* out);
 /* Second-order trimmed forms P2^- on the same mesh (BASELINE config 4; the
  * reference's P2^- is 2-D only, form_space.cpp:41-166 -- the 3-D element

@@ -156,6 +156,8 @@ _SIGS = {
     "sfeec_tetmesh_destroy": (None, [_P]),
     "sfeec_tetmesh_counts": (C.c_int, [_P, _PI64, _PI64, _PI64, _PI64]),
     "sfeec_tetmesh_geometry": (C.c_int, [_P, _PD, _PI64, _PI64, _PI64]),
+    "sfeec_tetmesh_project_cavity": (C.c_int, [_P, C.c_int, _PD]),
+    "sfeec_tet_l2_error": (C.c_int, [_P, _PD, C.c_int, C.c_int, C.c_int, _PD]),
     "sfeec_tetmesh_pulse": (C.c_int, [_P, C.c_int, _PD, _PD, C.c_double, C.c_int64, C.c_int64,
                                       _PD]),
     "sfeec_tetmesh_operator": (C.c_int, [_P, C.c_int, C.POINTER(sfeec_csr_owned)]),

@@ -97,6 +97,17 @@ struct DevBuf {
   }
 };
 
+// an owned non-blocking stream
+struct Stream {
+  cudaStream_t s = nullptr;
+  Stream() { SFEEC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+  Stream(const Stream&) = delete;
+  Stream& operator=(const Stream&) = delete;
+};
+
 // device CSR (int64 row pointers), produced by the device assembly
 struct DevCSR {
   int64_t rows = 0, cols = 0, nnz = 0;

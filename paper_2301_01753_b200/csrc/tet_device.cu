@@ -668,14 +668,6 @@ HostCSR download(DevCSR& a, cudaStream_t s) {
   return h;
 }
 
-struct Stream {
-  cudaStream_t s = nullptr;
-  Stream() { SFEEC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
-  ~Stream() {
-    if (s) cudaStreamDestroy(s);
-  }
-};
-
 }  // namespace
 
 extern "C" {

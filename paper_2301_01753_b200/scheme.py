@@ -561,6 +561,25 @@ class TetMesh:
                                             float(sigma), int(e0), e1, L.dptr(out)))
         return out
 
+    def project_cavity(self, mode: int = 1) -> np.ndarray:
+        """Canonical projection of A_m = sin(m pi y) sin(m pi z) dx (integral
+        DOFs on the DOF edges; the PEC cube's TE cavity potential)."""
+        out = np.zeros(self.n_edges)
+        L.check(L.lib().sfeec_tetmesh_project_cavity(self._h, int(mode), L.dptr(out)))
+        return out
+
+    def l2_error(self, w: np.ndarray, kind: int = 1, mode: int = 1, device: int = 0):
+        """(absolute, relative) L^2 error of the Whitney 1-form with DOFs w
+        against A_m (kind 0) or curl curl A_m (kind 1), on the device
+        (reference operators.cpp:181-257)."""
+        w = np.ascontiguousarray(w, np.float64)
+        if w.size != self.n_edges:
+            raise InvalidParameter("l2_error: cochain length mismatch")
+        out = np.zeros(2)
+        L.check(L.lib().sfeec_tet_l2_error(self._h, L.dptr(w), int(kind), int(mode), device,
+                                           L.dptr(out)))
+        return float(out[0]), float(out[1])
+
     def _op(self, which, symmetric=False) -> SparseOperator:
         out = L.sfeec_csr_owned()
         L.check(L.lib().sfeec_tetmesh_operator(self._h, which, C.byref(out)))
