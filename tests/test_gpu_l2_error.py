@@ -33,7 +33,7 @@ def test_fig3_chain_matches_numpy_at_small_size():
     s = S.tet_device_scheme(n, 0.1, 5)
     m, o = S.TetMesh(n, 0.1, 5), TO.OracleTetMesh(n, 0.1, 5)
     a = m.project_cavity(1)
-    w = s.curl_curl(a)
+    w = s.curl_of_curl(a)
     ops = S.tet_device_operators(n, 0.1, 5)
     csr = {k: sp.csr_matrix((v.val, v.col_idx, v.row_ptr), shape=(v.rows, v.cols))
            for k, v in ops.items()}
@@ -49,7 +49,7 @@ def test_fig3_curl_curl_error_converges():
     for n in (8, 16, 32):
         s = S.tet_device_scheme(n, 0.1, 5)
         m = S.TetMesh(n, 0.1, 5)
-        errs.append(m.l2_error(s.curl_curl(m.project_cavity(1)), 1, 1)[1])
+        errs.append(m.l2_error(s.curl_of_curl(m.project_cavity(1)), 1, 1)[1])
     rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     print("relative L2 errors", errs, "rates", rates)
     assert errs[0] > errs[1] > errs[2]
