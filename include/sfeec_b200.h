@@ -280,6 +280,11 @@ int sfeec_build_yee_curl(int nx, int ny, int nz, double dx, double dy, double dz
  * operators.cpp:29-42,133-179. Numbering contract: DESIGN.md. */
 typedef struct sfeec_tetmesh sfeec_tetmesh;
 int sfeec_tetmesh_create(int n, double jitter, uint64_t seed, sfeec_tetmesh** out);
+/* vertex planes [k0, k1] of the n x n x nzg mesh (spacing 1/n): a z-slab
+ * with the whole mesh's vertex jitter, entity order and PEC walls (the cut
+ * planes are not walls), so its complete rows equal the whole mesh's */
+int sfeec_tetmesh_create_slab(int n, int nzg, int k0, int k1, double jitter, uint64_t seed,
+                              sfeec_tetmesh** out);
 void sfeec_tetmesh_destroy(sfeec_tetmesh* h);
 int sfeec_tetmesh_counts(const sfeec_tetmesh* h, int64_t* n_vertices, int64_t* n_edges,
                          int64_t* n_faces, int64_t* n_tets);

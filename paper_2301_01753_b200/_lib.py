@@ -153,6 +153,8 @@ _SIGS = {
                                        C.c_double, C.c_int, C.POINTER(sfeec_csr_owned),
                                        C.POINTER(sfeec_csr_owned)]),
     "sfeec_tetmesh_create": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    "sfeec_tetmesh_create_slab": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                            C.POINTER(C.c_void_p)]),
     "sfeec_tetmesh_destroy": (None, [_P]),
     "sfeec_tetmesh_counts": (C.c_int, [_P, _PI64, _PI64, _PI64, _PI64]),
     "sfeec_tetmesh_geometry": (C.c_int, [_P, _PD, _PI64, _PI64, _PI64]),

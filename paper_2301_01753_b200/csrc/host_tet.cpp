@@ -373,6 +373,16 @@ int sfeec_tetmesh_create(int n, double jitter, uint64_t seed, sfeec_tetmesh** ou
   });
 }
 
+int sfeec_tetmesh_create_slab(int n, int nzg, int k0, int k1, double jitter, uint64_t seed,
+                              sfeec_tetmesh** out) {
+  return guarded([&] {
+    require(out != nullptr, "null out");
+    auto h = std::make_unique<sfeec_tetmesh>();
+    h->m.build_slab(n, nzg, k0, k1, jitter, seed);
+    *out = h.release();
+  });
+}
+
 void sfeec_tetmesh_destroy(sfeec_tetmesh* h) { delete h; }
 
 int sfeec_tetmesh_counts(const sfeec_tetmesh* h, int64_t* n_vertices, int64_t* n_edges,

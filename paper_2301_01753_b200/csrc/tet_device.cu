@@ -38,7 +38,8 @@ __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, 
 __device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b); }
 
 struct DMesh {
-  int n;
+  int n;   // cubes along x, y
+  int nz;  // cubes along z (TetMesh::nz: the whole mesh or a slab of it)
   const double* xyz;
   const int32_t* eid;  // nv * 7
   const int32_t* fid;  // nv * 12
@@ -113,7 +114,7 @@ struct DMesh {
       for (int dy = 1; dy >= 0; --dy)
         for (int dx = 1; dx >= 0; --dx) {
           int w[3] = {c0[0] - dx, c0[1] - dy, c0[2] - dz};
-          if (w[0] < 0 || w[0] >= n || w[1] < 0 || w[1] >= n || w[2] < 0 || w[2] >= n) continue;
+          if (w[0] < 0 || w[0] >= n || w[1] < 0 || w[1] >= n || w[2] < 0 || w[2] >= nz) continue;
           int64_t cube = (int64_t)w[0] + (int64_t)n * ((int64_t)w[1] + (int64_t)n * w[2]);
           for (int p = 0; p < 6; ++p) {
             int64_t vv[4];
@@ -601,7 +602,7 @@ void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out,
   et.upload(h.edge_t.data(), h.edge_t.size(), s);
   fv.upload(h.face_v.data(), h.face_v.size(), s);
   ft.upload(h.face_t.data(), h.face_t.size(), s);
-  DMesh m{h.n, xyz.p, eid.p, fid.p, ev.p, et.p, fv.p, ft.p};
+  DMesh m{h.n, h.nz, xyz.p, eid.p, fid.p, ev.p, et.p, fv.p, ft.p};
   out.n1 = h.n_edges;
   out.n2 = h.n_faces;
   out.nt = h.n_tets;

@@ -44,8 +44,18 @@ inline int type_of(int dx, int dy, int dz) {
 
 using namespace tetc;
 
+// The Kuhn mesh of an n x n x nzg box of cubes (spacing 1/n; the unit cube
+// when nzg = n), or a z-slab of it: local vertex planes 0..nz are the whole
+// mesh's planes kz0..kz0+nz. Vertex ids, jitter streams and PEC walls follow
+// the whole mesh (a slab's cut planes are not walls), so every entity of a
+// slab has the entity ids' relative order, geometry and DOF status of the
+// whole mesh -- a slab's complete rows are bitwise the whole mesh's.
 struct TetMesh {
-  int n = 0;
+  int n = 0;                  // cubes along x and y
+  int nz = 0;                 // cubes along z in this (slab of the) mesh
+  int nzg = 0;                // cubes along z of the whole mesh
+  int kz0 = 0;                // whole-mesh index of local vertex plane 0
+  bool wall_lo = true, wall_hi = true;  // local planes 0 / nz are PEC walls
   double amp = 0;
   uint64_t seed = 0;
   int64_t nv = 0, n_edges = 0, n_faces = 0, n_tets = 0;
@@ -66,16 +76,19 @@ struct TetMesh {
     c[2] = (int)(v / ((int64_t)(n + 1) * (n + 1)));
   }
   bool inside(const int c[3]) const {
-    for (int d = 0; d < 3; ++d)
-      if (c[d] < 0 || c[d] > n) return false;
-    return true;
+    return c[0] >= 0 && c[0] <= n && c[1] >= 0 && c[1] <= n && c[2] >= 0 && c[2] <= nz;
+  }
+  // coordinate c on axis d lies on a PEC wall
+  bool on_wall(int d, int c) const {
+    if (d < 2) return c == 0 || c == n;
+    return (c == 0 && wall_lo) || (c == nz && wall_hi);
   }
   // tet id -> ascending vertex ids
   void tet_vertices(int64_t tet, int64_t vv[4]) const {
     int64_t cube = tet / 6;
     int p = (int)(tet % 6);
     int c[3] = {(int)(cube % n), (int)((cube / n) % n), (int)(cube / ((int64_t)n * n))};
-    vv[0] = vid(c[0], c[1], c[2]);
+    vv[0] = vid(c[0], c[1], c[2]);  // cubes: n x n x nz, x fastest
     c[kPerm[p][0]] += 1;
     vv[1] = vid(c[0], c[1], c[2]);
     c[kPerm[p][1]] += 1;
@@ -113,7 +126,7 @@ struct TetMesh {
           int w[3] = {c0[0] - dx, c0[1] - dy, c0[2] - dz};
           bool ok = true;
           for (int d = 0; d < 3; ++d)
-            if (w[d] < 0 || w[d] >= n) ok = false;
+            if (w[d] < 0 || w[d] >= (d < 2 ? n : nz)) ok = false;
           if (!ok) continue;
           int64_t cube = (int64_t)w[0] + (int64_t)n * ((int64_t)w[1] + (int64_t)n * w[2]);
           for (int p = 0; p < 6; ++p) {
@@ -128,14 +141,24 @@ struct TetMesh {
     return cnt;
   }
 
-  void build(int n_, double amp_, uint64_t seed_) {
+  // the unit cube, n^3 cubes
+  void build(int n_, double amp_, uint64_t seed_) { build_slab(n_, n_, 0, n_, amp_, seed_); }
+
+  // vertex planes [k0, k1] of the n x n x nzg_ mesh
+  void build_slab(int n_, int nzg_, int k0, int k1, double amp_, uint64_t seed_) {
     n = n_;
+    nzg = nzg_;
+    kz0 = k0;
+    nz = k1 - k0;
+    wall_lo = k0 == 0;
+    wall_hi = k1 == nzg_;
     amp = amp_;
     seed = seed_;
-    require(n >= 1, "tet mesh: n must be >= 1");
+    require(n >= 1 && nzg >= 1, "tet mesh: n must be >= 1");
+    require(k0 >= 0 && k1 <= nzg && nz >= 1, "tet mesh: bad slab plane range");
     require(amp >= 0 && amp < 0.25, "tet mesh: jitter amplitude must be in [0, 0.25)");
-    nv = (int64_t)(n + 1) * (n + 1) * (n + 1);
-    n_tets = 6 * (int64_t)n * n * n;
+    nv = (int64_t)(n + 1) * (n + 1) * (nz + 1);
+    n_tets = 6 * (int64_t)n * n * nz;
     require(n_tets < ((int64_t)1 << 40), "tet mesh: too large");
     const double h = 1.0 / n;
     xyz.resize((size_t)(3 * nv));
@@ -143,12 +166,14 @@ struct TetMesh {
     for (int64_t v = 0; v < nv; ++v) {
       int c[3];
       coords(v, c);
-      bool interior = true;
-      for (int d = 0; d < 3; ++d)
-        if (c[d] == 0 || c[d] == n) interior = false;
+      const int kg = c[2] + kz0;  // whole-mesh plane
+      const bool interior = c[0] > 0 && c[0] < n && c[1] > 0 && c[1] < n && kg > 0 && kg < nzg;
+      // the whole mesh's vertex id keys the jitter stream
+      const uint64_t vg = (uint64_t)c[0] + (uint64_t)(n + 1) * ((uint64_t)c[1] + (uint64_t)(n + 1) * kg);
+      const int cg[3] = {c[0], c[1], kg};
       for (int d = 0; d < 3; ++d) {
-        double x = (double)c[d] * h;
-        if (interior && amp > 0) x = x + (amp * h) * (2.0 * u01(seed, (uint64_t)(3 * v + d)) - 1.0);
+        double x = (double)cg[d] * h;
+        if (interior && amp > 0) x = x + (amp * h) * (2.0 * u01(seed, 3 * vg + d) - 1.0);
         xyz[(size_t)(3 * v + d)] = x;
       }
     }
@@ -156,7 +181,7 @@ struct TetMesh {
     fid.assign((size_t)(nv * 12), -1);
     // numbering: (k, j, x-block of 32 vertices, type, i)
     int64_t ne = 0, nf = 0;
-    for (int k = 0; k <= n; ++k)
+    for (int k = 0; k <= nz; ++k)
       for (int j = 0; j <= n; ++j)
         for (int ib = 0; ib <= n; ib += kBlock) {
           const int ie = std::min(ib + kBlock, n + 1);
@@ -166,7 +191,7 @@ struct TetMesh {
               if (!inside(e)) continue;
               bool bnd = false;
               for (int d = 0; d < 3; ++d)
-                if (kET[t][d] == 0 && (c[d] == 0 || c[d] == n)) bnd = true;
+                if (kET[t][d] == 0 && on_wall(d, c[d])) bnd = true;
               if (bnd) continue;  // PEC: boundary edges are not DOFs
               eid[(size_t)(vid(i, j, k) * 7 + t)] = (int32_t)ne++;
             }

@@ -520,9 +520,19 @@ class TetMesh:
     """Jittered Kuhn/Freudenthal tet mesh of the unit cube, PEC walls, first-
     order Whitney forms (host C++ builder; numbering contract in DESIGN.md)."""
 
-    def __init__(self, n: int, jitter: float = 0.1, seed: int = 0):
+    def __init__(self, n: int, jitter: float = 0.1, seed: int = 0, nzg: int | None = None,
+                 planes: tuple[int, int] | None = None):
+        """n^3 cubes of the unit cube; or, with nzg / planes, vertex planes
+        [k0, k1] of the n x n x nzg mesh (a z-slab: the whole mesh's jitter,
+        entity order and PEC walls; its cut planes are not walls)."""
         h = C.c_void_p()
-        L.check(L.lib().sfeec_tetmesh_create(int(n), float(jitter), int(seed), C.byref(h)))
+        if nzg is None and planes is None:
+            L.check(L.lib().sfeec_tetmesh_create(int(n), float(jitter), int(seed), C.byref(h)))
+        else:
+            nzg = n if nzg is None else int(nzg)
+            k0, k1 = planes if planes is not None else (0, nzg)
+            L.check(L.lib().sfeec_tetmesh_create_slab(int(n), nzg, int(k0), int(k1), float(jitter),
+                                                      int(seed), C.byref(h)))
         self._h = h
         self.n = n
         c = [C.c_int64() for _ in range(4)]

@@ -150,3 +150,35 @@ def test_spai_columns_are_stationary():
         r = a @ qd[:, l]
         r[l] -= 1.0
         assert np.max(np.abs(a[:, idx].T @ r)) <= 1e-12
+
+
+@pytest.mark.parametrize("nzg,k0,k1", [(5, 1, 5), (5, 0, 3), (6, 2, 5)])
+def test_slab_rows_equal_whole_mesh_rows(nzg, k0, k1):
+    """A z-slab (vertex planes [k0, k1] of the n x n x nzg mesh) numbers its
+    entities as the whole mesh does, shifted: its complete rows of C, M1 and
+    M2 are bitwise the whole mesh's (the per-rank assembly of the lattice
+    slabs relies on this)."""
+    n = 4
+    whole = S.TetMesh(n, 0.12, 9, nzg=nzg)
+    slab = S.TetMesh(n, 0.12, 9, nzg=nzg, planes=(k0, k1))
+    xw, evw, fvw, _ = whole.geometry()
+    xs, evs, fvs, _ = slab.geometry()
+    nv_plane = (n + 1) ** 2
+    assert np.array_equal(xs, xw[k0 * nv_plane:(k1 + 1) * nv_plane])
+    # entity id offsets: the whole mesh's ids of the slab's first plane
+    eoff = int(np.searchsorted(evw[:, 0], k0 * nv_plane))
+    foff = int(np.searchsorted(fvw[:, 0], k0 * nv_plane))
+    vsh = k0 * nv_plane
+    # (rows whose columns all lie below the slab's top plane: the top plane
+    # lacks the edges leaving the slab, so its ids shift, not its order)
+    for ops, ents, off, lo, hi in ((("curl", "curl"), (fvs, fvw), (foff, eoff), k0, k1 - 2),
+                                   (("mass1", "mass1"), (evs, evw), (eoff, eoff), k0 + 1, k1 - 2),
+                                   (("mass2", "mass2"), (fvs, fvw), (foff, foff), k0 + 1, k1 - 2)):
+        a, b = getattr(slab, ops[0])(), getattr(whole, ops[1])()
+        lo, hi = (0 if k0 == 0 else lo), (k1 if k1 == nzg else hi)
+        rows = [r for r in range(a.rows) if lo <= (ents[0][r, 0] + vsh) // nv_plane <= hi]
+        assert rows
+        for r in rows:
+            assert np.array_equal(ents[0][r] + vsh, ents[1][r + off[0]])
+            assert np.array_equal(a.row_cols(r) + off[1], b.row_cols(r + off[0])), (ops, r)
+            assert np.array_equal(a.row_vals(r), b.row_vals(r + off[0])), (ops, r)
