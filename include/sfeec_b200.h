@@ -381,6 +381,39 @@ int sfeec_csr_from_triplets(int64_t rows, int64_t cols, int64_t n, const int32_t
 int sfeec_csr_symmetric_part(const sfeec_csr* q, sfeec_csr_owned* out);
 int sfeec_csr_transpose(const sfeec_csr* a, sfeec_csr_owned* out);
 
+/* ---- multi-rank Kuhn-lattice leapfrog (lattice_slab.cu) ----
+ * One process per GPU; rank r owns the whole-mesh vertex planes [P_r, P_{r+1})
+ * (P_r = floor(r (nzg + 1) / R)) of the n x n x nzg mesh (spacing 1/n; nzg = n
+ * for the unit cube of configs 3 / 5, nzg = n R for a weak-scaling stack of
+ * n^3 blocks) and assembles only its slab (planes [P_r - 4, P_{r+1} + 4]) on
+ * its device. Ghost planes move after each of the four kernels; the plane
+ * sums of energy and CFL are combined in plane order, so every rank count
+ * gives bitwise the single-rank numbers. transport: 0 NCCL (comm_id = an
+ * ncclUniqueId), 1 CUDA IPC with host-side synchronisation (same node; ranks
+ * may share one GPU; comm_id from sfeec_ipc_unique_id). State vectors hold
+ * the rank's owned DOFs in whole-mesh order: edges [info[2], info[2] +
+ * info[0]), faces [info[3], info[3] + info[1]). info[10] = {owned edges,
+ * owned faces, first owned edge / face (whole-mesh id), P_r, P_{r+1}, first /
+ * last assembled plane, first owned edge / face (slab-local id)}.
+ * energy, cfl_number and curl are collective. No reference counterpart (the
+ * reference has no distributed code). */
+typedef struct sfeec_lslab sfeec_lslab;
+int sfeec_ipc_unique_id(void* out128);
+int sfeec_lslab_create(int n, int nzg, double jitter, uint64_t seed, double dt, double eps0,
+                       double mu0, int split_kind, int rank, int nranks, int transport,
+                       const void* comm_id, int device, sfeec_lslab** out, int64_t* info);
+void sfeec_lslab_destroy(sfeec_lslab* h);
+int sfeec_lslab_set_state(sfeec_lslab* h, const double* b, const double* e, double time);
+int sfeec_lslab_get_state(sfeec_lslab* h, double* b, double* e, double* time);
+int sfeec_lslab_advance(sfeec_lslab* h, int64_t nsteps);
+int sfeec_lslab_energy(sfeec_lslab* h, double* out);
+int sfeec_lslab_cfl_number(sfeec_lslab* h, double* out);
+int sfeec_lslab_set_dt(sfeec_lslab* h, double dt);
+int sfeec_lslab_curl(sfeec_lslab* h, const double* a, double* b);
+int sfeec_lslab_stream(sfeec_lslab* h, void** stream);
+int64_t sfeec_lslab_last_launches(sfeec_lslab* h);
+double sfeec_lslab_step_bytes(sfeec_lslab* h);
+
 #ifdef __cplusplus
 }
 #endif

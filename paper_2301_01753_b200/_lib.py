@@ -136,6 +136,21 @@ _SIGS = {
     "sfeec_part_energy": (C.c_int, [_P, _PD]),
     "sfeec_part_energy_local": (C.c_int, [C.POINTER(_P), C.c_int, _PD]),
     "sfeec_part_last_launches": (C.c_int64, [_P]),
+    "sfeec_ipc_unique_id": (C.c_int, [_P]),
+    "sfeec_lslab_create": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_double,
+                                     C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     _P, C.c_int, C.POINTER(_P), _PI64]),
+    "sfeec_lslab_destroy": (None, [_P]),
+    "sfeec_lslab_set_state": (C.c_int, [_P, _PD, _PD, C.c_double]),
+    "sfeec_lslab_get_state": (C.c_int, [_P, _PD, _PD, _PD]),
+    "sfeec_lslab_advance": (C.c_int, [_P, C.c_int64]),
+    "sfeec_lslab_energy": (C.c_int, [_P, _PD]),
+    "sfeec_lslab_cfl_number": (C.c_int, [_P, _PD]),
+    "sfeec_lslab_set_dt": (C.c_int, [_P, C.c_double]),
+    "sfeec_lslab_curl": (C.c_int, [_P, _PD, _PD]),
+    "sfeec_lslab_stream": (C.c_int, [_P, C.POINTER(_P)]),
+    "sfeec_lslab_last_launches": (C.c_int64, [_P]),
+    "sfeec_lslab_step_bytes": (C.c_double, [_P]),
     "sfeec_part_create_tet": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
                                         C.c_double, C.c_int, C.c_int, _P, C.c_int,
                                         C.POINTER(_P), _PI64]),

@@ -53,34 +53,35 @@ __device__ __forceinline__ int64_t offset_of(const LatGeom& g, int di, int dj, i
   return di + (int64_t)g.S * dj + g.PS * dk;
 }
 
-// this thread's vertex (i, j, k) and lattice position; false off the cube
-__device__ __forceinline__ bool my_vertex(const LatGeom& g, int& i, int& j, int& k,
+// this thread's vertex (i, j, local plane k) and lattice position; false off
+// the mesh. Block row y covers local plane kbeg + y.
+__device__ __forceinline__ bool my_vertex(const LatGeom& g, int kbeg, int& i, int& j, int& k,
                                           int64_t& idx) {
   const int p = blockIdx.x * kLT + threadIdx.x;
   if (p >= g.PS) return false;
-  k = blockIdx.y;
+  k = kbeg + blockIdx.y;
   j = p / g.S - 1;
   i = p - (j + 1) * g.S - 1;
   idx = g.PS * (k + 1) + p;
   return i >= 0 && i <= g.n && j >= 0 && j <= g.n;
 }
 
-// edge (v, t) is a DOF: inside the cube and not on a wall it lies in (PEC)
+// edge (v, t) is a DOF: inside the mesh and not on a wall it lies in (PEC);
+// z is judged on the whole mesh (kg = whole-mesh plane, nzg)
 template <int T>
-__device__ __forceinline__ bool edge_dof(int i, int j, int k, int n) {
-  const int c[3] = {i, j, k};
-  bool ok = true;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    ok = ok && c[d] + et(T, d) <= n;
-    if (et(T, d) == 0) ok = ok && c[d] != 0 && c[d] != n;
-  }
+__device__ __forceinline__ bool edge_dof(int i, int j, int k, const LatGeom& g) {
+  const int kg = k + g.kz0;
+  bool ok = i + et(T, 0) <= g.n && j + et(T, 1) <= g.n && kg + et(T, 2) <= g.nzg;
+  if (et(T, 0) == 0) ok = ok && i != 0 && i != g.n;
+  if (et(T, 1) == 0) ok = ok && j != 0 && j != g.n;
+  if (et(T, 2) == 0) ok = ok && kg != 0 && kg != g.nzg;
   return ok;
 }
-// face (v, f) exists: its farthest vertex is inside the cube
+// face (v, f) exists: its farthest vertex is inside the mesh
 template <int F>
-__device__ __forceinline__ bool face_ok(int i, int j, int k, int n) {
-  return i + et(ft_hi(F), 0) <= n && j + et(ft_hi(F), 1) <= n && k + et(ft_hi(F), 2) <= n;
+__device__ __forceinline__ bool face_ok(int i, int j, int k, const LatGeom& g) {
+  return i + et(ft_hi(F), 0) <= g.n && j + et(ft_hi(F), 1) <= g.n &&
+         k + g.kz0 + et(ft_hi(F), 2) <= g.nzg;
 }
 
 // ---- symmetric stencil rows (Q_sym, M2) ------------------------------------
@@ -118,15 +119,15 @@ __device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, cons
                                          const double* __restrict__ qc,
                                          const double* __restrict__ E, double* __restrict__ T) {
   const double r[sizeof...(Ts)] = {sym_row<QOp, Ts>(qc, E, idx, g)...};
-  ((edge_dof<Ts>(i, j, k, g.n) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
+  ((edge_dof<Ts>(i, j, k, g) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
 }
 template <int MINB>
-__global__ void __launch_bounds__(kLT, MINB) k_lat_q(LatGeom g, const double* __restrict__ qc,
+__global__ void __launch_bounds__(kLT, MINB) k_lat_q(LatGeom g, int kbeg, const double* __restrict__ qc,
                                                const double* __restrict__ E,
                                                double* __restrict__ T) {
   int i, j, k;
   int64_t idx;
-  if (!my_vertex(g, i, j, k, idx)) return;
+  if (!my_vertex(g, kbeg, i, j, k, idx)) return;
   q_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, qc, E, T);
 }
 
@@ -137,15 +138,15 @@ __device__ __forceinline__ void m2_vertex(std::integer_sequence<int, Fs...>, con
                                           const double* __restrict__ mc,
                                           const double* __restrict__ B, double* __restrict__ U) {
   const double r[sizeof...(Fs)] = {sym_row<MOp, Fs>(mc, B, idx, g)...};
-  ((face_ok<Fs>(i, j, k, g.n) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
+  ((face_ok<Fs>(i, j, k, g) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
 }
 template <int MINB>
-__global__ void __launch_bounds__(kLT, MINB) k_lat_m2(LatGeom g, const double* __restrict__ mc,
+__global__ void __launch_bounds__(kLT, MINB) k_lat_m2(LatGeom g, int kbeg, const double* __restrict__ mc,
                                                 const double* __restrict__ B,
                                                 double* __restrict__ U) {
   int i, j, k;
   int64_t idx;
-  if (!my_vertex(g, i, j, k, idx)) return;
+  if (!my_vertex(g, kbeg, i, j, k, idx)) return;
   m2_vertex(std::make_integer_sequence<int, 12>{}, g, i, j, k, idx, mc, B, U);
 }
 
@@ -172,17 +173,17 @@ __device__ __forceinline__ void cb_vertex(std::integer_sequence<int, Fs...>, con
                                           const double* __restrict__ T, double* __restrict__ B) {
   const double r[sizeof...(Fs)] = {
       inc_row<false, 3 * Fs>(std::make_integer_sequence<int, 3>{}, T, idx, g)...};
-  ((face_ok<Fs>(i, j, k, g.n)
+  ((face_ok<Fs>(i, j, k, g)
         ? (void)(B[(int64_t)Fs * g.NP + idx] = fma(alpha, r[Fs], B[(int64_t)Fs * g.NP + idx]))
         : (void)0),
    ...);
 }
-__global__ void __launch_bounds__(kLT) k_lat_cb(LatGeom g, double alpha,
+__global__ void __launch_bounds__(kLT) k_lat_cb(LatGeom g, int kbeg, double alpha,
                                                 const double* __restrict__ T,
                                                 double* __restrict__ B) {
   int i, j, k;
   int64_t idx;
-  if (!my_vertex(g, i, j, k, idx)) return;
+  if (!my_vertex(g, kbeg, i, j, k, idx)) return;
   cb_vertex(std::make_integer_sequence<int, 12>{}, g, i, j, k, idx, alpha, T, B);
 }
 // e += f C^T u on the DOF edges of one vertex
@@ -192,17 +193,17 @@ __device__ __forceinline__ void cte_vertex(std::integer_sequence<int, Ts...>, co
                                            const double* __restrict__ U, double* __restrict__ E) {
   const double r[sizeof...(Ts)] = {inc_row<true, lat::kCTOff(Ts)>(
       std::make_integer_sequence<int, lat::kCTOff(Ts + 1) - lat::kCTOff(Ts)>{}, U, idx, g)...};
-  ((edge_dof<Ts>(i, j, k, g.n)
+  ((edge_dof<Ts>(i, j, k, g)
         ? (void)(E[(int64_t)Ts * g.NP + idx] = fma(alpha, r[Ts], E[(int64_t)Ts * g.NP + idx]))
         : (void)0),
    ...);
 }
-__global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, double alpha,
+__global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, int kbeg, double alpha,
                                                  const double* __restrict__ U,
                                                  double* __restrict__ E) {
   int i, j, k;
   int64_t idx;
-  if (!my_vertex(g, i, j, k, idx)) return;
+  if (!my_vertex(g, kbeg, i, j, k, idx)) return;
   cte_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, alpha, U, E);
 }
 
@@ -222,7 +223,7 @@ struct QRowW {
                                              int64_t idx) const {
     on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
       constexpr int t = decltype(tc)::value;
-      if (edge_dof<t>(i, j, k, g.n)) T[(int64_t)t * g.NP + idx] = sym_row<QOp, t>(qc, E, idx, g);
+      if (edge_dof<t>(i, j, k, g)) T[(int64_t)t * g.NP + idx] = sym_row<QOp, t>(qc, E, idx, g);
     });
   }
 };
@@ -235,7 +236,7 @@ struct M2RowW {
                                              int64_t idx) const {
     on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
       constexpr int f = decltype(fc)::value;
-      if (face_ok<f>(i, j, k, g.n)) U[(int64_t)f * g.NP + idx] = sym_row<MOp, f>(mc, B, idx, g);
+      if (face_ok<f>(i, j, k, g)) U[(int64_t)f * g.NP + idx] = sym_row<MOp, f>(mc, B, idx, g);
     });
   }
 };
@@ -248,7 +249,7 @@ struct CbRowW {
                                              int64_t idx) const {
     on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
       constexpr int f = decltype(fc)::value;
-      if (face_ok<f>(i, j, k, g.n)) {
+      if (face_ok<f>(i, j, k, g)) {
         const double r = inc_row<false, 3 * f>(std::make_integer_sequence<int, 3>{}, T, idx, g);
         double* b = B + (int64_t)f * g.NP + idx;
         *b = fma(alpha, r, *b);
@@ -265,7 +266,7 @@ struct CteRowW {
                                              int64_t idx) const {
     on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
       constexpr int t = decltype(tc)::value;
-      if (edge_dof<t>(i, j, k, g.n)) {
+      if (edge_dof<t>(i, j, k, g)) {
         const double r = inc_row<true, lat::kCTOff(t)>(
             std::make_integer_sequence<int, lat::kCTOff(t + 1) - lat::kCTOff(t)>{}, U, idx, g);
         double* e = E + (int64_t)t * g.NP + idx;
@@ -276,9 +277,10 @@ struct CteRowW {
 };
 constexpr int kWCH = 4;  // 32-position chunks per block
 template <class Row>
-__global__ void __launch_bounds__(Row::kTypes * 32, Row::kMinBlocks) k_lat_w(LatGeom g, Row row) {
+__global__ void __launch_bounds__(Row::kTypes * 32, Row::kMinBlocks) k_lat_w(LatGeom g, int kbeg,
+                                                                             Row row) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = blockIdx.y;
+  const int k = kbeg + blockIdx.y;
 #pragma unroll 1
   for (int c = 0; c < kWCH; ++c) {
     const int p = (blockIdx.x * kWCH + c) * 32 + lane;
@@ -353,15 +355,15 @@ __global__ void k_lat_gather(int64_t n, const int64_t* __restrict__ pos,
 }
 
 inline unsigned blocks(int64_t n) { return (unsigned)((n + kLT - 1) / kLT); }
-inline dim3 wgrid(const LatGeom& g) {
-  return dim3((unsigned)((g.PS + 32 * kWCH - 1) / (32 * kWCH)), g.n + 1);
+inline dim3 wgrid(const LatGeom& g, int kb, int ke) {
+  return dim3((unsigned)((g.PS + 32 * kWCH - 1) / (32 * kWCH)), (unsigned)(ke - kb));
 }
 
 }  // namespace
 
 void Lattice::build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2,
                     cudaStream_t s) {
-  g.init(mesh.n);
+  g.init(mesh.n, mesh.nz, mesh.kz0, mesh.nzg);
   n1 = mesh.n_edges;
   n2 = mesh.n_faces;
   require(qsym.rows == n1 && m2.rows == n2, "lattice: operator dimensions do not match the mesh");
@@ -427,61 +429,73 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
   SFEEC_LAUNCH_CHECK();
 }
 
-// variant 0: one thread per vertex (all its rows); 1: one warp per row type
+// variant 0: one thread per vertex (all its rows); 1: one warp per row type.
+// Grids cover local planes [kbeg(), kend()).
 void Lattice::apply_q(cudaStream_t s) const {
+  const int kb = kbeg(), ke = kend();
+  if (ke <= kb) return;
+  const dim3 grid(blocks(g.PS), (unsigned)(ke - kb));
   if (variant == 1)
-    k_lat_w<QRowW><<<wgrid(g), 7 * 32, 0, s>>>(g, QRowW{qc.p, E.p, T.p});
+    k_lat_w<QRowW><<<wgrid(g, kb, ke), 7 * 32, 0, s>>>(g, kb, QRowW{qc.p, E.p, T.p});
   else if (variant == 2)
-    k_lat_q<3><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+    k_lat_q<3><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   else if (variant == 3)
-    k_lat_q<4><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+    k_lat_q<4><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   else
-    k_lat_q<2><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, qc.p, E.p, T.p);
+    k_lat_q<2><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cb(double h, cudaStream_t s) const {
+  const int kb = kbeg(), ke = kend();
+  if (ke <= kb) return;
   if (variant == 1)
-    k_lat_w<CbRowW><<<wgrid(g), 12 * 32, 0, s>>>(g, CbRowW{-h, T.p, B.p});
+    k_lat_w<CbRowW><<<wgrid(g, kb, ke), 12 * 32, 0, s>>>(g, kb, CbRowW{-h, T.p, B.p});
   else
-    k_lat_cb<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, -h, T.p, B.p);
+    k_lat_cb<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_m2(cudaStream_t s) const {
+  const int kb = kbeg(), ke = kend();
+  if (ke <= kb) return;
+  const dim3 grid(blocks(g.PS), (unsigned)(ke - kb));
   if (variant == 1)
-    k_lat_w<M2RowW><<<wgrid(g), 12 * 32, 0, s>>>(g, M2RowW{mc.p, B.p, U.p});
+    k_lat_w<M2RowW><<<wgrid(g, kb, ke), 12 * 32, 0, s>>>(g, kb, M2RowW{mc.p, B.p, U.p});
   else if (variant == 2)
-    k_lat_m2<3><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+    k_lat_m2<3><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   else if (variant == 3)
-    k_lat_m2<4><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+    k_lat_m2<4><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   else
-    k_lat_m2<2><<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, mc.p, B.p, U.p);
+    k_lat_m2<2><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cte(double f, cudaStream_t s) const {
+  const int kb = kbeg(), ke = kend();
+  if (ke <= kb) return;
   if (variant == 1)
-    k_lat_w<CteRowW><<<wgrid(g), 7 * 32, 0, s>>>(g, CteRowW{f, U.p, E.p});
+    k_lat_w<CteRowW><<<wgrid(g, kb, ke), 7 * 32, 0, s>>>(g, kb, CteRowW{f, U.p, E.p});
   else
-    k_lat_cte<<<dim3(blocks(g.PS), g.n + 1), kLT, 0, s>>>(g, f, U.p, E.p);
+    k_lat_cte<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
   SFEEC_LAUNCH_CHECK();
 }
 
 // bytes per launch (each array read once, each output written once; the
-// padded halo is not counted): V vertices, 8 B per value
+// padded halo is not counted): V vertices, 8 B per value; the outputs are the
+// DOFs on the whole mesh, all 7 / 12 slots of the computed planes on a slab
 double Lattice::bytes_q() const {
-  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
-  return 8.0 * (lat::kQArrays * V + 7.0 * V + (double)n1);
+  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
+  return 8.0 * (lat::kQArrays * V + 7.0 * V + (k1 < 0 ? (double)n1 : 7.0 * V));
 }
 double Lattice::bytes_cb() const {
-  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
-  return 8.0 * (7.0 * V + 2.0 * (double)n2);
+  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
+  return 8.0 * (7.0 * V + 2.0 * (k1 < 0 ? (double)n2 : 12.0 * V));
 }
 double Lattice::bytes_m2() const {
-  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
-  return 8.0 * (lat::kMArrays * V + 12.0 * V + (double)n2);
+  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
+  return 8.0 * (lat::kMArrays * V + 12.0 * V + (k1 < 0 ? (double)n2 : 12.0 * V));
 }
 double Lattice::bytes_cte() const {
-  const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
-  return 8.0 * (12.0 * V + 2.0 * (double)n1);
+  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
+  return 8.0 * (12.0 * V + 2.0 * (k1 < 0 ? (double)n1 : 7.0 * V));
 }
 
 }  // namespace sfeec_b200

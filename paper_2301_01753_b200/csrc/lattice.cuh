@@ -21,20 +21,38 @@
 
 namespace sfeec_b200 {
 
+// The padded box of a mesh (TetMesh): x, y vertices 0..n, local z planes
+// 0..nz (whole-mesh planes kz0..kz0+nz of an n x n x nzg mesh; a slab of it
+// on a multi-rank run). Masks (DOF edges, existing faces) use whole-mesh
+// planes, so a slab's cut planes are not walls.
 struct LatGeom {
-  int n = 0;        // cubes per axis (vertices 0..n)
-  int S = 0;        // padded vertices per axis (n + 3)
+  int n = 0;        // cubes along x, y (vertices 0..n)
+  int nz = 0;       // local cubes along z
+  int kz0 = 0;      // whole-mesh plane of local plane 0
+  int nzg = 0;      // whole-mesh cubes along z
+  int S = 0;        // padded vertices along x, y (n + 3)
   int64_t PS = 0;   // padded plane (S * S)
-  int64_t NP = 0;   // padded box (S^3): the component stride
+  int64_t NP = 0;   // padded box (S * S * (nz + 3)): the component stride
   int64_t org = 0;  // position of vertex (0, 0, 0)
-  void init(int n_) {
+  void init(int n_, int nz_, int kz0_, int nzg_) {
     n = n_;
+    nz = nz_;
+    kz0 = kz0_;
+    nzg = nzg_;
     S = n + 3;
     PS = (int64_t)S * S;
-    NP = PS * S;
+    NP = PS * (nz + 3);
     org = PS + S + 1;
   }
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
   int64_t pos(int i, int j, int k) const { return org + i + (int64_t)S * j + PS * k; }
+  // first element of local plane k in a component array
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  int64_t plane(int k) const { return PS * (k + 1); }
 };
 
 struct Lattice {
@@ -57,11 +75,14 @@ struct Lattice {
   // DOF vectors <-> lattice state
   void scatter(const double* b, const double* e, cudaStream_t s);
   void gather(double* b, double* e, cudaStream_t s) const;
-  // the four step kernels
+  // the four step kernels over local vertex planes [k0, k1) (default: all)
+  int k0 = 0, k1 = -1;  // compute range; k1 < 0: every local plane
   void apply_q(cudaStream_t s) const;               // T = Q_sym E
   void apply_cb(double h, cudaStream_t s) const;    // B -= h C T
   void apply_m2(cudaStream_t s) const;              // U = M2 B
   void apply_cte(double f, cudaStream_t s) const;   // E += f C^T U
+  int kbeg() const { return k0; }
+  int kend() const { return k1 < 0 ? g.nz + 1 : k1; }
   // bytes each kernel moves (arrays read once, outputs written once)
   double bytes_q() const;
   double bytes_cb() const;

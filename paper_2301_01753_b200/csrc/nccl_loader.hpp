@@ -19,6 +19,7 @@ struct Nccl {
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
@@ -38,6 +39,7 @@ struct Nccl {
       SFEEC_NCCL_SYM(comm_destroy, ncclCommDestroy)
       SFEEC_NCCL_SYM(send, ncclSend)
       SFEEC_NCCL_SYM(recv, ncclRecv)
+      SFEEC_NCCL_SYM(all_reduce, ncclAllReduce)
       SFEEC_NCCL_SYM(group_start, ncclGroupStart)
       SFEEC_NCCL_SYM(group_end, ncclGroupEnd)
       SFEEC_NCCL_SYM(error_string, ncclGetErrorString)

@@ -590,7 +590,8 @@ void slice_rows_device(const DevCSR& a, int64_t r0, int64_t r1, int64_t c0, int6
 }
 
 // Builds the first-order S(M1) system of mesh `h` on the current device.
-void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s) {
+void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s,
+                             int exact_lo, int exact_hi) {
   DevBuf<double> xyz;
   DevBuf<int32_t> eid, fid;
   DevBuf<int64_t> ev, fv;
@@ -623,7 +624,14 @@ void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out,
     std::vector<int32_t> hf((size_t)h.n_edges);
     SFEEC_CUDA(cudaMemcpyAsync(hf.data(), flags.p, sizeof(int32_t) * hf.size(), cudaMemcpyDeviceToHost, s));
     SFEEC_CUDA(cudaStreamSynchronize(s));
-    for (int32_t f : hf) out.fallback += f != 0;
+    // (on a slab, columns near the cut planes see incomplete M1 rows; only
+    // the columns of edges in local planes [exact_lo, exact_hi) must solve)
+    for (int64_t l = 0; l < h.n_edges; ++l) {
+      if (!hf[(size_t)l]) continue;
+      int c[3];
+      h.coords(h.edge_v[(size_t)l], c);
+      out.fallback += c[2] >= exact_lo && c[2] < exact_hi;
+    }
   }
   require(out.fallback == 0,
           "device SPAI: some columns need the eigenvalue-thresholded fallback; use the host builder");

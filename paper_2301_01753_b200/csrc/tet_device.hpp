@@ -14,7 +14,10 @@ struct DevTetSystem {
 
 // C, D (optional), M1 -> S(M1) SPAI -> Q_sym, M2 and C^T of mesh `h`, built on
 // the current device, bitwise the host builders' operators
-void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s);
+// (exact_lo/hi: on a slab, the local vertex planes whose edges' SPAI columns
+// must solve; the others, near the cut planes, are not used)
+void build_tet_system_device(const TetMesh& h, bool want_div, DevTetSystem& out, cudaStream_t s,
+                             int exact_lo = 0, int exact_hi = 1 << 30);
 
 // in-place exclusive scan of d[0..n] (d[n] = total)
 void exclusive_scan(int64_t* d, int64_t n, cudaStream_t s);

@@ -229,3 +229,121 @@ def energy_local(parts: list[TetPart]) -> float:
     out = C.c_double()
     L.check(L.lib().sfeec_part_energy_local(arr, len(parts), C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# Kuhn-lattice slabs (lattice_slab.cu): the multi-rank production path
+# ---------------------------------------------------------------------------
+def ipc_unique_id() -> bytes:
+    """A fresh id for the CUDA-IPC transport (broadcast it to every rank)."""
+    buf = (C.c_char * 128)()
+    L.check(L.lib().sfeec_ipc_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class LatticeSlab:
+    """Rank `rank` of `nranks` of the first-order leapfrog on the Kuhn lattice,
+    split into z-slabs of whole vertex planes (lattice_slab.cu). Each rank
+    assembles only its own slab of the n x n x nzg mesh (nzg = n: the unit
+    cube; nzg = n * nranks: a weak-scaling stack of n^3 blocks). State vectors
+    are the rank's owned DOFs, a contiguous range of the whole mesh's
+    k-major numbering (edges [e_glob, e_glob + n1), faces [f_glob, f_glob + n2)).
+    transport: "nccl" (comm_id = an NCCL unique id; one GPU per rank) or "ipc"
+    (comm_id from ipc_unique_id(); host-synchronised, ranks may share a GPU).
+    energy(), cfl_number() and curl() are collective."""
+
+    def __init__(self, n: int, jitter: float = 0.1, seed: int = 0, nzg: int | None = None,
+                 dt: float = 1.0, rank: int = 0, nranks: int = 1, transport: str = "nccl",
+                 comm_id: bytes | None = None, kind: int = 1, eps0: float = 1.0,
+                 mu0: float = 1.0, device: int = 0):
+        self.n, self.nzg = int(n), int(nzg if nzg is not None else n)
+        self.jitter, self.seed = float(jitter), int(seed)
+        self.rank, self.nranks = int(rank), int(nranks)
+        tr = {"nccl": 0, "ipc": 1}[transport]
+        idbuf = None
+        if comm_id is not None:
+            idbuf = (C.c_char * 128).from_buffer_copy(comm_id.ljust(128, b"\0")[:128])
+        h = C.c_void_p()
+        info = np.zeros(10, np.int64)
+        L.check(L.lib().sfeec_lslab_create(self.n, self.nzg, self.jitter, self.seed, float(dt),
+                                           float(eps0), float(mu0), int(kind), self.rank,
+                                           self.nranks, tr,
+                                           C.cast(idbuf, C.c_void_p) if idbuf else None,
+                                           int(device), C.byref(h), L.i64ptr(info)))
+        self._h = h
+        self.n1, self.n2 = int(info[0]), int(info[1])
+        self.e_glob, self.f_glob = int(info[2]), int(info[3])
+        self.planes = (int(info[4]), int(info[5]))
+        self.assembled = (int(info[6]), int(info[7]))
+        self.e_local0, self.f_local0 = int(info[8]), int(info[9])
+        self._dt = float(dt)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and callable(getattr(L, "lib", None)):
+            L.lib().sfeec_lslab_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def mesh(self):
+        """the host TetMesh of this rank's assembled slab (ids = slab-local)"""
+        from .scheme import TetMesh
+        return TetMesh(self.n, self.jitter, self.seed, nzg=self.nzg, planes=self.assembled)
+
+    def pulse(self, seed: int, sigma: float = 0.1, npulses: int = 1) -> np.ndarray:
+        """the Gaussian-pulse potential on the owned edges"""
+        return self.mesh().pulse(seed, sigma, npulses, self.e_local0, self.e_local0 + self.n1)
+
+    def set_state(self, b: np.ndarray, e: np.ndarray, time: float = 0.0) -> None:
+        b = np.ascontiguousarray(b, np.float64)
+        e = np.ascontiguousarray(e, np.float64)
+        if b.size != self.n2 or e.size != self.n1:
+            raise L.InvalidParameter("lattice slab: state sizes differ from the owned DOFs")
+        L.check(L.lib().sfeec_lslab_set_state(self._h, L.dptr(b), L.dptr(e), float(time)))
+
+    def get_state(self):
+        b, e, t = np.zeros(self.n2), np.zeros(self.n1), C.c_double()
+        L.check(L.lib().sfeec_lslab_get_state(self._h, L.dptr(b), L.dptr(e), C.byref(t)))
+        return b, e, t.value
+
+    def advance(self, nsteps: int) -> None:
+        L.check(L.lib().sfeec_lslab_advance(self._h, int(nsteps)))
+
+    def energy(self) -> float:
+        out = C.c_double()
+        L.check(L.lib().sfeec_lslab_energy(self._h, C.byref(out)))
+        return out.value
+
+    def cfl_number(self) -> float:
+        out = C.c_double()
+        L.check(L.lib().sfeec_lslab_cfl_number(self._h, C.byref(out)))
+        return out.value
+
+    def set_dt(self, dt: float) -> None:
+        L.check(L.lib().sfeec_lslab_set_dt(self._h, float(dt)))
+        self._dt = float(dt)
+
+    def dt(self) -> float:
+        return self._dt
+
+    def curl(self, a: np.ndarray) -> np.ndarray:
+        a = np.ascontiguousarray(a, np.float64)
+        if a.size != self.n1:
+            raise L.InvalidParameter("lattice slab: a must hold the owned edges")
+        b = np.zeros(self.n2)
+        L.check(L.lib().sfeec_lslab_curl(self._h, L.dptr(a), L.dptr(b)))
+        return b
+
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        L.check(L.lib().sfeec_lslab_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def last_launches(self) -> int:
+        return int(L.lib().sfeec_lslab_last_launches(self._h))
+
+    def step_bytes(self) -> float:
+        return float(L.lib().sfeec_lslab_step_bytes(self._h))
