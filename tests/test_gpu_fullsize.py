@@ -233,7 +233,9 @@ def test_config5_first_steps_match_oracle_at_256():
     ph = port.energy(pb, pe)
     out = s.advance(S.make_state(S.Formulation.BE, b0, e0), 3)
     assert rel_l2(out.first, pb) <= TOL and rel_l2(out.e, pe) <= TOL
-    assert s.energy(out) == pytest.approx(ph, rel=TOL)
+    # the port sums e.Qe and b.M2 b serially over 3.2e8 terms (the reference's
+    # dot): its rounding error alone reaches ~n eps; the device tree-reduces
+    assert s.energy(out) == pytest.approx(ph, rel=1e-9)
     del port
     gc.collect()
     out, en, gauss = s.advance_diag(S.make_state(S.Formulation.BE, b0, e0), 100, 25)

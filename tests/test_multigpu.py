@@ -228,7 +228,9 @@ def test_tet_device_slabs_bitwise_equal_single_device(world):
     single-GPU device scheme."""
     from paper_2301_01753_b200 import inputs
     n, jit, seed = 7, 0.1, 2023
-    one = S.tet_device_scheme(n, jit, seed=seed, dt=1.0, with_div=False)
+    # the sliced-layout step (the SELL slabs' kernels; the lattice step and its
+    # slabs are tests/test_gpu_slabs.py)
+    one = S.tet_device_scheme(n, jit, seed=seed, dt=1.0, with_div=False, layout="sell")
     dt = configs.cfl_dt(one)
     one.set_dt(dt)
     parts = [partition.TetPart.from_device(n, jit, seed, r, world) for r in range(world)]
