@@ -42,15 +42,29 @@ def test_fig3_chain_matches_numpy_at_small_size():
     assert m.l2_error(w, 1, 1)[1] == pytest.approx(L2.l2_error(o, w, 1, 1)[1], rel=1e-12)
 
 
-def test_fig3_curl_curl_error_converges():
-    """the S(M1) SPAI curl-of-curl error against curl curl A_1 falls under
-    refinement (Fig. 3's quantity; the paper's 2-D S(M1) slope is ~h^0.73)"""
+def test_fig3_projection_converges_and_spai_tracks_exact_inverse():
+    """The device pipeline on refining meshes: the canonical projection of A_1
+    converges at first order; the S(M1)-SPAI curl-of-curl error (Fig. 3's
+    quantity) stays within a few percent of the exact-M1^-1 one. On these
+    3-D Kuhn meshes both curl-of-curl errors saturate near 0.46-0.48 (the
+    exact inverse too, so it is the P1- discretisation, not the SPAI: the
+    lowest-order saturation Fig. 3 shows for the diagonal Q)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
     errs = []
     for n in (8, 16, 32):
-        s = S.tet_device_scheme(n, 0.1, 5)
         m = S.TetMesh(n, 0.1, 5)
-        errs.append(m.l2_error(s.curl_of_curl(m.project_cavity(1)), 1, 1)[1])
+        errs.append(m.l2_error(m.project_cavity(1), 0, 1)[1])
     rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
-    print("relative L2 errors", errs, "rates", rates)
-    assert errs[0] > errs[1] > errs[2]
-    assert np.all(rates > 0.3)
+    assert np.all(rates > 0.9), (errs, rates)
+    n = 8
+    m = S.TetMesh(n, 0.1, 5)
+    s = S.tet_device_scheme(n, 0.1, 5)
+    a = m.project_cavity(1)
+    e_spai = m.l2_error(s.curl_of_curl(a), 1, 1)[1]
+    csr = lambda x: sp.csr_matrix((x.val, x.col_idx, x.row_ptr), shape=(x.rows, x.cols))
+    c, m1, m2 = csr(m.curl()), csr(m.mass1()), csr(m.mass2())
+    w_exact = spl.spsolve(m1.tocsc(), c.T @ (m2 @ (c @ a)))
+    e_exact = m.l2_error(w_exact, 1, 1)[1]
+    print("curl-of-curl relative L2 error: S(M1) SPAI", e_spai, "exact M1^-1", e_exact)
+    assert abs(e_spai - e_exact) <= 0.05 * e_exact
