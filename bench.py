@@ -409,6 +409,91 @@ class TetSlabRunner:
         return time.perf_counter() - t0
 
 
+class LatSlabRunner:
+    """Rank `rank` of the first-order tet leapfrog on Kuhn-lattice z-slabs
+    (lattice_slab.cu): every rank assembles only its slab on its own GPU and
+    exchanges one-plane ghosts over NCCL after each kernel. Weak scaling
+    (default): rank r holds the r-th n^3 block of an n x n x (n R) mesh;
+    --strong: the n^3 mesh of the config split into R slabs."""
+
+    kernel_label = ("lattice K-M2, K-CTe, K-Q, K-Cb on the owned vertex planes + NCCL "
+                    "one-plane ghost exchanges between them (lattice_slab.cu)")
+
+    def __init__(self, cfg, device, rank, world, dist, strong=False):
+        import paper_2301_01753_b200 as S
+        from paper_2301_01753_b200 import configs, inputs
+        from paper_2301_01753_b200.partition import LatticeSlab
+        t0 = time.perf_counter()
+        self.scaling = "strong" if strong else "weak"
+        ids = [None]
+        if dist is not None and world > 1:
+            ids = [S.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+        n = cfg["n"]
+        nzg = n if strong else n * world
+        self.s = LatticeSlab(n, cfg["jitter"], 2023, nzg=nzg, dt=1.0, rank=rank, nranks=world,
+                             transport="nccl", comm_id=ids[0], device=device)
+        s = self.s
+        if cfg["init"] == "gaussian":
+            a = inputs.gaussian_ids(7, np.arange(s.e_glob, s.e_glob + s.n1))
+        else:
+            a = s.pulse(7, 0.1, cfg.get("npulses", 1))
+        self.b0 = s.curl(a)
+        self.e0 = np.zeros(s.n1)
+        s.set_dt(configs.cfl_dt(s))
+        self.dt = s.dt()
+        self.n1, self.n2 = s.n1, s.n2
+        self.ndof = s.n1 + s.n2  # this rank's owned DOFs
+        self.setup_s = time.perf_counter() - t0
+        self._stream = None
+
+    def stream(self, torch):
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.s.stream_ptr())
+        return self._stream
+
+    def set_stream(self, ptr):
+        pass
+
+    def load(self):
+        self.s.set_state(self.b0, self.e0)
+
+    def advance(self, k):
+        self.s.advance(k)
+
+    def launches(self):
+        return self.s.last_launches()
+
+    def dominant(self, k_steps):
+        self.s.kernel_timing(True)
+        self.advance(k_steps)
+        t = self.s.kernel_timing(False)
+        self.per_kernel = {k: {"avg_ms": v["ms"] / max(v["launches"], 1),
+                               "launches": v["launches"],
+                               "bytes_per_launch": v["bytes_per_launch"],
+                               "gbs": v["bytes_per_launch"] / (v["ms"] / max(v["launches"], 1)
+                                                               * 1e-3) / 1e9
+                               if v["ms"] > 0 else None}
+                           for k, v in t.items()}
+        name = max(t, key=lambda k: t[k]["ms"])
+        d = t[name]
+        return name, d["bytes_per_launch"], d["ms"] / max(d["launches"], 1)
+
+    def step_bytes(self):
+        return self.s.step_bytes()
+
+    def diagnostics(self):
+        return self.s.energy(), None  # collective; the whole mesh's energy
+
+    def e2e(self, k, torch):
+        t0 = time.perf_counter()
+        self.s.set_state(self.b0, self.e0)
+        self.advance(k)
+        self.s.get_state()
+        self.e2e_bytes = 8 * (self.b0.size + self.e0.size)
+        return time.perf_counter() - t0
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -420,8 +505,10 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if cfg["kind"] == "yee":
         R = YeeRunner(cfg, local_rank, rank, world, dist)
+    elif cfg["kind"] == "tet" and (dist is not None or args.partitioned):
+        R = LatSlabRunner(cfg, local_rank, rank, world, dist, strong=args.strong)
     elif dist is not None or args.partitioned:
-        R = TetSlabRunner(cfg, local_rank, rank, world, dist)
+        R = TetSlabRunner(cfg, local_rank, rank, world, dist)  # P2-: sliced slabs
     else:
         R = TetRunner(cfg, local_rank)
     if hasattr(R, "stream"):
@@ -430,7 +517,14 @@ def run_ours(args, rank, world, local_rank):
         stream = torch.cuda.current_stream()
         R.set_stream(stream.cuda_stream)
     strong = getattr(R, "scaling", "weak") == "strong"
-    units = R.ndof if strong else world * R.ndof  # DOFs the whole job advances per step
+    if isinstance(R, LatSlabRunner):  # owned DOFs per rank: the job's total is their sum
+        units = R.ndof
+        if dist:
+            t_ = torch.tensor([float(R.ndof)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t_)
+            units = int(t_.item())
+    else:
+        units = R.ndof if strong else world * R.ndof  # DOFs the whole job advances per step
     R.load()
     energy0, gauss0 = R.diagnostics()
     R.advance(args.warmup)
@@ -449,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
     ms = start.elapsed_time(end)
     launches = R.launches()
     energy1, gauss1 = R.diagnostics()  # untimed: the state after warmup + steps
-    if dist:
+    if dist and not isinstance(R, LatSlabRunner):  # (the lattice slabs' energy is collective)
         t = torch.tensor([energy0, energy1], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)  # each rank holds its part of the energy sums
         energy0, energy1 = float(t[0]), float(t[1])
@@ -490,11 +584,14 @@ def run_ours(args, rank, world, local_rank):
                 + ", B0 = C A, E0 = 0)",
         "config": {"workload": f"{args.config}: {cfg['desc']}" + (
                        f" per GPU (global {cfg['n']}x{cfg['n']}x{cfg['n'] * world})"
-                       if world > 1 and cfg["kind"] == "yee" else (" (whole mesh over all GPUs)"
-                                                                    if world > 1 else "")),
+                       if world > 1 and not strong else (" (whole mesh over all GPUs)"
+                                                         if world > 1 else "")),
                    "dofs_per_gpu": ndof if not strong else ndof / world,
                    "n1_edges": R.n1, "n2_faces": R.n2, "dt": R.dt,
                    "parallelism": (f"z-slabs x{world}, NCCL ghost exchange" if cfg["kind"] == "yee"
+                                   else f"z-slabs x{world} of the Kuhn lattice, per-rank "
+                                        "assembly, NCCL one-plane ghost exchanges"
+                                   if isinstance(R, LatSlabRunner)
                                    else f"z-slabs x{world}, NCCL halo-plane exchange")
                                   if world > 1 else "single GPU",
                    "l2": "inputs larger than L2" if R.step_bytes() > 126e6 * 2
@@ -707,6 +804,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="tet configs at N=1: run the z-slab partition path (one slab)")
+    ap.add_argument("--strong", action="store_true",
+                    help="tet configs under torchrun: split the config's mesh (strong scaling) "
+                         "instead of one n^3 block per rank (weak scaling, the default)")
     ap.add_argument("--dist", action="store_true",
                     help="the multi-GPU code path (NCCL process group, slab runners, "
                          "max-over-ranks) even at world size 1, e.g. under torchrun with "

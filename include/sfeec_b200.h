@@ -413,6 +413,10 @@ int sfeec_lslab_curl(sfeec_lslab* h, const double* a, double* b);
 int sfeec_lslab_stream(sfeec_lslab* h, void** stream);
 int64_t sfeec_lslab_last_launches(sfeec_lslab* h);
 double sfeec_lslab_step_bytes(sfeec_lslab* h);
+/* per-kernel device time (ms[4], launches[4], bytes[4] per launch: 0 K-Q,
+ * 1 K-Cb, 2 K-CTe, 3 K-M2) since the last call, then (dis)arm the timing */
+int sfeec_lslab_kernel_timing(sfeec_lslab* h, int enable, double* ms, int64_t* launches,
+                              double* bytes);
 
 #ifdef __cplusplus
 }

@@ -151,6 +151,7 @@ _SIGS = {
     "sfeec_lslab_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "sfeec_lslab_last_launches": (C.c_int64, [_P]),
     "sfeec_lslab_step_bytes": (C.c_double, [_P]),
+    "sfeec_lslab_kernel_timing": (C.c_int, [_P, C.c_int, _PD, _PI64, _PD]),
     "sfeec_part_create_tet": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double,
                                         C.c_double, C.c_int, C.c_int, _P, C.c_int,
                                         C.POINTER(_P), _PI64]),

@@ -382,10 +382,43 @@ struct LatSlab {
   double dt = 0, eps0 = 1, mu0 = 1, time = 0, cfl_cache = -1;
   int kind = SFEEC_SPLIT_STRANG;
   int64_t launches = 0;
+  // per-kernel timing with CUDA events on the stream (classes: 0 K-Q, 1 K-Cb,
+  // 2 K-CTe, 3 K-M2); the exchanges fall between the events
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, size_t>> ev_used;
+  double class_ms[4] = {0, 0, 0, 0};
+  int64_t class_n[4] = {0, 0, 0, 0};
 
   ~LatSlab() {
     comm.reset();
+    for (auto e : ev_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+  }
+  void tic(int cls) {
+    if (!timing) return;
+    const size_t i = ev_used.size() * 2;
+    while (ev_pool.size() < i + 2) {
+      cudaEvent_t e;
+      SFEEC_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    ev_used.push_back({cls, i});
+    SFEEC_CUDA(cudaEventRecord(ev_pool[i], stream));
+  }
+  void toc() {
+    if (timing) SFEEC_CUDA(cudaEventRecord(ev_pool[ev_used.back().second + 1], stream));
+  }
+  void collect() {
+    if (ev_used.empty()) return;
+    SFEEC_CUDA(cudaStreamSynchronize(stream));
+    for (auto [cls, i] : ev_used) {
+      float ms = 0;
+      SFEEC_CUDA(cudaEventElapsedTime(&ms, ev_pool[i], ev_pool[i + 1]));
+      class_ms[cls] += ms;
+      class_n[cls] += 1;
+    }
+    ev_used.clear();
   }
   double c2() const { return 1.0 / (eps0 * mu0); }
   int o0() const { return P0 - K0; }
@@ -396,16 +429,24 @@ struct LatSlab {
   }
   // the four kernels + their ghost exchanges (see the file comment)
   void he(double h) {
+    tic(0);
     L.apply_q(stream);
+    toc();
     xch(L.T.p, 7, false, true);
+    tic(1);
     L.apply_cb(h, stream);
+    toc();
     xch(L.B.p, 12, true, true);
     launches += 2;
   }
   void ha(double h) {
+    tic(3);
     L.apply_m2(stream);
+    toc();
     xch(L.U.p, 12, true, false);
+    tic(2);
     L.apply_cte(h * c2(), stream);
+    toc();
     xch(L.E.p, 7, true, true);
     launches += 2;
   }
@@ -725,5 +766,31 @@ int64_t sfeec_lslab_last_launches(sfeec_lslab* h) { return h ? h->d.launches : -
 
 // bytes one step's four lattice kernels move on this rank (lattice.cu counts)
 double sfeec_lslab_step_bytes(sfeec_lslab* h) { return h ? h->d.L.step_bytes() : 0.0; }
+
+// device time per kernel class since the last call (0 K-Q, 1 K-Cb, 2 K-CTe,
+// 3 K-M2, as sfeec_dev_kernel_timing), launches and bytes per launch; then
+// (dis)arms the timing
+int sfeec_lslab_kernel_timing(sfeec_lslab* h, int enable, double* ms, int64_t* launches,
+                              double* bytes) {
+  return guarded([&] {
+    require(h, "null handle");
+    auto& d = h->d;
+    SFEEC_CUDA(cudaSetDevice(d.device));
+    d.collect();
+    for (int k = 0; k < 4; ++k) {
+      if (ms) ms[k] = d.class_ms[k];
+      if (launches) launches[k] = d.class_n[k];
+      d.class_ms[k] = 0;
+      d.class_n[k] = 0;
+    }
+    if (bytes) {
+      bytes[0] = d.L.bytes_q();
+      bytes[1] = d.L.bytes_cb();
+      bytes[2] = d.L.bytes_cte();
+      bytes[3] = d.L.bytes_m2();
+    }
+    d.timing = enable != 0;
+  });
+}
 
 }  // extern "C"

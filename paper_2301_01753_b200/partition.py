@@ -347,3 +347,12 @@ class LatticeSlab:
 
     def step_bytes(self) -> float:
         return float(L.lib().sfeec_lslab_step_bytes(self._h))
+
+    KERNEL_CLASSES = ("K-Q", "K-Cb", "K-CTe", "K-M2")
+
+    def kernel_timing(self, enable: bool = True) -> dict:
+        ms, n, by = np.zeros(4), np.zeros(4, np.int64), np.zeros(4)
+        L.check(L.lib().sfeec_lslab_kernel_timing(self._h, 1 if enable else 0, L.dptr(ms),
+                                                  L.i64ptr(n), L.dptr(by)))
+        return {k: {"ms": ms[i], "launches": int(n[i]), "bytes_per_launch": by[i]}
+                for i, k in enumerate(self.KERNEL_CLASSES)}
