@@ -259,6 +259,9 @@ class TetRunner:
         from paper_2301_01753_b200 import _lib as L
         self.S, self.L = S, L
         (self.n1, self.n2), self.s, self.b0, self.e0, self.setup_s = tet_setup(cfg, device)
+        if cfg["kind"] == "p2":  # second order: the sliced / ELL layouts
+            self.layout = "sell"
+            self.kernel_label = "SpMV chain K-M2, K-CTe, K-Q, K-Cb in sliced layouts (spmv_kernels.cu)"
         self.ndof = self.n1 + self.n2
         self.dt = self.s.dt()
 
@@ -313,7 +316,9 @@ class TetRunner:
                                             ctypes.byref(t)))
         return time.perf_counter() - t0
 
-    kernel_label = "SpMV chain K-M2, K-CTe, K-Q, K-Cb in sliced layouts (spmv_kernels.cu)"
+    kernel_label = ("Kuhn-lattice K-M2, K-CTe, K-Q, K-Cb: per-vertex stencils with per-vertex "
+                    "coefficient arrays, symmetric pairs stored once, no index streams (lattice.cu)")
+    layout = "lattice"
 
 
 class TetSlabRunner:
@@ -323,6 +328,7 @@ class TetSlabRunner:
     P1-, two-plane for config 4's S(M1^2) Q)."""
 
     scaling = "strong"
+    layout = "sell"
     kernel_label = ("SpMV chain K-M2, K-CTe, K-Q, K-Cb over the owned rows + NCCL halo-plane "
                     "exchange before each (partition.cu)")
 
@@ -418,6 +424,7 @@ class LatSlabRunner:
 
     kernel_label = ("lattice K-M2, K-CTe, K-Q, K-Cb on the owned vertex planes + NCCL "
                     "one-plane ghost exchanges between them (lattice_slab.cu)")
+    layout = "lattice"
 
     def __init__(self, cfg, device, rank, world, dist, strong=False):
         import paper_2301_01753_b200 as S
@@ -569,7 +576,7 @@ def run_ours(args, rank, world, local_rank):
     # under profiles/) over the CUDA-event launch time; the algorithmic count
     # (SURVEY.md 8(d) bytes per launch) over the same time beside it
     alg_achieved = kbytes / (k_avg_ms * 1e-3) / 1e9
-    traffic = committed_traffic(args.config)
+    traffic = committed_traffic(args.config, getattr(R, "layout", None))
     achieved = traffic / (k_avg_ms * 1e-3) / 1e9 if traffic else alg_achieved
     ndof = R.ndof
     value = units * args.steps / (ms * 1e-3)
@@ -643,12 +650,14 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def committed_traffic(config):
-    """ncu dram bytes per launch of the dominant kernel, from profiles/ (or None)."""
+def committed_traffic(config, layout=None):
+    """ncu dram bytes per launch of the dominant kernel, from profiles/ (or None);
+    keyed config/layout for the tet configs (lattice or sell)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(config)
+            d = json.load(f)
+        return d.get(f"{config}/{layout}" if layout else config)
     except Exception:
         return None
 
