@@ -81,6 +81,15 @@ struct Lattice {
   void apply_cb(double h, cudaStream_t s) const;    // B -= h C T
   void apply_m2(cudaStream_t s) const;              // U = M2 B
   void apply_cte(double f, cudaStream_t s) const;   // E += f C^T U
+  // the half-steps: He = K-Q then K-Cb, Ha = K-M2 then K-CTe, fused into one
+  // z-sweep kernel each when `fused` (t / u stay in shared memory; bitwise
+  // the same results)
+  bool fused = true;
+  void apply_he(double h, cudaStream_t s) const;   // B -= h C (Q E)
+  void apply_ha(double f, cudaStream_t s) const;   // E += f C^T (M2 B)
+  void fused_grid(int& ntx, int& nty, int& units) const;
+  double bytes_he() const;
+  double bytes_ha() const;
   int kbeg() const { return k0; }
   int kend() const { return k1 < 0 ? g.nz + 1 : k1; }
   // bytes each kernel moves (arrays read once, outputs written once)
