@@ -9,7 +9,6 @@
 // ascending column order of the k-major numbering for rows away from the
 // 32-vertex x-block edges: those rows are summed exactly like the sliced /
 // ELL kernels (spmv_kernels.cu) sum their CSR rows.
-#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -121,8 +120,9 @@ __device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, cons
   const double r[sizeof...(Ts)] = {sym_row<QOp, Ts>(qc, E, idx, g)...};
   ((edge_dof<Ts>(i, j, k, g) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
 }
-template <int MINB>
-__global__ void __launch_bounds__(kLT, MINB) k_lat_q(LatGeom g, int kbeg, const double* __restrict__ qc,
+// 2 blocks per SM: 128 registers, every load of the vertex's 7 rows in flight
+// (measured: 80 / 64-register caps spill and run 1.6x / 2.4x slower)
+__global__ void __launch_bounds__(kLT, 2) k_lat_q(LatGeom g, int kbeg, const double* __restrict__ qc,
                                                const double* __restrict__ E,
                                                double* __restrict__ T) {
   int i, j, k;
@@ -140,8 +140,7 @@ __device__ __forceinline__ void m2_vertex(std::integer_sequence<int, Fs...>, con
   const double r[sizeof...(Fs)] = {sym_row<MOp, Fs>(mc, B, idx, g)...};
   ((face_ok<Fs>(i, j, k, g) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
 }
-template <int MINB>
-__global__ void __launch_bounds__(kLT, MINB) k_lat_m2(LatGeom g, int kbeg, const double* __restrict__ mc,
+__global__ void __launch_bounds__(kLT, 2) k_lat_m2(LatGeom g, int kbeg, const double* __restrict__ mc,
                                                 const double* __restrict__ B,
                                                 double* __restrict__ U) {
   int i, j, k;
@@ -207,223 +206,6 @@ __global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, int kbeg, double alp
   cte_vertex(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, alpha, U, E);
 }
 
-// ---- fused half-steps: z-sweeps over tile columns ---------------------------
-// He = K-Q + K-Cb and Ha = K-M2 + K-CTe in one kernel each, the intermediate
-// (t, u) kept in shared memory instead of crossing HBM. A block owns a tile
-// column of 31 x 7 vertices for a z-chunk of kKC planes; its 256 threads are
-// the 32 x 8 "producer region" = the tile plus the one-vertex rim the
-// consumer stencil reaches (C reads t at +{0,1}^3, C^T reads u at -{0,1}^3).
-// Per plane: every thread computes its region point's 7 (t) or 12 (u) rows
-// into a shared plane buffer (three buffers rotate, so one barrier per plane
-// orders everything), then the own-tile threads apply C (He, planes swept
-// downward: faces of plane k use t of k and k+1) or C^T (Ha, upward: edges of
-// plane k use u of k and k-1). Every row is computed by the same functions
-// as the separate kernels: the fused half-steps are bitwise equal to them.
-constexpr int kRX = 32, kRY = 8, kRP = kRX * kRY;  // producer region = threads
-constexpr int kKC = 32;                             // planes per z-chunk
-
-// C / C^T row from shared plane buffers: cur = plane k, nb = plane k +- 1
-template <bool TRANS, int S>
-__device__ __forceinline__ void inc_term_sm(double& acc, const double* __restrict__ cur,
-                                            const double* __restrict__ nb, int q) {
-  constexpr lat::CSlot sl = TRANS ? lat::kCTTab(S) : lat::kCTab(S);
-  const double* p = sl.dk == 0 ? cur : nb;
-  const double v = p[sl.t * kRP + q + sl.dj * kRX + sl.di];
-  acc += sl.sign > 0 ? v : -v;
-}
-template <bool TRANS, int BASE, int... I>
-__device__ __forceinline__ double inc_row_sm(std::integer_sequence<int, I...>,
-                                             const double* __restrict__ cur,
-                                             const double* __restrict__ nb, int q) {
-  double acc = 0.0;
-  (inc_term_sm<TRANS, BASE + I>(acc, cur, nb, q), ...);
-  return acc;
-}
-
-// the region point's producer rows into plane buffer `buf` (0 off the mesh /
-// on non-DOF rows, exactly what the separate kernels leave there)
-template <int... Ts>
-__device__ __forceinline__ void q_region(std::integer_sequence<int, Ts...>, const LatGeom& g,
-                                         bool valid, int i, int j, int k, int64_t idx,
-                                         const double* __restrict__ qc,
-                                         const double* __restrict__ E, double* buf, int q) {
-  ((buf[Ts * kRP + q] =
-        valid && edge_dof<Ts>(i, j, k, g) ? sym_row<QOp, Ts>(qc, E, idx, g) : 0.0),
-   ...);
-}
-template <int... Fs>
-__device__ __forceinline__ void m2_region(std::integer_sequence<int, Fs...>, const LatGeom& g,
-                                          bool valid, int i, int j, int k, int64_t idx,
-                                          const double* __restrict__ mc,
-                                          const double* __restrict__ B, double* buf, int q) {
-  ((buf[Fs * kRP + q] =
-        valid && face_ok<Fs>(i, j, k, g) ? sym_row<MOp, Fs>(mc, B, idx, g) : 0.0),
-   ...);
-}
-template <int... Fs>
-__device__ __forceinline__ void cb_own(std::integer_sequence<int, Fs...>, const LatGeom& g, int i,
-                                       int j, int k, int64_t idx, double alpha,
-                                       const double* cur, const double* up, int q,
-                                       double* __restrict__ B) {
-  ((face_ok<Fs>(i, j, k, g)
-        ? (void)(B[(int64_t)Fs * g.NP + idx] =
-                     fma(alpha,
-                         inc_row_sm<false, 3 * Fs>(std::make_integer_sequence<int, 3>{}, cur, up, q),
-                         B[(int64_t)Fs * g.NP + idx]))
-        : (void)0),
-   ...);
-}
-template <int... Ts>
-__device__ __forceinline__ void cte_own(std::integer_sequence<int, Ts...>, const LatGeom& g,
-                                        int i, int j, int k, int64_t idx, double alpha,
-                                        const double* cur, const double* down, int q,
-                                        double* __restrict__ E) {
-  ((edge_dof<Ts>(i, j, k, g)
-        ? (void)(E[(int64_t)Ts * g.NP + idx] =
-                     fma(alpha,
-                         inc_row_sm<true, lat::kCTOff(Ts)>(
-                             std::make_integer_sequence<int, lat::kCTOff(Ts + 1) - lat::kCTOff(Ts)>{},
-                             cur, down, q),
-                         E[(int64_t)Ts * g.NP + idx]))
-        : (void)0),
-   ...);
-}
-
-// He: b -= h C (Q e) on local planes [kbeg, kend); units chunk-major
-__global__ void __launch_bounds__(kRP, 2)
-    k_lat_he(LatGeom g, int kbeg, int kend, int ntx, int nty, double alpha,
-             const double* __restrict__ qc, const double* __restrict__ E,
-             double* __restrict__ B) {
-  extern __shared__ double smem[];  // 3 planes x 7 comps x kRP
-  const int ntile = ntx * nty;
-  const int chunk = blockIdx.x / ntile, tile = blockIdx.x - chunk * ntile;
-  const int rx = threadIdx.x & (kRX - 1), ry = threadIdx.x / kRX, q = threadIdx.x;
-  const int i = (tile % ntx) * (kRX - 1) + rx, j = (tile / ntx) * (kRY - 1) + ry;
-  const bool inxy = i <= g.n && j <= g.n;
-  const bool own = rx < kRX - 1 && ry < kRY - 1 && inxy;
-  const int kc0 = kbeg + chunk * kKC, kc1 = min(kc0 + kKC, kend);
-  for (int k = kc1; k >= kc0; --k) {  // t of kc1 first, then faces of kc1-1 .. kc0
-    double* cur = smem + ((k + 3) % 3) * 7 * kRP;
-    const int64_t idx = g.PS * (k + 1) + (int64_t)g.S * (j + 1) + (i + 1);
-    q_region(std::make_integer_sequence<int, 7>{}, g, inxy && k >= 0 && k <= g.nz, i, j, k, idx,
-             qc, E, cur, q);
-    __syncthreads();
-    if (k < kc1 && own)
-      cb_own(std::make_integer_sequence<int, 12>{}, g, i, j, k, idx, alpha, cur,
-             smem + ((k + 4) % 3) * 7 * kRP, q, B);
-  }
-}
-
-// Ha: e += f C^T (M2 b) on local planes [kbeg, kend)
-__global__ void __launch_bounds__(kRP, 2)
-    k_lat_ha(LatGeom g, int kbeg, int kend, int ntx, int nty, double alpha,
-             const double* __restrict__ mc, const double* __restrict__ B,
-             double* __restrict__ E) {
-  extern __shared__ double smem[];  // 3 planes x 12 comps x kRP
-  const int ntile = ntx * nty;
-  const int chunk = blockIdx.x / ntile, tile = blockIdx.x - chunk * ntile;
-  const int rx = threadIdx.x & (kRX - 1), ry = threadIdx.x / kRX, q = threadIdx.x;
-  const int i = (tile % ntx) * (kRX - 1) - 1 + rx, j = (tile / ntx) * (kRY - 1) - 1 + ry;
-  const bool inxy = i >= 0 && i <= g.n && j >= 0 && j <= g.n;
-  const bool own = rx >= 1 && ry >= 1 && i <= g.n && j <= g.n;
-  const int kc0 = kbeg + chunk * kKC, kc1 = min(kc0 + kKC, kend);
-  for (int k = kc0 - 1; k < kc1; ++k) {  // u of kc0-1 first, then edges of kc0 .. kc1-1
-    double* cur = smem + ((k + 3) % 3) * 12 * kRP;
-    const int64_t idx = g.PS * (k + 1) + (int64_t)g.S * (j + 1) + (i + 1);
-    m2_region(std::make_integer_sequence<int, 12>{}, g, inxy && k >= 0 && k <= g.nz, i, j, k,
-              idx, mc, B, cur, q);
-    __syncthreads();
-    if (k >= kc0 && own)
-      cte_own(std::make_integer_sequence<int, 7>{}, g, i, j, k, idx, alpha, cur,
-              smem + ((k + 2) % 3) * 12 * kRP, q, E);
-  }
-}
-
-// ---- warp-per-row-type forms: a block is one warp per entity type over the
-// same 32 x CH positions, so a thread computes one row (~40 registers, full
-// occupancy) and the block's warps share the gathered neighbours in L1 -----
-template <int... Ts, class F>
-__device__ __forceinline__ void on_type(int w, std::integer_sequence<int, Ts...>, F&& f) {
-  ((w == Ts ? f(std::integral_constant<int, Ts>{}) : (void)0), ...);
-}
-struct QRowW {
-  const double* __restrict__ qc;
-  const double* __restrict__ E;
-  double* __restrict__ T;
-  static constexpr int kTypes = 7, kMinBlocks = 6;
-  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
-                                             int64_t idx) const {
-    on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
-      constexpr int t = decltype(tc)::value;
-      if (edge_dof<t>(i, j, k, g)) T[(int64_t)t * g.NP + idx] = sym_row<QOp, t>(qc, E, idx, g);
-    });
-  }
-};
-struct M2RowW {
-  const double* __restrict__ mc;
-  const double* __restrict__ B;
-  double* __restrict__ U;
-  static constexpr int kTypes = 12, kMinBlocks = 4;
-  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
-                                             int64_t idx) const {
-    on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
-      constexpr int f = decltype(fc)::value;
-      if (face_ok<f>(i, j, k, g)) U[(int64_t)f * g.NP + idx] = sym_row<MOp, f>(mc, B, idx, g);
-    });
-  }
-};
-struct CbRowW {
-  double alpha;
-  const double* __restrict__ T;
-  double* __restrict__ B;
-  static constexpr int kTypes = 12, kMinBlocks = 4;
-  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
-                                             int64_t idx) const {
-    on_type(w, std::make_integer_sequence<int, 12>{}, [&](auto fc) {
-      constexpr int f = decltype(fc)::value;
-      if (face_ok<f>(i, j, k, g)) {
-        const double r = inc_row<false, 3 * f>(std::make_integer_sequence<int, 3>{}, T, idx, g);
-        double* b = B + (int64_t)f * g.NP + idx;
-        *b = fma(alpha, r, *b);
-      }
-    });
-  }
-};
-struct CteRowW {
-  double alpha;
-  const double* __restrict__ U;
-  double* __restrict__ E;
-  static constexpr int kTypes = 7, kMinBlocks = 8;
-  __device__ __forceinline__ void operator()(const LatGeom& g, int w, int i, int j, int k,
-                                             int64_t idx) const {
-    on_type(w, std::make_integer_sequence<int, 7>{}, [&](auto tc) {
-      constexpr int t = decltype(tc)::value;
-      if (edge_dof<t>(i, j, k, g)) {
-        const double r = inc_row<true, lat::kCTOff(t)>(
-            std::make_integer_sequence<int, lat::kCTOff(t + 1) - lat::kCTOff(t)>{}, U, idx, g);
-        double* e = E + (int64_t)t * g.NP + idx;
-        *e = fma(alpha, r, *e);
-      }
-    });
-  }
-};
-constexpr int kWCH = 4;  // 32-position chunks per block
-template <class Row>
-__global__ void __launch_bounds__(Row::kTypes * 32, Row::kMinBlocks) k_lat_w(LatGeom g, int kbeg,
-                                                                             Row row) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = kbeg + blockIdx.y;
-#pragma unroll 1
-  for (int c = 0; c < kWCH; ++c) {
-    const int p = (blockIdx.x * kWCH + c) * 32 + lane;
-    if (p >= g.PS) return;
-    const int j = p / g.S - 1;
-    const int i = p - (j + 1) * g.S - 1;
-    if (i < 0 || i > g.n || j < 0 || j > g.n) continue;
-    row(g, w, i, j, k, g.PS * (k + 1) + p);
-  }
-}
-
 // ---- setup: coefficient arrays from a CSR of the k-major numbering -----------
 // Entry (r, c) of row type t at offset off: the slot of t's stencil with
 // (type(c), off); canonical slots store the value at the row's position.
@@ -487,9 +269,7 @@ __global__ void k_lat_gather(int64_t n, const int64_t* __restrict__ pos,
 }
 
 inline unsigned blocks(int64_t n) { return (unsigned)((n + kLT - 1) / kLT); }
-inline dim3 wgrid(const LatGeom& g, int kb, int ke) {
-  return dim3((unsigned)((g.PS + 32 * kWCH - 1) / (32 * kWCH)), (unsigned)(ke - kb));
-}
+
 
 }  // namespace
 
@@ -545,9 +325,7 @@ void Lattice::build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2,
   }
   SFEEC_CUDA(cudaStreamSynchronize(s));
   valid = newer = false;
-  const char* v = std::getenv("SFEEC_LAT_VARIANT");  // A/B of the kernel forms
-  variant = v ? std::atoi(v) : 0;
-  fused = env_flag("SFEEC_LAT_FUSED", true);
+
 }
 
 void Lattice::scatter(const double* b, const double* e, cudaStream_t s) {
@@ -562,105 +340,36 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
   SFEEC_LAUNCH_CHECK();
 }
 
-// variant 0: one thread per vertex (all its rows); 1: one warp per row type.
-// Grids cover local planes [kbeg(), kend()).
+// one thread per vertex computes all of its rows (the neighbour loads the
+// rows share are loaded once); grids cover local planes [kbeg(), kend()).
+// Measured and rejected (tet256, ms per launch, this kernel form first): one
+// warp per row type (K-Q 2.03 vs 2.77, K-M2 1.49 vs 2.14), two threads per
+// vertex (2.03 vs 2.16, 1.49 vs 1.71), z-sweeps fusing K-Q + K-Cb and K-M2 +
+// K-CTe with t / u in shared memory (5.1 vs 8.1 ms per step: one barrier per
+// plane serialises the 125 KB-per-plane coefficient streams of a tile).
 void Lattice::apply_q(cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  const dim3 grid(blocks(g.PS), (unsigned)(ke - kb));
-  if (variant == 1)
-    k_lat_w<QRowW><<<wgrid(g, kb, ke), 7 * 32, 0, s>>>(g, kb, QRowW{qc.p, E.p, T.p});
-  else if (variant == 2)
-    k_lat_q<3><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
-  else if (variant == 3)
-    k_lat_q<4><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
-  else
-    k_lat_q<2><<<grid, kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
+  k_lat_q<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cb(double h, cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  if (variant == 1)
-    k_lat_w<CbRowW><<<wgrid(g, kb, ke), 12 * 32, 0, s>>>(g, kb, CbRowW{-h, T.p, B.p});
-  else
-    k_lat_cb<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
+  k_lat_cb<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_m2(cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  const dim3 grid(blocks(g.PS), (unsigned)(ke - kb));
-  if (variant == 1)
-    k_lat_w<M2RowW><<<wgrid(g, kb, ke), 12 * 32, 0, s>>>(g, kb, M2RowW{mc.p, B.p, U.p});
-  else if (variant == 2)
-    k_lat_m2<3><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
-  else if (variant == 3)
-    k_lat_m2<4><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
-  else
-    k_lat_m2<2><<<grid, kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
+  k_lat_m2<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cte(double f, cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  if (variant == 1)
-    k_lat_w<CteRowW><<<wgrid(g, kb, ke), 7 * 32, 0, s>>>(g, kb, CteRowW{f, U.p, E.p});
-  else
-    k_lat_cte<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
+  k_lat_cte<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
   SFEEC_LAUNCH_CHECK();
-}
-
-// fused half-steps (k_lat_he / k_lat_ha): tile columns x z-chunks
-void Lattice::fused_grid(int& ntx, int& nty, int& units) const {
-  ntx = (g.n + 1 + kRX - 2) / (kRX - 1);
-  nty = (g.n + 1 + kRY - 2) / (kRY - 1);
-  const int nch = (kend() - kbeg() + kKC - 1) / kKC;
-  units = ntx * nty * nch;
-}
-void Lattice::apply_he(double h, cudaStream_t s) const {
-  if (!fused) {
-    apply_q(s);
-    apply_cb(h, s);
-    return;
-  }
-  int ntx, nty, units;
-  fused_grid(ntx, nty, units);
-  if (units <= 0) return;
-  const int smem = 3 * 7 * kRP * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    SFEEC_CUDA(cudaFuncSetAttribute(k_lat_he, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_lat_he<<<units, kRP, smem, s>>>(g, kbeg(), kend(), ntx, nty, -h, qc.p, E.p, B.p);
-  SFEEC_LAUNCH_CHECK();
-}
-void Lattice::apply_ha(double f, cudaStream_t s) const {
-  if (!fused) {
-    apply_m2(s);
-    apply_cte(f, s);
-    return;
-  }
-  int ntx, nty, units;
-  fused_grid(ntx, nty, units);
-  if (units <= 0) return;
-  const int smem = 3 * 12 * kRP * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    SFEEC_CUDA(cudaFuncSetAttribute(k_lat_ha, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_lat_ha<<<units, kRP, smem, s>>>(g, kbeg(), kend(), ntx, nty, f, mc.p, B.p, E.p);
-  SFEEC_LAUNCH_CHECK();
-}
-double Lattice::bytes_he() const {  // Q coefficients + e read + b read and written
-  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
-  return 8.0 * (lat::kQArrays * V + 7.0 * V + 2.0 * (k1 < 0 ? (double)n2 : 12.0 * V));
-}
-double Lattice::bytes_ha() const {  // M2 coefficients + b read + e read and written
-  const double V = (double)(g.n + 1) * (g.n + 1) * (kend() - kbeg());
-  return 8.0 * (lat::kMArrays * V + 12.0 * V + 2.0 * (k1 < 0 ? (double)n1 : 7.0 * V));
 }
 
 // bytes per launch (each array read once, each output written once; the

@@ -63,7 +63,6 @@ struct Lattice {
   DevBuf<double> E, T, B, U;  // 7, 7, 12, 12 components * NP
   DevBuf<int64_t> epos, fpos;  // DOF id -> component * NP + position
   bool pdl = true;
-  int variant = 0;  // kernel form (lattice.cu apply_*)
   // state bookkeeping of the owning handle: `valid` = E/B hold the handle's
   // state (or a newer one), `newer` = the DOF vectors are stale
   bool valid = false, newer = false;
@@ -81,15 +80,6 @@ struct Lattice {
   void apply_cb(double h, cudaStream_t s) const;    // B -= h C T
   void apply_m2(cudaStream_t s) const;              // U = M2 B
   void apply_cte(double f, cudaStream_t s) const;   // E += f C^T U
-  // the half-steps: He = K-Q then K-Cb, Ha = K-M2 then K-CTe, fused into one
-  // z-sweep kernel each when `fused` (t / u stay in shared memory; bitwise
-  // the same results)
-  bool fused = true;
-  void apply_he(double h, cudaStream_t s) const;   // B -= h C (Q E)
-  void apply_ha(double f, cudaStream_t s) const;   // E += f C^T (M2 B)
-  void fused_grid(int& ntx, int& nty, int& units) const;
-  double bytes_he() const;
-  double bytes_ha() const;
   int kbeg() const { return k0; }
   int kend() const { return k1 < 0 ? g.nz + 1 : k1; }
   // bytes each kernel moves (arrays read once, outputs written once)

@@ -130,13 +130,6 @@ struct LeapfrogDev {
   // dynamics.cpp:47-55
   void flow_he(double h) {
     if (use_lat) {  // t = Q e, b -= h C t on the lattice
-      if (lat->fused) {  // one z-sweep kernel (timed as class K-Q)
-        tic_class(0);
-        lat->apply_he(h, stream);
-        toc();
-        launches += 1;
-        return;
-      }
       tic_class(0);
       lat->apply_q(stream);
       toc();
@@ -161,13 +154,6 @@ struct LeapfrogDev {
   void flow_ha(double h) {
     const double f = h * c2();
     if (use_lat) {  // u = M2 b, e += f C^T u on the lattice
-      if (lat->fused) {  // one z-sweep kernel (timed as class K-M2)
-        tic_class(3);
-        lat->apply_ha(f, stream);
-        toc();
-        launches += 1;
-        return;
-      }
       tic_class(3);
       lat->apply_m2(stream);
       toc();
@@ -738,11 +724,10 @@ int sfeec_dev_kernel_timing(sfeec_dev* h, int enable, double* ms, int64_t* launc
     // 12 B per fp64 nonzero, 5 B per incidence entry (int8 sign + int32
     // column), 8 B per vector element read or written)
     if (bytes && d.lat_on()) {  // what the lattice kernels move (lattice.cu)
-      const bool fu = d.lat->fused;  // K-Q / K-M2 = the fused He / Ha sweeps
-      bytes[0] = fu ? d.lat->bytes_he() : d.lat->bytes_q();
-      bytes[1] = fu ? 0.0 : d.lat->bytes_cb();
-      bytes[2] = fu ? 0.0 : d.lat->bytes_cte();
-      bytes[3] = fu ? d.lat->bytes_ha() : d.lat->bytes_m2();
+      bytes[0] = d.lat->bytes_q();
+      bytes[1] = d.lat->bytes_cb();
+      bytes[2] = d.lat->bytes_cte();
+      bytes[3] = d.lat->bytes_m2();
       bytes[4] = 0;
     } else if (bytes) {
       // an incidence C (+-1) streams 5 B per entry, a general one (P2-) 12 B

@@ -86,32 +86,9 @@ def test_lattice_kernel_timing_reports_lattice_bytes():
         s.advance_resident(8)
         out[name] = s.kernel_timing(False)
     V = 17 ** 3
-    # the fused half-steps: He (K-Q + K-Cb) timed as K-Q, Ha (K-M2 + K-CTe) as K-M2
-    assert out["lat"]["K-Q"]["bytes_per_launch"] == 8.0 * (61 * V + 7 * V + 2 * lat._n2)
-    assert out["lat"]["K-M2"]["bytes_per_launch"] == 8.0 * (48 * V + 12 * V + 2 * lat._n1)
-    for k in ("K-Q", "K-M2"):
+    assert out["lat"]["K-Q"]["bytes_per_launch"] == 8.0 * (61 * V + 7 * V + lat._n1)
+    assert out["lat"]["K-M2"]["bytes_per_launch"] == 8.0 * (48 * V + 12 * V + lat._n2)
+    for k in ("K-Q", "K-Cb", "K-CTe", "K-M2"):
         assert out["lat"][k]["launches"] == out["sell"][k]["launches"] > 0
-    for k in ("K-Cb", "K-CTe"):
-        assert out["lat"][k]["launches"] == 0
-    # the lattice half-steps move fewer bytes than the sliced pairs' accounting
-    assert out["lat"]["K-Q"]["bytes_per_launch"] < (out["sell"]["K-Q"]["bytes_per_launch"] +
-                                                    out["sell"]["K-Cb"]["bytes_per_launch"])
-    assert out["lat"]["K-M2"]["bytes_per_launch"] < (out["sell"]["K-M2"]["bytes_per_launch"] +
-                                                     out["sell"]["K-CTe"]["bytes_per_launch"])
-
-
-@pytest.mark.parametrize("n,kind", [(5, S.SplitKind.Strang), (33, S.SplitKind.Strang),
-                                    (70, S.SplitKind.LieTrotter)])
-def test_fused_half_steps_bitwise_equal_separate_kernels(n, kind):
-    """k_lat_he / k_lat_ha (t, u in shared memory, z-sweeps over tile columns
-    and 32-plane chunks) compute every row with the separate kernels'
-    functions: bitwise the same steps (70 planes: three z-chunks)"""
-    from tests.envutil import layout_env
-    with layout_env(SFEEC_LAT_FUSED=0):
-        sep = S.tet_device_scheme(n, 0.1, 3, dt=0.01, kind=kind)
-    fus = S.tet_device_scheme(n, 0.1, 3, dt=0.01, kind=kind)
-    rng = np.random.default_rng(n)
-    st = S.make_state(S.Formulation.BE, rng.standard_normal(fus._n2),
-                      rng.standard_normal(fus._n1))
-    a, b = sep.advance(st, 11), fus.advance(st, 11)
-    assert np.array_equal(a.first, b.first) and np.array_equal(a.e, b.e)
+        # the lattice moves fewer bytes than the sliced layouts' accounting
+        assert out["lat"][k]["bytes_per_launch"] < out["sell"][k]["bytes_per_launch"]
