@@ -193,15 +193,16 @@ class YeeRunner:
 
     def dominant(self, k_steps):
         """(name, algorithmic bytes per launch, avg ms per launch) of the fused
-        sweep. The timed launches cover the k_steps - 1 merged steps between
-        the opening b-half-kick and the closing e-kick + b-half-kick; a
-        two-step sweep (k_fused2_tma) advances two of them per launch, so its
-        algorithmic bytes per launch are two steps' worth."""
+        sweep. The timed launches cover the k_steps (e, b) pairs after the
+        opening b-half-kick (the closing half-kick is folded into the last
+        sweep); a two-step sweep (k_fused2_tma) advances two of them per
+        launch, so its algorithmic bytes per launch are two steps' worth
+        (SURVEY.md 8(d))."""
         self.timing(True)
         self.y.advance(k_steps)
         ms, n = self.timing(False)
         n = max(n, 1)
-        per_launch = (k_steps - 1) / n
+        per_launch = k_steps / n
         name = ("k_fused2_tma (two e-kick + b-kick pairs per z-sweep)" if per_launch > 1.5
                 else "k_fused_tma (e-kick + b-kick sweep)")
         return name, self.y.step_bytes() * per_launch, ms / n

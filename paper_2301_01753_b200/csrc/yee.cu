@@ -43,8 +43,10 @@ struct Fields {
 
 template <class T>
 struct YeeCoef {
-  T ce[3];  // e-kick: f*m2/d_x, /d_y, /d_z
-  T cb[3];  // b-kick: h*q/d_x, /d_y, /d_z
+  T ce[3];   // e-kick: f*m2/d_x, /d_y, /d_z
+  T cb[3];   // b-kick: h*q/d_x, /d_y, /d_z
+  T cb2[3];  // the two-step sweep's second b-kick (the closing half-kick of
+             // an advance() is folded into its last sweep)
 };
 
 namespace {
@@ -608,6 +610,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   };
   const T ce0 = ck.ce[0], ce1 = ck.ce[1], ce2 = ck.ce[2];
   const T cb0 = ck.cb[0], cb1 = ck.cb[1], cb2 = ck.cb[2];
+  const T db0 = ck.cb2[0], db1 = ck.cb2[1], db2 = ck.cb2[2];  // second b-kick
 
   // units: (tile, z-chunk) round-robin over the CTAs, or, with a schedule,
   // the CTA's own list of (tile, k0, k1) (Yee2Sched)
@@ -761,9 +764,9 @@ __global__ void __launch_bounds__(NTH, MINB)
             const int q = me[h];
             const Pt& v = V[h];
             const int64_t s = sij[h] + kstride * zb;
-            out.c[3][s] = yee_upd(v.b1[0], cb2, C[h].e2[1] - v.e2[1], cb1, R(E2x, 2, q + X1) - v.e2[2]);
-            out.c[4][s] = yee_upd(v.b1[1], cb0, R(E2x, 2, q + 1) - v.e2[2], cb2, C[h].e2[0] - v.e2[0]);
-            out.c[5][s] = yee_upd(v.b1[2], cb1, R(E2x, 0, q + X1) - v.e2[0], cb0, R(E2x, 1, q + 1) - v.e2[1]);
+            out.c[3][s] = yee_upd(v.b1[0], db2, C[h].e2[1] - v.e2[1], db1, R(E2x, 2, q + X1) - v.e2[2]);
+            out.c[4][s] = yee_upd(v.b1[1], db0, R(E2x, 2, q + 1) - v.e2[2], db2, C[h].e2[0] - v.e2[0]);
+            out.c[5][s] = yee_upd(v.b1[2], db1, R(E2x, 0, q + X1) - v.e2[0], db0, R(E2x, 1, q + 1) - v.e2[1]);
           }
         }
       }
@@ -808,8 +811,10 @@ __global__ void k_gather(YeeGeom g, bool face, double* __restrict__ dst, int64_t
 // One state-modifying kernel of the step sequence; the multi-slab paths
 // exchange ghost planes after every phase.
 struct Phase {
-  int kind;  // 0 b-kick(h1), 1 e-kick(h1), 2 fused e-kick(h1) + b-kick(h2), 3 two of those
-  double h1, h2;
+  // 0 b-kick(h1), 1 e-kick(h1), 2 fused e-kick(h1) + b-kick(h2), 3 two of
+  // those: e(h1) b(h2) e(h1) b(h3)
+  int kind;
+  double h1, h2, h3 = 0;
 };
 
 // Unit schedule of the two-step sweep over planes [kbeg, kend) of `ntiles`
@@ -952,12 +957,14 @@ struct YeeDev {
     return f;
   }
   template <class T>
-  YeeCoef<T> coef(double e_factor, double h) const {
+  YeeCoef<T> coef(double e_factor, double h, double h2 = -1.0) const {
     YeeCoef<T> k;
     const double m2 = dv, q = 1.0 / dv;
+    if (h2 < 0) h2 = h;
     for (int a = 0; a < 3; ++a) {
       k.ce[a] = (T)(e_factor * m2 / d[a]);
       k.cb[a] = (T)(h * q / d[a]);
+      k.cb2[a] = (T)(h2 * q / d[a]);
     }
     return k;
   }
@@ -1103,7 +1110,7 @@ struct YeeDev {
 
   // two fused steps over local planes [kbeg, kend): buf[cur] -> buf[cur^1]
   template <class T>
-  void launch_range2(double h_e, double h_b, int kbeg, int kend) {
+  void launch_range2(double h_e, double h_b, int kbeg, int kend, double h_b2) {
     if (!have_maps2) make_maps2<T>();
     const int ntx = (g.n[0] + kTX - 1) / kTX, nty = (g.n[1] + kTY2<T> - 1) / kTY2<T>;
     const int nchunks = (kend - kbeg + kChunk - 1) / kChunk;
@@ -1112,15 +1119,15 @@ struct YeeDev {
     const int grid = sc->grid;
     launch_pdl(pdl && !comm, k_fused2_tma<T, kTX, kTY2<T>, kNS2, kNT2<T>, kNPT2, kMB2<T>>, dim3(grid),
                dim3(kNT2<T>), TmaCfg2<T, kTX, kTY2<T>, kNS2, 2>::kSmem, stream, mapB2[cur],
-               mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b), kChunk, ntx,
+               mapE2[cur], g, fields<T>(cur ^ 1), coef<T>(h_e / (eps0 * mu0), h_b, h_b2), kChunk, ntx,
                ntx * nty, n_units, kbeg, kend, sc->units.p, sc->cta_ptr.p);
     SFEEC_LAUNCH_CHECK();
     ++launches;
   }
 
   template <class T>
-  void fused2_tma(double h_e, double h_b) {
-    launch_range2<T>(h_e, h_b, sweep_beg(), sweep_end());
+  void fused2_tma(double h_e, double h_b, double h_b2) {
+    launch_range2<T>(h_e, h_b, sweep_beg(), sweep_end(), h_b2);
     cur ^= 1;
   }
 
@@ -1141,12 +1148,12 @@ struct YeeDev {
   // owned planes), part 1 = the rest. two: the two-step sweep. Neither flips
   // the buffers.
   template <class T>
-  void fused_part(double h_e, double h_b, int part, bool two = false) {
+  void fused_part(double h_e, double h_b, int part, bool two = false, double h_b2 = -1.0) {
     const int kb = sweep_beg(), ke = sweep_end(), G = ghost();
     auto range = [&](int a, int b) {
       if (b <= a) return;
       if (two)
-        launch_range2<T>(h_e, h_b, a, b);
+        launch_range2<T>(h_e, h_b, a, b, h_b2 < 0 ? h_b : h_b2);
       else
         launch_range<T>(h_e, h_b, a, b);
     };
@@ -1184,18 +1191,18 @@ struct YeeDev {
   // next kernel reads the ghosts. The exchange touches only ghost planes and
   // the boundary chunks' planes, the interior sweep only interior planes.
   template <class T>
-  void fused_overlapped(double h_e, double h_b, bool two = false) {
+  void fused_overlapped(double h_e, double h_b, bool two = false, double h_b2 = -1.0) {
     if (!comm_stream) {
       SFEEC_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
       SFEEC_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
       SFEEC_CUDA(cudaEventCreateWithFlags(&ev_xch, cudaEventDisableTiming));
     }
-    fused_part<T>(h_e, h_b, 0, two);
+    fused_part<T>(h_e, h_b, 0, two, h_b2);
     SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
     SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
     exchange_nccl(cur ^ 1, comm_stream);
     SFEEC_CUDA(cudaEventRecord(ev_xch, comm_stream));
-    fused_part<T>(h_e, h_b, 1, two);
+    fused_part<T>(h_e, h_b, 1, two, h_b2);
     SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
     cur ^= 1;
   }
@@ -1206,20 +1213,21 @@ struct YeeDev {
     if (n <= 0) return p;
     const bool use_fused = variant >= 1 && g.bc == SFEEC_BC_PEC;
     const bool two = variant == 4 && g.bc == SFEEC_BC_PEC && (!slab() || ghost() >= 2);
+    // merged Strang b(h/2) [e(h) b(h)]^(n-1) e(h) b(h/2) = b(h/2), then n
+    // (e, b) pairs whose last b-kick is the closing half-kick: folded into the
+    // last sweep (bitwise the separate kick: every update is yee_upd)
     p.push_back({0, 0.5 * dt, 0});
-    for (int64_t s = 0; s + 1 < n; ++s) {
-      if (two && s + 2 < n) {  // two fused steps per sweep
-        p.push_back({3, dt, dt});
+    for (int64_t s = 0; s < n; ++s) {
+      if (two && s + 1 < n) {  // two fused steps per sweep
+        p.push_back({3, dt, dt, s + 2 == n ? 0.5 * dt : dt});
         ++s;
       } else if (use_fused) {
-        p.push_back({2, dt, dt});
+        p.push_back({2, dt, s + 1 == n ? 0.5 * dt : dt});
       } else {
         p.push_back({1, dt, 0});
-        p.push_back({0, dt, 0});
+        p.push_back({0, s + 1 == n ? 0.5 * dt : dt, 0});
       }
     }
-    p.push_back({1, dt, 0});
-    p.push_back({0, 0.5 * dt, 0});
     return p;
   }
 
@@ -1230,7 +1238,7 @@ struct YeeDev {
     else if (p.kind == 1)
       ekick<T>(p.h1);
     else if (p.kind == 3)
-      fused2_tma<T>(p.h1, p.h2);
+      fused2_tma<T>(p.h1, p.h2, p.h3);
     else if (variant >= 2 || slab())
       fused_tma<T>(p.h1, p.h2);
     else
@@ -1282,24 +1290,24 @@ struct YeeDev {
     const bool t = timing && n > 1;
     const bool overlap = slab() && comm && variant >= 2;
     for (size_t i = 0; i < p.size(); ++i) {
-      if (t && i == 1) SFEEC_CUDA(cudaEventRecord(ev[0], stream));
-      if (t && i + 2 == p.size()) SFEEC_CUDA(cudaEventRecord(ev[1], stream));
+      if (t && i == 1) SFEEC_CUDA(cudaEventRecord(ev[0], stream));  // the sweeps: phases 1..
       if (overlap && (p[i].kind == 2 || p[i].kind == 3)) {
         if (prec == 8)
-          fused_overlapped<double>(p[i].h1, p[i].h2, p[i].kind == 3);
+          fused_overlapped<double>(p[i].h1, p[i].h2, p[i].kind == 3, p[i].h3);
         else
-          fused_overlapped<float>(p[i].h1, p[i].h2, p[i].kind == 3);
+          fused_overlapped<float>(p[i].h1, p[i].h2, p[i].kind == 3, p[i].h3);
         continue;
       }
       run(p[i]);
       exchange_nccl();
     }
     if (t) {
+      SFEEC_CUDA(cudaEventRecord(ev[1], stream));
       SFEEC_CUDA(cudaEventSynchronize(ev[1]));
       float ms = 0;
       SFEEC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       kernel_ms += ms;
-      kernel_launches += (int64_t)p.size() - 3;
+      kernel_launches += (int64_t)p.size() - 1;
     }
     for (int64_t s = 0; s < n; ++s) time = time + dt;
   }
@@ -1481,16 +1489,16 @@ struct YeeGroup {
       const bool two = p.kind == 3;
       for (auto& d : s) {
         if (d->prec == 8)
-          d->fused_part<double>(p.h1, p.h2, 0, two);
+          d->fused_part<double>(p.h1, p.h2, 0, two, p.h3);
         else
-          d->fused_part<float>(p.h1, p.h2, 0, two);
+          d->fused_part<float>(p.h1, p.h2, 0, two, p.h3);
       }
       exchange(1);
       for (auto& d : s) {
         if (d->prec == 8)
-          d->fused_part<double>(p.h1, p.h2, 1, two);
+          d->fused_part<double>(p.h1, p.h2, 1, two, p.h3);
         else
-          d->fused_part<float>(p.h1, p.h2, 1, two);
+          d->fused_part<float>(p.h1, p.h2, 1, two, p.h3);
         d->cur ^= 1;
       }
       return;
