@@ -346,9 +346,15 @@ int sfeec_p2_spai_device(const sfeec_csr* m1, int device, sfeec_csr_owned* q, in
  * (the sfeec_dev_create path). STENCIL_LAYOUT (16) is rejected (the
  * table-driven stencil layout was measured slower and removed). By default
  * advance() runs on the Kuhn-lattice form of the system (per-vertex
- * coefficient arrays, no index streams); NO_LATTICE keeps the
- * sliced / ELL kernels for the step too. */
-enum { SFEEC_TET_HOST_LAYOUT = 8, SFEEC_TET_STENCIL_LAYOUT = 16, SFEEC_TET_NO_LATTICE = 32 };
+ * coefficient arrays, no index streams) for n >= 48 and on the
+ * sliced / ELL kernels below (faster for the small, launch-bound meshes);
+ * NO_LATTICE / LATTICE force either. */
+enum {
+  SFEEC_TET_HOST_LAYOUT = 8,
+  SFEEC_TET_STENCIL_LAYOUT = 16,
+  SFEEC_TET_NO_LATTICE = 32,
+  SFEEC_TET_LATTICE = 64
+};
 int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                          int split_kind, int device, int flags, int with_div, sfeec_dev** out,
                          int64_t* counts);

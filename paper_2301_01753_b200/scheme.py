@@ -636,11 +636,12 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
                       device: int = 0) -> "SplitScheme":
     """First-order S(M1) tet system assembled on the B200 (C, D, M1, M2, SPAI,
     Q_sym), wrapped as a (b, e) SplitScheme. Operators stay in HBM.
-    layout: "device" (default: advance() runs on the Kuhn-lattice layout --
-    per-vertex coefficient arrays, no index streams; the
-    other entry points use sliced/ELL operators built on the GPU), "sell"
-    (sliced/ELL kernels for the step too) or "host" (generic sliced/ELL
-    layouts built through the host)."""
+    layout: "device" (default: for n >= 48 advance() runs on the Kuhn-lattice
+    layout -- per-vertex coefficient arrays, no index streams (DESIGN.md
+    3.4); below, and for the other entry points, sliced/ELL operators built
+    on the GPU), "lattice" (the lattice step at any n), "sell" (sliced/ELL
+    kernels for the step too) or "host" (generic sliced/ELL layouts built
+    through the host)."""
     units = units or UnitSystem()
     h = C.c_void_p()
     counts = np.zeros(3, np.int64)
@@ -649,8 +650,10 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
         flags |= 8  # SFEEC_TET_HOST_LAYOUT
     elif layout == "sell":
         flags |= 32  # SFEEC_TET_NO_LATTICE
+    elif layout == "lattice":
+        flags |= 64  # SFEEC_TET_LATTICE
     elif layout != "device":
-        raise InvalidParameter("layout must be 'device', 'sell' or 'host'")
+        raise InvalidParameter("layout must be 'device', 'lattice', 'sell' or 'host'")
     L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                          units.mu0, int(SplitKind(kind)), device, flags,
                                          1 if with_div else 0, C.byref(h), L.i64ptr(counts)))

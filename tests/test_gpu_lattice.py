@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _pair(n, jit=0.1, seed=3, dt=0.01, kind=S.SplitKind.Strang):
-    lat = S.tet_device_scheme(n, jit, seed, dt=dt, kind=kind)
+    lat = S.tet_device_scheme(n, jit, seed, dt=dt, kind=kind, layout="lattice")
     sell = S.tet_device_scheme(n, jit, seed, dt=dt, kind=kind, layout="sell")
     return lat, sell
 

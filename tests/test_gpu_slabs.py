@@ -27,7 +27,7 @@ def _state(n1, n2, seed):
 def test_one_rank_slab_equals_single_gpu_lattice():
     n, dt = 12, 0.01
     one = LatticeSlab(n, 0.1, 3, dt=dt)
-    ref = S.tet_device_scheme(n, 0.1, 3, dt=dt)
+    ref = S.tet_device_scheme(n, 0.1, 3, dt=dt, layout="lattice")
     assert (one.n1, one.n2) == (ref._n1, ref._n2) and one.e_glob == one.f_glob == 0
     b0, e0 = _state(one.n1, one.n2, 1)
     one.set_state(b0, e0)
