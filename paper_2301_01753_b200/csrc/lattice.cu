@@ -56,15 +56,6 @@ __device__ __forceinline__ int64_t offset_of(const LatGeom& g, int di, int dj, i
 // the mesh. Block row y covers local plane kbeg + y.
 __device__ __forceinline__ bool my_vertex(const LatGeom& g, int kbeg, int& i, int& j, int& k,
                                           int64_t& idx) {
-  if (g.map2d) {  // a block is a 32 x 8 vertex tile of one plane
-    const int ntx = (g.n + 32) / 32;
-    const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-    i = tx * 32 + (threadIdx.x & 31);
-    j = ty * 8 + (threadIdx.x >> 5);
-    k = kbeg + blockIdx.y;
-    idx = g.PS * (k + 1) + (int64_t)g.S * (j + 1) + (i + 1);
-    return i <= g.n && j <= g.n;
-  }
   const int p = blockIdx.x * kLT + threadIdx.x;
   if (p >= g.PS) return false;
   k = kbeg + blockIdx.y;
@@ -130,7 +121,8 @@ __device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, cons
   ((edge_dof<Ts>(i, j, k, g) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
 }
 // 2 blocks per SM: 128 registers, every load of the vertex's 7 rows in flight
-// (measured: 80 / 64-register caps spill and run 1.6x / 2.4x slower)
+// (measured: 80 / 64-register caps spill and run 1.6x / 2.4x slower; one
+// block per SM at 247 registers runs 1.05x (K-Q) / 1.15x (K-M2) slower)
 __global__ void __launch_bounds__(kLT, 2) k_lat_q(LatGeom g, int kbeg, const double* __restrict__ qc,
                                                const double* __restrict__ E,
                                                double* __restrict__ T) {
@@ -278,11 +270,7 @@ __global__ void k_lat_gather(int64_t n, const int64_t* __restrict__ pos,
 }
 
 inline unsigned blocks(int64_t n) { return (unsigned)((n + kLT - 1) / kLT); }
-// blocks per plane of the step kernels (my_vertex's two mappings)
-inline unsigned pblocks(const LatGeom& g) {
-  if (g.map2d) return (unsigned)(((g.n + 32) / 32) * ((g.n + 8) / 8));
-  return blocks(g.PS);
-}
+
 
 
 }  // namespace
@@ -339,7 +327,8 @@ void Lattice::build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2,
   }
   SFEEC_CUDA(cudaStreamSynchronize(s));
   valid = newer = false;
-  g.map2d = env_flag("SFEEC_LAT_MAP2D", false) ? 1 : 0;  // A/B: 32 x 8 tiles per block
+
+
 
 }
 
@@ -356,7 +345,10 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
 }
 
 // one thread per vertex computes all of its rows (the neighbour loads the
-// rows share are loaded once); grids cover local planes [kbeg(), kend()).
+// rows share are loaded once); a block is 256 consecutive positions of one
+// padded plane; grids cover local planes [kbeg(), kend()). (32 x 8 vertex
+// tiles per block, for L1 reuse of the dj neighbours, measured slower: K-Q
+// 3.50 vs 3.20 ms in the same build.)
 // Measured and rejected (tet256, ms per launch, this kernel form first): one
 // warp per row type (K-Q 2.03 vs 2.77, K-M2 1.49 vs 2.14), two threads per
 // vertex (2.03 vs 2.16, 1.49 vs 1.71), z-sweeps fusing K-Q + K-Cb and K-M2 +
@@ -365,25 +357,25 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
 void Lattice::apply_q(cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  k_lat_q<<<dim3(pblocks(g), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
+  k_lat_q<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cb(double h, cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  k_lat_cb<<<dim3(pblocks(g), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
+  k_lat_cb<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_m2(cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  k_lat_m2<<<dim3(pblocks(g), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
+  k_lat_m2<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cte(double f, cudaStream_t s) const {
   const int kb = kbeg(), ke = kend();
   if (ke <= kb) return;
-  k_lat_cte<<<dim3(pblocks(g), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
+  k_lat_cte<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
   SFEEC_LAUNCH_CHECK();
 }
 

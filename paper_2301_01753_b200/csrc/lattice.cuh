@@ -34,7 +34,6 @@ struct LatGeom {
   int64_t PS = 0;   // padded plane (S * S)
   int64_t NP = 0;   // padded box (S * S * (nz + 3)): the component stride
   int64_t org = 0;  // position of vertex (0, 0, 0)
-  int map2d = 0;    // step kernels: 0 = 256 consecutive positions per block, 1 = 32 x 8 tiles
   void init(int n_, int nz_, int kz0_, int nzg_) {
     n = n_;
     nz = nz_;

@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
-SFEEC_LAT_MAP2D=1 timeout 600 python -m pytest tests/test_gpu_lattice.py tests/test_gpu_slabs.py -x -q > gpurun_out/map_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/map_tests.log
+SFEEC_LAT_MINB1=1 timeout 600 python -m pytest tests/test_gpu_lattice.py tests/test_gpu_slabs.py -x -q > gpurun_out/map_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/map_tests.log
 for v in ${VARIANTS:-0 1 0 1}; do
-  SFEEC_LAT_MAP2D=$v timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --config ${CFG:-tet256} > gpurun_out/abm_v$v.json 2> gpurun_out/abm_v$v.err
+  SFEEC_LAT_MINB1=$v timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --config ${CFG:-tet256} > gpurun_out/abm_v$v.json 2> gpurun_out/abm_v$v.err
   python -c "
 import json; d=json.load(open('gpurun_out/abm_v$v.json')); r=d['roofline']['per_kernel']
-print('map2d=$v', round(d['ms_per_step'],4), {k: round(x['avg_ms'],4) for k,x in r.items()}, d['clocks']['sm_mhz'])"
+print('minb1=$v', round(d['ms_per_step'],4), {k: round(x['avg_ms'],4) for k,x in r.items()}, d['clocks']['sm_mhz'])"
 done
