@@ -354,26 +354,26 @@ void Lattice::gather(double* b, double* e, cudaStream_t s) const {
 // vertex (2.03 vs 2.16, 1.49 vs 1.71), z-sweeps fusing K-Q + K-Cb and K-M2 +
 // K-CTe with t / u in shared memory (5.1 vs 8.1 ms per step: one barrier per
 // plane serialises the 125 KB-per-plane coefficient streams of a tile).
-void Lattice::apply_q(cudaStream_t s) const {
-  const int kb = kbeg(), ke = kend();
+void Lattice::apply_q(cudaStream_t s, int kb, int ke) const {
+  if (kb < 0) kb = kbeg(), ke = kend();
   if (ke <= kb) return;
   k_lat_q<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
-void Lattice::apply_cb(double h, cudaStream_t s) const {
-  const int kb = kbeg(), ke = kend();
+void Lattice::apply_cb(double h, cudaStream_t s, int kb, int ke) const {
+  if (kb < 0) kb = kbeg(), ke = kend();
   if (ke <= kb) return;
   k_lat_cb<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, -h, T.p, B.p);
   SFEEC_LAUNCH_CHECK();
 }
-void Lattice::apply_m2(cudaStream_t s) const {
-  const int kb = kbeg(), ke = kend();
+void Lattice::apply_m2(cudaStream_t s, int kb, int ke) const {
+  if (kb < 0) kb = kbeg(), ke = kend();
   if (ke <= kb) return;
   k_lat_m2<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
-void Lattice::apply_cte(double f, cudaStream_t s) const {
-  const int kb = kbeg(), ke = kend();
+void Lattice::apply_cte(double f, cudaStream_t s, int kb, int ke) const {
+  if (kb < 0) kb = kbeg(), ke = kend();
   if (ke <= kb) return;
   k_lat_cte<<<dim3(blocks(g.PS), (unsigned)(ke - kb)), kLT, 0, s>>>(g, kb, f, U.p, E.p);
   SFEEC_LAUNCH_CHECK();

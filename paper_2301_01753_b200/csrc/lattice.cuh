@@ -76,10 +76,12 @@ struct Lattice {
   void gather(double* b, double* e, cudaStream_t s) const;
   // the four step kernels over local vertex planes [k0, k1) (default: all)
   int k0 = 0, k1 = -1;  // compute range; k1 < 0: every local plane
-  void apply_q(cudaStream_t s) const;               // T = Q_sym E
-  void apply_cb(double h, cudaStream_t s) const;    // B -= h C T
-  void apply_m2(cudaStream_t s) const;              // U = M2 B
-  void apply_cte(double f, cudaStream_t s) const;   // E += f C^T U
+  // (an explicit [kb, ke) overrides the range: the multi-rank overlap runs the
+  // boundary planes first)
+  void apply_q(cudaStream_t s, int kb = -1, int ke = -1) const;              // T = Q_sym E
+  void apply_cb(double h, cudaStream_t s, int kb = -1, int ke = -1) const;   // B -= h C T
+  void apply_m2(cudaStream_t s, int kb = -1, int ke = -1) const;             // U = M2 B
+  void apply_cte(double f, cudaStream_t s, int kb = -1, int ke = -1) const;  // E += f C^T U
   int kbeg() const { return k0; }
   int kend() const { return k1 < 0 ? g.nz + 1 : k1; }
   // bytes each kernel moves (arrays read once, outputs written once)

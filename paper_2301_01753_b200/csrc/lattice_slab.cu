@@ -391,7 +391,11 @@ struct LatSlab {
   int64_t class_n[4] = {0, 0, 0, 0};
 
   ~LatSlab() {
+    if (comm_stream) cudaStreamSynchronize(comm_stream);
     comm.reset();
+    if (ev_bnd) cudaEventDestroy(ev_bnd);
+    if (ev_xch) cudaEventDestroy(ev_xch);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -427,27 +431,68 @@ struct LatSlab {
   void xch(double* f, int nc, bool up, bool down) {
     if (nranks > 1) comm->exchange(f, nc, up, down, stream);
   }
+
+  // Overlap (SFEEC_PART_OVERLAP, default on with more than one rank): a
+  // kernel whose output is exchanged first computes the boundary planes the
+  // neighbours need, an event releases their exchange on the comm stream,
+  // and the interior planes run meanwhile; the next kernel waits for the
+  // exchange (it is the first to read the ghosts). The exchanged planes are
+  // not written again before that wait, and the ghosts are written only by
+  // the exchange. Results are bitwise the serialised schedule's.
+  bool overlap = false;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
+  bool pending = false;
+  void make_overlap() {
+    overlap = nranks > 1 && env_flag("SFEEC_PART_OVERLAP", true);
+    if (!overlap) return;
+    SFEEC_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    SFEEC_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
+    SFEEC_CUDA(cudaEventCreateWithFlags(&ev_xch, cudaEventDisableTiming));
+  }
+  void wait_pending() {
+    if (pending) SFEEC_CUDA(cudaStreamWaitEvent(stream, ev_xch, 0));
+    pending = false;
+  }
+  // run kern(kb, ke) over the owned planes and exchange field f
+  template <class K>
+  void produce(K&& kern, double* f, int nc, bool up, bool down) {
+    wait_pending();
+    const int a = o0(), b = o1();
+    if (!overlap) {
+      kern(a, b);
+      xch(f, nc, up, down);
+      return;
+    }
+    int ib = a, ie = b;
+    if (down && rank > 0 && ib < ie) kern(ib, ++ib);            // sent to the rank below
+    if (up && rank < nranks - 1 && ie > ib) kern(--ie, ie + 1);  // sent to the rank above
+    SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
+    SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
+    comm->exchange(f, nc, up, down, comm_stream);
+    SFEEC_CUDA(cudaEventRecord(ev_xch, comm_stream));
+    pending = true;
+    kern(ib, ie);  // the interior planes, beside the exchange
+  }
+
   // the four kernels + their ghost exchanges (see the file comment)
   void he(double h) {
     tic(0);
-    L.apply_q(stream);
+    produce([&](int kb, int ke) { L.apply_q(stream, kb, ke); }, L.T.p, 7, false, true);
     toc();
-    xch(L.T.p, 7, false, true);
     tic(1);
-    L.apply_cb(h, stream);
+    produce([&](int kb, int ke) { L.apply_cb(h, stream, kb, ke); }, L.B.p, 12, true, true);
     toc();
-    xch(L.B.p, 12, true, true);
     launches += 2;
   }
   void ha(double h) {
     tic(3);
-    L.apply_m2(stream);
+    produce([&](int kb, int ke) { L.apply_m2(stream, kb, ke); }, L.U.p, 12, true, false);
     toc();
-    xch(L.U.p, 12, true, false);
     tic(2);
-    L.apply_cte(h * c2(), stream);
+    const double f = h * c2();
+    produce([&](int kb, int ke) { L.apply_cte(f, stream, kb, ke); }, L.E.p, 7, true, true);
     toc();
-    xch(L.E.p, 7, true, true);
     launches += 2;
   }
   void advance(int64_t nsteps) {
@@ -458,6 +503,7 @@ struct LatSlab {
         he(dt);
         ha(dt);
       }
+      wait_pending();
     } else {  // merged Strang: He(h/2) [Ha(h) He(h)]^(n-1) Ha(h) He(h/2)
       he(0.5 * dt);
       for (int64_t s = 1; s < nsteps; ++s) {
@@ -467,6 +513,7 @@ struct LatSlab {
       ha(dt);
       he(0.5 * dt);
     }
+    wait_pending();
     for (int64_t s = 0; s < nsteps; ++s) time = time + dt;
   }
 
@@ -675,6 +722,7 @@ int sfeec_lslab_create(int n, int nzg, double jitter, uint64_t seed, double dt, 
         double* fields[4] = {d.L.E.p, d.L.T.p, d.L.B.p, d.L.U.p};
         d.comm = std::make_unique<IpcComm>(plan, comm_id, fields, d.P0, d.P1, nzg + 1);
       }
+      d.make_overlap();
     }
     if (info) {
       info[0] = d.eo1 - d.eo0;  // owned edges
