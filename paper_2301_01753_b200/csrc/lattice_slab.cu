@@ -465,8 +465,14 @@ struct LatSlab {
       return;
     }
     int ib = a, ie = b;
-    if (down && rank > 0 && ib < ie) kern(ib, ++ib);            // sent to the rank below
-    if (up && rank < nranks - 1 && ie > ib) kern(--ie, ie + 1);  // sent to the rank above
+    if (down && rank > 0 && ib < ie) {  // the first owned plane goes to the rank below
+      kern(ib, ib + 1);
+      ib += 1;
+    }
+    if (up && rank < nranks - 1 && ie > ib) {  // the last one to the rank above
+      kern(ie - 1, ie);
+      ie -= 1;
+    }
     SFEEC_CUDA(cudaEventRecord(ev_bnd, stream));
     SFEEC_CUDA(cudaStreamWaitEvent(comm_stream, ev_bnd, 0));
     comm->exchange(f, nc, up, down, comm_stream);

@@ -97,3 +97,11 @@ def test_processes_over_ipc_equal_one_rank_weak_stack():
 
 def test_processes_lie_trotter():
     _multi(2, dict(n=7, nzg=7, jitter=0.1, seed=2, dt=0.02, kind=0, steps=9))
+
+
+def test_processes_serialised_exchange():
+    """SFEEC_PART_OVERLAP=0: the exchange after the whole kernel instead of
+    beside its interior planes -- the same bitwise result"""
+    from tests.envutil import layout_env
+    with layout_env(SFEEC_PART_OVERLAP=0):
+        _multi(2, dict(n=9, nzg=9, jitter=0.1, seed=8, dt=0.01, kind=1, steps=10))
