@@ -16,7 +16,7 @@ def _pair(n, jit=0.1, seed=3, dt=0.01, kind=S.SplitKind.Strang):
     return lat, sell
 
 
-@pytest.mark.parametrize("n", [3, 12, 33, 40])
+@pytest.mark.parametrize("n", [1, 2, 3, 12, 33, 40])
 @pytest.mark.parametrize("kind", [S.SplitKind.Strang, S.SplitKind.LieTrotter])
 def test_lattice_step_matches_sliced_step(n, kind):
     """33 and 40 vertices per row span two 32-vertex x-blocks (rows at the
