@@ -30,8 +30,8 @@ struct LatGeom {
   int nz = 0;       // local cubes along z
   int kz0 = 0;      // whole-mesh plane of local plane 0
   int nzg = 0;      // whole-mesh cubes along z
-  int S = 0;        // padded vertices along x, y (n + 3)
-  int64_t PS = 0;   // padded plane (S * S)
+  int S = 0;        // row pitch: padded vertices along x (n + 3)
+  int64_t PS = 0;   // padded plane (S * (n + 3) rows)
   int64_t NP = 0;   // padded box (S * S * (nz + 3)): the component stride
   int64_t org = 0;  // position of vertex (0, 0, 0)
   void init(int n_, int nz_, int kz0_, int nzg_) {
@@ -40,7 +40,7 @@ struct LatGeom {
     kz0 = kz0_;
     nzg = nzg_;
     S = n + 3;
-    PS = (int64_t)S * S;
+    PS = (int64_t)S * (n + 3);
     NP = PS * (nz + 3);
     org = PS + S + 1;
   }
