@@ -13,6 +13,12 @@ Two checkers, loaded with ctypes:
           (oracle/sfeec_oracle.c) -- bitwise equal to `ref` on the same
           inputs; pinned against `ref` and against tests/golden/*.npz.
 
+  * refsetup  oracle/_ref/libsfeec_ref_setup.so: the WHOLE unmodified
+          reference library (setup code included: form_space, operators,
+          spai) over the Eigen-subset stand-in oracle/eigen_shim, behind
+          oracle/ref_shim_setup.cpp: the reference's own make_pattern,
+          spai_approximate_inverse, mass_matrix and derivative_matrix.
+
 Parity status: the step arithmetic, the sparse utilities, the Yee FDTD and
 the periodic cubical curl are pinned by the reference itself (bitwise). The
 3-D tet construction has no reference counterpart; it is pinned by the
@@ -40,7 +46,7 @@ def build(with_ref: bool = True) -> None:
     """Compile the checkers (oracle/Makefile). The ref build needs /root/reference."""
     targets = ["_build/libsfeec_oracle.so"]
     if with_ref and os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "refsetup"]
     subprocess.run(["make", "-s", *targets], cwd=HERE, check=True)
 
 
@@ -147,6 +153,80 @@ def ref_spmv(a, x):
     ref_lib().sfeec_ref_spmv(rows, cols, _ip(rp32), _ip(ci32), va.ctypes.data_as(_PD),
                              x.ctypes.data_as(_PD), y.ctypes.data_as(_PD))
     return y
+
+
+# --------------------------------------------------------------------------
+# the reference's setup code (make_pattern, SPAI, Q1 operators)
+# --------------------------------------------------------------------------
+REFSETUP_PATH = os.path.join(HERE, "_ref", "libsfeec_ref_setup.so")
+_refs = None
+
+
+def refsetup_available() -> bool:
+    return os.path.exists(REFSETUP_PATH)
+
+
+def refs_lib():
+    global _refs
+    if _refs is None:
+        l = C.CDLL(REFSETUP_PATH)
+        l.sfeec_refs_last_error.restype = C.c_char_p
+        for f in ("sfeec_refs_pattern", "sfeec_refs_spai", "sfeec_refs_cubical"):
+            getattr(l, f).restype = C.c_void_p
+        l.sfeec_refs_pattern.argtypes = [C.c_int, _PI, _PI, _PD, C.c_int]
+        l.sfeec_refs_spai.argtypes = [C.c_int, _PI, _PI, _PD, C.c_int, C.c_int]
+        l.sfeec_refs_cubical.argtypes = [C.c_int] * 3 + [C.c_double] * 3 + [C.c_int]
+        for f in ("sfeec_refs_op_rows", "sfeec_refs_op_cols", "sfeec_refs_op_nnz",
+                  "sfeec_refs_op_destroy"):
+            getattr(l, f).argtypes = [C.c_void_p]
+        l.sfeec_refs_op_export.argtypes = [C.c_void_p, _PI, _PI, _PD, _PD]
+        _refs = l
+    return _refs
+
+
+def _refs_take(h):
+    """(rows, cols, row_ptr, col_idx, val), report from an operator handle."""
+    l = refs_lib()
+    if not h:
+        raise ValueError(l.sfeec_refs_last_error().decode())
+    rows, cols, nnz = l.sfeec_refs_op_rows(h), l.sfeec_refs_op_cols(h), l.sfeec_refs_op_nnz(h)
+    rp, ci, va = np.zeros(rows + 1, np.int32), np.zeros(nnz, np.int32), np.zeros(nnz)
+    rep = np.zeros(4)
+    l.sfeec_refs_op_export(h, _ip(rp), _ip(ci), va.ctypes.data_as(_PD), rep.ctypes.data_as(_PD))
+    l.sfeec_refs_op_destroy(h)
+    return (rows, cols, rp.astype(np.int64), ci, va), rep
+
+
+_PATTERN_KINDS = {"diagonal": 0, "m1": 1, "m1sq": 2, "dense": 3}
+
+
+def ref_make_pattern(m, kind):
+    """The reference's make_pattern (spai.cpp:31-72) of a symmetric operator
+    m = (rows, cols, row_ptr, col_idx, val): row l = the index set I_l."""
+    rows, _, rp, ci, va = m
+    va = np.ascontiguousarray(va, np.float64)
+    h = refs_lib().sfeec_refs_pattern(rows, _ip(_i32(rp)), _ip(_i32(ci)), va.ctypes.data_as(_PD),
+                                      _PATTERN_KINDS[kind])
+    return _refs_take(h)[0]
+
+
+def ref_spai(m, kind, use_cg=False):
+    """The reference's spai_approximate_inverse (spai.cpp:127-286) on
+    make_pattern(m, kind) -> (Q, report dict)."""
+    rows, _, rp, ci, va = m
+    va = np.ascontiguousarray(va, np.float64)
+    h = refs_lib().sfeec_refs_spai(rows, _ip(_i32(rp)), _ip(_i32(ci)), va.ctypes.data_as(_PD),
+                                   _PATTERN_KINDS[kind], 1 if use_cg else 0)
+    q, rep = _refs_take(h)
+    return q, {"frobenius_residual": rep[0], "avg_nnz_per_row": rep[1],
+               "max_column_residual": rep[2], "fallback_columns": int(rep[3])}
+
+
+def ref_cubical_operator(nx, ny, nz, dx, dy, dz, which):
+    """Q1 operators of the reference's periodic lattice from its own
+    build_space + derivative_matrix / mass_matrix: 'c', 'm1', 'm2' or 'd'."""
+    k = {"c": 0, "m1": 1, "m2": 2, "d": 3}[which]
+    return _refs_take(refs_lib().sfeec_refs_cubical(nx, ny, nz, dx, dy, dz, k))[0]
 
 
 class RefScheme:
