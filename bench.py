@@ -237,8 +237,9 @@ def tet_setup(cfg, device):
     from paper_2301_01753_b200 import configs, inputs
     t0 = time.perf_counter()
     if cfg["kind"] == "p2":
+        # SFEEC_P2_LAYOUT=sell keeps the sliced / ELL step (A/B against the lattice)
         s = S.p2_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
-                               device=device)
+                               layout=os.environ.get("SFEEC_P2_LAYOUT", "device"), device=device)
         b0 = s.apply("c", inputs.gaussian(7, s._n1))
         s.set_dt(configs.cfl_dt(s))
         return (s._n1, s._n2), s, b0, np.zeros(s._n1), time.perf_counter() - t0
@@ -260,9 +261,15 @@ class TetRunner:
         from paper_2301_01753_b200 import _lib as L
         self.S, self.L = S, L
         (self.n1, self.n2), self.s, self.b0, self.e0, self.setup_s = tet_setup(cfg, device)
-        if cfg["kind"] == "p2":  # second order: the sliced / ELL layouts
+        if cfg["kind"] == "p2" and os.environ.get("SFEEC_P2_LAYOUT", "device") == "sell":
             self.layout = "sell"
             self.kernel_label = "SpMV chain K-M2, K-CTe, K-Q, K-Cb in sliced layouts (spmv_kernels.cu)"
+        elif cfg["kind"] == "p2":  # second order: the table-driven lattice
+            self.layout = "table"
+            self.kernel_label = ("table-driven Kuhn-lattice K-M2, K-CTe, K-Q, K-Cb: one thread per "
+                                 "(vertex, DOF type), per-vertex coefficient arrays with symmetric "
+                                 "pairs stored once, C / C^T as stencil constants "
+                                 "(table_lattice.cu)")
         self.ndof = self.n1 + self.n2
         self.dt = self.s.dt()
 

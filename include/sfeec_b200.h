@@ -348,12 +348,18 @@ int sfeec_p2_spai_device(const sfeec_csr* m1, int device, sfeec_csr_owned* q, in
  * advance() runs on the Kuhn-lattice form of the system (per-vertex
  * coefficient arrays, no index streams) for n >= 48 and on the
  * sliced / ELL kernels below (faster for the small, launch-bound meshes);
- * NO_LATTICE / LATTICE force either. */
+ * NO_LATTICE / LATTICE force either. TABLE_LATTICE runs the step on the
+ * table-driven lattice instead (table_lattice.cuh: stencils read off the
+ * assembled operators at build time, n >= 4) -- the layout of the
+ * second-order system (sfeec_p2_dev_create: on by default for n >= 12,
+ * LATTICE forces it from n >= 6, NO_LATTICE keeps the sliced kernels),
+ * available here as a cross-check of the compile-time-unrolled kernels. */
 enum {
   SFEEC_TET_HOST_LAYOUT = 8,
   SFEEC_TET_STENCIL_LAYOUT = 16,
   SFEEC_TET_NO_LATTICE = 32,
-  SFEEC_TET_LATTICE = 64
+  SFEEC_TET_LATTICE = 64,
+  SFEEC_TET_TABLE_LATTICE = 128
 };
 int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double eps0, double mu0,
                          int split_kind, int device, int flags, int with_div, sfeec_dev** out,

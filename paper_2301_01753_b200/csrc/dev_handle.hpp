@@ -15,7 +15,7 @@ sfeec_dev* make_dev_from_ops(sfeec_b200::DevOperator&& q, sfeec_b200::DevOperato
                              sfeec_b200::DevOperator&& ct, sfeec_b200::DevOperator&& m2,
                              sfeec_b200::DevOperator* div, int64_t n1, int64_t n2, double dt,
                              double eps0, double mu0, int split_kind, int device, int flags,
-                             cudaStream_t s, std::unique_ptr<sfeec_b200::Lattice> lat = nullptr);
+                             cudaStream_t s, std::unique_ptr<sfeec_b200::LatticeOps> lat = nullptr);
 // a handle from host CSR operators (Q already symmetric)
 sfeec_dev* make_dev_from_host(sfeec_b200::HostCSR&& hq, sfeec_b200::HostCSR&& hc,
                               sfeec_b200::HostCSR&& hm2, sfeec_b200::HostCSR* hdiv, double dt,

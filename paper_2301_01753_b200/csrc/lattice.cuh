@@ -55,7 +55,29 @@ struct LatGeom {
   int64_t plane(int k) const { return PS * (k + 1); }
 };
 
-struct Lattice {
+// What LeapfrogDev::advance() needs of a lattice form of the step: the state
+// maps and the four kernels, over the whole mesh. Two implementations: the
+// first-order Kuhn lattice below (stencils unrolled at compile time) and the
+// table-driven lattice of table_lattice.cuh (any order; config 4).
+struct LatticeOps {
+  // state bookkeeping of the owning handle: `valid` = the lattice fields hold
+  // the handle's state (or a newer one), `newer` = the DOF vectors are stale
+  bool valid = false, newer = false;
+  virtual ~LatticeOps() = default;
+  virtual void scatter(const double* b, const double* e, cudaStream_t s) = 0;
+  virtual void gather(double* b, double* e, cudaStream_t s) const = 0;
+  virtual void apply_q(cudaStream_t s) const = 0;              // T = Q_sym E
+  virtual void apply_cb(double h, cudaStream_t s) const = 0;   // B -= h C T
+  virtual void apply_m2(cudaStream_t s) const = 0;             // U = M2 B
+  virtual void apply_cte(double f, cudaStream_t s) const = 0;  // E += f C^T U
+  // bytes each kernel moves (arrays read once, outputs written once)
+  virtual double bytes_q() const = 0;
+  virtual double bytes_cb() const = 0;
+  virtual double bytes_m2() const = 0;
+  virtual double bytes_cte() const = 0;
+};
+
+struct Lattice : LatticeOps {
   LatGeom g;
   int64_t n1 = 0, n2 = 0;
   DevBuf<double> qc;         // kQArrays * NP: canonical Q_sym coefficients
@@ -63,32 +85,33 @@ struct Lattice {
   DevBuf<double> E, T, B, U;  // 7, 7, 12, 12 components * NP
   DevBuf<int64_t> epos, fpos;  // DOF id -> component * NP + position
   bool pdl = true;
-  // state bookkeeping of the owning handle: `valid` = E/B hold the handle's
-  // state (or a newer one), `newer` = the DOF vectors are stale
-  bool valid = false, newer = false;
 
   // coefficient arrays from the device CSRs of the k-major numbering (the
   // CSRs are read, not consumed); throws if an entry falls outside the
   // interior stencil (it cannot for the Kuhn mesh)
   void build(const TetMesh& mesh, const DevCSR& qsym, const DevCSR& m2, cudaStream_t s);
   // DOF vectors <-> lattice state
-  void scatter(const double* b, const double* e, cudaStream_t s);
-  void gather(double* b, double* e, cudaStream_t s) const;
+  void scatter(const double* b, const double* e, cudaStream_t s) override;
+  void gather(double* b, double* e, cudaStream_t s) const override;
   // the four step kernels over local vertex planes [k0, k1) (default: all)
   int k0 = 0, k1 = -1;  // compute range; k1 < 0: every local plane
   // (an explicit [kb, ke) overrides the range: the multi-rank overlap runs the
   // boundary planes first)
-  void apply_q(cudaStream_t s, int kb = -1, int ke = -1) const;              // T = Q_sym E
-  void apply_cb(double h, cudaStream_t s, int kb = -1, int ke = -1) const;   // B -= h C T
-  void apply_m2(cudaStream_t s, int kb = -1, int ke = -1) const;             // U = M2 B
-  void apply_cte(double f, cudaStream_t s, int kb = -1, int ke = -1) const;  // E += f C^T U
+  void apply_q(cudaStream_t s, int kb, int ke) const;              // T = Q_sym E
+  void apply_cb(double h, cudaStream_t s, int kb, int ke) const;   // B -= h C T
+  void apply_m2(cudaStream_t s, int kb, int ke) const;             // U = M2 B
+  void apply_cte(double f, cudaStream_t s, int kb, int ke) const;  // E += f C^T U
+  void apply_q(cudaStream_t s) const override { apply_q(s, -1, -1); }
+  void apply_cb(double h, cudaStream_t s) const override { apply_cb(h, s, -1, -1); }
+  void apply_m2(cudaStream_t s) const override { apply_m2(s, -1, -1); }
+  void apply_cte(double f, cudaStream_t s) const override { apply_cte(f, s, -1, -1); }
   int kbeg() const { return k0; }
   int kend() const { return k1 < 0 ? g.nz + 1 : k1; }
   // bytes each kernel moves (arrays read once, outputs written once)
-  double bytes_q() const;
-  double bytes_cb() const;
-  double bytes_m2() const;
-  double bytes_cte() const;
+  double bytes_q() const override;
+  double bytes_cb() const override;
+  double bytes_m2() const override;
+  double bytes_cte() const override;
   double step_bytes() const { return bytes_q() + bytes_cb() + bytes_m2() + bytes_cte(); }
 };
 

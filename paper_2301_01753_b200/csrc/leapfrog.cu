@@ -54,7 +54,7 @@ struct LeapfrogDev {
   // Kuhn-lattice layout (lattice.cuh) of a device-assembled first-order tet
   // system: advance() runs the step on the lattice state; every other entry
   // point works on the DOF vectors, gathered back when the lattice is newer
-  std::unique_ptr<Lattice> lat;
+  std::unique_ptr<LatticeOps> lat;
   bool use_lat = false;  // inside advance(): the flows run on the lattice
   bool lat_on() const { return lat && !strict() && form == SFEEC_FORM_BE; }
   void sync_dof() {
@@ -397,7 +397,7 @@ sfeec_dev* make_dev_from_host(HostCSR&& hq, HostCSR&& hc, HostCSR&& hm2, HostCSR
 sfeec_dev* make_dev_from_ops(DevOperator&& q, DevOperator&& c, DevOperator&& ct, DevOperator&& m2,
                              DevOperator* div, int64_t n1, int64_t n2, double dt, double eps0,
                              double mu0, int split_kind, int device, int flags, cudaStream_t s,
-                             std::unique_ptr<Lattice> lat) {  // (dev_handle.hpp)
+                             std::unique_ptr<LatticeOps> lat) {  // (dev_handle.hpp)
   require(!(flags & SFEEC_STRICT), "strict mode needs CSR operators (use the host builders)");
   select_device(device);
   auto h = std::make_unique<sfeec_dev>();

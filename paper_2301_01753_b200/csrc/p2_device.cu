@@ -22,6 +22,7 @@
 #include "dev_handle.hpp"
 #include "device_util.cuh"
 #include "p2_device.hpp"
+#include "table_lattice.cuh"
 #include "spmv_kernels.cuh"
 #include "tet_device.hpp"
 
@@ -502,6 +503,46 @@ HostCSR download_csr(DevCSR& a, cudaStream_t s) {
   return h;
 }
 
+// (type, vertex) of every P2- DOF for the table lattice: 1-forms = edge type
+// t, moment s -> 2 t + s, then face type f, moment s -> 14 + 2 f + s; 2-forms
+// = face f, moment s -> 3 f + s, then tet permutation p, moment s -> 36 + 3 p
+// + s at the cube's lowest vertex (the order of p2_mesh.hpp's numbering)
+void p2_table_dofs(const TetMesh& m, const P2Dofs& d, TLDofs& d1, TLDofs& d2) {
+  d1.ntypes = 38;
+  d2.ntypes = 54;
+  d1.type.resize((size_t)d.n1);
+  d1.vertex.resize((size_t)d.n1);
+  d2.type.resize((size_t)d.n2);
+  d2.vertex.resize((size_t)d.n2);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < d.n1; ++r) {
+    const int64_t ent = d.ent1[(size_t)r];
+    const int kind = d.ks1[(size_t)r] & 1, slot = d.ks1[(size_t)r] >> 1;
+    if (kind == 0) {
+      d1.type[(size_t)r] = 2 * m.edge_t[(size_t)ent] + slot;
+      d1.vertex[(size_t)r] = m.edge_v[(size_t)ent];
+    } else {
+      d1.type[(size_t)r] = 14 + 2 * m.face_t[(size_t)ent] + slot;
+      d1.vertex[(size_t)r] = m.face_v[(size_t)ent];
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < d.n2; ++r) {
+    const int64_t ent = d.ent2[(size_t)r];
+    const int kind = d.ks2[(size_t)r] & 1, slot = d.ks2[(size_t)r] >> 1;
+    if (kind == 0) {
+      d2.type[(size_t)r] = 3 * m.face_t[(size_t)ent] + slot;
+      d2.vertex[(size_t)r] = m.face_v[(size_t)ent];
+    } else {
+      const int64_t cube = ent / 6;
+      const int i = (int)(cube % m.n), j = (int)((cube / m.n) % m.n);
+      const int k = (int)(cube / ((int64_t)m.n * m.n));
+      d2.type[(size_t)r] = 36 + 3 * (int)(ent % 6) + slot;
+      d2.vertex[(size_t)r] = m.vid(i, j, k);
+    }
+  }
+}
+
 struct P2Stream {
   cudaStream_t s = nullptr;
   P2Stream() { SFEEC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -536,6 +577,21 @@ int sfeec_p2_dev_create(int n, double jitter, uint64_t seed, double dt, double e
       counts[3] = sys.qsym.nnz;
       counts[4] = sys.fallback;
     }
+    // advance() runs on the table-driven Kuhn lattice (table_lattice.cuh):
+    // Q_sym and M2 as per-vertex coefficient arrays with each symmetric pair
+    // stored once, C / C^T as constants of the slot tables; the sliced / ELL
+    // operators below serve every other entry point. Small meshes are
+    // launch-bound either way and keep the sliced step.
+    std::unique_ptr<LatticeOps> lat;
+    const bool want_lat = !(flags & SFEEC_STRICT) && !(flags & SFEEC_TET_NO_LATTICE) &&
+                          (n >= 12 || ((flags & SFEEC_TET_LATTICE) && n >= 6));
+    if (want_lat) {
+      TLDofs d1, d2;
+      p2_table_dofs(mesh, dofs, d1, d2);
+      auto tl = std::make_unique<TableLattice>();
+      tl->build(n, 2, d1, d2, sys.qsym, sys.m2, sys.c, sys.ct, st.s);
+      lat = std::move(tl);
+    }
     mesh = TetMesh();
     dofs = P2Dofs();
     DevOperator q, c, ct, m2, div;
@@ -548,7 +604,8 @@ int sfeec_p2_dev_create(int n, double jitter, uint64_t seed, double dt, double e
     SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
     *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
                              with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0, split_kind,
-                             device, flags, hs);
+                             device, flags & ~(SFEEC_TET_NO_LATTICE | SFEEC_TET_LATTICE), hs,
+                             std::move(lat));
   });
 }
 

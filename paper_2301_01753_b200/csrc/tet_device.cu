@@ -16,6 +16,7 @@
 #include "dev_handle.hpp"
 #include "device_util.cuh"
 #include "spmv_kernels.cuh"
+#include "table_lattice.cuh"
 #include "tet_device.hpp"
 #include "tet_mesh.hpp"
 
@@ -708,14 +709,27 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       // plus, by default, the Kuhn-lattice form of Q_sym and M2 that
       // advance() runs on (lattice.cuh; SFEEC_TET_NO_LATTICE keeps the
       // sliced / ELL kernels for the step as well)
-      std::unique_ptr<Lattice> lat;
+      std::unique_ptr<LatticeOps> lat;
       // the lattice kernels' one-wave grids are latency-bound below ~48^3
       // cubes, where the sliced kernels (PDL, CUDA graphs) step faster:
       // tet16 0.0179 vs 0.0089 ms per step
       const bool want_lat = (flags & SFEEC_TET_LATTICE) || (!(flags & SFEEC_TET_NO_LATTICE) && n >= 48);
-      if (want_lat && !(flags & SFEEC_STRICT)) {
-        lat = std::make_unique<Lattice>();
-        lat->build(mesh, sys.qsym, sys.m2, st.s);
+      if ((flags & SFEEC_TET_TABLE_LATTICE) && !(flags & SFEEC_STRICT)) {
+        // the table-driven lattice (config 4's layout) on the first-order system
+        TLDofs d1, d2;
+        d1.ntypes = 7;
+        d1.type.assign(mesh.edge_t.begin(), mesh.edge_t.end());
+        d1.vertex = mesh.edge_v;
+        d2.ntypes = 12;
+        d2.type.assign(mesh.face_t.begin(), mesh.face_t.end());
+        d2.vertex = mesh.face_v;
+        auto tl = std::make_unique<TableLattice>();
+        tl->build(n, 1, d1, d2, sys.qsym, sys.m2, sys.c, sys.ct, st.s);
+        lat = std::move(tl);
+      } else if (want_lat && !(flags & SFEEC_STRICT)) {
+        auto l1 = std::make_unique<Lattice>();
+        l1->build(mesh, sys.qsym, sys.m2, st.s);
+        lat = std::move(l1);
       }
       DevOperator q, c, ct, m2, div;
       q.upload_device(std::move(sys.qsym), st.s);
@@ -727,7 +741,7 @@ int sfeec_tet_dev_create(int n, double jitter, uint64_t seed, double dt, double 
       SFEEC_CUDA(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
       *out = make_dev_from_ops(std::move(q), std::move(c), std::move(ct), std::move(m2),
                                with_div ? &div : nullptr, sys.n1, sys.n2, dt, eps0, mu0,
-                               split_kind, device, flags & ~(SFEEC_TET_NO_LATTICE | SFEEC_TET_LATTICE), hs,
+                               split_kind, device, flags & ~(SFEEC_TET_NO_LATTICE | SFEEC_TET_LATTICE | SFEEC_TET_TABLE_LATTICE), hs,
                                std::move(lat));
       return;
     }

@@ -641,7 +641,8 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
     3.4); below, and for the other entry points, sliced/ELL operators built
     on the GPU), "lattice" (the lattice step at any n), "sell" (sliced/ELL
     kernels for the step too) or "host" (generic sliced/ELL layouts built
-    through the host)."""
+    through the host). "table": the step on the table-driven lattice (the
+    layout of the second-order system) as a cross-check."""
     units = units or UnitSystem()
     h = C.c_void_p()
     counts = np.zeros(3, np.int64)
@@ -652,8 +653,10 @@ def tet_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.
         flags |= 32  # SFEEC_TET_NO_LATTICE
     elif layout == "lattice":
         flags |= 64  # SFEEC_TET_LATTICE
+    elif layout == "table":
+        flags |= 128  # SFEEC_TET_TABLE_LATTICE
     elif layout != "device":
-        raise InvalidParameter("layout must be 'device', 'lattice', 'sell' or 'host'")
+        raise InvalidParameter("layout must be 'device', 'lattice', 'table', 'sell' or 'host'")
     L.check(L.lib().sfeec_tet_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                          units.mu0, int(SplitKind(kind)), device, flags,
                                          1 if with_div else 0, C.byref(h), L.i64ptr(counts)))
@@ -678,15 +681,26 @@ def tet_device_operators(n: int, jitter: float = 0.1, seed: int = 0, device: int
 
 def p2_device_scheme(n: int, jitter: float = 0.1, seed: int = 0, dt: float = 1.0,
                      kind: SplitKind = SplitKind.Strang, units: UnitSystem | None = None,
-                     with_div: bool = True, warn_cfl: bool = False,
+                     with_div: bool = True, warn_cfl: bool = False, layout: str = "device",
                      device: int = 0) -> "SplitScheme":
     """Second-order P2^- system with the S(M1^2) SPAI (BASELINE config 4):
     C, M1, M2, D from the host builders; S(M1^2), SPAI, Q_sym and C^T on the
-    B200; wrapped as a (b, e) SplitScheme."""
+    B200; wrapped as a (b, e) SplitScheme. layout: "device" (default: for
+    n >= 12 advance() runs on the table-driven Kuhn lattice, DESIGN.md 3.6 --
+    Q_sym / M2 as per-vertex coefficient arrays with each symmetric pair
+    stored once, C / C^T as stencil constants; sliced / ELL kernels below and
+    for every other entry point), "lattice" (the lattice step from n >= 6) or
+    "sell" (sliced / ELL kernels for the step too)."""
     units = units or UnitSystem()
     h = C.c_void_p()
     counts = np.zeros(5, np.int64)
     flags = 0 if warn_cfl else L.NO_CFL_WARN
+    if layout == "sell":
+        flags |= 32  # SFEEC_TET_NO_LATTICE
+    elif layout == "lattice":
+        flags |= 64  # SFEEC_TET_LATTICE
+    elif layout != "device":
+        raise InvalidParameter("layout must be 'device', 'lattice' or 'sell'")
     L.check(L.lib().sfeec_p2_dev_create(int(n), float(jitter), int(seed), float(dt), units.eps0,
                                         units.mu0, int(SplitKind(kind)), device, flags,
                                         1 if with_div else 0, C.byref(h), L.i64ptr(counts)))

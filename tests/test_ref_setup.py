@@ -98,3 +98,31 @@ def test_cubical_spai_matches_the_references():
     rq, _ = O.ref_spai(tup(m1), "m1")
     assert same_pattern(rq, q)
     assert np.max(np.abs(q.val - rq[4])) <= 1e-12 * np.abs(rq[4]).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [5, 8])
+def test_device_assembled_q_sym_is_the_references(n):
+    """The device-assembled Q_sym of the tet system (tet_device.cu: one warp
+    per SPAI column, Cholesky in shared memory) against symmetric_part of the
+    reference's own SPAI of the same M1."""
+    ops = S.tet_device_operators(n, 0.1, 2023)
+    m1 = S.TetMesh(n, 0.1, 2023).mass1()
+    rq, rep = O.ref_spai(tup(m1), "m1")
+    assert rep["fallback_columns"] == 0
+    want = O.port_symmetric_part(rq)
+    got = ops["q_sym"]
+    assert np.array_equal(got.row_ptr, want[2]) and np.array_equal(got.col_idx, want[3])
+    assert np.max(np.abs(got.val - want[4])) <= 1e-11 * np.abs(want[4]).max()
+
+
+@pytest.mark.gpu
+def test_device_p2_spai_is_the_references():
+    """The S(M1^2) SPAI of the second-order M1 on the device (p2_device.cu: one
+    CTA per column, blocked Cholesky) against the reference's."""
+    m1 = S.TetMesh(2, 0.1, 3).p2_operator("m1")
+    q, fb = S.spai_device(m1)
+    rq, rep = O.ref_spai(tup(m1), "m1sq")
+    assert fb == 0 and rep["fallback_columns"] == 0
+    assert same_pattern(rq, q)
+    assert np.max(np.abs(q.val - rq[4])) <= 1e-10 * np.abs(rq[4]).max()
