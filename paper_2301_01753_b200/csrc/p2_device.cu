@@ -509,6 +509,7 @@ HostCSR download_csr(DevCSR& a, cudaStream_t s) {
 // + s at the cube's lowest vertex (the order of p2_mesh.hpp's numbering)
 void p2_table_dofs(const TetMesh& m, const P2Dofs& d, TLDofs& d1, TLDofs& d2) {
   d1.ntypes = 38;
+  d1.mb = 2;  // both moments of an edge / face couple to the same entities: 2 x 2 blocks
   d2.ntypes = 54;
   d1.type.resize((size_t)d.n1);
   d1.vertex.resize((size_t)d.n1);

@@ -55,11 +55,13 @@ struct TLCSlot {  // constant operator: y_r(v) += val * x[xoff + v]
 };
 
 struct TLSym {
+  int mb = 1;  // moments per entity: the tables are per entity type, a slot is an mb x mb block
   int ntypes = 0, narrays = 0;
   int64_t nslots = 0;
+  int max_slots = 0;       // longest row type's table (staged in shared memory)
   DevBuf<int> beg;         // ntypes + 1: slot range of each row type
   DevBuf<TLSlot> slots;
-  DevBuf<double> coef;     // narrays * NP
+  DevBuf<double> coef;     // narrays * NP * mb * mb (a block's values row-major per position)
 };
 struct TLInc {
   int ntypes = 0;
@@ -71,6 +73,7 @@ struct TLInc {
 // DOF -> (type, vertex id of the (n + 1)^3 vertex numbering)
 struct TLDofs {
   int ntypes = 0;
+  int mb = 1;  // moments per entity: type = entity type * mb + moment
   std::vector<int32_t> type;
   std::vector<int64_t> vertex;
 };
@@ -83,8 +86,9 @@ struct TableLattice : LatticeOps {
   TLInc c, ct;
   DevBuf<double> E, T, B, U;       // nt1, nt1, nt2, nt2 arrays of NP
   DevBuf<int64_t> epos, fpos;      // DOF id -> type * NP + position
+  DevBuf<int64_t> eaddr;           // mb1 > 1: DOF id -> element of the interleaved E / T
+  int mb1 = 1;  // moments per 1-form entity: E / T hold (moment 0, moment 1, ..) per entity
   DevBuf<uint64_t> mask1, mask2;   // per position: bit t = (vertex, type t) is a DOF
-  double cb_alpha_sign = -1.0;
 
   // tables and coefficient arrays from the device CSRs (read, not consumed).
   // Throws if the mesh is too small for an interior reference vertex
