@@ -243,8 +243,9 @@ def tet_setup(cfg, device):
         b0 = s.apply("c", inputs.gaussian(7, s._n1))
         s.set_dt(configs.cfl_dt(s))
         return (s._n1, s._n2), s, b0, np.zeros(s._n1), time.perf_counter() - t0
+    # SFEEC_TET_LAYOUT=table|sell|lattice: A/B of the step layouts (default: device)
     s = S.tet_device_scheme(cfg["n"], cfg["jitter"], seed=2023, dt=1.0, with_div=True,
-                            device=device)
+                            layout=os.environ.get("SFEEC_TET_LAYOUT", "device"), device=device)
     if cfg["init"] == "gaussian":
         a = inputs.gaussian(7, s._n1)
     else:  # host C++ projection of the pulses (sfeec_tetmesh_pulse)

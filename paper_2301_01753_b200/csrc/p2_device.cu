@@ -511,6 +511,7 @@ void p2_table_dofs(const TetMesh& m, const P2Dofs& d, TLDofs& d1, TLDofs& d2) {
   d1.ntypes = 38;
   d1.mb = 2;  // both moments of an edge / face couple to the same entities: 2 x 2 blocks
   d2.ntypes = 54;
+  d2.mb = 3;  // the three moments of a face / tet: 3 x 3 blocks of M2
   d1.type.resize((size_t)d.n1);
   d1.vertex.resize((size_t)d.n1);
   d2.type.resize((size_t)d.n2);

@@ -38,14 +38,11 @@ constexpr int kUnroll = 8;  // slots per trip
 struct TLMap {
   int ntypes, chunks;  // chunks per plane
 };
-__device__ __forceinline__ bool tl_vertex(const TLGeom& g, const TLMap& m, int& r,
-                                          int64_t& idx) {
-  int64_t b = blockIdx.x;
-  r = (int)(b % m.ntypes);
-  b /= m.ntypes;
-  const int chunk = (int)(b % m.chunks);
-  const int k = (int)(b / m.chunks);
-  const int p = chunk * kTL + threadIdx.x;  // over the padded rows j = 0..n of the plane
+// grid = (row types, chunks, planes): x is the fastest block index
+__device__ __forceinline__ bool tl_vertex(const TLGeom& g, const TLMap&, int& r, int64_t& idx) {
+  r = (int)blockIdx.x;
+  const int k = (int)blockIdx.z;
+  const int p = (int)blockIdx.y * kTL + (int)threadIdx.x;  // over the padded rows j = 0..n
   if (p >= (g.n + 1) * g.S) return false;
   const int i = p % g.S - g.H;
   idx = g.PS * (k + g.H) + (int64_t)g.S * g.H + p;
@@ -157,6 +154,64 @@ __global__ void __launch_bounds__(kTL, 6)
   y[(int64_t)r * g.NP + idx] = make_double2(a0, a1);
 }
 
+// Moment blocks with plain (type-major) fields: one thread per (vertex,
+// entity type) computes the MB moment rows of its entity; a slot is an MB x MB
+// block whose MB * MB values are MB * MB consecutive coefficient ARRAYS (so
+// every load stays a coalesced run over the positions) and whose MB x values
+// serve all MB rows. Used for the P2- 2-forms (MB = 3: three moments per face
+// and per tet): 9 coefficient loads, 3 x loads and one table entry per nine
+// multiply-adds, where scalar slots need 18 loads and 9 entries.
+template <int MB>
+__global__ void __launch_bounds__(kTL, 6)
+    k_tl_symb(TLGeom g, TLMap map, const int* __restrict__ beg,
+              const TLSlot* __restrict__ slots, const double* __restrict__ coef,
+              const double* __restrict__ x, double* __restrict__ y,
+              const uint64_t* __restrict__ mask) {
+  extern __shared__ __align__(16) longlong2 tab[];
+  int r;
+  int64_t idx;
+  const bool on = tl_vertex(g, map, r, idx);
+  const int ns = beg[r + 1] - beg[r];
+  tl_stage_table(slots, beg[r], beg[r + 1], tab);
+  if (!on || !((mask[idx] >> (MB * r)) & 1)) return;
+  const double* cb = coef + idx;
+  const double* xb = x + idx;
+  double acc[MB];
+#pragma unroll
+  for (int m = 0; m < MB; ++m) acc[m] = 0.0;
+  int s = 0;
+  auto trip = [&](auto n_) {
+    constexpr int N = decltype(n_)::value;
+    longlong2 sl[N];
+    double c[N][MB * MB], v[N][MB];
+#pragma unroll
+    for (int u = 0; u < N; ++u) sl[u] = tab[s + u];
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+      for (int e = 0; e < MB * MB; ++e) c[u][e] = __ldg(cb + sl[u].x + (int64_t)e * g.NP);
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) v[u][m] = __ldg(xb + (sl[u].y >> 1) + (int64_t)m * g.NP);
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+      const bool mirror = (sl[u].y & 1) != 0;  // the neighbour's block, transposed
+#pragma unroll
+      for (int mr = 0; mr < MB; ++mr)
+#pragma unroll
+        for (int mc = 0; mc < MB; ++mc)
+          acc[mr] = fma(mirror ? c[u][mc * MB + mr] : c[u][mr * MB + mc], v[u][mc], acc[mr]);
+    }
+    s += N;
+  };
+#pragma unroll 1
+  while (s + 2 <= ns) trip(std::integral_constant<int, 2>{});
+  if (s < ns) trip(std::integral_constant<int, 1>{});
+#pragma unroll
+  for (int m = 0; m < MB; ++m) y[(int64_t)(MB * r + m) * g.NP + idx] = acc[m];
+}
+
 // y_r += alpha * sum_s val_s x(s); mbx / mby = moments per entity of the x / y
 // space (element (type t, position p) of a field with mb moments per entity
 // lives at ((t / mb) NP + p) mb + t % mb; the slots' xoff is in elements)
@@ -198,7 +253,7 @@ __global__ void k_tl_fill(int64_t rows, const int64_t* __restrict__ rp,
                           int64_t NP, const int* __restrict__ kbeg,
                           const int64_t* __restrict__ keys, const int* __restrict__ karr,
                           const double* __restrict__ kval, double* __restrict__ coef, int mb,
-                          int* __restrict__ bad) {
+                          int soa, int* __restrict__ bad) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -227,7 +282,11 @@ __global__ void k_tl_fill(int64_t rows, const int64_t* __restrict__ rp,
     if (kval) {
       if (kval[lo] != val[q]) atomicExch(bad, 2);
     } else if (karr[lo] >= 0) {
-      coef[(((int64_t)karr[lo] * NP + idx) * mb + mr) * mb + mc] = val[q];
+      // a block's values: interleaved per position, or (soa) mb * mb arrays
+      if (soa)
+        coef[(((int64_t)karr[lo] * mb + mr) * mb + mc) * NP + idx] = val[q];
+      else
+        coef[(((int64_t)karr[lo] * NP + idx) * mb + mr) * mb + mc] = val[q];
     }
   }
 }
@@ -347,7 +406,7 @@ KeyTable key_table(const std::vector<std::vector<HostSlot>>& st) {
 }
 
 void fill(const DevCSR& a, const int64_t* rpos, const int64_t* cpos, int64_t NP,
-          const KeyTable& kt, bool constant, double* coef, int mb, const char* name,
+          const KeyTable& kt, bool constant, double* coef, int mb, bool soa, const char* name,
           cudaStream_t s) {
   DevBuf<int> kbeg, karr, bad;
   DevBuf<int64_t> keys;
@@ -361,7 +420,8 @@ void fill(const DevCSR& a, const int64_t* rpos, const int64_t* cpos, int64_t NP,
   if (a.rows)
     k_tl_fill<<<blocks256(a.rows * 32), 256, 0, s>>>(a.rows, a.rp.p, a.ci.p, a.val.p, rpos, cpos,
                                                      NP, kbeg.p, keys.p, karr.p,
-                                                     constant ? kval.p : nullptr, coef, mb, bad.p);
+                                                     constant ? kval.p : nullptr, coef, mb,
+                                                     soa ? 1 : 0, bad.p);
   SFEEC_LAUNCH_CHECK();
   int hbad = 0;
   SFEEC_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -405,8 +465,11 @@ std::vector<std::vector<HostSlot>> entity_stencils(
   return out;
 }
 
-void build_sym(const Builder& b, const DevCSR& a, const TLDofs& d, int mb, const int64_t* pos,
-               const char* name, TLSym& out, cudaStream_t s) {
+// soa: an mb x mb block is mb * mb arrays and the field stays type-major
+// (k_tl_symb); otherwise the block and the field are interleaved per position
+// (k_tl_sym2, mb = 2)
+void build_sym(const Builder& b, const DevCSR& a, const TLDofs& d, int mb, bool soa,
+               const int64_t* pos, const char* name, TLSym& out, cudaStream_t s) {
   auto st = entity_stencils(b.stencils(a, d, d, s), mb, name);
   const int ne = d.ntypes / mb;
   // canonical slots get the arrays, in (row type, slot) order
@@ -430,14 +493,15 @@ void build_sym(const Builder& b, const DevCSR& a, const TLDofs& d, int mb, const
       }
   out.ntypes = ne;
   out.mb = mb;
+  out.soa = soa;
   out.narrays = narr;
   std::vector<int> beg{0};
   std::vector<TLSlot> slots;
   for (int t = 0; t < ne; ++t) {
     for (const HostSlot& sl : st[(size_t)t]) {
-      const int64_t xoff = (int64_t)sl.ctype * b.g.NP + sl.off;
-      // (blocked kernel: bit 0 of the second word flags a transposed slot)
-      slots.push_back({(int64_t)sl.array * b.g.NP + (sl.mirror ? sl.off : 0),
+      // (blocked kernels: bit 0 of the second word flags a transposed slot)
+      const int64_t xoff = (int64_t)sl.ctype * (soa ? mb : 1) * b.g.NP + sl.off;
+      slots.push_back({(int64_t)sl.array * (soa ? mb * mb : 1) * b.g.NP + (sl.mirror ? sl.off : 0),
                        mb == 1 ? xoff : (xoff << 1) | (sl.mirror ? 1 : 0)});
     }
     beg.push_back((int)slots.size());
@@ -450,7 +514,7 @@ void build_sym(const Builder& b, const DevCSR& a, const TLDofs& d, int mb, const
   out.slots.upload(slots.data(), slots.size(), s);
   out.coef.alloc((size_t)narr * (size_t)b.g.NP * (size_t)(mb * mb));
   out.coef.zero(s);
-  fill(a, pos, pos, b.g.NP, key_table(st), false, out.coef.p, mb, name, s);
+  fill(a, pos, pos, b.g.NP, key_table(st), false, out.coef.p, mb, soa, name, s);
 }
 
 // mbx: moments per entity of the column (x) space; xoff in elements
@@ -470,7 +534,7 @@ void build_inc(const Builder& b, const DevCSR& a, const TLDofs& rows, const TLDo
   out.nslots = (int64_t)slots.size();
   out.beg.upload(beg.data(), beg.size(), s);
   out.slots.upload(slots.data(), slots.size(), s);
-  fill(a, rpos, cpos, b.g.NP, key_table(st), true, nullptr, 1, name, s);
+  fill(a, rpos, cpos, b.g.NP, key_table(st), true, nullptr, 1, false, name, s);
 }
 
 }  // namespace
@@ -481,8 +545,9 @@ void TableLattice::build(int n, int halo, const TLDofs& d1, const TLDofs& d2, co
   require(halo >= 1 && n >= 2 * halo + 2,
           "table lattice: the mesh is too small for an interior reference vertex");
   require(d1.ntypes <= 64 && d2.ntypes <= 64, "table lattice: at most 64 DOF types per vertex");
-  require((d1.mb == 1 || d1.mb == 2) && d1.ntypes % d1.mb == 0 && d2.mb == 1,
-          "table lattice: moment blocks of 1 or 2 (1-forms), 1 (2-forms)");
+  require((d1.mb == 1 || d1.mb == 2) && d1.ntypes % d1.mb == 0 &&
+              (d2.mb == 1 || d2.mb == 3) && d2.ntypes % d2.mb == 0,
+          "table lattice: moment blocks of 1 or 2 (1-forms), 1 or 3 (2-forms)");
   mb1 = d1.mb;
   g.init(n, halo);
   n1 = (int64_t)d1.type.size();
@@ -529,8 +594,8 @@ void TableLattice::build(int n, int halo, const TLDofs& d1, const TLDofs& d2, co
     k_tl_mask<<<blocks256(n2), 256, 0, s>>>(n2, fpos.p, g.NP,
                                             reinterpret_cast<unsigned long long*>(mask2.p));
   SFEEC_LAUNCH_CHECK();
-  build_sym(b, qsym, d1, mb1, epos.p, "Q_sym", q, s);
-  build_sym(b, m2csr, d2, 1, fpos.p, "M2", m2, s);
+  build_sym(b, qsym, d1, mb1, false, epos.p, "Q_sym", q, s);
+  build_sym(b, m2csr, d2, d2.mb, true, fpos.p, "M2", m2, s);
   build_inc(b, ccsr, d2, d1, mb1, fpos.p, epos.p, "C", c, s);
   build_inc(b, ctcsr, d1, d2, 1, epos.p, fpos.p, "C^T", ct, s);
   for (auto* f : {&E, &T}) {
@@ -560,8 +625,8 @@ namespace {
 TLMap tl_map(const TLGeom& g, int ntypes) {
   return TLMap{ntypes, ((g.n + 1) * g.S + kTL - 1) / kTL};
 }
-unsigned tl_grid(const TLGeom& g, const TLMap& m) {
-  return (unsigned)((int64_t)m.ntypes * m.chunks * (g.n + 1));
+dim3 tl_grid(const TLGeom& g, const TLMap& m) {
+  return dim3((unsigned)m.ntypes, (unsigned)m.chunks, (unsigned)(g.n + 1));
 }
 }  // namespace
 
@@ -578,9 +643,14 @@ void TableLattice::apply_q(cudaStream_t s) const {
   SFEEC_LAUNCH_CHECK();
 }
 void TableLattice::apply_m2(cudaStream_t s) const {
-  const TLMap m = tl_map(g, nt2);
-  k_tl_sym<<<tl_grid(g, m), kTL, sizeof(TLSlot) * (size_t)m2.max_slots, s>>>(
-      g, m, m2.beg.p, m2.slots.p, m2.coef.p, B.p, U.p, mask2.p);
+  const TLMap m = tl_map(g, m2.ntypes);
+  const size_t smem = sizeof(TLSlot) * (size_t)m2.max_slots;
+  if (m2.mb == 3)
+    k_tl_symb<3><<<tl_grid(g, m), kTL, smem, s>>>(g, m, m2.beg.p, m2.slots.p, m2.coef.p, B.p, U.p,
+                                                  mask2.p);
+  else
+    k_tl_sym<<<tl_grid(g, m), kTL, smem, s>>>(g, m, m2.beg.p, m2.slots.p, m2.coef.p, B.p, U.p,
+                                              mask2.p);
   SFEEC_LAUNCH_CHECK();
 }
 void TableLattice::apply_cb(double h, cudaStream_t s) const {
@@ -603,7 +673,7 @@ double TableLattice::bytes_q() const {
 }
 double TableLattice::bytes_m2() const {
   const double V = (double)(g.n + 1) * (g.n + 1) * (g.n + 1);
-  return 8.0 * (m2.narrays * V + (double)n2 + (double)n2);
+  return 8.0 * ((double)m2.narrays * m2.mb * m2.mb * V + (double)n2 + (double)n2);
 }
 double TableLattice::bytes_cb() const { return 8.0 * ((double)n1 + 2.0 * (double)n2); }
 double TableLattice::bytes_cte() const { return 8.0 * ((double)n2 + 2.0 * (double)n1); }

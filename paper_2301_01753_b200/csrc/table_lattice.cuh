@@ -56,6 +56,7 @@ struct TLCSlot {  // constant operator: y_r(v) += val * x[xoff + v]
 
 struct TLSym {
   int mb = 1;  // moments per entity: the tables are per entity type, a slot is an mb x mb block
+  bool soa = false;  // blocks as mb * mb arrays (type-major fields) instead of interleaved
   int ntypes = 0, narrays = 0;
   int64_t nslots = 0;
   int max_slots = 0;       // longest row type's table (staged in shared memory)
