@@ -19,4 +19,7 @@ if [ -n "$NCU" ]; then
   ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_lat_" -c 4 \
       -o gpurun_out/lat_tet256_r2 python tools/profile_kq.py tet256 > gpurun_out/ncu.log 2>&1
   echo "ncu rc=$?"
+  python tools/profile_kq.py p2_64 > gpurun_out/prof_plain3.log 2>&1 && \
+  ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_p2_64.csv python tools/profile_kq.py p2_64 > gpurun_out/ncu_l2.log 2>&1
 fi
