@@ -189,6 +189,17 @@ int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double d
                           double eps0, double mu0, int precision, int rank, int nranks,
                           const void* nccl_id /* 128 bytes from rank 0 */, int device,
                           sfeec_yee** out);
+/* The same slab with the ghost transport chosen: SFEEC_TRANSPORT_NCCL (comm_id
+ * = the 128-byte ncclUniqueId; one GPU per rank) or SFEEC_TRANSPORT_IPC (CUDA
+ * IPC on one node, comm_id from sfeec_ipc_unique_id: the neighbours' buffers
+ * are mapped and the ghost planes pulled between two host-side barriers, so
+ * no kernel waits on another rank and the ranks may share one GPU). */
+#define SFEEC_TRANSPORT_NCCL 0
+#define SFEEC_TRANSPORT_IPC 1
+int sfeec_yee_create_slab_transport(int nx, int ny, int nz, double dx, double dy, double dz,
+                                    double dt, double eps0, double mu0, int precision, int rank,
+                                    int nranks, int transport, const void* comm_id, int device,
+                                    sfeec_yee** out);
 int sfeec_yee_slab_dof_counts(int nx, int ny, int nz, int rank, int nranks, int64_t* n_edges,
                               int64_t* n_faces);
 int sfeec_yee_slab_dof_map(int nx, int ny, int nz, int rank, int nranks, int64_t* edge_map,

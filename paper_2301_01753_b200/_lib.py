@@ -107,6 +107,10 @@ _SIGS = {
                                         C.c_double, C.c_double, C.c_double, C.c_double,
                                         C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.POINTER(_P)]),
+    "sfeec_yee_create_slab_transport": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
+                                                  C.c_double, C.c_double, C.c_double, C.c_double,
+                                                  C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                  C.c_void_p, C.c_int, C.POINTER(_P)]),
     "sfeec_yee_slab_dof_counts": (C.c_int, [C.c_int] * 5 + [_PI64, _PI64]),
     "sfeec_yee_slab_dof_map": (C.c_int, [C.c_int] * 5 + [_PI64, _PI64]),
     "sfeec_yee_group_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,

@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include "device_util.cuh"
+#include "ipc_group.hpp"
 #include "nccl_loader.hpp"
 #include "yee_layout.hpp"
 
@@ -920,6 +921,16 @@ struct YeeDev {
   // z-slab decomposition (yee_layout.hpp make_yee_slab)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  // CUDA-IPC transport (host-synchronised; the ranks may share a GPU): the
+  // neighbours' two ping-pong buffers mapped into this process
+  struct IpcSlot {
+    cudaIpcMemHandle_t h[2];
+    int64_t npts;  // that slab's component stride
+    int s2;        // its z planes, ghosts included
+  };
+  std::unique_ptr<IpcGroup> ipc;
+  char* peer_lo[2] = {nullptr, nullptr};
+  char* peer_hi[2] = {nullptr, nullptr};
   cudaStream_t comm_stream = nullptr;  // overlapped halo exchange
   cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
   // host-state copies: a copy stream, so one vector's scatter / gather runs
@@ -943,6 +954,8 @@ struct YeeDev {
     if (ev_xch) cudaEventDestroy(ev_xch);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (comm) Nccl::get().comm_destroy(comm);
+    for (char* q : {peer_lo[0], peer_lo[1], peer_hi[0], peer_hi[1]})
+      if (q) cudaIpcCloseMemHandle(q);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -1256,8 +1269,62 @@ struct YeeDev {
   // owned planes go up into the upper neighbour's bottom ghosts (B only when
   // G = 1: the one-step kernels never read E below). Each component's G
   // planes are contiguous, so one message per component and direction.
+  // join the ranks' shared segment and map the neighbours' buffers
+  void init_ipc(const void* id128) {
+    ipc = std::make_unique<IpcGroup>("sfeec_yee", id128, rank, nranks, sizeof(IpcSlot));
+    IpcSlot& me = *(IpcSlot*)ipc->slot(rank);
+    for (int b = 0; b < 2; ++b) SFEEC_CUDA(cudaIpcGetMemHandle(&me.h[b], buf[b].p));
+    me.npts = g.npts();
+    me.s2 = g.S[2];
+    ipc->barrier();
+    for (int b = 0; b < 2; ++b) {
+      void* q = nullptr;
+      if (rank > 0) {
+        SFEEC_CUDA(cudaIpcOpenMemHandle(&q, ((IpcSlot*)ipc->slot(rank - 1))->h[b],
+                                        cudaIpcMemLazyEnablePeerAccess));
+        peer_lo[b] = (char*)q;
+      }
+      if (rank < nranks - 1) {
+        SFEEC_CUDA(cudaIpcOpenMemHandle(&q, ((IpcSlot*)ipc->slot(rank + 1))->h[b],
+                                        cudaIpcMemLazyEnablePeerAccess));
+        peer_hi[b] = (char*)q;
+      }
+    }
+    ipc->barrier();
+    ipc->unlink_name();
+  }
+  // the same planes and components as exchange_nccl, pulled from the
+  // neighbours' buffers between two host barriers
+  void exchange_ipc(int bufsel, cudaStream_t es) {
+    const int G = ghost();
+    const size_t pb = (size_t)plane() * (size_t)prec, cnt = pb * (size_t)G;
+    char* base = buf[bufsel].p;
+    auto at = [&](char* b0, int64_t npts, int comp, int pl) {
+      return b0 + ((size_t)comp * (size_t)npts) * (size_t)prec + (size_t)pl * pb;
+    };
+    const int c_up = G == 1 ? 3 : 0;
+    SFEEC_CUDA(cudaStreamSynchronize(es));  // our planes are written ...
+    ipc->barrier();                         // ... and so are the neighbours'
+    if (rank > 0) {  // bottom ghosts <- the lower neighbour's top owned planes
+      const IpcSlot& lo = *(const IpcSlot*)ipc->slot(rank - 1);
+      for (int c = c_up; c < 6; ++c)
+        SFEEC_CUDA(cudaMemcpyAsync(at(base, g.npts(), c, 0),
+                                   at(peer_lo[bufsel], lo.npts, c, lo.s2 - 2 * G), cnt,
+                                   cudaMemcpyDeviceToDevice, es));
+    }
+    if (rank < nranks - 1) {  // top ghosts <- the upper neighbour's first owned planes
+      const IpcSlot& hi = *(const IpcSlot*)ipc->slot(rank + 1);
+      for (int c = 0; c < 6; ++c)
+        SFEEC_CUDA(cudaMemcpyAsync(at(base, g.npts(), c, g.S[2] - G),
+                                   at(peer_hi[bufsel], hi.npts, c, G), cnt,
+                                   cudaMemcpyDeviceToDevice, es));
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(es));  // our pulls are done ...
+    ipc->barrier();                         // ... before anyone overwrites a source plane
+  }
   void exchange_nccl() { exchange_nccl(cur, stream); }
   void exchange_nccl(int bufsel, cudaStream_t es) {
+    if (slab() && ipc) return exchange_ipc(bufsel, es);
     if (!slab() || !comm) return;
     const Nccl& nc = Nccl::get();
     const ncclDataType_t ty = prec == 8 ? ncclFloat64 : ncclFloat32;
@@ -1620,8 +1687,19 @@ int sfeec_nccl_selftest(int device, int64_t n, double* max_err) {
 int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double dz, double dt,
                           double eps0, double mu0, int precision, int rank, int nranks,
                           const void* nccl_id, int device, sfeec_yee** out) {
+  return sfeec_yee_create_slab_transport(nx, ny, nz, dx, dy, dz, dt, eps0, mu0, precision, rank,
+                                         nranks, SFEEC_TRANSPORT_NCCL, nccl_id, device, out);
+}
+
+int sfeec_yee_create_slab_transport(int nx, int ny, int nz, double dx, double dy, double dz,
+                                    double dt, double eps0, double mu0, int precision, int rank,
+                                    int nranks, int transport, const void* comm_id, int device,
+                                    sfeec_yee** out) {
+  const void* nccl_id = comm_id;
   return guarded([&] {
     require(out != nullptr, "sfeec_yee_create_slab: null out");
+    require(transport == SFEEC_TRANSPORT_NCCL || transport == SFEEC_TRANSPORT_IPC,
+            "sfeec_yee_create_slab: unknown transport");
     *out = nullptr;
     check_lattice(nx, ny, nz, dx, dy, dz, dt, SFEEC_BC_PEC, precision);
     require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
@@ -1632,13 +1710,18 @@ int sfeec_yee_create_slab(int nx, int ny, int nz, double dx, double dy, double d
     if (nranks == 1) {
       d.init(device, make_yee_geom(nx, ny, nz, SFEEC_BC_PEC), dx, dy, dz, dt, eps0, mu0, precision);
     } else {
-      require(nccl_id != nullptr, "multi-rank slab needs an NCCL unique id");
+      require(nccl_id != nullptr, "multi-rank slab needs a communicator id");
       d.init(device, make_yee_slab(nx, ny, nz, rank, nranks), dx, dy, dz, dt, eps0, mu0, precision);
       d.rank = rank;
       d.nranks = nranks;
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
-      Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, nranks, id, rank), "ncclCommInitRank");
+      if (transport == SFEEC_TRANSPORT_IPC) {
+        d.init_ipc(comm_id);
+      } else {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        Nccl::get().check(Nccl::get().comm_init_rank(&d.comm, nranks, id, rank),
+                          "ncclCommInitRank");
+      }
     }
     *out = h.release();
   });

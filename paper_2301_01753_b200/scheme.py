@@ -436,18 +436,23 @@ def yee_slab_dofs(nx, ny, nz, rank, nranks):
 
 
 class YeeSlab(YeeScheme):
-    """One z-slab of a PEC Yee lattice per GPU (one process per GPU); ghost
-    planes exchanged over NCCL after every kernel. State in the slab's local
-    numbering (yee_slab_dofs); energy() returns this slab's part."""
+    """One z-slab of a PEC Yee lattice per process; ghost planes exchanged
+    after every kernel over NCCL (transport="nccl", nccl_id = an NCCL unique
+    id; one GPU per rank) or CUDA IPC (transport="ipc", nccl_id from
+    partition.ipc_unique_id(); host-synchronised, ranks may share a GPU). State
+    in the slab's local numbering (yee_slab_dofs); energy() returns this
+    slab's part."""
 
     def __init__(self, nx, ny, nz, dx, dy, dz, dt, rank, nranks, nccl_id: bytes | None,
-                 units: UnitSystem | None = None, precision: int = 8, device: int = 0):
+                 units: UnitSystem | None = None, precision: int = 8, device: int = 0,
+                 transport: str = "nccl"):
         units = units or UnitSystem()
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        L.check(L.lib().sfeec_yee_create_slab(nx, ny, nz, dx, dy, dz, dt, units.eps0, units.mu0,
-                                              precision, rank, nranks, idbuf, device,
-                                              C.byref(h)))
+        idbuf = ((C.c_char * 128).from_buffer_copy(nccl_id.ljust(128, b"\0")[:128])
+                 if nccl_id else None)
+        L.check(L.lib().sfeec_yee_create_slab_transport(
+            nx, ny, nz, dx, dy, dz, dt, units.eps0, units.mu0, precision, rank, nranks,
+            {"nccl": 0, "ipc": 1}[transport], idbuf, device, C.byref(h)))
         self._h = h
         ne, nf = C.c_int64(), C.c_int64()
         L.check(L.lib().sfeec_yee_dof_counts(h, C.byref(ne), C.byref(nf)))
