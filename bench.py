@@ -138,7 +138,7 @@ def yee_setup(n, precision, device):
     return y, b0, np.zeros(y.n_edges), dt
 
 
-def yee_slab_setup(n, precision, device, rank, world, dist):
+def yee_slab_setup(n, precision, device, rank, world, dist, transport="nccl"):
     """Rank `rank` of a 256 x 256 x (256 world) PEC lattice (weak scaling): the
     z-slab with NCCL ghost exchange; A drawn by global edge id."""
     import paper_2301_01753_b200 as S
@@ -146,10 +146,12 @@ def yee_slab_setup(n, precision, device, rank, world, dist):
     h = 1.0 / n
     dt = 0.5 / (np.sqrt(3.0) * n)
     nz = n * world
-    ids = [S.nccl_unique_id() if rank == 0 else None]
+    from paper_2301_01753_b200.partition import ipc_unique_id
+    new_id = ipc_unique_id if transport == "ipc" else S.nccl_unique_id
+    ids = [new_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     y = S.YeeSlab(n, n, nz, h, h, h, dt, rank, world, ids[0], precision=precision,
-                  device=device)
+                  device=device, transport=transport)
     em, _ = S.yee_slab_dofs(n, n, nz, rank, world)
     a = inputs.gaussian_ids(20260101, em)
     y.load(np.zeros(y.n_faces), a)          # exchanges the ghost planes
@@ -159,12 +161,13 @@ def yee_slab_setup(n, precision, device, rank, world, dist):
 
 
 class YeeRunner:
-    def __init__(self, cfg, device, rank=0, world=1, dist=None):
+    def __init__(self, cfg, device, rank=0, world=1, dist=None, transport="nccl"):
         from paper_2301_01753_b200 import _lib as L
         self.L = L
         if dist is not None:
             self.y, self.b0, self.e0, self.dt = yee_slab_setup(cfg["n"], cfg["precision"],
-                                                                device, rank, world, dist)
+                                                                device, rank, world, dist,
+                                                                transport)
             self.kernel_label = ("two-step fused TMA sweep per z-slab (two ghost planes) + "
                                  "NCCL ghost-plane exchange overlapped with the interior chunks")
         else:
@@ -435,20 +438,21 @@ class LatSlabRunner:
                     "one-plane ghost exchanges between them (lattice_slab.cu)")
     layout = "lattice"
 
-    def __init__(self, cfg, device, rank, world, dist, strong=False):
+    def __init__(self, cfg, device, rank, world, dist, strong=False, transport="nccl"):
         import paper_2301_01753_b200 as S
         from paper_2301_01753_b200 import configs, inputs
-        from paper_2301_01753_b200.partition import LatticeSlab
+        from paper_2301_01753_b200.partition import LatticeSlab, ipc_unique_id
         t0 = time.perf_counter()
         self.scaling = "strong" if strong else "weak"
         ids = [None]
         if dist is not None and world > 1:
-            ids = [S.nccl_unique_id() if rank == 0 else None]
+            new_id = ipc_unique_id if transport == "ipc" else S.nccl_unique_id
+            ids = [new_id() if rank == 0 else None]
             dist.broadcast_object_list(ids, src=0)
         n = cfg["n"]
         nzg = n if strong else n * world
         self.s = LatticeSlab(n, cfg["jitter"], 2023, nzg=nzg, dt=1.0, rank=rank, nranks=world,
-                             transport="nccl", comm_id=ids[0], device=device)
+                             transport=transport, comm_id=ids[0], device=device)
         s = self.s
         if cfg["init"] == "gaussian":
             a = inputs.gaussian_ids(7, np.arange(s.e_glob, s.e_glob + s.n1))
@@ -514,15 +518,22 @@ def run_ours(args, rank, world, local_rank):
     import torch
 
     cfg = CONFIGS[args.config]
+    ipc = args.transport == "ipc"
+    if ipc:  # ranks may share a GPU (host-synchronised transport)
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1 or args.dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if ipc:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    tr = args.transport
     if cfg["kind"] == "yee":
-        R = YeeRunner(cfg, local_rank, rank, world, dist)
+        R = YeeRunner(cfg, local_rank, rank, world, dist, transport=tr)
     elif cfg["kind"] == "tet" and (dist is not None or args.partitioned):
-        R = LatSlabRunner(cfg, local_rank, rank, world, dist, strong=args.strong)
+        R = LatSlabRunner(cfg, local_rank, rank, world, dist, strong=args.strong, transport=tr)
     elif dist is not None or args.partitioned:
         R = TetSlabRunner(cfg, local_rank, rank, world, dist)  # P2-: sliced slabs
     else:
@@ -532,11 +543,12 @@ def run_ours(args, rank, world, local_rank):
     else:
         stream = torch.cuda.current_stream()
         R.set_stream(stream.cuda_stream)
+    rdev = "cpu" if ipc else "cuda"  # gloo reduces host tensors
     strong = getattr(R, "scaling", "weak") == "strong"
     if isinstance(R, LatSlabRunner):  # owned DOFs per rank: the job's total is their sum
         units = R.ndof
         if dist:
-            t_ = torch.tensor([float(R.ndof)], device="cuda", dtype=torch.float64)
+            t_ = torch.tensor([float(R.ndof)], device=rdev, dtype=torch.float64)
             dist.all_reduce(t_)
             units = int(t_.item())
     else:
@@ -560,13 +572,13 @@ def run_ours(args, rank, world, local_rank):
     launches = R.launches()
     energy1, gauss1 = R.diagnostics()  # untimed: the state after warmup + steps
     if dist and not isinstance(R, LatSlabRunner):  # (the lattice slabs' energy is collective)
-        t = torch.tensor([energy0, energy1], device="cuda", dtype=torch.float64)
+        t = torch.tensor([energy0, energy1], device=rdev, dtype=torch.float64)
         dist.all_reduce(t)  # each rank holds its part of the energy sums
         energy0, energy1 = float(t[0]), float(t[1])
     # dominant kernel: average launch duration with CUDA events on the launch stream
     kname, kbytes, k_avg_ms = R.dominant(min(args.steps, 200))
     if dist:
-        t = torch.tensor([ms, k_avg_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms, k_avg_ms], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, k_avg_ms = float(t[0]), float(t[1])
     if dist:
@@ -576,10 +588,12 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     e2e_s = R.e2e(args.steps, torch)
     if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
 
+    trname = ("CUDA-IPC (host-synchronised; ranks share GPUs: functional check)" if ipc
+              else "NCCL")
     peak, peak_src = hbm_peak()
     # roofline of the dominant kernel: DRAM bytes per launch (ncu, committed
     # under profiles/) over the CUDA-event launch time; the algorithmic count
@@ -604,9 +618,9 @@ def run_ours(args, rank, world, local_rank):
                                                          if world > 1 else "")),
                    "dofs_per_gpu": ndof if not strong else ndof / world,
                    "n1_edges": R.n1, "n2_faces": R.n2, "dt": R.dt,
-                   "parallelism": (f"z-slabs x{world}, NCCL ghost exchange" if cfg["kind"] == "yee"
+                   "parallelism": (f"z-slabs x{world}, {trname} ghost exchange" if cfg["kind"] == "yee"
                                    else f"z-slabs x{world} of the Kuhn lattice, per-rank "
-                                        "assembly, NCCL one-plane ghost exchanges"
+                                        f"assembly, {trname} one-plane ghost exchanges"
                                    if isinstance(R, LatSlabRunner)
                                    else f"z-slabs x{world}, NCCL halo-plane exchange")
                                   if world > 1 else "single GPU",
@@ -829,6 +843,12 @@ def main():
                     help="the multi-GPU code path (NCCL process group, slab runners, "
                          "max-over-ranks) even at world size 1, e.g. under torchrun with "
                          "one process")
+    ap.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
+                    help="ghost-plane transport of a multi-rank run. nccl: one GPU per rank "
+                         "(the driver's launch). ipc: the product's host-synchronised CUDA-IPC "
+                         "transport with gloo for the plumbing; ranks share GPUs when there "
+                         "are fewer GPUs than ranks (a functional check of the multi-rank "
+                         "flow on a one-GPU box, not a scaling number)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=60.0)
     args = ap.parse_args()
