@@ -344,17 +344,21 @@ class TetSlabRunner:
     kernel_label = ("SpMV chain K-M2, K-CTe, K-Q, K-Cb over the owned rows + NCCL halo-plane "
                     "exchange before each (partition.cu)")
 
-    def __init__(self, cfg, device, rank, world, dist):
+    def __init__(self, cfg, device, rank, world, dist, transport="nccl"):
         import paper_2301_01753_b200 as S
         from paper_2301_01753_b200 import inputs, partition
         t0 = time.perf_counter()
         ids = [None]
+        ipc = transport == "ipc" and world > 1
         if dist is not None:
-            ids = [S.nccl_unique_id() if rank == 0 else None]
+            new_id = partition.ipc_unique_id if ipc else S.nccl_unique_id
+            ids = [new_id() if rank == 0 else None]
             dist.broadcast_object_list(ids, src=0)
         self.p = partition.TetPart.from_device(cfg["n"], cfg["jitter"], 2023, rank, world,
-                                               nccl_id=ids[0], device=device,
+                                               nccl_id=None if ipc else ids[0], device=device,
                                                order=2 if cfg["kind"] == "p2" else 1)
+        if ipc:
+            self.p.attach_ipc(ids[0])
         ls = self.p.ls
         eg, er, fg = ls.edge_global, ls.edge_range, ls.face_global
         if cfg["init"] == "gaussian":
@@ -535,7 +539,7 @@ def run_ours(args, rank, world, local_rank):
     elif cfg["kind"] == "tet" and (dist is not None or args.partitioned):
         R = LatSlabRunner(cfg, local_rank, rank, world, dist, strong=args.strong, transport=tr)
     elif dist is not None or args.partitioned:
-        R = TetSlabRunner(cfg, local_rank, rank, world, dist)  # P2-: sliced slabs
+        R = TetSlabRunner(cfg, local_rank, rank, world, dist, transport=tr)  # P2-: sliced slabs
     else:
         R = TetRunner(cfg, local_rank)
     if hasattr(R, "stream"):
@@ -622,7 +626,7 @@ def run_ours(args, rank, world, local_rank):
                                    else f"z-slabs x{world} of the Kuhn lattice, per-rank "
                                         f"assembly, {trname} one-plane ghost exchanges"
                                    if isinstance(R, LatSlabRunner)
-                                   else f"z-slabs x{world}, NCCL halo-plane exchange")
+                                   else f"z-slabs x{world}, {trname} halo-plane exchange")
                                   if world > 1 else "single GPU",
                    "l2": "inputs larger than L2" if R.step_bytes() > 126e6 * 2
                          else "working set fits in L2 (latency-bound parity config)",

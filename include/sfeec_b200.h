@@ -238,6 +238,12 @@ int sfeec_part_get_state(sfeec_part* h, double* b_owned, double* e_owned, double
 int sfeec_part_advance(sfeec_part* h, int64_t nsteps);
 /* the same program for all ranks' handles on one device, halos copied */
 int sfeec_part_advance_local(sfeec_part** hs, int nranks, int64_t nsteps);
+/* Gives a multi-rank handle created without an NCCL id (nccl_id = NULL) the
+ * host-synchronised CUDA-IPC transport (ipc_id from sfeec_ipc_unique_id, the
+ * same bytes on every rank; collective over the ranks of one node, which may
+ * share a GPU): sfeec_part_advance / _set_state / _energy then pull the halo
+ * rows sfeec_part's NCCL path sends from the neighbours' mapped vectors. */
+int sfeec_part_attach_ipc(sfeec_part* h, const void* ipc_id);
 int sfeec_part_energy(sfeec_part* h, double* out);  /* this rank's part */
 int sfeec_part_energy_local(sfeec_part** hs, int nranks, double* out);
 int64_t sfeec_part_last_launches(sfeec_part* h);

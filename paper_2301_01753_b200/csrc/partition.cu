@@ -22,6 +22,7 @@
 
 #include "dev_handle.hpp"
 #include "device_util.cuh"
+#include "ipc_group.hpp"
 #include "nccl_loader.hpp"
 #include "spmv_kernels.cuh"
 #include "p2_device.hpp"
@@ -80,6 +81,15 @@ struct PartDev {
   bool overlap = true, xch_pending = false;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  // CUDA-IPC transport (host-synchronised; the ranks may share a GPU): the
+  // neighbours' e, t, b, u vectors mapped into this process
+  struct IpcSlot {
+    cudaIpcMemHandle_t h[4];
+    PartRange r1, r2;
+  };
+  std::unique_ptr<IpcGroup> ipc;
+  double* peer_lo[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* peer_hi[4] = {nullptr, nullptr, nullptr, nullptr};
   double dt = 0, eps0 = 1, mu0 = 1;
   PartRange r1, r2;  // edges, faces
   SplitOp q, c, ct, m2;
@@ -99,6 +109,10 @@ struct PartDev {
     if (ev_bnd) cudaEventDestroy(ev_bnd);
     if (ev_xch) cudaEventDestroy(ev_xch);
     if (comm) Nccl::get().comm_destroy(comm);
+    for (int f = 0; f < 4; ++f) {
+      if (peer_lo[f]) cudaIpcCloseMemHandle(peer_lo[f]);
+      if (peer_hi[f]) cudaIpcCloseMemHandle(peer_hi[f]);
+    }
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -214,8 +228,63 @@ struct PartDev {
   double* vec(Op x) { return x == kXe ? e.p : x == kXt ? t.p : x == kXb ? b.p : u.p; }
   const PartRange& range(Op x) const { return (x == kXe || x == kXt) ? r1 : r2; }
 
+  static int vec_index(Op x) { return x == kXe ? 0 : x == kXt ? 1 : x == kXb ? 2 : 3; }
+  // join the ranks' shared segment and map the neighbours' vectors (collective)
+  void attach_ipc(const void* id128) {
+    require(nranks > 1 && !comm && !ipc, "attach_ipc: a multi-rank handle without a transport");
+    ipc = std::make_unique<IpcGroup>("sfeec_part", id128, rank, nranks, sizeof(IpcSlot));
+    IpcSlot& me = *(IpcSlot*)ipc->slot(rank);
+    double* mine[4] = {e.p, t.p, b.p, u.p};
+    for (int f = 0; f < 4; ++f) SFEEC_CUDA(cudaIpcGetMemHandle(&me.h[f], mine[f]));
+    me.r1 = r1;
+    me.r2 = r2;
+    ipc->barrier();
+    for (int f = 0; f < 4; ++f) {
+      void* q = nullptr;
+      if (rank > 0) {
+        SFEEC_CUDA(cudaIpcOpenMemHandle(&q, ((IpcSlot*)ipc->slot(rank - 1))->h[f],
+                                        cudaIpcMemLazyEnablePeerAccess));
+        peer_lo[f] = (double*)q;
+      }
+      if (rank < nranks - 1) {
+        SFEEC_CUDA(cudaIpcOpenMemHandle(&q, ((IpcSlot*)ipc->slot(rank + 1))->h[f],
+                                        cudaIpcMemLazyEnablePeerAccess));
+        peer_hi[f] = (double*)q;
+      }
+    }
+    ipc->barrier();
+    ipc->unlink_name();
+  }
+  // the ranges exchange_nccl sends, pulled from the neighbours' vectors
+  // between two host barriers
+  void exchange_ipc(Op x, cudaStream_t st) {
+    const int f = vec_index(x);
+    const bool edges = x == kXe || x == kXt;
+    const PartRange& R = range(x);
+    double* v = vec(x);
+    SFEEC_CUDA(cudaStreamSynchronize(st));  // our rows are written ...
+    ipc->barrier();                         // ... and so are the neighbours'
+    if (rank > 0) {  // halo below <- the lower neighbour's last owned plane(s)
+      const IpcSlot& lo = *(const IpcSlot*)ipc->slot(rank - 1);
+      const PartRange& Lr = edges ? lo.r1 : lo.r2;
+      require(Lr.last_len == R.own_lo, "partition: halo sizes disagree");
+      SFEEC_CUDA(cudaMemcpyAsync(v, peer_lo[f] + Lr.own_hi - Lr.last_len,
+                                 sizeof(double) * (size_t)R.own_lo, cudaMemcpyDeviceToDevice, st));
+    }
+    if (rank < nranks - 1) {  // halo above <- the upper neighbour's first owned plane(s)
+      const IpcSlot& hi = *(const IpcSlot*)ipc->slot(rank + 1);
+      const PartRange& Hr = edges ? hi.r1 : hi.r2;
+      require(Hr.first_len == R.len - R.own_hi, "partition: halo sizes disagree");
+      SFEEC_CUDA(cudaMemcpyAsync(v + R.own_hi, peer_hi[f] + Hr.own_lo,
+                                 sizeof(double) * (size_t)(R.len - R.own_hi),
+                                 cudaMemcpyDeviceToDevice, st));
+    }
+    SFEEC_CUDA(cudaStreamSynchronize(st));  // our pulls are done ...
+    ipc->barrier();                         // ... before anyone overwrites a source row
+  }
   void exchange_nccl(Op x) { exchange_nccl(x, stream); }
   void exchange_nccl(Op x, cudaStream_t stream) {
+    if (nranks > 1 && ipc) return exchange_ipc(x, stream);
     if (nranks == 1 || !comm) return;
     const Nccl& nc = Nccl::get();
     const PartRange& R = range(x);
@@ -240,8 +309,8 @@ struct PartDev {
     for (size_t i = 0; i < prog.size(); ++i) {
       const Step& s = prog[i];
       if (s.op <= kXu) {
-        if (nranks == 1 || !comm) continue;
-        if (overlap && i > 0 && prog[i - 1].op >= kQ && produced(prog[i - 1].op) == s.op)
+        if (nranks == 1 || (!comm && !ipc)) continue;
+        if (comm && overlap && i > 0 && prog[i - 1].op >= kQ && produced(prog[i - 1].op) == s.op)
           continue;  // already in flight beside the interior rows
         tic(4);
         exchange_nccl(s.op, stream);
@@ -492,10 +561,19 @@ int sfeec_part_advance(sfeec_part* h, int64_t nsteps) {
   return guarded([&] {
     require(h, "null handle");
     require(nsteps >= 0, "advance: nsteps must be >= 0");
-    require(h->d.nranks == 1 || h->d.comm, "multi-rank handle without NCCL: use sfeec_part_advance_local");
+    require(h->d.nranks == 1 || h->d.comm || h->d.ipc,
+            "multi-rank handle without a transport: use sfeec_part_advance_local");
     SFEEC_CUDA(cudaSetDevice(h->d.device));
     h->d.advance(nsteps);
     SFEEC_CUDA(cudaStreamSynchronize(h->d.stream));
+  });
+}
+
+int sfeec_part_attach_ipc(sfeec_part* h, const void* ipc_id) {
+  return guarded([&] {
+    require(h && ipc_id, "null argument");
+    SFEEC_CUDA(cudaSetDevice(h->d.device));
+    h->d.attach_ipc(ipc_id);
   });
 }
 

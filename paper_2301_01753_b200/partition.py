@@ -163,6 +163,13 @@ class TetPart:
     def handle(self):
         return self._h
 
+    def attach_ipc(self, comm_id: bytes) -> None:
+        """Collective: the host-synchronised CUDA-IPC halo transport for a
+        multi-rank handle created without an NCCL id (comm_id from
+        ipc_unique_id(); the ranks may share a GPU)."""
+        idbuf = (C.c_char * 128).from_buffer_copy(comm_id.ljust(128, b"\0")[:128])
+        L.check(L.lib().sfeec_part_attach_ipc(self._h, C.cast(idbuf, C.c_void_p)))
+
     def load_global(self, b, e, time=0.0):
         eg, fg = self.ls.edge_global, self.ls.face_global
         bo = np.ascontiguousarray(b[fg[1]:fg[2]], np.float64)
