@@ -25,13 +25,7 @@
 //         mappings, with a process-shared barrier in POSIX shared memory.
 //         No kernel ever waits on another rank, so ranks may share one GPU:
 //         this is the transport the single-GPU multi-process tests use.
-#include <fcntl.h>
-#include <sched.h>
-#include <sys/mman.h>
-#include <unistd.h>
 
-#include <atomic>
-#include <chrono>
 #include <climits>
 #include <cstring>
 #include <memory>
@@ -40,6 +34,7 @@
 #include <vector>
 
 #include "device_util.cuh"
+#include "ipc_group.hpp"
 #include "lattice.cuh"
 #include "nccl_loader.hpp"
 #include "tet_device.hpp"
@@ -220,72 +215,28 @@ struct IpcRank {
   cudaIpcMemHandle_t h[4];  // E, T, B, U
   int64_t np = 0;           // component stride of that rank's box
   int kz0 = 0, p0 = 0, p1 = 0;
-  int ready = 0;
-};
-struct IpcShared {
-  std::atomic<int> magic;
-  std::atomic<int> count;
-  std::atomic<int> gen;
-  int nranks, nred;
-  IpcRank r[kIpcMaxRanks];
-  // followed by nranks * nred doubles (all-reduce rows)
+  // followed by nred doubles: this rank's row of an all-reduce
 };
 
+// The shared segment, its barrier and the per-rank slots are ipc_group.hpp's;
+// a slot holds IpcRank and the rank's reduction row.
 struct IpcComm final : SlabComm {
   SlabPlan p;
-  std::string name;
-  IpcShared* sh = nullptr;
-  size_t bytes = 0;
-  double* rows = nullptr;
+  int nred;
+  IpcGroup grp;
   double* peer[kIpcMaxRanks][4] = {};
   double* mine[4] = {};
 
-  IpcComm(const SlabPlan& plan, const void* id128, double* fields[4], int p0, int p1, int nred)
-      : p(plan) {
+  const IpcRank& info(int q) const { return *(const IpcRank*)grp.slot(q); }
+  double* row(int q) const { return (double*)((char*)grp.slot(q) + sizeof(IpcRank)); }
+
+  IpcComm(const SlabPlan& plan, const void* id128, double* fields[4], int p0, int p1, int nred_)
+      : p(plan),
+        nred(nred_),
+        grp("sfeec_lslab", id128, plan.rank, plan.nranks,
+            sizeof(IpcRank) + sizeof(double) * (size_t)nred_) {
     require(p.nranks <= kIpcMaxRanks, "IPC transport: at most 16 ranks");
-    char hex[40];
-    const unsigned char* b = (const unsigned char*)id128;
-    for (int i = 0; i < 16; ++i) std::snprintf(hex + 2 * i, 3, "%02x", b[i]);
-    name = std::string("/sfeec_lslab_") + hex;
-    bytes = sizeof(IpcShared) + sizeof(double) * (size_t)p.nranks * (size_t)nred;
-    int fd = -1;
-    const auto t0 = std::chrono::steady_clock::now();
-    if (p.rank == 0) {
-      fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
-      require(fd >= 0, "IPC transport: shm_open failed");
-      require(ftruncate(fd, (off_t)bytes) == 0, "IPC transport: ftruncate failed");
-    } else {
-      while ((fd = shm_open(name.c_str(), O_RDWR, 0600)) < 0) {
-        require(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(120),
-                "IPC transport: rank 0's segment did not appear");
-        usleep(1000);
-      }
-      // wait until rank 0 has sized it
-      while (lseek(fd, 0, SEEK_END) < (off_t)bytes) {
-        require(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(120),
-                "IPC transport: segment not sized");
-        usleep(1000);
-      }
-    }
-    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-    close(fd);
-    require(m != MAP_FAILED, "IPC transport: mmap failed");
-    sh = (IpcShared*)m;
-    rows = (double*)((char*)m + sizeof(IpcShared));
-    if (p.rank == 0) {
-      sh->count.store(0);
-      sh->gen.store(0);
-      sh->nranks = p.nranks;
-      sh->nred = nred;
-      sh->magic.store(0x5feec, std::memory_order_release);
-    } else {
-      while (sh->magic.load(std::memory_order_acquire) != 0x5feec) {
-        require(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(120),
-                "IPC transport: segment not initialised");
-        usleep(1000);
-      }
-    }
-    IpcRank& me = sh->r[p.rank];
+    IpcRank& me = *(IpcRank*)grp.slot(p.rank);
     for (int f = 0; f < 4; ++f) {
       mine[f] = fields[f];
       SFEEC_CUDA(cudaIpcGetMemHandle(&me.h[f], fields[f]));
@@ -294,38 +245,24 @@ struct IpcComm final : SlabComm {
     me.kz0 = p.g.kz0;
     me.p0 = p0;
     me.p1 = p1;
-    barrier();
+    grp.barrier();
     for (int q = 0; q < p.nranks; ++q) {
       if (q == p.rank || (q != p.rank - 1 && q != p.rank + 1)) continue;
       for (int f = 0; f < 4; ++f) {
         void* ptr = nullptr;
-        SFEEC_CUDA(cudaIpcOpenMemHandle(&ptr, sh->r[q].h[f], cudaIpcMemLazyEnablePeerAccess));
+        SFEEC_CUDA(cudaIpcOpenMemHandle(&ptr, info(q).h[f], cudaIpcMemLazyEnablePeerAccess));
         peer[q][f] = (double*)ptr;
       }
     }
-    barrier();
-    if (p.rank == 0) shm_unlink(name.c_str());  // every rank has it mapped
+    grp.barrier();
+    grp.unlink_name();  // every rank has it mapped
   }
   ~IpcComm() override {
     for (int q = 0; q < kIpcMaxRanks; ++q)
       for (int f = 0; f < 4; ++f)
         if (peer[q][f]) cudaIpcCloseMemHandle(peer[q][f]);
-    if (sh) munmap(sh, bytes);
   }
-  void barrier() {
-    const int g = sh->gen.load(std::memory_order_acquire);
-    if (sh->count.fetch_add(1, std::memory_order_acq_rel) + 1 == p.nranks) {
-      sh->count.store(0, std::memory_order_relaxed);
-      sh->gen.fetch_add(1, std::memory_order_acq_rel);
-      return;
-    }
-    const auto t0 = std::chrono::steady_clock::now();
-    while (sh->gen.load(std::memory_order_acquire) == g) {
-      require(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(300),
-              "IPC transport: barrier timed out (a rank died?)");
-      sched_yield();
-    }
-  }
+  void barrier() { grp.barrier(); }
   int field_index(const double* f) const {
     for (int i = 0; i < 4; ++i)
       if (mine[i] == f) return i;
@@ -333,7 +270,7 @@ struct IpcComm final : SlabComm {
   }
   // peer q's local plane holding whole-mesh plane kg
   const double* peer_plane(int q, int fi, int c, int kg) const {
-    const IpcRank& pr = sh->r[q];
+    const IpcRank& pr = info(q);
     return peer[q][fi] + (int64_t)c * pr.np + p.g.PS * (int64_t)(kg - pr.kz0 + 1);
   }
   void exchange(double* f, int ncomp, bool up, bool down, cudaStream_t s) override {
@@ -345,23 +282,24 @@ struct IpcComm final : SlabComm {
       double* base = f + (int64_t)c * p.g.NP;
       if (down && p.rank < p.nranks - 1)  // ghost above <- rank+1's first owned plane
         SFEEC_CUDA(cudaMemcpyAsync(base + p.g.plane(p.o1),
-                                   peer_plane(p.rank + 1, fi, c, sh->r[p.rank + 1].p0), b,
+                                   peer_plane(p.rank + 1, fi, c, info(p.rank + 1).p0), b,
                                    cudaMemcpyDeviceToDevice, s));
       if (up && p.rank > 0)  // ghost below <- rank-1's last owned plane
         SFEEC_CUDA(cudaMemcpyAsync(base + p.g.plane(p.o0 - 1),
-                                   peer_plane(p.rank - 1, fi, c, sh->r[p.rank - 1].p1 - 1), b,
+                                   peer_plane(p.rank - 1, fi, c, info(p.rank - 1).p1 - 1), b,
                                    cudaMemcpyDeviceToDevice, s));
     }
     SFEEC_CUDA(cudaStreamSynchronize(s));  // our pulls are done ...
     barrier();                             // ... before anyone overwrites a source plane
   }
   void allreduce_disjoint(double* host, int n, cudaStream_t s) override {
-    require(n <= sh->nred, "IPC transport: reduction longer than the segment row");
-    std::memcpy(rows + (size_t)p.rank * sh->nred, host, sizeof(double) * n);
+    (void)s;
+    require(n <= nred, "IPC transport: reduction longer than the segment row");
+    std::memcpy(row(p.rank), host, sizeof(double) * n);
     barrier();
     for (int i = 0; i < n; ++i) {
       double v = 0.0;
-      for (int q = 0; q < p.nranks; ++q) v += rows[(size_t)q * sh->nred + i];
+      for (int q = 0; q < p.nranks; ++q) v += row(q)[i];
       host[i] = v;
     }
     barrier();
