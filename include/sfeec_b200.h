@@ -428,6 +428,10 @@ int sfeec_csr_transpose(const sfeec_csr* a, sfeec_csr_owned* out);
  * reference has no distributed code). */
 typedef struct sfeec_lslab sfeec_lslab;
 int sfeec_ipc_unique_id(void* out128);
+/* Host-only self-check of the IPC transport's shared segment and barrier
+ * (ipc_group.hpp): `rounds` barrier-separated all-sums of (rank + round) over
+ * the ranks' slots; *out = the last sum. No CUDA call. */
+int sfeec_ipc_group_selftest(const void* id128, int rank, int nranks, int rounds, double* out);
 int sfeec_lslab_create(int n, int nzg, double jitter, uint64_t seed, double dt, double eps0,
                        double mu0, int split_kind, int rank, int nranks, int transport,
                        const void* comm_id, int device, sfeec_lslab** out, int64_t* info);

@@ -138,6 +138,7 @@ _SIGS = {
     "sfeec_part_advance": (C.c_int, [_P, C.c_int64]),
     "sfeec_part_advance_local": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int64]),
     "sfeec_part_attach_ipc": (C.c_int, [_P, C.c_void_p]),
+    "sfeec_ipc_group_selftest": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _PD]),
     "sfeec_part_energy": (C.c_int, [_P, _PD]),
     "sfeec_part_energy_local": (C.c_int, [C.POINTER(_P), C.c_int, _PD]),
     "sfeec_part_last_launches": (C.c_int64, [_P]),

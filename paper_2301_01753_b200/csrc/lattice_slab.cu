@@ -594,6 +594,28 @@ int sfeec_ipc_unique_id(void* out128) {
   });
 }
 
+// Host-only check of the IPC group (ipc_group.hpp): every rank writes
+// rank + round into its slot, and after a barrier sums all slots; `rounds`
+// rounds, the last sum out. No CUDA call: runs without a GPU.
+int sfeec_ipc_group_selftest(const void* id128, int rank, int nranks, int rounds, double* out) {
+  return guarded([&] {
+    require(id128 && out && nranks >= 1 && rank >= 0 && rank < nranks && rounds >= 1,
+            "sfeec_ipc_group_selftest: bad argument");
+    IpcGroup g("sfeec_selftest", id128, rank, nranks, sizeof(double));
+    g.barrier();
+    g.unlink_name();
+    double sum = 0.0;
+    for (int r = 0; r < rounds; ++r) {
+      *(double*)g.slot(rank) = (double)(rank + r);
+      g.barrier();  // every slot of this round is written
+      sum = 0.0;
+      for (int q = 0; q < nranks; ++q) sum += *(const double*)g.slot(q);
+      g.barrier();  // ... and read, before the next round overwrites it
+    }
+    *out = sum;
+  });
+}
+
 int sfeec_lslab_create(int n, int nzg, double jitter, uint64_t seed, double dt, double eps0,
                        double mu0, int split_kind, int rank, int nranks, int transport,
                        const void* comm_id, int device, sfeec_lslab** out, int64_t* info) {
