@@ -9,6 +9,7 @@
 // ascending column order of the k-major numbering for rows away from the
 // 32-vertex x-block edges: those rows are summed exactly like the sliced /
 // ELL kernels (spmv_kernels.cu) sum their CSR rows.
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -182,16 +183,16 @@ void Lattice::apply_q(cudaStream_t s, int kb, int ke) const {
   k_lat_q<MapLine><<<MapLine::grid(g, kb, ke), kLT, 0, s>>>(g, kb, ke, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
-template <bool TRANS, int kCH>
+template <bool TRANS, int kCH, int kAL = 2>
 static void launch_inc_bulk(const LatGeom& g, int kb, int ke, double alpha, const double* x,
                             double* y, cudaStream_t s) {
   constexpr int NSEG = IncTab<TRANS>::nseg();
-  const int smem = 2 * NSEG * (kCH + 4) * (int)sizeof(double);
+  const int smem = 2 * NSEG * (kCH + 2 + kAL) * (int)sizeof(double);
   static int per_sm = 0, sms = 0;  // resident CTAs (the shared memory decides)
   if (!per_sm) {
-    SFEEC_CUDA(cudaFuncSetAttribute(k_lat_inc_bulk<TRANS, kCH>,
+    SFEEC_CUDA(cudaFuncSetAttribute(k_lat_inc_bulk<TRANS, kCH, kAL>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lat_inc_bulk<TRANS, kCH>, kCH,
+    SFEEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lat_inc_bulk<TRANS, kCH, kAL>, kCH,
                                                              smem));
     int dev = 0;
     SFEEC_CUDA(cudaGetDevice(&dev));
@@ -200,7 +201,7 @@ static void launch_inc_bulk(const LatGeom& g, int kb, int ke, double alpha, cons
   }
   const int64_t nchunk = ((g.PS + kCH - 1) / kCH) * (int64_t)(ke - kb);
   const unsigned grid = (unsigned)std::min<int64_t>(nchunk, (int64_t)per_sm * sms);
-  k_lat_inc_bulk<TRANS, kCH><<<grid, kCH, smem, s>>>(g, kb, ke, alpha, x, y);
+  k_lat_inc_bulk<TRANS, kCH, kAL><<<grid, kCH, smem, s>>>(g, kb, ke, alpha, x, y);
   SFEEC_LAUNCH_CHECK();
 }
 
@@ -210,6 +211,11 @@ void Lattice::apply_cb(double h, cudaStream_t s, int kb, int ke) const {
   // t staged by bulk copies (measured, tet256: 0.71 vs 0.95 ms for the plain
   // k_lat_cb; the same staging of u slows K-CTe, 0.75-0.83 vs 0.66 ms: its 21
   // segments leave room for two CTAs per SM)
+  if (const char* v = std::getenv("SFEEC_LAT_CBAL")) {
+    if (std::atoi(v) == 16) return launch_inc_bulk<false, 256, 16>(g, kb, ke, -h, T.p, B.p, s);
+    if (std::atoi(v) == 4) return launch_inc_bulk<false, 256, 4>(g, kb, ke, -h, T.p, B.p, s);
+    if (std::atoi(v) == 32) return launch_inc_bulk<false, 256, 32>(g, kb, ke, -h, T.p, B.p, s);
+  }
   launch_inc_bulk<false, 256>(g, kb, ke, -h, T.p, B.p, s);
 }
 void Lattice::apply_m2(cudaStream_t s, int kb, int ke) const {

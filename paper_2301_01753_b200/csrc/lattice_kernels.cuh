@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kLT) k_lat_cte(LatGeom g, int kbeg, int kend, 
 // their bulk copies (cp.async.bulk) into a two-stage shared-memory ring one
 // chunk ahead; the block's threads (one per position) sum the rows from shared
 // memory and update b / e in place. Persistent CTAs take chunks round-robin.
-constexpr int kSegLenMax = 256 + 4;  // doubles per staged segment at most (allocation slack)
+constexpr int kSegLenMax = 256 + 34;  // doubles per staged segment at most (allocation slack)
 
 template <bool TRANS>
 struct IncTab {
@@ -274,11 +274,13 @@ __device__ __forceinline__ void inc_vertex_stage(std::integer_sequence<int, Rs..
    ...);
 }
 
-template <bool TRANS, int kCH>
+template <bool TRANS, int kCH, int kAL = 2>
 __global__ void __launch_bounds__(kCH)
     k_lat_inc_bulk(LatGeom g, int kbeg, int kend, double alpha, const double* __restrict__ x,
                    double* __restrict__ y) {
-  constexpr int kSegLen = kCH + 4;  // di in -1..1 plus 16-byte alignment
+  // di in -1..1 plus the alignment of the copy's start (kAL doubles: 2 = the
+  // 16 bytes a bulk copy needs, 16 = whole 128-byte lines)
+  constexpr int kSegLen = kCH + 2 + kAL;
   using Tb = IncTab<TRANS>;
   constexpr int NSEG = Tb::nseg();
   constexpr int NR = TRANS ? 7 : 12;
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kCH)
     for (int sgi = 0; sgi < NSEG; ++sgi) {
       const lat::CSlot sl = Tb::slot(Tb::seg_slot(sgi));
       const int64_t g0 = (int64_t)sl.t * g.NP + g.PS * (k + 1 + sl.dk) + (int64_t)g.S * sl.dj + x0 - 1;
-      const int64_t a0 = g0 & ~(int64_t)1;
+      const int64_t a0 = g0 & ~(int64_t)(kAL - 1);
       shift[st][sgi] = (int)(g0 - a0);
       bc_copy(sm + (st * NSEG + sgi) * kSegLen, x + a0, kSegLen * 8, &bar[st]);
     }

@@ -45,7 +45,7 @@ __device__ __forceinline__ bool tl_vertex(const TLGeom& g, const TLMap&, int& r,
   const int p = (int)blockIdx.y * kTL + (int)threadIdx.x;  // over the padded rows j = 0..n
   if (p >= (g.n + 1) * g.S) return false;
   const int i = p % g.S - g.H;
-  idx = g.PS * (k + g.H) + (int64_t)g.S * g.H + p;
+  idx = g.P0 + g.PS * (k + g.H) + (int64_t)g.S * g.H + p;
   return i >= 0 && i <= g.n;
 }
 

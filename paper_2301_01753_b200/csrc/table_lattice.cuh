@@ -32,17 +32,26 @@ struct TLGeom {
   int S = 0;        // padded vertices per axis (n + 1 + 2 H)
   int64_t PS = 0;   // padded plane
   int64_t NP = 0;   // padded box: the type stride
+  static constexpr int64_t kAlign = 32;  // positions
+  int64_t P0 = 0;   // leading pad: puts the first swept position of a plane on an aligned address
   void init(int n_, int h_) {
     n = n_;
     H = h_;
     S = n + 1 + 2 * H;
-    PS = (int64_t)S * S;
-    NP = PS * S;
+    // The plane pitch and the first swept position of a plane (row j = 0) are
+    // multiples of kAlign positions, so a block's 128 positions start on a
+    // sector boundary in every array (measured on config 4: step 4.05 -> 3.95
+    // ms with 32 or 128, bitwise the same state).
+    PS = ((int64_t)S * S + kAlign - 1) / kAlign * kAlign;
+    P0 = (kAlign - ((int64_t)S * H) % kAlign) % kAlign;
+    NP = (PS * S + P0 + kAlign - 1) / kAlign * kAlign;
   }
 #ifdef __CUDACC__
   __host__ __device__
 #endif
-  int64_t pos(int i, int j, int k) const { return (i + H) + (int64_t)S * (j + H) + PS * (k + H); }
+  int64_t pos(int i, int j, int k) const {
+    return P0 + (i + H) + (int64_t)S * (j + H) + PS * (k + H);
+  }
 };
 
 struct TLSlot {   // symmetric operator: y_r(v) += coef[coff + v] * x[xoff + v]
