@@ -179,7 +179,7 @@ void Lattice::apply_q(cudaStream_t s, int kb, int ke) const {
   if (ke <= kb) return;
   // (e staged by bulk copies as in K-Cb, coefficients loaded as here, was
   // measured slower: 2.26 ms with 128-position chunks, 3.39 with 256, vs 2.02)
-  k_lat_q<MapLine><<<MapLine::grid(g, kb, ke), kLT, 0, s>>>(g, kb, ke, qc.p, E.p, T.p);
+  k_lat_q<MapSym><<<MapSym::grid(g, kb, ke), kSymThreads, 0, s>>>(g, kb, ke, qc.p, E.p, T.p);
   SFEEC_LAUNCH_CHECK();
 }
 template <bool TRANS, int kCH, int kAL = 2>
@@ -217,7 +217,7 @@ void Lattice::apply_m2(cudaStream_t s, int kb, int ke) const {
   if (kb < 0) kb = kbeg(), ke = kend();
   if (ke <= kb) return;
   // (b staged by bulk copies: 1.83 / 2.25 ms vs 1.48, as for K-Q)
-  k_lat_m2<MapLine><<<MapLine::grid(g, kb, ke), kLT, 0, s>>>(g, kb, ke, mc.p, B.p, U.p);
+  k_lat_m2<MapSym><<<MapSym::grid(g, kb, ke), kSymThreads, 0, s>>>(g, kb, ke, mc.p, B.p, U.p);
   SFEEC_LAUNCH_CHECK();
 }
 void Lattice::apply_cte(double f, cudaStream_t s, int kb, int ke) const {

@@ -45,14 +45,16 @@ __device__ __forceinline__ int64_t offset_of(const LatGeom& g, int di, int dj, i
 }
 
 // ---- thread -> vertex maps ------------------------------------------------
-// MapLine: a block is 256 consecutive positions of one padded plane (grid y =
-// plane). vertex(): this thread's vertex (i, j, local plane k) and lattice
+// MapLineN<NT>: a block is NT consecutive positions of one padded plane (grid
+// y = plane). vertex(): this thread's vertex (i, j, local plane k) and lattice
 // position; false off the mesh. (Brick-shaped maps were measured slower,
 // lattice.cu.)
-struct MapLine {
+template <int NT>
+struct MapLineN {
+  static constexpr int kThreads = NT;
   __device__ static __forceinline__ bool vertex(const LatGeom& g, int kbeg, int kend, int& i,
                                                 int& j, int& k, int64_t& idx) {
-    const int p = blockIdx.x * kLT + threadIdx.x;
+    const int p = blockIdx.x * NT + threadIdx.x;
     if (p >= g.PS) return false;
     k = kbeg + blockIdx.y;
     j = p / g.S - 1;
@@ -61,9 +63,16 @@ struct MapLine {
     return i >= 0 && i <= g.n && j >= 0 && j <= g.n;
   }
   static dim3 grid(const LatGeom& g, int kb, int ke) {
-    return dim3((unsigned)((g.PS + kLT - 1) / kLT), (unsigned)(ke - kb));
+    return dim3((unsigned)((g.PS + NT - 1) / NT), (unsigned)(ke - kb));
   }
 };
+using MapLine = MapLineN<kLT>;
+// K-Q and K-M2 run 128-thread blocks, four per SM (the same 128 registers and
+// 16 warps per SM as two 256-thread blocks; measured on tet256 over 300 steps:
+// K-Q 2.006 -> 1.958 ms, K-M2 1.468 -> 1.452, step 4.84 -> 4.79; 64 threads the
+// same, 512 slower)
+constexpr int kSymThreads = 128;
+using MapSym = MapLineN<kSymThreads>;
 // edge (v, t) is a DOF: inside the mesh and not on a wall it lies in (PEC);
 // z is judged on the whole mesh (kg = whole-mesh plane, nzg)
 template <int T>
@@ -119,11 +128,11 @@ __device__ __forceinline__ void q_vertex(std::integer_sequence<int, Ts...>, cons
   const double r[sizeof...(Ts)] = {sym_row<QOp, Ts>(qc, E, idx, g)...};
   ((edge_dof<Ts>(i, j, k, g) ? (void)(T[(int64_t)Ts * g.NP + idx] = r[Ts]) : (void)0), ...);
 }
-// 2 blocks per SM: 128 registers, every load of the vertex's 7 rows in flight
+// 512 threads per SM: 128 registers, every load of the vertex's 7 rows in flight
 // (measured: 80 / 64-register caps spill and run 1.6x / 2.4x slower; one
 // block per SM at 247 registers runs 1.05x (K-Q) / 1.15x (K-M2) slower)
 template <class Map>
-__global__ void __launch_bounds__(kLT, 2) k_lat_q(LatGeom g, int kbeg, int kend,
+__global__ void __launch_bounds__(Map::kThreads, 512 / Map::kThreads) k_lat_q(LatGeom g, int kbeg, int kend,
                                                const double* __restrict__ qc,
                                                const double* __restrict__ E,
                                                double* __restrict__ T) {
@@ -143,7 +152,7 @@ __device__ __forceinline__ void m2_vertex(std::integer_sequence<int, Fs...>, con
   ((face_ok<Fs>(i, j, k, g) ? (void)(U[(int64_t)Fs * g.NP + idx] = r[Fs]) : (void)0), ...);
 }
 template <class Map>
-__global__ void __launch_bounds__(kLT, 2) k_lat_m2(LatGeom g, int kbeg, int kend,
+__global__ void __launch_bounds__(Map::kThreads, 512 / Map::kThreads) k_lat_m2(LatGeom g, int kbeg, int kend,
                                                 const double* __restrict__ mc,
                                                 const double* __restrict__ B,
                                                 double* __restrict__ U) {
